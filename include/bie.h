@@ -1,0 +1,159 @@
+/*
+ * bie.h -- C ABI of libbie.so, the B200 (sm_100a) hot path of the
+ * boundary-integral GMRES method of arxiv 1609.04484 (2D Stokes flow in
+ * porous media), scoped per SURVEY.md s8:
+ *   completed double-layer (DLP) matvec  -> bie_dlp_apply
+ *   block-diagonal (BD) preconditioner   -> bie_blockdiag_factor / _apply
+ *   left-preconditioned full GMRES       -> bie_gmres_solve
+ *
+ * Citations: P:l.N = PAPER.md line N (arxiv 1609.04484 LaTeX body); readings
+ * C1..C19 are listed in DESIGN.md s3.
+ *
+ * Conventions for every call:
+ *  - Returns BIE_OK (0) or a negative BIE_E* code; bie_last_error() returns a
+ *    thread-local message describing the last failure on the calling thread.
+ *  - "device" pointers are CUDA device (or managed) memory owned by the caller
+ *    (e.g. torch.Tensor.data_ptr()); "host" pointers are ordinary host memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls documented "async" only enqueue work on that stream.
+ *  - All floating point is IEEE FP64.  Vectors of unknowns are interleaved
+ *    (sigma_x, sigma_y) per node, 2N doubles per vector, in dof order:
+ *    pore 1 nodes, ..., pore M nodes, then the outer wall Gamma_0
+ *    (P:l.734-736: "the first 2x128x22 dofs" are the pores).  A batch of
+ *    nvec vectors is [nvec][2N], vector-major.
+ *  - One geometry handle owns one workspace: calls that use the same
+ *    geometry (or a blockdiag built from it) must be serialised on one stream.
+ */
+#ifndef BIE_H
+#define BIE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BIE_OK 0
+#define BIE_EINVAL (-1)     /* bad argument, null handle, wrong handle kind */
+#define BIE_EGEOM (-2)      /* invalid geometry (pore radius <= 0, ...) */
+#define BIE_ESINGULAR (-3)  /* a BD block has a zero pivot (S:l.386: fail loudly) */
+#define BIE_ECUDA (-4)      /* CUDA launch/runtime error */
+#define BIE_ENOMEM (-5)     /* device or host allocation failed */
+
+/* bie_dlp_apply flags */
+#define BIE_FULL 0u    /* -1/2 I + D + self term + N0 + pore completion (reading C5/C6) */
+#define BIE_D_ONLY 1u  /* PV trapezoid DLP sum + self term only (Gauss-identity pins) */
+
+#define BIE_MAX_NVEC 16
+
+#if defined(__GNUC__)
+#define BIE_API __attribute__((visibility("default")))
+#else
+#define BIE_API
+#endif
+
+typedef struct bie_geometry_s *bie_geometry_t;
+typedef struct bie_blockdiag_s *bie_blockdiag_t;
+
+/*
+ * bie_geometry_create -- A1: derive the node table on the
+ * device and allocate the matvec workspace.
+ *   P:l.191-204 (Gamma_0 = mollified rectangle, pores = circles),
+ *   P:l.296-309 (collocation at N = M N_int + N_ext points),
+ *   P:l.318-319, P:l.354 (w_j = arclength element x trapezoid weight).
+ * Inputs (host):
+ *   outer_xy, outer_dxy, outer_ddxy : [n_outer][2] samples x(t_j), x'(t_j),
+ *       x''(t_j) of the outer wall at t_j = j*outer_period/n_outer, CCW.
+ *   pore_c : [n_pores][2] centres, pore_r : [n_pores] radii (> 0).
+ *   nodes_per_pore : N_int; pore node j at theta_j = 2 pi j/N_int (C12).
+ * Derived per node: w = |x'| T/n (C7); t = x'/|x'|; n = out of the fluid
+ * domain (C2): (t_y,-t_x) on Gamma_0, -(cos,sin) on pores; kappa_n =
+ * x''.n/|x'|^2.  The handle owns all device data; destroy frees it.
+ * Errors: BIE_EINVAL (null pointer, n_outer or nodes_per_pore < 16 or odd
+ * (S:l.55-57), n_pores < 0, outer_period <= 0), BIE_EGEOM (radius <= 0 or
+ * non-finite input), BIE_ENOMEM, BIE_ECUDA.  Synchronous.
+ */
+BIE_API int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const double *outer_ddxy,
+                        int n_outer, double outer_period, const double *pore_c, const double *pore_r,
+                        int n_pores, int nodes_per_pore, bie_geometry_t *out);
+BIE_API int bie_geometry_destroy(bie_geometry_t g);
+/* N = number of nodes (2N unknowns), M = number of pores. */
+BIE_API int bie_geometry_info(bie_geometry_t g, int *N, int *M);
+/* Copy node positions to host: pos_host [N][2]. Synchronous. */
+BIE_API int bie_geometry_nodes(bie_geometry_t g, double *pos_host);
+
+/*
+ * bie_dlp_apply -- A2-A5: out = A sigma for nvec densities (async on stream).
+ *   y_i = -1/2 sigma_i                                        (jump, C3)
+ *       + sum_{j != i} (w_j/pi)(r.n_j)(r.sigma_j) r / rho^4    (P:l.243-248, trapezoid P:l.310-319)
+ *       + (w_i/2pi) kappa_n,i (t_i.sigma_i) t_i                (diagonal limit, C4)
+ *       + [i in Gamma_0] nu n_i                                (N0 term, C5)
+ *       + sum_k Stokeslet(x_i-c_k) lambda_k + r_k rotlet(x_i-c_k) mu_k   (completion, C5;
+ *         forms of P:l.944-948)
+ *   r = x_i - x_j, rho = |r|; moments lambda_k, mu_k, nu as in DESIGN.md s2.
+ * sigma, out : device [nvec][2N]; out must not alias sigma.
+ * nvec in [1, BIE_MAX_NVEC].  flags: BIE_FULL or BIE_D_ONLY.
+ * Errors: BIE_EINVAL (null, nvec out of range, out == sigma, bad flags),
+ * BIE_ECUDA (launch error; asynchronous faults surface at the next sync).
+ * Never synchronises.
+ */
+BIE_API int bie_dlp_apply(bie_geometry_t g, const double *sigma, double *out, int nvec, unsigned flags, void *stream);
+
+/*
+ * bie_dlp_apply_rows -- same operator restricted to target nodes
+ * [row_begin, row_end) (row sharding).  sigma is the full
+ * [nvec][2N] density; out is [nvec][2*(row_end-row_begin)].  Async.
+ */
+BIE_API int bie_dlp_apply_rows(bie_geometry_t g, const double *sigma, double *out, int nvec, unsigned flags,
+                       int row_begin, int row_end, void *stream);
+
+/*
+ * bie_dlp_apply_host -- end-to-end variant: sigma_host / out_host are HOST
+ * buffers [nvec][2N] (pinned for full speed, pageable accepted).  Copies
+ * H2D, applies, copies D2H and synchronises the stream before returning.
+ */
+BIE_API int bie_dlp_apply_host(bie_geometry_t g, const double *sigma_host, double *out_host, int nvec, unsigned flags,
+                       void *stream);
+
+/*
+ * bie_blockdiag_factor -- A6: block-diagonal preconditioner, P:l.651-657
+ * ("diagonal blocks corresponding to the self-interactions of the individual
+ * pores and the outer boundary ... assembled, factorized, and inverted
+ * exactly").  Block b = rows/cols of the completed operator on body b (pore
+ * blocks include their own Stokeslet/rotlet columns; the Gamma_0 block
+ * includes N0).  Each block is inverted explicitly by Gauss-Jordan
+ * elimination with partial pivoting (row of max |.|).  The handle owns the
+ * inverses (sum_b (2 n_b)^2 doubles of device memory).
+ * Synchronises `stream` once to read the pivot status.
+ * Errors: BIE_ESINGULAR (message names the body), BIE_ENOMEM, BIE_ECUDA, BIE_EINVAL.
+ */
+BIE_API int bie_blockdiag_factor(bie_geometry_t g, bie_blockdiag_t *out, void *stream);
+/* A7: out_b = B_b^{-1} in_b for every body, nvec vectors, device [nvec][2N]; async; in != out. */
+BIE_API int bie_blockdiag_apply(bie_blockdiag_t bd, const double *in, double *out, int nvec, void *stream);
+BIE_API int bie_blockdiag_destroy(bie_blockdiag_t bd);
+/* Copy the explicit inverse of body b ([2n_b][2n_b] row-major) to host (test hook). Synchronous. */
+BIE_API int bie_blockdiag_block_inverse(bie_blockdiag_t bd, int body, double *host, long long host_len);
+
+/*
+ * bie_gmres_solve -- A8/A9: left-preconditioned full GMRES (no restart),
+ * x0 = 0, CGS2 orthogonalisation, Givens rotations (reading C13), tolerance on
+ * the preconditioned relative residual estimate |g_{k+1}|/||P^{-1} f||
+ * (P:l.596-601, P:l.661-663, P:l.678-681).  bd == NULL -> no preconditioner.
+ *   f, x : device [2N] (x is written).
+ *   hist_host : host [max_iter+1]; hist_host[0..*iters] = estimates (hist[0] = 1).
+ *   iters, converged : host outputs (converged = 0 at the iteration cap, S:l.376;
+ *     happy breakdown counts as converged, S:l.377).
+ *   res_pc, res_true : host outputs ||P^{-1}(f-Ax)||/||P^{-1}f|| and ||f-Ax||/||f||
+ *     (P:l.678-686), from one extra matvec at the end.
+ * The Krylov basis lives in device memory: (max_iter+1)*2N doubles.
+ * Synchronises once per iteration (8-byte D2H of the estimate).
+ * Errors: BIE_EINVAL, BIE_ENOMEM (basis allocation), BIE_ECUDA.
+ */
+BIE_API int bie_gmres_solve(bie_geometry_t g, bie_blockdiag_t bd, const double *f, double *x, double tol, int max_iter,
+                    double *hist_host, int *iters, double *res_pc, double *res_true, int *converged,
+                    void *stream);
+
+BIE_API const char *bie_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIE_H */

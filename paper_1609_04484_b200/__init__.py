@@ -1,0 +1,25 @@
+"""B200-native hot path of arxiv 1609.04484 (2D Stokes BIE-GMRES in porous media).
+
+Thin ctypes binding of the C ABI declared in include/bie.h and implemented by
+paper_1609_04484_b200/lib/libbie.so (CUDA, sm_100a).  Argument marshalling
+only: every step of the path runs in the library's kernels.  There is no CPU
+fallback -- importing the binding on a machine without the built library, or
+calling a compute entry point without a CUDA device, raises.
+"""
+from ._bie import (  # noqa: F401
+    BIE_D_ONLY,
+    BIE_FULL,
+    BIE_MAX_NVEC,
+    BieError,
+    BlockDiag,
+    Geometry,
+    blockdiag_apply,
+    blockdiag_factor,
+    dlp_apply,
+    dlp_apply_host,
+    dlp_apply_rows,
+    gmres_solve,
+    lib,
+    lib_path,
+    EXPORTED_SYMBOLS,
+)

@@ -1,0 +1,234 @@
+"""ctypes binding of libbie.so (names mirror include/bie.h)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libbie.so")
+
+BIE_OK = 0
+BIE_EINVAL = -1
+BIE_EGEOM = -2
+BIE_ESINGULAR = -3
+BIE_ECUDA = -4
+BIE_ENOMEM = -5
+BIE_FULL = 0
+BIE_D_ONLY = 1
+BIE_MAX_NVEC = 16
+
+_CODES = {BIE_EINVAL: "BIE_EINVAL", BIE_EGEOM: "BIE_EGEOM", BIE_ESINGULAR: "BIE_ESINGULAR",
+          BIE_ECUDA: "BIE_ECUDA", BIE_ENOMEM: "BIE_ENOMEM"}
+
+EXPORTED_SYMBOLS = (
+    "bie_geometry_create", "bie_geometry_destroy", "bie_geometry_info", "bie_geometry_nodes",
+    "bie_dlp_apply", "bie_dlp_apply_rows", "bie_dlp_apply_host",
+    "bie_blockdiag_factor", "bie_blockdiag_apply", "bie_blockdiag_destroy", "bie_blockdiag_block_inverse",
+    "bie_gmres_solve", "bie_last_error",
+)
+
+
+class BieError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_CODES.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libbie.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"libbie.so not built: {_LIB_PATH} missing (run __graft_entry__.build())")
+    L = ctypes.CDLL(_LIB_PATH)
+    vp, dp, ip = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
+    c_int, c_uint, c_double = ctypes.c_int, ctypes.c_uint, ctypes.c_double
+    sig = {
+        "bie_geometry_create": [dp, dp, dp, c_int, c_double, dp, dp, c_int, c_int, ctypes.POINTER(vp)],
+        "bie_geometry_destroy": [vp],
+        "bie_geometry_info": [vp, ip, ip],
+        "bie_geometry_nodes": [vp, dp],
+        "bie_dlp_apply": [vp, vp, vp, c_int, c_uint, vp],
+        "bie_dlp_apply_rows": [vp, vp, vp, c_int, c_uint, c_int, c_int, vp],
+        "bie_dlp_apply_host": [vp, dp, dp, c_int, c_uint, vp],
+        "bie_blockdiag_factor": [vp, ctypes.POINTER(vp), vp],
+        "bie_blockdiag_apply": [vp, vp, vp, c_int, vp],
+        "bie_blockdiag_destroy": [vp],
+        "bie_blockdiag_block_inverse": [vp, c_int, dp, ctypes.c_longlong],
+        "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = c_int
+    L.bie_last_error.argtypes = []
+    L.bie_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != BIE_OK:
+        raise BieError(rc, lib().bie_last_error().decode(errors="replace"))
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_ptr(t, name, n_expected=None):
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor on a CUDA device")
+    if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+    if n_expected is not None and t.numel() < n_expected:
+        raise ValueError(f"{name} has {t.numel()} elements, needs {n_expected}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Geometry:
+    """bie_geometry_t: device node table + matvec workspace (A1)."""
+
+    def __init__(self, outer_xy, outer_dxy, outer_ddxy, period, pore_c, pore_r, nodes_per_pore):
+        L = lib()
+        c = lambda a: np.ascontiguousarray(a, dtype=np.float64).reshape(-1)  # noqa: E731
+        self._arrays = [c(outer_xy), c(outer_dxy), c(outer_ddxy), c(pore_c), c(pore_r)]
+        n_outer = self._arrays[0].size // 2
+        M = self._arrays[4].size
+        h = ctypes.c_void_p()
+        _check(L.bie_geometry_create(_dp(self._arrays[0]), _dp(self._arrays[1]), _dp(self._arrays[2]), n_outer,
+                                     float(period), _dp(self._arrays[3]) if M else None,
+                                     _dp(self._arrays[4]) if M else None, M, int(nodes_per_pore), ctypes.byref(h)))
+        self.h = h
+        N, Mo = ctypes.c_int(), ctypes.c_int()
+        _check(L.bie_geometry_info(h, ctypes.byref(N), ctypes.byref(Mo)))
+        self.N, self.M = N.value, Mo.value
+        self.n_pore = int(nodes_per_pore) if M else 0
+
+    @classmethod
+    def from_problem(cls, p):
+        """Duck-typed: any object with outer_xy/outer_dxy/outer_ddxy/period/pore_c/pore_r/n_pore."""
+        return cls(p.outer_xy, p.outer_dxy, p.outer_ddxy, p.period, p.pore_c, p.pore_r, p.n_pore)
+
+    def nodes(self) -> np.ndarray:
+        out = np.zeros(2 * self.N)
+        _check(lib().bie_geometry_nodes(self.h, _dp(out)))
+        return out.reshape(-1, 2)
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            _check(lib().bie_geometry_destroy(self.h))
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dlp_apply(g: Geometry, sigma, out, nvec: int = 1, flags: int = BIE_FULL, stream=None):
+    """out = A sigma on the device (bie_dlp_apply); sigma/out: float64 CUDA [nvec*2N]."""
+    n = nvec * 2 * g.N
+    _check(lib().bie_dlp_apply(g.h, _dev_ptr(sigma, "sigma", n), _dev_ptr(out, "out", n), nvec, flags,
+                               _stream_ptr(stream)))
+    return out
+
+
+def dlp_apply_rows(g: Geometry, sigma, out, row_begin: int, row_end: int, nvec: int = 1, flags: int = BIE_FULL,
+                   stream=None):
+    _check(lib().bie_dlp_apply_rows(g.h, _dev_ptr(sigma, "sigma", nvec * 2 * g.N),
+                                    _dev_ptr(out, "out", nvec * 2 * (row_end - row_begin)), nvec, flags,
+                                    row_begin, row_end, _stream_ptr(stream)))
+    return out
+
+
+def dlp_apply_host(g: Geometry, sigma_host: np.ndarray, out_host: np.ndarray, nvec: int = 1,
+                   flags: int = BIE_FULL, stream=None):
+    """End-to-end: host buffers in and out (bie_dlp_apply_host); synchronises."""
+    assert sigma_host.dtype == np.float64 and out_host.dtype == np.float64
+    assert sigma_host.size >= nvec * 2 * g.N and out_host.size >= nvec * 2 * g.N
+    st = _stream_ptr(stream) if stream is not None else ctypes.c_void_p(0)
+    _check(lib().bie_dlp_apply_host(g.h, _dp(sigma_host), _dp(out_host), nvec, flags, st))
+    return out_host
+
+
+def dlp_apply_host_ptr(g: Geometry, sigma_ptr: int, out_ptr: int, nvec: int = 1, flags: int = BIE_FULL,
+                       stream=None):
+    """Same as dlp_apply_host for raw (e.g. pinned torch) host pointers."""
+    st = _stream_ptr(stream) if stream is not None else ctypes.c_void_p(0)
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(lib().bie_dlp_apply_host(g.h, ctypes.cast(sigma_ptr, dp), ctypes.cast(out_ptr, dp), nvec, flags, st))
+
+
+class BlockDiag:
+    """bie_blockdiag_t: explicit per-body inverses (A6)."""
+
+    def __init__(self, g: Geometry, stream=None):
+        h = ctypes.c_void_p()
+        _check(lib().bie_blockdiag_factor(g.h, ctypes.byref(h), _stream_ptr(stream)))
+        self.h = h
+        self.g = g
+
+    def block_inverse(self, body: int) -> np.ndarray:
+        g = self.g
+        n = g.n_pore if body < g.M else g.N - g.M * g.n_pore
+        out = np.zeros((2 * n, 2 * n))
+        _check(lib().bie_blockdiag_block_inverse(self.h, body, _dp(out), out.size))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            _check(lib().bie_blockdiag_destroy(self.h))
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def blockdiag_factor(g: Geometry, stream=None) -> BlockDiag:
+    return BlockDiag(g, stream)
+
+
+def blockdiag_apply(bd: BlockDiag, inp, out, nvec: int = 1, stream=None):
+    n = nvec * 2 * bd.g.N
+    _check(lib().bie_blockdiag_apply(bd.h, _dev_ptr(inp, "in", n), _dev_ptr(out, "out", n), nvec,
+                                     _stream_ptr(stream)))
+    return out
+
+
+def gmres_solve(g: Geometry, bd: BlockDiag | None, f, x, tol: float = 1e-8, max_iter: int = 1000, stream=None):
+    """bie_gmres_solve; returns dict(iters, hist, res_pc, res_true, converged)."""
+    hist = np.zeros(max_iter + 1)
+    it, conv = ctypes.c_int(0), ctypes.c_int(0)
+    rp, rt = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().bie_gmres_solve(g.h, None if bd is None else bd.h, _dev_ptr(f, "f", 2 * g.N),
+                                 _dev_ptr(x, "x", 2 * g.N), float(tol), int(max_iter), _dp(hist), ctypes.byref(it),
+                                 ctypes.byref(rp), ctypes.byref(rt), ctypes.byref(conv), _stream_ptr(stream)))
+    return dict(iters=it.value, hist=hist[: it.value + 1].copy(), res_pc=rp.value, res_true=rt.value,
+                converged=bool(conv.value))

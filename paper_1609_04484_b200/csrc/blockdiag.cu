@@ -1,0 +1,587 @@
+// blockdiag.cu -- block-diagonal preconditioner (A6 factor, A7 apply).
+//
+// P:l.651-657: "a block-diagonal preconditioner (with the diagonal blocks
+// corresponding to the self-interactions of the individual pores and the
+// outer boundary) ... The diagonal blocks are assembled, factorized, and
+// inverted exactly."  Block b = rows/cols of the completed operator on body b.
+//
+// Factor: every block is inverted in place by blocked Gauss-Jordan elimination
+// with partial pivoting.  For a panel K of NB columns:
+//   1. k_panel    : LU with partial pivoting of the panel rows >= k0 (one CTA per
+//                   matrix) -> pivots; A11^{-1} from L11 U11.
+//   2. k_swap     : apply the panel's row swaps to the whole matrix.
+//   3. k_copy_T   : T = M[:, K];   k_make_G : G = A11^{-1} M[K, :], G[:, K] = A11^{-1}
+//   4. k_update   : M[i, :] = (i in K) ? G[i-k0, :] : base(i, :) - T[i, :] G
+//                   (base = M off K, 0 on K)  -- the rank-NB sweep, DFMA tiles.
+// After the last panel, columns are unpermuted (A^{-1} = M P).  Batched over
+// all blocks of one size class (pores share one size; Gamma_0 is its own class).
+// Apply: one warp per row of the explicit inverses (HBM-bound batched GEMV).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace bie {
+
+constexpr int NB = 32;  // panel width
+
+struct BDView {            // one size class
+    double *mat;           // first matrix
+    long long mstride;     // doubles between consecutive matrices
+    int n2;                // matrix order
+    int count;             // matrices in the class
+    int body0;             // body index of the first matrix
+};
+
+struct BDScratch {
+    double *W;      // [count][n2][NB]   panel LU workspace
+    double *T;      // [count][n2][NB]
+    double *G;      // [count][NB][n2]
+    double *A11i;   // [count][NB][NB]
+    int *piv;       // [count][n2]
+    int *flag;      // [count]
+};
+
+// ------------------------------------------------------------------ assembly
+// Entry (2x2 node block) for nodes i, j of body b (same formula as the operator):
+//   i != j : c r r^T with c = (r . nw_j)/rho^4          (DLP, P:l.243-248)
+//   i == j : selfc_i t t^T - 1/2 I                      (C4, C3)
+//   pore k : + (w_j/|Gamma_k|) [S(x_i - c_k) + R(x_i - c_k) ((x_j - c_k)^perp)^T]   (C5)
+//   wall   : + n_i n_j^T w_j / |Gamma_0|                (C5, N0)
+__global__ void k_bd_assemble(BDView v, int lo0, int nodes, int is_wall, const double2 *__restrict__ pos,
+                              const double2 *__restrict__ nw, const double2 *__restrict__ nrm,
+                              const double2 *__restrict__ tan, const double *__restrict__ w,
+                              const double *__restrict__ selfc, const double4 *__restrict__ pore, double wall_len) {
+    const int m = blockIdx.y;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)nodes * nodes) return;
+    const int li = (int)(e / nodes), lj = (int)(e % nodes);
+    const int lo = lo0 + m * nodes;
+    const int i = lo + li, j = lo + lj;
+    double e00, e01, e10, e11;
+    const double2 xi = pos[i], xj = pos[j];
+    if (i != j) {
+        const double rx = xi.x - xj.x, ry = xi.y - xj.y;
+        const double rho2 = rx * rx + ry * ry;
+        const double2 nj = nw[j];
+        const double c = (rx * nj.x + ry * nj.y) / (rho2 * rho2);
+        e00 = c * rx * rx;
+        e01 = c * rx * ry;
+        e10 = e01;
+        e11 = c * ry * ry;
+    } else {
+        const double2 t = tan[i];
+        const double a = selfc[i];
+        e00 = a * t.x * t.x - 0.5;
+        e01 = a * t.x * t.y;
+        e10 = e01;
+        e11 = a * t.y * t.y - 0.5;
+    }
+    if (!is_wall) {
+        const double4 pk = pore[v.body0 + m];
+        const double rx = xi.x - pk.x, ry = xi.y - pk.y;
+        const double rho2 = rx * rx + ry * ry;
+        const double lg = 0.5 * log(rho2);
+        const double f = w[j] / pk.w;
+        constexpr double k4pi = 1.0 / (4.0 * kPi);
+        const double s00 = k4pi * (-lg + rx * rx / rho2);
+        const double s01 = k4pi * (rx * ry / rho2);
+        const double s11 = k4pi * (-lg + ry * ry / rho2);
+        const double Rx = ry / rho2, Ry = -rx / rho2;
+        const double qx = xj.y - pk.y, qy = -(xj.x - pk.x);
+        e00 += f * (s00 + Rx * qx);
+        e01 += f * (s01 + Rx * qy);
+        e10 += f * (s01 + Ry * qx);
+        e11 += f * (s11 + Ry * qy);
+    } else {
+        const double f = w[j] / wall_len;
+        const double2 ni = nrm[i], nj = nrm[j];
+        e00 += f * ni.x * nj.x;
+        e01 += f * ni.x * nj.y;
+        e10 += f * ni.y * nj.x;
+        e11 += f * ni.y * nj.y;
+    }
+    double *M = v.mat + (long long)m * v.mstride;
+    const long long n2 = v.n2;
+    M[(2LL * li) * n2 + 2 * lj] = e00;
+    M[(2LL * li) * n2 + 2 * lj + 1] = e01;
+    M[(2LL * li + 1) * n2 + 2 * lj] = e10;
+    M[(2LL * li + 1) * n2 + 2 * lj + 1] = e11;
+}
+
+// ------------------------------------------------------------------ panel LU
+// One CTA per matrix.  Rows [k0, n2) of panel columns [k0, k0+nbe).
+// Pivot = max |value|, lowest row index on ties (as the oracle).
+__global__ void __launch_bounds__(1024) k_panel(BDView v, BDScratch s, int k0, int nbe) {
+    const int m = blockIdx.x;
+    const int n2 = v.n2;
+    const double *M = v.mat + (long long)m * v.mstride;
+    double *W = s.W + (long long)m * n2 * NB;  // W[r][c], r = row index (global), c < NB
+    int *piv = s.piv + (long long)m * n2;
+    __shared__ double red_v[32];
+    __shared__ int red_i[32];
+    __shared__ int s_p;
+    __shared__ double s_d;
+    __shared__ double L11[NB][NB + 1], U11[NB][NB + 1];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (long long q = tid; q < (long long)(n2 - k0) * nbe; q += nt) {
+        int r = k0 + (int)(q / nbe), c = (int)(q % nbe);
+        W[(long long)r * NB + c] = M[(long long)r * n2 + k0 + c];
+    }
+    __syncthreads();
+    for (int c = 0; c < nbe; ++c) {
+        const int k = k0 + c;
+        double best = -1.0;
+        int bi = n2;
+        for (int r = k + tid; r < n2; r += nt) {
+            double a = fabs(W[(long long)r * NB + c]);
+            if (a > best) { best = a; bi = r; }
+        }
+        // warp argmax (lowest index on ties)
+        for (int o = 16; o > 0; o >>= 1) {
+            double ob = __shfl_down_sync(0xffffffffu, best, o);
+            int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
+        __syncthreads();
+        if (tid < 32) {
+            int nw = (nt + 31) >> 5;
+            best = tid < nw ? red_v[tid] : -1.0;
+            bi = tid < nw ? red_i[tid] : n2;
+            for (int o = 16; o > 0; o >>= 1) {
+                double ob = __shfl_down_sync(0xffffffffu, best, o);
+                int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (tid == 0) {
+                if (!(best > 0.0) || bi >= n2) {
+                    s.flag[m] = 1;
+                    bi = k;
+                }
+                s_p = bi;
+                piv[k] = bi;
+            }
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (p != k && tid < nbe) {
+            double t = W[(long long)k * NB + tid];
+            W[(long long)k * NB + tid] = W[(long long)p * NB + tid];
+            W[(long long)p * NB + tid] = t;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double d = W[(long long)k * NB + c];
+            s_d = (d != 0.0) ? d : 1.0;
+        }
+        __syncthreads();
+        const double d = s_d;
+        // L column and trailing panel update (rows > k)
+        for (long long q = tid; q < (long long)(n2 - k - 1) * (nbe - c); q += nt) {
+            int r = k + 1 + (int)(q / (nbe - c));
+            int cc = c + (int)(q % (nbe - c));
+            if (cc == c) continue;
+            double l = W[(long long)r * NB + c] / d;
+            W[(long long)r * NB + cc] -= l * W[(long long)k * NB + cc];
+        }
+        __syncthreads();
+        for (int r = k + 1 + tid; r < n2; r += nt) W[(long long)r * NB + c] /= d;
+        __syncthreads();
+    }
+    // A11 = L11 U11 (rows k0..k0+nbe); A11^{-1} by solving A11 X = I (column per thread)
+    for (int q = tid; q < nbe * nbe; q += nt) {
+        int r = q / nbe, c = q % nbe;
+        double val = W[(long long)(k0 + r) * NB + c];
+        L11[r][c] = (c < r) ? val : (c == r ? 1.0 : 0.0);
+        U11[r][c] = (c >= r) ? val : 0.0;
+    }
+    __syncthreads();
+    if (tid < nbe) {
+        const int col = tid;
+        double z[NB];
+        for (int r = 0; r < nbe; ++r) {
+            double acc = (r == col) ? 1.0 : 0.0;
+            for (int q = 0; q < r; ++q) acc -= L11[r][q] * z[q];
+            z[r] = acc;
+        }
+        for (int r = nbe - 1; r >= 0; --r) {
+            double acc = z[r];
+            for (int q = r + 1; q < nbe; ++q) acc -= U11[r][q] * z[q];
+            z[r] = acc / U11[r][r];
+        }
+        // note: the panel rows were permuted inside W; A11 here is P_panel * M[K, K]
+        double *Ai = s.A11i + (long long)m * NB * NB;
+        for (int r = 0; r < nbe; ++r) Ai[r * NB + col] = z[r];
+    }
+}
+
+// Apply the panel's row swaps to all columns of M (sequential in k, parallel over columns).
+__global__ void k_swap(BDView v, BDScratch s, int k0, int nbe) {
+    const int m = blockIdx.y;
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n2 = v.n2;
+    if (col >= n2) return;
+    double *M = v.mat + (long long)m * v.mstride;
+    const int *piv = s.piv + (long long)m * n2;
+    for (int c = 0; c < nbe; ++c) {
+        int k = k0 + c, p = piv[k];
+        if (p != k) {
+            double t = M[(long long)k * n2 + col];
+            M[(long long)k * n2 + col] = M[(long long)p * n2 + col];
+            M[(long long)p * n2 + col] = t;
+        }
+    }
+}
+
+__global__ void k_copy_T(BDView v, BDScratch s, int k0, int nbe) {
+    const int m = blockIdx.y;
+    const int n2 = v.n2;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)n2 * NB) return;
+    const int r = (int)(q / NB), c = (int)(q % NB);
+    const double *M = v.mat + (long long)m * v.mstride;
+    s.T[(long long)m * n2 * NB + q] = c < nbe ? M[(long long)r * n2 + k0 + c] : 0.0;
+}
+
+// G[c][j] = sum_c' A11i[c][c'] M[k0+c'][j]  (j outside K);  G[c][K] = A11i.
+__global__ void k_make_G(BDView v, BDScratch s, int k0, int nbe) {
+    const int m = blockIdx.y;
+    const int n2 = v.n2;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ double Ai[NB][NB];
+    const double *A = s.A11i + (long long)m * NB * NB;
+    for (int q = threadIdx.x; q < NB * NB; q += blockDim.x) Ai[q / NB][q % NB] = A[q];
+    __syncthreads();
+    if (j >= n2) return;
+    const double *M = v.mat + (long long)m * v.mstride;
+    double *G = s.G + (long long)m * NB * n2;
+    if (j >= k0 && j < k0 + nbe) {
+        for (int c = 0; c < NB; ++c) G[(long long)c * n2 + j] = c < nbe ? Ai[c][j - k0] : 0.0;
+        return;
+    }
+    double col[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) col[c] = c < nbe ? M[(long long)(k0 + c) * n2 + j] : 0.0;
+    for (int c = 0; c < NB; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) acc = fma(Ai[c][q], col[q], acc);
+        G[(long long)c * n2 + j] = c < nbe ? acc : 0.0;
+    }
+}
+
+// The sweep: 64x64 output tile per CTA, 256 threads, 4x4 outputs per thread.
+constexpr int UT = 64;
+__global__ void __launch_bounds__(256) k_update(BDView v, BDScratch s, int k0, int nbe) {
+    const int m = blockIdx.z;
+    const int n2 = v.n2;
+    const int i0 = blockIdx.y * UT, j0 = blockIdx.x * UT;
+    __shared__ double Ts[UT][NB + 1];
+    __shared__ double Gs[NB][UT + 1];
+    const double *T = s.T + (long long)m * n2 * NB;
+    const double *G = s.G + (long long)m * NB * n2;
+    double *M = v.mat + (long long)m * v.mstride;
+    const int tid = threadIdx.x;
+    for (int q = tid; q < UT * NB; q += 256) {
+        int r = q / NB, c = q % NB;
+        int gi = i0 + r;
+        Ts[r][c] = gi < n2 ? T[(long long)gi * NB + c] : 0.0;
+    }
+    for (int q = tid; q < NB * UT; q += 256) {
+        int c = q / UT, jj = q % UT;
+        int gj = j0 + jj;
+        Gs[c][jj] = gj < n2 ? G[(long long)c * n2 + gj] : 0.0;
+    }
+    __syncthreads();
+    const int tr = tid / 16, tc = tid % 16;  // rows tr + 16*a, cols tc + 16*b
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < NB; ++c) {
+        double ta[4], gb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ta[a] = Ts[tr + 16 * a][c];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) gb[b] = Gs[c][tc + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(ta[a], gb[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int gi = i0 + tr + 16 * a;
+        if (gi >= n2) continue;
+        const bool rowK = gi >= k0 && gi < k0 + nbe;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int gj = j0 + tc + 16 * b;
+            if (gj >= n2) continue;
+            double *dst = M + (long long)gi * n2 + gj;
+            if (rowK) {
+                *dst = Gs[gi - k0][tc + 16 * b];
+            } else {
+                const bool colK = gj >= k0 && gj < k0 + nbe;
+                const double base = colK ? 0.0 : *dst;
+                *dst = base - acc[a][b];
+            }
+        }
+    }
+}
+
+// Column unpermutation: A^{-1}[:, q[r]] = M[:, r], q = row order after all swaps.
+__global__ void k_perm(BDView v, BDScratch s) {
+    const int m = blockIdx.x;
+    const int n2 = v.n2;
+    int *q = s.piv + (long long)m * n2;  // in place: piv -> q (single thread, sequential)
+    if (threadIdx.x != 0) return;
+    // q built in W's int view is avoided: reuse T as int storage
+    int *perm = reinterpret_cast<int *>(s.T + (long long)m * n2 * NB);
+    for (int r = 0; r < n2; ++r) perm[r] = r;
+    for (int k = 0; k < n2; ++k) {
+        int p = q[k];
+        int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+    }
+}
+
+__global__ void k_unpermute(BDView v, BDScratch s) {
+    extern __shared__ double row[];
+    const int m = blockIdx.y, r = blockIdx.x;
+    const int n2 = v.n2;
+    double *M = v.mat + (long long)m * v.mstride + (long long)r * n2;
+    const int *perm = reinterpret_cast<const int *>(s.T + (long long)m * n2 * NB);
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) row[j] = M[j];
+    __syncthreads();
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) M[perm[j]] = row[j];
+}
+
+// ------------------------------------------------------------------ apply (A7)
+// One warp per row of the explicit inverse; NVA vectors per pass.
+template <int NVA>
+__global__ void __launch_bounds__(256) k_bd_apply(const double *__restrict__ inv, const long long *__restrict__ off,
+                                                  int wall_lo, int n_pore, int nb, int N, const double *in,
+                                                  double *out, long long stride, int v0) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= 2 * N) return;
+    const int node = warp >> 1;
+    int b, lo, n;
+    if (node < wall_lo) {
+        b = node / n_pore;
+        lo = b * n_pore;
+        n = n_pore;
+    } else {
+        b = nb - 1;
+        lo = wall_lo;
+        n = N - wall_lo;
+    }
+    const int n2 = 2 * n;
+    const int lr = warp - 2 * lo;
+    const double2 *row = reinterpret_cast<const double2 *>(inv + off[b] + (long long)lr * n2);
+    double acc[NVA];
+#pragma unroll
+    for (int v = 0; v < NVA; ++v) acc[v] = 0.0;
+    for (int c = lane; c < n; c += 32) {
+        const double2 a = __ldcs(row + c);
+#pragma unroll
+        for (int v = 0; v < NVA; ++v) {
+            const double2 x = reinterpret_cast<const double2 *>(in + (long long)(v0 + v) * stride + 2LL * lo)[c];
+            acc[v] = fma(a.x, x.x, fma(a.y, x.y, acc[v]));
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < NVA; ++v) {
+        double t = acc[v];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) out[(long long)(v0 + v) * stride + warp] = t;
+    }
+}
+
+static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall, cudaStream_t st,
+                        int *d_flag) {
+    if (v.count == 0) return BIE_OK;
+    const int n2 = v.n2;
+    BDScratch s{};
+    size_t wbytes = sizeof(double) * (size_t)v.count * n2 * NB;
+    BIE_CUDA_TRY(cudaMallocAsync(&s.W, wbytes, st));
+    BIE_CUDA_TRY(cudaMallocAsync(&s.T, wbytes, st));
+    BIE_CUDA_TRY(cudaMallocAsync(&s.G, wbytes, st));
+    BIE_CUDA_TRY(cudaMallocAsync(&s.A11i, sizeof(double) * (size_t)v.count * NB * NB, st));
+    BIE_CUDA_TRY(cudaMallocAsync(&s.piv, sizeof(int) * (size_t)v.count * n2, st));
+    s.flag = d_flag;
+    {
+        long long elems = (long long)nodes * nodes;
+        dim3 grid((unsigned)((elems + 255) / 256), v.count);
+        k_bd_assemble<<<grid, 256, 0, st>>>(v, lo0, nodes, is_wall ? 1 : 0, g->pos, g->nw, g->nrm, g->tan, g->w,
+                                            g->selfc, g->pore, g->wall_len);
+        BIE_CUDA_TRY(cudaGetLastError());
+    }
+    int panel_threads = n2 >= 1024 ? 1024 : (n2 >= 256 ? 256 : 128);
+    for (int k0 = 0; k0 < n2; k0 += NB) {
+        int nbe = std::min(NB, n2 - k0);
+        k_panel<<<v.count, panel_threads, 0, st>>>(v, s, k0, nbe);
+        k_swap<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
+        k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), v.count), 256, 0, st>>>(v, s, k0, nbe);
+        k_make_G<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
+        k_update<<<dim3((n2 + UT - 1) / UT, (n2 + UT - 1) / UT, v.count), 256, 0, st>>>(v, s, k0, nbe);
+        BIE_CUDA_TRY(cudaGetLastError());
+    }
+    k_perm<<<v.count, 32, 0, st>>>(v, s);
+    size_t rowbytes = sizeof(double) * (size_t)n2;
+    if (rowbytes > 48 * 1024)
+        BIE_CUDA_TRY(cudaFuncSetAttribute(k_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowbytes));
+    k_unpermute<<<dim3(n2, v.count), 256, rowbytes, st>>>(v, s);
+    BIE_CUDA_TRY(cudaGetLastError());
+    cudaFreeAsync(s.W, st);
+    cudaFreeAsync(s.T, st);
+    cudaFreeAsync(s.G, st);
+    cudaFreeAsync(s.A11i, st);
+    cudaFreeAsync(s.piv, st);
+    return BIE_OK;
+}
+
+int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec, cudaStream_t st) {
+    Geometry *g = bd->g;
+    const long long stride = 2LL * g->N;
+    const int rows = 2 * g->N;
+    const int threads = 256;
+    const int blocks = (int)(((long long)rows * 32 + threads - 1) / threads);
+    int v = 0;
+    while (v < nvec) {
+        int rem = nvec - v;
+        if (rem >= 4) {
+            k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
+                                                      out, stride, v);
+            v += 4;
+        } else if (rem >= 2) {
+            k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
+                                                      out, stride, v);
+            v += 2;
+        } else {
+            k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
+                                                      out, stride, v);
+            v += 1;
+        }
+        BIE_CUDA_TRY(cudaGetLastError());
+    }
+    return BIE_OK;
+}
+
+}  // namespace bie
+
+using namespace bie;
+
+extern "C" {
+
+int bie_blockdiag_destroy(bie_blockdiag_t h) {
+    BlockDiag *bd = as_bd(h);
+    if (!bd) {
+        set_error("bie_blockdiag_destroy: invalid blockdiag handle");
+        return BIE_EINVAL;
+    }
+    cudaFree(bd->inv);
+    cudaFree(bd->d_off);
+    bd->magic = 0;
+    delete bd;
+    return BIE_OK;
+}
+
+int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out) {
+        set_error("bie_blockdiag_factor: invalid geometry handle or null output");
+        return BIE_EINVAL;
+    }
+    *out = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    BlockDiag *bd = new BlockDiag();
+    bd->g = g;
+    bd->nb = g->M + 1;
+    long long off = 0;
+    for (int b = 0; b < bd->nb; ++b) {
+        int lo = b < g->M ? b * g->n_pore : g->wall_lo;
+        int n = b < g->M ? g->n_pore : g->n_outer;
+        bd->lo.push_back(lo);
+        bd->n.push_back(n);
+        bd->off.push_back(off);
+        off += 4LL * n * n;
+    }
+    bd->off.push_back(off);
+    int *d_flag = nullptr;
+    auto fail = [&](int rc) {
+        cudaFree(d_flag);
+        bie_blockdiag_destroy(reinterpret_cast<bie_blockdiag_t>(bd));
+        return rc;
+    };
+    cudaError_t e = cudaMalloc(&bd->inv, sizeof(double) * (size_t)off);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(blockdiag inverses)"));
+    e = cudaMalloc(&bd->d_off, sizeof(long long) * bd->off.size());
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(blockdiag offsets)"));
+    e = cudaMemcpy(bd->d_off, bd->off.data(), sizeof(long long) * bd->off.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemcpy(blockdiag offsets)"));
+    e = cudaMalloc(&d_flag, sizeof(int) * (size_t)bd->nb);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(flags)"));
+    e = cudaMemsetAsync(d_flag, 0, sizeof(int) * (size_t)bd->nb, st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemsetAsync(flags)"));
+    int rc;
+    if (g->M > 0) {
+        BDView pv{bd->inv, 4LL * g->n_pore * g->n_pore, 2 * g->n_pore, g->M, 0};
+        rc = factor_class(g, pv, 0, g->n_pore, false, st, d_flag);
+        if (rc) return fail(rc);
+    }
+    {
+        BDView wv{bd->inv + bd->off[g->M], 0, 2 * g->n_outer, 1, g->M};
+        rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + g->M);
+        if (rc) return fail(rc);
+    }
+    std::vector<int> flags(bd->nb);
+    e = cudaMemcpyAsync(flags.data(), d_flag, sizeof(int) * (size_t)bd->nb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemcpyAsync(flags)"));
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "bie_blockdiag_factor (kernels)"));
+    for (int b = 0; b < bd->nb; ++b) {
+        if (flags[b]) {
+            set_error("bie_blockdiag_factor: block of body " + std::to_string(b) +
+                      (b < g->M ? " (pore)" : " (outer wall)") + " is singular (zero pivot)");
+            return fail(BIE_ESINGULAR);
+        }
+    }
+    cudaFree(d_flag);
+    *out = reinterpret_cast<bie_blockdiag_t>(bd);
+    return BIE_OK;
+}
+
+int bie_blockdiag_apply(bie_blockdiag_t h, const double *in, double *out, int nvec, void *stream) {
+    BlockDiag *bd = as_bd(h);
+    if (!bd || !in || !out || nvec < 1 || nvec > BIE_MAX_NVEC || in == out) {
+        set_error("bie_blockdiag_apply: invalid handle/pointers, nvec out of [1,16], or in == out");
+        return BIE_EINVAL;
+    }
+    return blockdiag_apply_impl(bd, in, out, nvec, (cudaStream_t)stream);
+}
+
+int bie_blockdiag_block_inverse(bie_blockdiag_t h, int body, double *host, long long host_len) {
+    BlockDiag *bd = as_bd(h);
+    if (!bd || !host || body < 0 || body >= bd->nb) {
+        set_error("bie_blockdiag_block_inverse: invalid handle, body or buffer");
+        return BIE_EINVAL;
+    }
+    long long n = bd->off[body + 1] - bd->off[body];
+    if (host_len < n) {
+        set_error("bie_blockdiag_block_inverse: host buffer too small");
+        return BIE_EINVAL;
+    }
+    BIE_CUDA_TRY(cudaMemcpy(host, bd->inv + bd->off[body], sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
+    return BIE_OK;
+}
+
+}  // extern "C"

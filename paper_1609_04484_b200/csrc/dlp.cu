@@ -1,0 +1,547 @@
+// dlp.cu -- the completed double-layer matvec (A2-A5 of SURVEY.md s8(a)).
+//
+//   k_moments   (A2)  per-pore lambda_k, mu_k and the wall scalar nu     O(N)
+//   k_dlp_pairs (A3)  all-pairs FP64 trapezoid DLP sum                   O(N^2)  <- hot
+//   k_epilogue  (A4+A5) split reduction, -1/2 sigma, self term, N0,
+//                       Stokeslet/rotlet completion                      O(N M)
+//
+// Operator (P:l.243-248 with trapezoid weights P:l.310-319; readings C3-C5):
+//   y_i = -1/2 s_i + sum_{j != i} (r.nw_j)(r.s_j) r / rho^4 + selfc_i (t_i.s_i) t_i
+//         + [i in Gamma_0] nu n_i + sum_k S(x_i - c_k) lambda_k + r_k R(x_i - c_k) mu_k
+//   nw_j = w_j n_j / pi,  r = x_i - x_j,  selfc_i = w_i kappa_n,i / (2 pi).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+
+#include "internal.cuh"
+
+namespace bie {
+
+constexpr int kPairThreads = 128;
+
+// Pair-kernel variants: vectors per launch, targets per thread, sources per tile.
+struct Variant {
+    int nv, R, TS;
+};
+static const Variant kVariants[5] = {{1, 4, 256}, {2, 2, 256}, {4, 2, 256}, {8, 1, 128}, {16, 1, 64}};
+
+__device__ __forceinline__ double rcp_approx(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src, int src_bytes) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem_src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// CTA that owns work unit u under the static partition u0(p) = floor(p U / P).
+__host__ __device__ __forceinline__ int unit_owner(long long u, long long U, int P) {
+    return (int)(((u + 1) * (long long)P - 1) / U);
+}
+
+struct PairArgs {
+    const double2 *pos;   // [N] source (and target) positions
+    const double2 *nw;    // [N] w n / pi
+    const double *sigma;  // first vector of this chunk; vector v at sigma + v * sig_stride
+    long long sig_stride; // 2N
+    double *partial;      // [S][nvec_total][2 Nt]
+    int nvec_total, v0;   // total vectors of the call, first vector of this chunk
+    int N, row_begin, Nt; // sources, first target, number of targets
+    int nTS;
+    long long U;
+};
+
+// A3: all-pairs DLP sum.  Each persistent CTA walks a contiguous range of
+// (target block, source tile) units; sources are staged in shared memory by
+// cp.async double buffering and read as warp-broadcast LDS.128; each thread
+// keeps R targets and their NV accumulators in registers.  The self pair
+// (r = 0) needs no branch: rho^2 gets +1e-300 (below one ulp of any real
+// pair distance), so 1/rho^2 stays finite and r.nw = 0 zeroes the term.
+// 1/rho^2: MUFU.RCP64H seed + one cubic Newton step (3 DFMA, rel. err ~2^-60).
+template <int NV, int R, int TS>
+__global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
+    extern __shared__ double2 smem[];  // [2][(2 + NV) * TS]
+    constexpr int NT = kPairThreads;
+    constexpr int TB = NT * R;
+    constexpr int STAGE = (2 + NV) * TS;
+    static_assert(STAGE % NT == 0, "stage must be a multiple of the CTA size");
+    const int tid = threadIdx.x;
+    const int P = gridDim.x, p = blockIdx.x;
+    const long long U = a.U;
+    const long long u0 = ((long long)p * U) / P, u1 = ((long long)(p + 1) * U) / P;
+    if (u0 >= u1) return;
+    const int N = a.N, nTS = a.nTS;
+
+    auto load_tile = [&](int buf, int ts) {
+        double2 *s = smem + buf * STAGE;
+        const int j0 = ts * TS;
+#pragma unroll
+        for (int q0 = 0; q0 < STAGE; q0 += NT) {
+            const int q = q0 + tid;
+            const int arr = q / TS;
+            const int j = j0 + (q - arr * TS);
+            const bool ok = j < N;
+            const double2 *src;
+            if (arr == 0)
+                src = a.pos + (ok ? j : 0);
+            else if (arr == 1)
+                src = a.nw + (ok ? j : 0);
+            else
+                src = reinterpret_cast<const double2 *>(a.sigma + (long long)(arr - 2) * a.sig_stride) + (ok ? j : 0);
+            cp_async16(s + q, src, ok ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+
+    double tx[R], ty[R];
+    double2 acc[R][NV];
+    auto load_targets = [&](int tb) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            int it = tb * TB + r * NT + tid;
+            double2 x = make_double2(0.0, 0.0);
+            if (it < a.Nt) x = a.pos[a.row_begin + it];
+            tx[r] = x.x;
+            ty[r] = x.y;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[r][v] = make_double2(0.0, 0.0);
+        }
+    };
+
+    long long u = u0;
+    int tb = (int)(u / nTS);
+    load_targets(tb);
+    load_tile(0, (int)(u % nTS));
+    int buf = 0;
+    for (; u < u1; ++u) {
+        if (u + 1 < u1)
+            load_tile(buf ^ 1, (int)((u + 1) % nTS));
+        else
+            cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double2 *sp = smem + buf * STAGE;
+#pragma unroll 2
+        for (int j = 0; j < TS; ++j) {
+            const double2 xj = sp[j];
+            const double2 nj = sp[TS + j];
+            double2 sj[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) sj[v] = sp[(2 + v) * TS + j];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double rx = tx[r] - xj.x;
+                const double ry = ty[r] - xj.y;
+                const double rho2 = fma(rx, rx, fma(ry, ry, 1e-300));
+                const double rn = fma(rx, nj.x, ry * nj.y);
+                double inv = rcp_approx(rho2);
+                const double e = fma(-rho2, inv, 1.0);
+                inv = fma(inv, fma(e, e, e), inv);
+                const double q = (rn * inv) * inv;  // (r.nw)/rho^4
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const double c = q * fma(rx, sj[v].x, ry * sj[v].y);
+                    acc[r][v].x = fma(c, rx, acc[r][v].x);
+                    acc[r][v].y = fma(c, ry, acc[r][v].y);
+                }
+            }
+        }
+        __syncthreads();
+        buf ^= 1;
+        const bool seg_end = (u + 1 == u1) || ((u + 1) % nTS == 0);
+        if (seg_end) {
+            const int slot = p - unit_owner((long long)tb * nTS, U, P);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                int it = tb * TB + r * NT + tid;
+                if (it < a.Nt) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        double2 *dst = reinterpret_cast<double2 *>(
+                            a.partial + ((long long)slot * a.nvec_total + a.v0 + v) * 2LL * a.Nt);
+                        dst[it] = acc[r][v];
+                    }
+                }
+            }
+            if (u + 1 < u1) {
+                tb = (int)((u + 1) / nTS);
+                load_targets(tb);
+            }
+        }
+    }
+}
+
+// A2: moments (reading C5).  Block b < M: pore b; block M: Gamma_0.
+// Deterministic fixed-shape tree reduction.
+__global__ void k_moments(const double2 *__restrict__ pos, const double2 *__restrict__ nrm,
+                          const double *__restrict__ w, const double4 *__restrict__ pore, const double *sigma,
+                          long long sig_stride, int nvec, int M, int n_pore, int wall_lo, int N, double wall_len,
+                          double *moments /* [nvec][M][3], then [nvec] nu */) {
+    __shared__ double red[3][256];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    for (int v = 0; v < nvec; ++v) {
+        const double2 *s = reinterpret_cast<const double2 *>(sigma + (long long)v * sig_stride);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if (b < M) {
+            double4 pk = pore[b];
+            for (int j = b * n_pore + tid; j < (b + 1) * n_pore; j += blockDim.x) {
+                double2 sj = s[j], xj = pos[j];
+                double px = xj.y - pk.y, py = -(xj.x - pk.x);  // (x - c)^perp
+                a0 += w[j] * sj.x;
+                a1 += w[j] * sj.y;
+                a2 += w[j] * (sj.x * px + sj.y * py);
+            }
+        } else {
+            for (int j = wall_lo + tid; j < N; j += blockDim.x) {
+                double2 sj = s[j], nj = nrm[j];
+                a0 += w[j] * (nj.x * sj.x + nj.y * sj.y);
+            }
+        }
+        red[0][tid] = a0;
+        red[1][tid] = a1;
+        red[2][tid] = a2;
+        __syncthreads();
+        for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+            if (tid < h) {
+                red[0][tid] += red[0][tid + h];
+                red[1][tid] += red[1][tid + h];
+                red[2][tid] += red[2][tid + h];
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            if (b < M) {
+                double4 pk = pore[b];
+                double *m = moments + ((long long)v * M + b) * 3;
+                m[0] = red[0][0] / pk.w;
+                m[1] = red[1][0] / pk.w;
+                m[2] = red[2][0] / (pk.w * pk.z);
+            } else {
+                moments[(long long)nvec * M * 3 + v] = red[0][0] / wall_len;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+struct Chunk {
+    int v0, nv, TB, nTS, P;
+    long long U;
+};
+struct EpiArgs {
+    const double2 *pos, *nrm, *tan;
+    const double *selfc;
+    const double4 *pore;
+    const double *sigma;
+    long long sig_stride;
+    const double *partial;
+    const double *moments;
+    double *out;
+    int nvec, N, M, wall_lo, row_begin, Nt;
+    unsigned flags;
+    int nchunks;
+    Chunk ch[5];
+};
+
+// A4 + A5: reduce the split partials in fixed slot order, then add the local
+// terms and the completion field of every pore.
+__global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;
+    if (it >= a.Nt) return;
+    const int i = a.row_begin + it;
+    const double2 xi = a.pos[i];
+    const double2 ti = a.tan[i];
+    const double sc = a.selfc[i];
+    const bool full = !(a.flags & BIE_D_ONLY);
+    constexpr double k4pi = 1.0 / (4.0 * kPi);
+    double2 u[BIE_MAX_NVEC];
+    for (int c = 0; c < a.nchunks; ++c) {
+        const Chunk ch = a.ch[c];
+        const int tb = it / ch.TB;
+        const int first = unit_owner((long long)tb * ch.nTS, ch.U, ch.P);
+        const int last = unit_owner((long long)(tb + 1) * ch.nTS - 1, ch.U, ch.P);
+        for (int v = ch.v0; v < ch.v0 + ch.nv; ++v) {
+            double2 acc = make_double2(0.0, 0.0);
+            for (int sl = 0; sl <= last - first; ++sl) {
+                const double2 pv = reinterpret_cast<const double2 *>(
+                    a.partial + ((long long)sl * a.nvec + v) * 2LL * a.Nt)[it];
+                acc.x += pv.x;
+                acc.y += pv.y;
+            }
+            u[v] = acc;
+        }
+    }
+    for (int v = 0; v < a.nvec; ++v) {
+        const double2 si = reinterpret_cast<const double2 *>(a.sigma + (long long)v * a.sig_stride)[i];
+        const double ts = sc * (ti.x * si.x + ti.y * si.y);
+        u[v].x += ts * ti.x;
+        u[v].y += ts * ti.y;
+        if (full) {
+            u[v].x += -0.5 * si.x;
+            u[v].y += -0.5 * si.y;
+            if (i >= a.wall_lo) {
+                const double nu = a.moments[(long long)a.nvec * a.M * 3 + v];
+                const double2 ni = a.nrm[i];
+                u[v].x += nu * ni.x;
+                u[v].y += nu * ni.y;
+            }
+        }
+    }
+    if (full) {
+        for (int k = 0; k < a.M; ++k) {
+            const double4 pk = a.pore[k];
+            const double rx = xi.x - pk.x, ry = xi.y - pk.y;
+            const double rho2 = rx * rx + ry * ry;
+            const double ir = 1.0 / rho2;
+            const double lg = 0.5 * log(rho2);
+            const double rk = pk.z * ir;
+            for (int v = 0; v < a.nvec; ++v) {
+                const double *m = a.moments + ((long long)v * a.M + k) * 3;
+                const double lx = m[0], ly = m[1], mu = m[2];
+                const double rl = (rx * lx + ry * ly) * ir;
+                u[v].x += k4pi * (-lg * lx + rx * rl) + rk * ry * mu;
+                u[v].y += k4pi * (-lg * ly + ry * rl) - rk * rx * mu;
+            }
+        }
+    }
+    for (int v = 0; v < a.nvec; ++v)
+        reinterpret_cast<double2 *>(a.out + (long long)v * 2LL * a.Nt)[it] = u[v];
+}
+
+template <int NV, int R, int TS>
+static void *pair_kernel_ptr() {
+    return reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS>);
+}
+
+static void *variant_kernel(int idx) {
+    switch (idx) {
+        case 0: return pair_kernel_ptr<1, 4, 256>();
+        case 1: return pair_kernel_ptr<2, 2, 256>();
+        case 2: return pair_kernel_ptr<4, 2, 256>();
+        case 3: return pair_kernel_ptr<8, 1, 128>();
+        default: return pair_kernel_ptr<16, 1, 64>();
+    }
+}
+
+static int variant_index(int nv) {
+    switch (nv) {
+        case 1: return 0;
+        case 2: return 1;
+        case 4: return 2;
+        case 8: return 3;
+        default: return 4;
+    }
+}
+
+// Fill the schedule of one variant for Nt targets and N sources.
+static void make_sched(const Geometry *g, int vi, int Nt, PairSched &s) {
+    const Variant &V = kVariants[vi];
+    s.nv = V.nv;
+    s.R = V.R;
+    s.TS = V.TS;
+    s.TB = kPairThreads * V.R;
+    s.nTB = (Nt + s.TB - 1) / s.TB;
+    s.nTS = (g->N + s.TS - 1) / s.TS;
+    s.U = (long long)s.nTB * s.nTS;
+    s.smem = 2 * (2 + V.nv) * V.TS * (int)sizeof(double2);
+    long long Pmax = (long long)g->num_sms * std::max(1, g->occ[vi]);
+    s.P = (int)std::min<long long>(Pmax, s.U);
+    // max slots per target block: ceil(P / nTB) + 1 bounds it; compute exactly
+    int S = 1;
+    for (int tb = 0; tb < s.nTB; ++tb) {
+        int f = unit_owner((long long)tb * s.nTS, s.U, s.P);
+        int l = unit_owner((long long)(tb + 1) * s.nTS - 1, s.U, s.P);
+        S = std::max(S, l - f + 1);
+    }
+    s.S = S;
+}
+
+int build_schedules(Geometry *g) {
+    size_t need = 0;
+    for (int vi = 0; vi < 5; ++vi) {
+        const Variant &V = kVariants[vi];
+        int smem = 2 * (2 + V.nv) * V.TS * (int)sizeof(double2);
+        cudaError_t e = cudaFuncSetAttribute(variant_kernel(vi), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_dlp_pairs)");
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, variant_kernel(vi), kPairThreads, smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        g->occ[vi] = std::max(1, occ);
+        PairSched s;
+        make_sched(g, vi, g->N, s);
+        g->sched[vi] = s;
+        need = std::max(need, (size_t)s.S * BIE_MAX_NVEC * 2 * (size_t)g->N);
+    }
+    cudaError_t e = cudaMalloc(&g->partial, need * sizeof(double));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(partial)");
+    g->partial_elems = need;
+    return BIE_OK;
+}
+
+static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStream_t st) {
+    switch (vi) {
+        case 0: k_dlp_pairs<1, 4, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        case 1: k_dlp_pairs<2, 2, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        case 2: k_dlp_pairs<4, 2, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        case 3: k_dlp_pairs<8, 1, 128><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        default: k_dlp_pairs<16, 1, 64><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+    }
+}
+
+int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, int row_begin,
+                   int row_end, cudaStream_t st) {
+    const int N = g->N;
+    const int Nt = row_end - row_begin;
+    if (Nt <= 0) return BIE_OK;
+    const long long stride = 2LL * N;
+    const bool full = !(flags & BIE_D_ONLY);
+    if (full) {
+        k_moments<<<g->M + 1, 256, 0, st>>>(g->pos, g->nrm, g->w, g->pore, sigma, stride, nvec, g->M, g->n_pore,
+                                            g->wall_lo, N, g->wall_len, g->moments);
+        BIE_CUDA_TRY(cudaGetLastError());
+    }
+    // decompose nvec into variant chunks (16, 8, 4, 2, 1)
+    EpiArgs ea{};
+    int v = 0;
+    PairSched sch[5];
+    int vis[5];
+    int nch = 0;
+    size_t need = 0;
+    while (v < nvec) {
+        int rem = nvec - v;
+        int nv = rem >= 16 ? 16 : rem >= 8 ? 8 : rem >= 4 ? 4 : rem >= 2 ? 2 : 1;
+        int vi = variant_index(nv);
+        PairSched s;
+        if (row_begin == 0 && row_end == N)
+            s = g->sched[vi];
+        else
+            make_sched(g, vi, Nt, s);
+        need = std::max(need, (size_t)s.S * nvec * 2 * (size_t)Nt);
+        sch[nch] = s;
+        vis[nch] = vi;
+        ea.ch[nch] = Chunk{v, nv, s.TB, s.nTS, s.P, s.U};
+        ++nch;
+        v += nv;
+    }
+    if (need > g->partial_elems) {
+        BIE_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaFree(g->partial);
+        g->partial = nullptr;
+        g->partial_elems = 0;
+        BIE_CUDA_TRY(cudaMalloc(&g->partial, need * sizeof(double)));
+        g->partial_elems = need;
+    }
+    for (int c = 0; c < nch; ++c) {
+        PairArgs a;
+        a.pos = g->pos;
+        a.nw = g->nw;
+        a.sigma = sigma + (long long)ea.ch[c].v0 * stride;
+        a.sig_stride = stride;
+        a.partial = g->partial;
+        a.nvec_total = nvec;
+        a.v0 = ea.ch[c].v0;
+        a.N = N;
+        a.row_begin = row_begin;
+        a.Nt = Nt;
+        a.nTS = sch[c].nTS;
+        a.U = sch[c].U;
+        launch_pairs(vis[c], sch[c], a, st);
+        BIE_CUDA_TRY(cudaGetLastError());
+    }
+    ea.pos = g->pos;
+    ea.nrm = g->nrm;
+    ea.tan = g->tan;
+    ea.selfc = g->selfc;
+    ea.pore = g->pore;
+    ea.sigma = sigma;
+    ea.sig_stride = stride;
+    ea.partial = g->partial;
+    ea.moments = g->moments;
+    ea.out = out;
+    ea.nvec = nvec;
+    ea.N = N;
+    ea.M = g->M;
+    ea.wall_lo = g->wall_lo;
+    ea.row_begin = row_begin;
+    ea.Nt = Nt;
+    ea.flags = flags;
+    ea.nchunks = nch;
+    k_epilogue<<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+}  // namespace bie
+
+using namespace bie;
+
+extern "C" {
+
+static int check_apply_args(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, const char *fn) {
+    if (!g) {
+        set_error(std::string(fn) + ": invalid geometry handle");
+        return BIE_EINVAL;
+    }
+    if (!sigma || !out) {
+        set_error(std::string(fn) + ": null sigma/out");
+        return BIE_EINVAL;
+    }
+    if (nvec < 1 || nvec > BIE_MAX_NVEC) {
+        set_error(std::string(fn) + ": nvec must be in [1, 16]");
+        return BIE_EINVAL;
+    }
+    if (flags & ~BIE_D_ONLY) {
+        set_error(std::string(fn) + ": unknown flags");
+        return BIE_EINVAL;
+    }
+    if ((const void *)sigma == (const void *)out) {
+        set_error(std::string(fn) + ": out must not alias sigma");
+        return BIE_EINVAL;
+    }
+    return BIE_OK;
+}
+
+int bie_dlp_apply(bie_geometry_t gh, const double *sigma, double *out, int nvec, unsigned flags, void *stream) {
+    Geometry *g = as_geom(gh);
+    int rc = check_apply_args(g, sigma, out, nvec, flags, "bie_dlp_apply");
+    if (rc) return rc;
+    return dlp_apply_impl(g, sigma, out, nvec, flags, 0, g->N, (cudaStream_t)stream);
+}
+
+int bie_dlp_apply_rows(bie_geometry_t gh, const double *sigma, double *out, int nvec, unsigned flags, int row_begin,
+                       int row_end, void *stream) {
+    Geometry *g = as_geom(gh);
+    int rc = check_apply_args(g, sigma, out, nvec, flags, "bie_dlp_apply_rows");
+    if (rc) return rc;
+    if (row_begin < 0 || row_end > g->N || row_begin > row_end) {
+        set_error("bie_dlp_apply_rows: row range out of [0, N]");
+        return BIE_EINVAL;
+    }
+    return dlp_apply_impl(g, sigma, out, nvec, flags, row_begin, row_end, (cudaStream_t)stream);
+}
+
+int bie_dlp_apply_host(bie_geometry_t gh, const double *sigma_host, double *out_host, int nvec, unsigned flags,
+                       void *stream) {
+    Geometry *g = as_geom(gh);
+    int rc = check_apply_args(g, sigma_host, out_host, nvec, flags, "bie_dlp_apply_host");
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t bytes = sizeof(double) * 2 * (size_t)g->N * nvec;
+    BIE_CUDA_TRY(cudaMemcpyAsync(g->stage_in, sigma_host, bytes, cudaMemcpyHostToDevice, st));
+    rc = dlp_apply_impl(g, g->stage_in, g->stage_out, nvec, flags, 0, g->N, st);
+    if (rc) return rc;
+    BIE_CUDA_TRY(cudaMemcpyAsync(out_host, g->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+    BIE_CUDA_TRY(cudaStreamSynchronize(st));
+    return BIE_OK;
+}
+
+}  // extern "C"

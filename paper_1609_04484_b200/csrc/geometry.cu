@@ -1,0 +1,237 @@
+// geometry.cu -- bie_geometry_* and error plumbing (A1 of SURVEY.md s8(a)).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace bie {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char *what) {
+    set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation) return BIE_ENOMEM;
+    return BIE_ECUDA;
+}
+
+Geometry *as_geom(bie_geometry_t g) {
+    Geometry *p = reinterpret_cast<Geometry *>(g);
+    if (!p || p->magic != kGeomMagic) return nullptr;
+    return p;
+}
+
+BlockDiag *as_bd(bie_blockdiag_t b) {
+    BlockDiag *p = reinterpret_cast<BlockDiag *>(b);
+    if (!p || p->magic != kBlockMagic) return nullptr;
+    return p;
+}
+
+// A1 node kernel.  P:l.296-309, P:l.318-319, P:l.354; readings C2, C7, C12.
+// Pores (node i = k*n_pore + j): x = c + r(cos, sin), n = -(cos, sin),
+// w = 2 pi r / n_pore, t = (-sin, cos), kappa_n = x_ss . n = 1/r.
+// Gamma_0 (node i = wall_lo + j): w = |x'| T/n_outer, t = x'/|x'|,
+// n = (t_y, -t_x), kappa_n = x''.n / |x'|^2.
+__global__ void k_nodes(int N, int M, int n_pore, int n_outer, double T, const double2 *__restrict__ oxy,
+                        const double2 *__restrict__ odxy, const double2 *__restrict__ oddxy,
+                        const double4 *__restrict__ pore, double2 *pos, double2 *nw, double2 *nrm, double2 *tan,
+                        double *w, double *selfc) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int wall_lo = M * n_pore;
+    double2 x, n, t;
+    double wi, kn;
+    if (i < wall_lo) {
+        int k = i / n_pore, j = i - k * n_pore;
+        double4 p = pore[k];
+        double s, c;
+        sincospi(2.0 * (double)j / (double)n_pore, &s, &c);
+        x = make_double2(p.x + p.z * c, p.y + p.z * s);
+        n = make_double2(-c, -s);
+        t = make_double2(-s, c);
+        wi = 2.0 * kPi * p.z / (double)n_pore;
+        kn = 1.0 / p.z;
+    } else {
+        int j = i - wall_lo;
+        double2 d1 = odxy[j], d2 = oddxy[j];
+        double sp = sqrt(d1.x * d1.x + d1.y * d1.y);
+        t = make_double2(d1.x / sp, d1.y / sp);
+        n = make_double2(t.y, -t.x);
+        x = oxy[j];
+        wi = sp * T / (double)n_outer;
+        kn = (d2.x * n.x + d2.y * n.y) / (sp * sp);
+    }
+    pos[i] = x;
+    nrm[i] = n;
+    tan[i] = t;
+    w[i] = wi;
+    nw[i] = make_double2(wi * n.x / kPi, wi * n.y / kPi);
+    selfc[i] = wi * kn / (2.0 * kPi);
+}
+
+}  // namespace bie
+
+using namespace bie;
+
+extern "C" {
+
+const char *bie_last_error(void) { return g_last_error.c_str(); }
+
+int bie_geometry_destroy(bie_geometry_t gh) {
+    Geometry *g = as_geom(gh);
+    if (!g) {
+        set_error("bie_geometry_destroy: invalid geometry handle");
+        return BIE_EINVAL;
+    }
+    cudaFree(g->pos);
+    cudaFree(g->nw);
+    cudaFree(g->nrm);
+    cudaFree(g->tan);
+    cudaFree(g->w);
+    cudaFree(g->selfc);
+    cudaFree(g->pore);
+    cudaFree(g->partial);
+    cudaFree(g->moments);
+    cudaFree(g->stage_in);
+    cudaFree(g->stage_out);
+    g->magic = 0;
+    delete g;
+    return BIE_OK;
+}
+
+int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const double *outer_ddxy, int n_outer,
+                        double outer_period, const double *pore_c, const double *pore_r, int n_pores,
+                        int nodes_per_pore, bie_geometry_t *out) {
+    if (!out || !outer_xy || !outer_dxy || !outer_ddxy || (n_pores > 0 && (!pore_c || !pore_r))) {
+        set_error("bie_geometry_create: null pointer argument");
+        return BIE_EINVAL;
+    }
+    *out = nullptr;
+    if (n_outer < 16 || (n_outer & 1) || n_pores < 0 ||
+        (n_pores > 0 && (nodes_per_pore < 16 || (nodes_per_pore & 1))) || !(outer_period > 0.0)) {
+        set_error("bie_geometry_create: n_outer and nodes_per_pore must be even and >= 16, n_pores >= 0, "
+                  "outer_period > 0");
+        return BIE_EINVAL;
+    }
+    long long Nll = (long long)n_pores * (n_pores > 0 ? nodes_per_pore : 0) + n_outer;
+    if (Nll > (1LL << 28)) {
+        set_error("bie_geometry_create: too many nodes");
+        return BIE_EINVAL;
+    }
+    for (int k = 0; k < n_pores; ++k) {
+        if (!(pore_r[k] > 0.0) || !std::isfinite(pore_r[k]) || !std::isfinite(pore_c[2 * k]) ||
+            !std::isfinite(pore_c[2 * k + 1])) {
+            set_error("bie_geometry_create: pore " + std::to_string(k) + " has a non-positive or non-finite radius/centre");
+            return BIE_EGEOM;
+        }
+    }
+    for (int j = 0; j < 2 * n_outer; ++j) {
+        if (!std::isfinite(outer_xy[j]) || !std::isfinite(outer_dxy[j]) || !std::isfinite(outer_ddxy[j])) {
+            set_error("bie_geometry_create: non-finite outer-curve sample");
+            return BIE_EGEOM;
+        }
+    }
+    for (int j = 0; j < n_outer; ++j) {
+        if (outer_dxy[2 * j] == 0.0 && outer_dxy[2 * j + 1] == 0.0) {
+            set_error("bie_geometry_create: outer curve has a zero derivative sample");
+            return BIE_EGEOM;
+        }
+    }
+    Geometry *g = new Geometry();
+    g->N = (int)Nll;
+    g->M = n_pores;
+    g->n_pore = n_pores > 0 ? nodes_per_pore : 0;
+    g->n_outer = n_outer;
+    g->wall_lo = g->M * g->n_pore;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    int N = g->N;
+    int rc = BIE_OK;
+    double2 *d_oxy = nullptr, *d_odxy = nullptr, *d_oddxy = nullptr;
+    std::vector<double4> hp(n_pores > 0 ? n_pores : 1);
+    double wall_len = 0.0;
+    auto fail = [&](int code) {
+        cudaFree(d_oxy);
+        cudaFree(d_odxy);
+        cudaFree(d_oddxy);
+        bie_geometry_destroy(reinterpret_cast<bie_geometry_t>(g));
+        return code;
+    };
+#define TRY(expr)                                             \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return fail(cuda_fail(_e, #expr)); \
+    } while (0)
+    TRY(cudaMalloc(&g->pos, sizeof(double2) * N));
+    TRY(cudaMalloc(&g->nw, sizeof(double2) * N));
+    TRY(cudaMalloc(&g->nrm, sizeof(double2) * N));
+    TRY(cudaMalloc(&g->tan, sizeof(double2) * N));
+    TRY(cudaMalloc(&g->w, sizeof(double) * N));
+    TRY(cudaMalloc(&g->selfc, sizeof(double) * N));
+    TRY(cudaMalloc(&g->pore, sizeof(double4) * (n_pores > 0 ? n_pores : 1)));
+    TRY(cudaMalloc(&d_oxy, sizeof(double2) * n_outer));
+    TRY(cudaMalloc(&d_odxy, sizeof(double2) * n_outer));
+    TRY(cudaMalloc(&d_oddxy, sizeof(double2) * n_outer));
+    TRY(cudaMemcpy(d_oxy, outer_xy, sizeof(double2) * n_outer, cudaMemcpyHostToDevice));
+    TRY(cudaMemcpy(d_odxy, outer_dxy, sizeof(double2) * n_outer, cudaMemcpyHostToDevice));
+    TRY(cudaMemcpy(d_oddxy, outer_ddxy, sizeof(double2) * n_outer, cudaMemcpyHostToDevice));
+    // |Gamma_k| = sum_j w_j over the pore's nodes (reading C5); on an equispaced
+    // circle every w_j = 2 pi r / n, so the sum is n * w (computed the same way
+    // as the kernel's w to keep the ratio w_j/|Gamma_k| exact).
+    for (int k = 0; k < n_pores; ++k) {
+        double wk = 2.0 * kPi * pore_r[k] / (double)nodes_per_pore;
+        double len = 0.0;
+        for (int j = 0; j < nodes_per_pore; ++j) len += wk;
+        hp[k] = make_double4(pore_c[2 * k], pore_c[2 * k + 1], pore_r[k], len);
+        g->h_pore_r.push_back(pore_r[k]);
+    }
+    TRY(cudaMemcpy(g->pore, hp.data(), sizeof(double4) * (n_pores > 0 ? n_pores : 1), cudaMemcpyHostToDevice));
+    k_nodes<<<(N + 255) / 256, 256>>>(N, g->M, g->n_pore, n_outer, outer_period, d_oxy, d_odxy, d_oddxy, g->pore,
+                                      g->pos, g->nw, g->nrm, g->tan, g->w, g->selfc);
+    TRY(cudaGetLastError());
+    {
+        std::vector<double> hw(n_outer);
+        TRY(cudaMemcpy(hw.data(), g->w + g->wall_lo, sizeof(double) * n_outer, cudaMemcpyDeviceToHost));
+        for (int j = 0; j < n_outer; ++j) wall_len += hw[j];
+        g->wall_len = wall_len;
+    }
+    TRY(cudaMalloc(&g->moments, sizeof(double) * (size_t)BIE_MAX_NVEC * (3 * (size_t)(n_pores > 0 ? n_pores : 1) + 1)));
+    TRY(cudaMalloc(&g->stage_in, sizeof(double) * (size_t)BIE_MAX_NVEC * 2 * N));
+    TRY(cudaMalloc(&g->stage_out, sizeof(double) * (size_t)BIE_MAX_NVEC * 2 * N));
+    rc = build_schedules(g);
+    if (rc != BIE_OK) return fail(rc);
+    TRY(cudaDeviceSynchronize());
+#undef TRY
+    cudaFree(d_oxy);
+    cudaFree(d_odxy);
+    cudaFree(d_oddxy);
+    *out = reinterpret_cast<bie_geometry_t>(g);
+    return BIE_OK;
+}
+
+int bie_geometry_info(bie_geometry_t gh, int *N, int *M) {
+    Geometry *g = as_geom(gh);
+    if (!g || !N || !M) {
+        set_error("bie_geometry_info: invalid handle or null output");
+        return BIE_EINVAL;
+    }
+    *N = g->N;
+    *M = g->M;
+    return BIE_OK;
+}
+
+int bie_geometry_nodes(bie_geometry_t gh, double *pos_host) {
+    Geometry *g = as_geom(gh);
+    if (!g || !pos_host) {
+        set_error("bie_geometry_nodes: invalid handle or null output");
+        return BIE_EINVAL;
+    }
+    BIE_CUDA_TRY(cudaMemcpy(pos_host, g->pos, sizeof(double2) * g->N, cudaMemcpyDeviceToHost));
+    return BIE_OK;
+}
+
+}  // extern "C"

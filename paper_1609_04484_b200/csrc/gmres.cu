@@ -1,0 +1,337 @@
+// gmres.cu -- left-preconditioned full GMRES on one GPU (A8, A9).
+//
+// P:l.596-601 (GMRES, tol 1e-8 on the relative residual), P:l.661-663 (left
+// preconditioning P^{-1} A sigma = P^{-1} f), P:l.678-686 (the residual pair).
+// Reading C13: x0 = 0, no restart, CGS2, Givens, happy breakdown when
+// H[k+1,k] <= 1e-14 ||P^{-1} A v_k||, strict "<" on the estimate.
+//
+// The Krylov basis V[0..max_iter] lives in HBM ([max_iter+1][2N]).  Vector
+// kernels are deterministic two-stage reductions (fixed chunking, fixed order):
+//   k_multidot  : partial[chunk][j] = V[j, chunk] . w[chunk], j = 0..k   (reads V once)
+//   k_reduce    : h[j] = sum_chunk partial[chunk][j]
+//   k_multiaxpy : w -= V[0..k]^T h   (or x = V^T y)                     (reads V once)
+//   k_givens    : Hessenberg column update + new rotation on one thread
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace bie {
+
+constexpr int kChunk = 4096;      // elements of the 2N dimension per multidot CTA
+constexpr int kDotThreads = 256;
+
+// partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv)
+__global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restrict__ V, long long ldv, int nv,
+                                                          const double *__restrict__ w, long long n,
+                                                          double *partial, int ldp) {
+    __shared__ double ws[kChunk];
+    __shared__ double red[kDotThreads / 32];
+    const long long e0 = (long long)blockIdx.x * kChunk;
+    const int len = (int)std::min<long long>(kChunk, n - e0);
+    for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int j = 0; j < nv; ++j) {
+        const double *vj = V + (long long)j * ldv + e0;
+        double acc = 0.0;
+        for (int q = threadIdx.x; q < len; q += kDotThreads) acc = fma(vj[q], ws[q], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) red[wid] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < kDotThreads / 32; ++q) t += red[q];
+            partial[(long long)blockIdx.x * ldp + j] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// out[j] = (accumulate ? out[j] : 0) + sum_c partial[c * ldp + j]  (fixed order)
+__global__ void k_reduce(const double *__restrict__ partial, int ldp, int nchunks, int nv, double *out,
+                         int accumulate) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nv) return;
+    double t = 0.0;
+    for (int c = 0; c < nchunks; ++c) t += partial[(long long)c * ldp + j];
+    out[j] = accumulate ? out[j] + t : t;
+}
+
+// y[e] = beta * y[e] + alpha * sum_j V[j][e] * c[j]   (c in device memory, nv <= max_iter+1)
+__global__ void __launch_bounds__(256) k_multiaxpy(const double *__restrict__ V, long long ldv, int nv,
+                                                   const double *__restrict__ c, double alpha, double beta,
+                                                   double *y, long long n) {
+    extern __shared__ double cs[];
+    for (int q = threadIdx.x; q < nv; q += blockDim.x) cs[q] = c[q];
+    __syncthreads();
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double acc = 0.0;
+    int j = 0;
+    for (; j + 4 <= nv; j += 4) {
+        const double a0 = V[(long long)j * ldv + e], a1 = V[(long long)(j + 1) * ldv + e];
+        const double a2 = V[(long long)(j + 2) * ldv + e], a3 = V[(long long)(j + 3) * ldv + e];
+        acc = fma(a0, cs[j], acc);
+        acc = fma(a1, cs[j + 1], acc);
+        acc = fma(a2, cs[j + 2], acc);
+        acc = fma(a3, cs[j + 3], acc);
+    }
+    for (; j < nv; ++j) acc = fma(V[(long long)j * ldv + e], cs[j], acc);
+    y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
+}
+
+__global__ void k_sqrt(const double *in, double *out) { *out = sqrt(*in); }
+
+// y = x / (*s)
+__global__ void k_scale_div(const double *x, const double *s, double *y, long long n) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) y[e] = x[e] / *s;
+}
+
+__global__ void k_sub(const double *a, const double *b, double *y, long long n) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) y[e] = a[e] - b[e];
+}
+
+struct GmState {
+    double *H;      // column-major: H[k * ldh + j], ldh = max_iter + 1
+    double *cs, *sn, *g;
+    double *h, *h2; // CGS passes
+    double *scal;   // [0] beta, [1] w0^2 -> w0, [2] hk1^2 -> hk1, [3] est, [4] breakdown flag, [5] tmp
+};
+
+// Hessenberg column k: H[:,k] = h + h2, H[k+1,k] = hk1; apply old rotations, new rotation.
+__global__ void k_givens(GmState s, int k, int ldh) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double *Hk = s.H + (long long)k * ldh;
+    for (int j = 0; j <= k; ++j) Hk[j] = s.h[j] + s.h2[j];
+    const double hk1 = s.scal[2];
+    Hk[k + 1] = hk1;
+    for (int j = 0; j < k; ++j) {
+        const double a = Hk[j], b = Hk[j + 1];
+        Hk[j] = s.cs[j] * a + s.sn[j] * b;
+        Hk[j + 1] = -s.sn[j] * a + s.cs[j] * b;
+    }
+    const double a = Hk[k], b = Hk[k + 1];
+    const double d = hypot(a, b);
+    s.cs[k] = a / d;
+    s.sn[k] = b / d;
+    Hk[k] = d;
+    Hk[k + 1] = 0.0;
+    s.g[k + 1] = -s.sn[k] * s.g[k];
+    s.g[k] = s.cs[k] * s.g[k];
+    s.scal[3] = fabs(s.g[k + 1]) / s.scal[0];
+    s.scal[4] = (hk1 <= 1e-14 * s.scal[1]) ? 1.0 : 0.0;
+}
+
+// y = H^{-1} g (upper triangular, iters x iters), one CTA
+__global__ void k_trisolve(const double *H, int ldh, const double *g, double *y, int iters) {
+    __shared__ double red[32];
+    __shared__ double yi_s;
+    for (int i = iters - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int j = i + 1 + threadIdx.x; j < iters; j += blockDim.x) acc = fma(H[(long long)j * ldh + i], y[j], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+            yi_s = (g[i] - t) / H[(long long)i * ldh + i];
+            y[i] = yi_s;
+        }
+        __syncthreads();
+    }
+}
+
+struct Dot {
+    double *partial = nullptr;
+    int nchunks = 0;
+    int ldp = 0;
+};
+
+// out[0..nv) = V[0..nv)^T w (deterministic)
+static int multidot(const double *V, long long ldv, int nv, const double *w, long long n, Dot &d, double *out,
+                    cudaStream_t st) {
+    k_multidot<<<d.nchunks, kDotThreads, 0, st>>>(V, ldv, nv, w, n, d.partial, d.ldp);
+    k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, out, 0);
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+static int multiaxpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,
+                     long long n, cudaStream_t st) {
+    size_t smem = sizeof(double) * (size_t)std::max(nv, 1);
+    k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, smem, st>>>(V, ldv, nv, c, alpha, beta, y, n);
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+}  // namespace bie
+
+using namespace bie;
+
+extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f, double *x, double tol,
+                               int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
+                               int *converged, void *stream) {
+    Geometry *g = as_geom(gh);
+    BlockDiag *bd = bdh ? as_bd(bdh) : nullptr;
+    if (!g || (bdh && !bd) || !f || !x || !hist_host || !iters || !res_pc || !res_true || !converged ||
+        max_iter < 1 || !(tol > 0.0) || f == x) {
+        set_error("bie_gmres_solve: invalid handle, null pointer, f == x, max_iter < 1 or tol <= 0");
+        return BIE_EINVAL;
+    }
+    if (bd && bd->g != g) {
+        set_error("bie_gmres_solve: blockdiag was built from another geometry");
+        return BIE_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = 2LL * g->N;
+    const int ldh = max_iter + 1;
+    double *V = nullptr, *w = nullptr, *t = nullptr;
+    GmState s{};
+    Dot d;
+    double *pinned = nullptr;
+    int rc = BIE_OK;
+    d.nchunks = (int)((n + kChunk - 1) / kChunk);
+    d.ldp = ldh;
+    auto cleanup = [&]() {
+        cudaFree(V);
+        cudaFree(w);
+        cudaFree(t);
+        cudaFree(s.H);
+        cudaFree(s.cs);
+        cudaFree(s.sn);
+        cudaFree(s.g);
+        cudaFree(s.h);
+        cudaFree(s.h2);
+        cudaFree(s.scal);
+        cudaFree(d.partial);
+        cudaFreeHost(pinned);
+    };
+#define GM_TRY(expr)                                       \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) {                           \
+            rc = cuda_fail(_e, #expr);                     \
+            cleanup();                                     \
+            return rc;                                     \
+        }                                                  \
+    } while (0)
+#define GM_RC(expr)                                        \
+    do {                                                   \
+        rc = (expr);                                       \
+        if (rc != BIE_OK) {                                \
+            cleanup();                                     \
+            return rc;                                     \
+        }                                                  \
+    } while (0)
+    GM_TRY(cudaMalloc(&V, sizeof(double) * (size_t)ldh * n));
+    GM_TRY(cudaMalloc(&w, sizeof(double) * n));
+    GM_TRY(cudaMalloc(&t, sizeof(double) * n));
+    GM_TRY(cudaMalloc(&s.H, sizeof(double) * (size_t)ldh * max_iter));
+    GM_TRY(cudaMalloc(&s.cs, sizeof(double) * max_iter));
+    GM_TRY(cudaMalloc(&s.sn, sizeof(double) * max_iter));
+    GM_TRY(cudaMalloc(&s.g, sizeof(double) * ldh));
+    GM_TRY(cudaMalloc(&s.h, sizeof(double) * ldh));
+    GM_TRY(cudaMalloc(&s.h2, sizeof(double) * ldh));
+    GM_TRY(cudaMalloc(&s.scal, sizeof(double) * 8));
+    GM_TRY(cudaMalloc(&d.partial, sizeof(double) * (size_t)d.nchunks * ldh));
+    GM_TRY(cudaMallocHost(&pinned, sizeof(double) * 8));
+    GM_TRY(cudaMemsetAsync(s.g, 0, sizeof(double) * ldh, st));
+    GM_TRY(cudaMemsetAsync(s.H, 0, sizeof(double) * (size_t)ldh * max_iter, st));
+
+    auto apply_op = [&](const double *in, double *out) -> int {  // out = P^{-1} A in
+        if (bd) {
+            int r = dlp_apply_impl(g, in, t, 1, BIE_FULL, 0, g->N, st);
+            if (r) return r;
+            return blockdiag_apply_impl(bd, t, out, 1, st);
+        }
+        return dlp_apply_impl(g, in, out, 1, BIE_FULL, 0, g->N, st);
+    };
+    auto norm_to = [&](const double *v, double *dst) -> int {  // dst = ||v|| (device)
+        int r = multidot(v, 0, 1, v, n, d, s.scal + 5, st);
+        if (r) return r;
+        k_sqrt<<<1, 1, 0, st>>>(s.scal + 5, dst);
+        BIE_CUDA_TRY(cudaGetLastError());
+        return BIE_OK;
+    };
+    const unsigned eb = (unsigned)((n + 255) / 256);
+
+    // r0 = P^{-1} f, beta = ||r0||, v0 = r0 / beta
+    if (bd) {
+        GM_RC(blockdiag_apply_impl(bd, f, w, 1, st));
+    } else {
+        GM_TRY(cudaMemcpyAsync(w, f, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    }
+    GM_RC(norm_to(w, s.scal + 0));
+    GM_TRY(cudaMemcpyAsync(pinned, s.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+    GM_TRY(cudaStreamSynchronize(st));
+    const double beta = pinned[0];
+    hist_host[0] = 1.0;
+    *iters = 0;
+    *converged = 0;
+    GM_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    if (beta == 0.0) {
+        *converged = 1;
+        *res_pc = 0.0;
+        *res_true = 0.0;
+        cleanup();
+        return BIE_OK;
+    }
+    k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 0, V, n);
+    GM_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    int it = 0;
+    for (int k = 0; k < max_iter; ++k) {
+        double *vk = V + (long long)k * n;
+        GM_RC(apply_op(vk, w));
+        GM_RC(norm_to(w, s.scal + 1));  // w0 = ||P^{-1} A v_k||
+        // CGS2
+        GM_RC(multidot(V, n, k + 1, w, n, d, s.h, st));
+        GM_RC(multiaxpy(V, n, k + 1, s.h, -1.0, 1.0, w, n, st));
+        GM_RC(multidot(V, n, k + 1, w, n, d, s.h2, st));
+        GM_RC(multiaxpy(V, n, k + 1, s.h2, -1.0, 1.0, w, n, st));
+        GM_RC(norm_to(w, s.scal + 2));  // hk1
+        k_givens<<<1, 1, 0, st>>>(s, k, ldh);
+        GM_TRY(cudaGetLastError());
+        GM_TRY(cudaMemcpyAsync(pinned + 3, s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (k + 1 < max_iter) k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, V + (long long)(k + 1) * n, n);
+        GM_TRY(cudaStreamSynchronize(st));
+        const double est = pinned[3];
+        const bool brk = pinned[4] != 0.0;
+        hist_host[k + 1] = est;
+        it = k + 1;
+        if (est < tol || brk) {
+            *converged = 1;
+            break;
+        }
+    }
+    *iters = it;
+    // y = H^{-1} g, x = V y
+    k_trisolve<<<1, 256, 0, st>>>(s.H, ldh, s.g, s.h, it);
+    GM_TRY(cudaGetLastError());
+    GM_RC(multiaxpy(V, n, it, s.h, 1.0, 0.0, x, n, st));
+    // residual pair (P:l.678-686): r = f - A x
+    GM_RC(dlp_apply_impl(g, x, t, 1, BIE_FULL, 0, g->N, st));
+    k_sub<<<eb, 256, 0, st>>>(f, t, w, n);
+    GM_RC(norm_to(w, s.scal + 6));
+    GM_RC(norm_to(f, s.scal + 7));
+    if (bd) {
+        GM_RC(blockdiag_apply_impl(bd, w, t, 1, st));
+        GM_RC(norm_to(t, s.scal + 5));
+        GM_TRY(cudaMemcpyAsync(pinned + 5, s.scal + 5, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    } else {
+        GM_TRY(cudaMemcpyAsync(pinned + 6, s.scal + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    GM_TRY(cudaStreamSynchronize(st));
+    *res_true = pinned[6] / pinned[7];
+    *res_pc = bd ? pinned[5] / beta : *res_true;
+#undef GM_TRY
+#undef GM_RC
+    cleanup();
+    return BIE_OK;
+}

@@ -1,0 +1,85 @@
+// internal.cuh -- private structures of libbie.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/bie.h"
+
+namespace bie {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr uint32_t kGeomMagic = 0x4745304du;   // "GEOM"
+constexpr uint32_t kBlockMagic = 0x424c4b44u;  // "BLKD"
+
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+#define BIE_CUDA_TRY(expr)                                          \
+    do {                                                            \
+        cudaError_t _e = (expr);                                    \
+        if (_e != cudaSuccess) return ::bie::cuda_fail(_e, #expr);  \
+    } while (0)
+
+// Static, perfectly balanced partition of the (target-block x source-tile)
+// work units of the all-pairs kernel over a persistent grid.
+struct PairSched {
+    int nv = 0;         // vectors per launch (template variant)
+    int R = 0;          // targets per thread
+    int TS = 0;         // sources per smem tile
+    int TB = 0;         // targets per CTA tile (= threads * R)
+    int nTB = 0, nTS = 0;
+    long long U = 0;    // nTB * nTS units
+    int P = 0;          // persistent CTAs
+    int S = 0;          // max partial slots per target block
+    int smem = 0;
+};
+
+struct Geometry {
+    uint32_t magic = kGeomMagic;
+    int N = 0, M = 0, n_pore = 0, n_outer = 0;
+    int wall_lo = 0;          // first Gamma_0 node (= M * n_pore)
+    // node table (device, SoA)
+    double2 *pos = nullptr;   // x_j
+    double2 *nw = nullptr;    // w_j n_j / pi (folded DLP source weight)
+    double2 *nrm = nullptr;   // n_j
+    double2 *tan = nullptr;   // t_j
+    double *w = nullptr;      // w_j
+    double *selfc = nullptr;  // w_j kappa_n,j / (2 pi)
+    double4 *pore = nullptr;  // (cx, cy, r, |Gamma_k|)
+    double wall_len = 0.0;    // |Gamma_0|
+    // host copies needed for scheduling / BD
+    std::vector<double> h_pore_r;
+    // workspace
+    double *partial = nullptr;  // [S][nvec<=16][2N]
+    size_t partial_elems = 0;
+    double *moments = nullptr;  // [16][M][3] (lambda_x, lambda_y, mu) + [16] nu
+    double *stage_in = nullptr, *stage_out = nullptr;  // e2e staging [16][2N] each
+    PairSched sched[5];         // nv = 1, 2, 4, 8, 16
+    int occ[5] = {0, 0, 0, 0, 0};  // resident pair CTAs per SM per variant
+    int num_sms = 0;
+};
+
+struct BlockDiag {
+    uint32_t magic = kBlockMagic;
+    Geometry *g = nullptr;
+    int nb = 0;                     // number of bodies
+    std::vector<int> lo, n;         // node range per body
+    std::vector<long long> off;     // offset of body b's inverse (doubles)
+    double *inv = nullptr;          // explicit inverses, row-major [2n_b][2n_b]
+    long long *d_off = nullptr;
+    int *d_lo = nullptr, *d_n = nullptr;
+};
+
+Geometry *as_geom(bie_geometry_t g);
+BlockDiag *as_bd(bie_blockdiag_t b);
+
+// dlp.cu
+int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, int row_begin,
+                   int row_end, cudaStream_t s);
+int build_schedules(Geometry *g);
+// blockdiag.cu
+int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec, cudaStream_t s);
+// gmres.cu kernels used by other units
+}  // namespace bie

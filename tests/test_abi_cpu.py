@@ -1,0 +1,88 @@
+"""C-ABI contract checks that need no GPU: the library loads, exports every
+symbol include/bie.h declares, and argument validation fails loudly before
+any device call."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bie():
+    from paper_1609_04484_b200 import build as b
+
+    b.build()
+    import paper_1609_04484_b200 as pkg
+
+    return pkg
+
+
+def _declared():
+    hdr = open(os.path.join(ROOT, "include", "bie.h")).read()
+    return sorted(set(re.findall(r"BIE_API\s+(?:int|const char \*)\s*(bie_\w+)\(", hdr)))
+
+
+def test_header_declares_boundary():
+    names = _declared()
+    for n in ("bie_geometry_create", "bie_dlp_apply", "bie_blockdiag_factor", "bie_blockdiag_apply",
+              "bie_gmres_solve", "bie_last_error"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(bie):
+    L = bie.lib()
+    for n in _declared():
+        assert hasattr(L, n), n
+    assert set(_declared()) == set(bie.EXPORTED_SYMBOLS)
+    out = subprocess.run(["nm", "-D", "--defined-only", bie.lib_path()], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (bie_\w+)", out))
+    assert exported == set(_declared())  # nothing else leaks
+
+
+def test_sass_is_sm100a(bie):
+    out = subprocess.run(["cuobjdump", "-lelf", bie.lib_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_invalid_arguments_fail_before_device(bie):
+    L = bie.lib()
+    h = ctypes.c_void_p()
+    xy = np.zeros(2 * 32)
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    # odd / too small node counts (S:l.55-57)
+    assert L.bie_geometry_create(dp(xy), dp(xy), dp(xy), 15, 1.0, None, None, 0, 0, ctypes.byref(h)) == -1
+    assert b"even" in L.bie_last_error()
+    assert L.bie_geometry_create(dp(xy), dp(xy), dp(xy), 32, 1.0, None, None, 1, 32, ctypes.byref(h)) == -1
+    assert L.bie_geometry_create(None, dp(xy), dp(xy), 32, 1.0, None, None, 0, 0, ctypes.byref(h)) == -1
+    # non-positive radius -> BIE_EGEOM
+    c = np.zeros(2)
+    r = np.array([-0.1])
+    assert L.bie_geometry_create(dp(xy), dp(xy), dp(xy), 32, 1.0, dp(c), dp(r), 1, 32, ctypes.byref(h)) == -2
+    # null handles -> BIE_EINVAL
+    assert L.bie_dlp_apply(None, None, None, 1, 0, None) == -1
+    assert L.bie_geometry_destroy(None) == -1
+    assert L.bie_blockdiag_apply(None, None, None, 1, None) == -1
+    assert L.bie_gmres_solve(None, None, None, None, 1e-8, 10, None, None, None, None, None, None) == -1
+
+
+def test_binding_raises_without_library(tmp_path, monkeypatch):
+    import paper_1609_04484_b200._bie as m
+
+    monkeypatch.setattr(m, "_LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(m, "_lib", None)
+    with pytest.raises(ImportError):
+        m.lib()
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1609_04484_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("no oracle", ""), f

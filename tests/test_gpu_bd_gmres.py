@@ -1,0 +1,197 @@
+"""GPU parity of the block-diagonal preconditioner (A6/A7) and GMRES (A8/A9)
+against the CPU oracle, through the C ABI.
+
+Bars (BASELINE.json north_star, readings C13/C14): GMRES iteration count equal
+and residual history within 1e-10 relative at tol 1e-8.  BD inverses: the
+explicit inverse is unique, so GPU and oracle agree to rounding x cond(B)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from bie_inputs import density, make_problem, rhs_pipe, rhs_rotation_outer, rhs_shear_all, rhs_shear_outer
+from bie_inputs.geometry import make_circle_problem, make_pipe
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def bie(cuda_ok):
+    from paper_1609_04484_b200 import build as b
+
+    b.build()
+    import paper_1609_04484_b200 as pkg
+
+    return pkg
+
+
+_cache = {}
+
+
+def _setup(bie, problem, with_bd=True):
+    key = problem.name
+    if key not in _cache:
+        g = bie.Geometry.from_problem(problem)
+        og = oracle.OracleGeometry(problem)
+        _cache[key] = dict(g=g, og=og, bd=None, obd=None)
+    c = _cache[key]
+    if with_bd and c["bd"] is None:
+        c["bd"] = bie.BlockDiag(c["g"])
+    return c
+
+
+def _obd(c):
+    if c["obd"] is None:
+        c["obd"] = oracle.OracleBD(c["og"])
+    return c["obd"]
+
+
+def _t(a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64).reshape(-1)).cuda()
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_bd_inverse_parity(bie, cid):
+    c = _setup(bie, make_problem(cid))
+    obd = _obd(c)
+    for b in sorted({0, c["og"].M - 1, c["og"].M}):
+        gi = c["bd"].block_inverse(b)
+        oi = obd.block_inverse(b)
+        assert np.abs(gi - oi).max() / np.abs(oi).max() < 1e-12, b
+        B = c["og"].bd_block(b)
+        assert np.abs(gi @ B - np.eye(B.shape[0])).max() < 1e-12
+
+
+def test_bd_apply_parity(bie):
+    import torch
+
+    c = _setup(bie, make_problem(2))
+    obd = _obd(c)
+    v = density(c["og"].problem, nvec=5, vec_id=3)
+    out = torch.zeros(v.size, dtype=torch.float64, device="cuda")
+    bie.blockdiag_apply(c["bd"], _t(v), out, nvec=5)
+    torch.cuda.synchronize()
+    z = out.cpu().numpy().reshape(5, -1)
+    for k in range(5):
+        ref = obd.apply(v[k])
+        assert np.abs(z[k] - ref).max() / np.abs(ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("cid", [3, 4])
+def test_bd_large_blocks_inverse_property(bie, cid):
+    """Sizes the oracle cannot invert in seconds: check B (B^{-1} v) = v with the
+    oracle-assembled blocks (wall: 4096^2 / 16384^2; a few pores)."""
+    import torch
+
+    p = make_problem(cid)
+    c = _setup(bie, p)
+    og = c["og"]
+    v = density(p, nvec=1, vec_id=9)[0]
+    out = torch.zeros(v.size, dtype=torch.float64, device="cuda")
+    bie.blockdiag_apply(c["bd"], _t(v), out)
+    torch.cuda.synchronize()
+    z = out.cpu().numpy()
+    for b in (0, p.M // 2, p.M - 1, p.M):
+        lo, hi = og.body_range(b)
+        B = og.bd_block(b)
+        r = B @ z[2 * lo:2 * hi] - v[2 * lo:2 * hi]
+        assert np.abs(r).max() / np.abs(v[2 * lo:2 * hi]).max() < 1e-10, b
+
+
+def _cmp_gmres(res, ref, tol_hist=1e-10):
+    assert res["iters"] == ref["iters"], (res["iters"], ref["iters"])
+    assert res["converged"] == ref["converged"]
+    h, hr = np.asarray(res["hist"]), np.asarray(ref["hist"])
+    assert h.shape == hr.shape
+    rel = np.abs(h - hr) / np.abs(hr)
+    assert rel.max() <= tol_hist, rel.max()
+
+
+CASES = {
+    "c1_rotation": (lambda: make_problem(1), rhs_rotation_outer),
+    "c1_shear_outer": (lambda: make_problem(1), rhs_shear_outer),
+    "c1_offcentre_shear": (lambda: make_circle_problem(64, 1.0, ((0.2, -0.1, 0.3),), 64, 1, "c1off"), rhs_shear_outer),
+    "c2_pipe": (lambda: make_problem(2), rhs_pipe),
+    "c2_shear_all": (lambda: make_problem(2), rhs_shear_all),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("pc", ["bd", "none"])
+def test_gmres_parity(bie, case, pc):
+    import torch
+
+    mk, rhs = CASES[case]
+    p = mk()
+    c = _setup(bie, p)
+    f = rhs(p)
+    ref = oracle.gmres(c["og"], f, _obd(c) if pc == "bd" else None, tol=1e-8, max_iter=1000)
+    x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    res = bie.gmres_solve(c["g"], c["bd"] if pc == "bd" else None, _t(f), x, tol=1e-8, max_iter=1000)
+    _cmp_gmres(res, ref)
+    xs = x.cpu().numpy()
+    assert np.abs(xs - ref["x"]).max() / np.abs(ref["x"]).max() < 1e-9
+    assert abs(res["res_true"] - ref["res_true"]) <= 1e-6 * ref["res_true"] + 1e-15
+    assert abs(res["res_pc"] - ref["res_pc"]) <= 1e-6 * ref["res_pc"] + 1e-15
+
+
+def test_gmres_single_body_one_iteration(bie):
+    import torch
+
+    p = make_pipe(0, 10.0, 256, 0, (0.1, 0.2), 0.05, 16)
+    c = _setup(bie, p)
+    f = rhs_pipe(p)
+    x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    res = bie.gmres_solve(c["g"], c["bd"], _t(f), x, tol=1e-8, max_iter=20)
+    assert res["iters"] == 1 and res["converged"]
+
+
+def test_gmres_cap_not_converged(bie):
+    import torch
+
+    p = make_problem(2)
+    c = _setup(bie, p)
+    f = rhs_pipe(p)
+    x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    res = bie.gmres_solve(c["g"], None, _t(f), x, tol=1e-8, max_iter=7)
+    assert res["iters"] == 7 and not res["converged"]
+    ref = oracle.gmres(c["og"], f, None, tol=1e-8, max_iter=7)
+    _cmp_gmres(res, ref)
+
+
+def test_gmres_deterministic(bie):
+    import torch
+
+    p = make_problem(2)
+    c = _setup(bie, p)
+    f = _t(rhs_pipe(p))
+    outs = []
+    for _ in range(2):
+        x = torch.zeros_like(f)
+        r = bie.gmres_solve(c["g"], c["bd"], f, x, tol=1e-8, max_iter=200)
+        outs.append((r["hist"], x.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_none_pipe_prefix"])
+def test_gmres_golden(bie, name):
+    """Large configs: histories produced by tools/make_golden.py (oracle only)."""
+    import torch
+
+    path = os.path.join(GOLDEN, f"gmres_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"golden {path} not generated")
+    gd = json.load(open(path))
+    p = make_problem(gd["config"])
+    c = _setup(bie, p, with_bd=gd["pc"] == "bd")
+    f = rhs_pipe(p)
+    assert abs(np.linalg.norm(f) - gd["f_norm"]) < 1e-12 * gd["f_norm"]
+    x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    res = bie.gmres_solve(c["g"], c["bd"] if gd["pc"] == "bd" else None, _t(f), x, tol=gd["tol"],
+                          max_iter=gd["max_iter"])
+    _cmp_gmres(res, gd)
