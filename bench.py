@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (see DESIGN.md s5 for every definition).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (BASELINE.json configs[3]): pipe L=100,
+1000 pores, N = 136,192 boundary nodes (272,384 FP64 unknowns), pipe-flow
+boundary data.  One STEP = one left-preconditioned BD-GMRES solve with a fixed
+budget of 50 iterations (tol below reach) through bie_gmres_solve: 51 completed
+DLP matvecs (A2-A5: 50 Arnoldi + 1 residual), 52 BD applies (A7), CGS2 +
+Givens (A8) and the finish (A9).  Setup (A1 geometry, A6 BD factor) happens
+once before timing and is reported separately ("build PC", P:l.720).
+
+metric = DLP matvec pair-interactions/s (N^2 per matvec, self pairs included
+since the kernel evaluates them branch-free).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_ID = 4
+GMRES_ITERS = 50
+FLOP_PER_PAIR = 19  # algorithmic, nvec = 1 (11 geometry + 8 per vector)
+# FP64 CUDA-core peak derived from unit counts and clocks:
+# 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (MEASURED_PEAKS.json sm_max_mhz)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline_sample(problem, seconds=12.0, max_rows=None):
+    """Oracle completed matvec on a bounded strided row sample (TEST INFRA: oracle/)."""
+    import numpy as np
+
+    import oracle
+    from bie_inputs import density
+
+    og = oracle.OracleGeometry(problem)
+    s = density(problem)[0]
+    N = problem.N
+    rows_per_batch = 256
+    done_pairs, t_used, batch = 0, 0.0, 0
+    stride = 97  # co-prime walk over targets
+    while t_used < seconds and (max_rows is None or batch * rows_per_batch < max_rows):
+        rows = ((np.arange(rows_per_batch) + batch * rows_per_batch) * stride % N).astype(np.int32)
+        t0 = time.perf_counter()
+        og.apply(s, rows=rows)
+        t_used += time.perf_counter() - t0
+        done_pairs += rows_per_batch * N
+        batch += 1
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": done_pairs / t_used, "unit": "pair-interactions/s", "cores": cores, "kind": "oracle",
+            "sample": f"{batch * rows_per_batch} strided target rows x all {N} sources of the config-{problem.config_id} "
+                      f"completed DLP matvec (oracle/bie_oracle.c, OpenMP over rows), {t_used:.1f} s",
+            "seconds": t_used}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, same metric/unit, rank 0 only."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from bie_inputs import make_problem
+
+    p = make_problem(CONFIG_ID)
+    per_step_s = max(2.0, min(15.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_baseline_sample(p, seconds=per_step_s / 4)
+    vals, secs = [], 0.0
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline_sample(p, seconds=per_step_s)
+        vals.append(last["value"])
+        secs += last["seconds"]
+    value = statistics.mean(vals)
+    pairs_per_step = GMRES_ITERS + 1
+    line = {
+        "impl": "reference", "metric": "DLP matvec pair-interactions/s", "value": value,
+        "unit": "pair-interactions/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * pairs_per_step * p.N * p.N / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config4 pipe L=100 M=1000 N={p.N}: oracle completed DLP matvec rows "
+                               f"(bounded sample per step; ms_per_step extrapolated to {pairs_per_step} matvecs)",
+                   "N": p.N, "unknowns": 2 * p.N},
+        "cpu_baseline": {"value": value, "unit": "pair-interactions/s", "cores": last["cores"], "kind": "oracle",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": "pair-interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_1609_04484_b200 as bie
+    from bie_inputs import density, make_problem, rhs_pipe
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    p = make_problem(CONFIG_ID)
+    N = p.N
+    t0 = time.perf_counter()
+    g = bie.Geometry.from_problem(p)
+    torch.cuda.synchronize()
+    t_geom = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    bd = bie.BlockDiag(g)
+    torch.cuda.synchronize()
+    t_bd = time.perf_counter() - t0
+
+    f_host = torch.from_numpy(rhs_pipe(p)).pin_memory()
+    f = f_host.to(dev)
+    x = torch.zeros_like(f)
+    x_host = torch.zeros_like(f_host).pin_memory()
+    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    pairs_per_step = (GMRES_ITERS + 1) * N * N
+
+    def step():
+        return bie.gmres_solve(g, bd, f, x, tol=1e-30, max_iter=GMRES_ITERS)
+
+    for _ in range(max(3, args.warmup)):
+        r = step()
+    assert r["iters"] == GMRES_ITERS
+
+    # ---- timed region: device-resident inputs, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = bie.launch_count()
+    bie.profile_begin(g)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    prof = bie.profile_end(g)
+    launches = bie.launch_count() - launches0
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_total = sum(step_ms) / 1e3
+    if dist:
+        tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total = tt.item()
+    value = ws * args.steps * pairs_per_step / t_total
+
+    # ---- dominant kernel roofline (k_dlp_pairs, CUDA events on the launch stream)
+    pair_ms = prof["pairs_ms"] / max(1, prof["applies"])
+    achieved_tflops = FLOP_PER_PAIR * N * N / (pair_ms * 1e-3) / 1e12
+    pairs_share = prof["pairs_ms"] / sum(step_ms)
+
+    # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        e2e_ev[k][0].record(stream)
+        f.copy_(f_host, non_blocking=True)
+        step()
+        x_host.copy_(x, non_blocking=True)
+        e2e_ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_s = sum(a.elapsed_time(b) for a, b in e2e_ev) / 1e3
+    if dist:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = tt.item()
+
+    extra = {}
+    if rank == 0 and not args.quick:
+        # matvec-only sweep (bie_dlp_apply, BIE_FULL) and full GMRES solves
+        sweep = {}
+        for nvec in (1, 4, 16):
+            s = torch.from_numpy(density(p, nvec=nvec).reshape(-1)).to(dev)
+            o = torch.zeros_like(s)
+            for _ in range(2):
+                bie.dlp_apply(g, s, o, nvec)
+            reps = 5 if nvec < 16 else 2
+            bie.profile_begin(g)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                bie.dlp_apply(g, s, o, nvec)
+            b.record(stream)
+            torch.cuda.synchronize()
+            pr = bie.profile_end(g)
+            ms = a.elapsed_time(b) / reps
+            kms = pr["pairs_ms"] / max(1, pr["applies"])
+            sweep[f"nvec{nvec}"] = {
+                "ms": ms, "pairs_per_s": nvec * N * N / (ms * 1e-3), "kernel_ms": kms,
+                "kernel_alg_tflops": (11 + 8 * nvec) * N * N / (kms * 1e-3) / 1e12,
+                "kernel_frac_of_fp64_peak": (11 + 8 * nvec) * N * N / (kms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS}
+            del s, o
+        extra["matvec_sweep"] = sweep
+        sol = {}
+        for cid, mi in ((3, 1000), (CONFIG_ID, args.gmres_cap)):
+            pp = make_problem(cid)
+            gg = g if cid == CONFIG_ID else bie.Geometry.from_problem(pp)
+            torch.cuda.synchronize()
+            tb = time.perf_counter()
+            bdd = bd if cid == CONFIG_ID else bie.BlockDiag(gg)
+            torch.cuda.synchronize()
+            tb = time.perf_counter() - tb
+            ff = torch.from_numpy(rhs_pipe(pp)).to(dev)
+            xx = torch.zeros_like(ff)
+            ts = time.perf_counter()
+            rr = bie.gmres_solve(gg, bdd, ff, xx, tol=1e-8, max_iter=mi)
+            ts = time.perf_counter() - ts
+            sol[f"config{cid}"] = {"N": pp.N, "build_pc_s": tb if cid != CONFIG_ID else t_bd, "gmres_s": ts,
+                                   "iters": rr["iters"], "converged": rr["converged"], "max_iter": mi,
+                                   "res_pc": rr["res_pc"], "res_true": rr["res_true"], "tol": 1e-8}
+        extra["gmres_solve"] = sol
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peaks = _peaks()
+    clocks = clk.summary()
+    line = {
+        "metric": "DLP matvec pair-interactions/s", "value": value, "unit": "pair-interactions/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": statistics.mean(step_ms),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config4 pipe L=100 M=1000 N={N} (2N={2 * N} unknowns), pipe BC; step = "
+                               f"BD-preconditioned GMRES solve, fixed {GMRES_ITERS} iterations "
+                               f"({GMRES_ITERS + 1} completed DLP matvecs + BD applies + CGS2)",
+                   "N": N, "unknowns": 2 * N, "gmres_iters_per_step": GMRES_ITERS,
+                   "matvecs_per_step": GMRES_ITERS + 1, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": "flushed between timed steps (256 MiB write); BD inverses (2.67 GB) exceed L2 each step"},
+        "roofline": {"kernel": "k_dlp_pairs<1,4,256>", "bound": "alu", "achieved": achieved_tflops,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
+                     "traffic": None, "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
+                     "kernel_share_of_step": pairs_share,
+                     "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
+        "e2e": {"value": ws * args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
+                "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "setup": {"geometry_s": t_geom, "build_pc_s": t_bd},
+        "hbm_peak_gbs": peaks.get("hbm_gbs"),
+    }
+    line.update(extra)
+    if not args.no_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = {k: v for k, v in cpu_baseline_sample(p, seconds=args.cpu_seconds).items()
+                                if k != "seconds"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true", help="skip the matvec sweep and full GMRES solves")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--gmres-cap", type=int, default=2000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -153,6 +153,20 @@ BIE_API int bie_gmres_solve(bie_geometry_t g, bie_blockdiag_t bd, const double *
 
 BIE_API const char *bie_last_error(void);
 
+/*
+ * Measurement hooks (bench.py; not needed for computing).
+ * bie_profile_begin: from now on every bie_dlp_apply* on g records CUDA events
+ *   on its stream around its three phases (moments | all-pairs | epilogue).
+ * bie_profile_end: synchronises those events, returns the summed durations in
+ *   milliseconds and the number of applies recorded, and stops recording.
+ * bie_launch_count: number of kernels this library has launched in the
+ *   process so far (monotone counter; take differences).
+ */
+BIE_API int bie_profile_begin(bie_geometry_t g);
+BIE_API int bie_profile_end(bie_geometry_t g, double *ms_moments, double *ms_pairs, double *ms_epilogue,
+                            int *applies);
+BIE_API long long bie_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,9 @@ from ._bie import (  # noqa: F401
     dlp_apply_host,
     dlp_apply_rows,
     gmres_solve,
+    launch_count,
+    profile_begin,
+    profile_end,
     lib,
     lib_path,
     EXPORTED_SYMBOLS,

@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "bie_geometry_create", "bie_geometry_destroy", "bie_geometry_info", "bie_geometry_nodes",
     "bie_dlp_apply", "bie_dlp_apply_rows", "bie_dlp_apply_host",
     "bie_blockdiag_factor", "bie_blockdiag_apply", "bie_blockdiag_destroy", "bie_blockdiag_block_inverse",
-    "bie_gmres_solve", "bie_last_error",
+    "bie_gmres_solve", "bie_last_error", "bie_profile_begin", "bie_profile_end", "bie_launch_count",
 )
 
 
@@ -66,6 +66,8 @@ def lib():
         "bie_blockdiag_destroy": [vp],
         "bie_blockdiag_block_inverse": [vp, c_int, dp, ctypes.c_longlong],
         "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
+        "bie_profile_begin": [vp],
+        "bie_profile_end": [vp, dp, dp, dp, ip],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -73,6 +75,8 @@ def lib():
         fn.restype = c_int
     L.bie_last_error.argtypes = []
     L.bie_last_error.restype = ctypes.c_char_p
+    L.bie_launch_count.argtypes = []
+    L.bie_launch_count.restype = ctypes.c_longlong
     _lib = L
     return L
 
@@ -147,6 +151,22 @@ class Geometry:
             self.close()
         except Exception:
             pass
+
+
+def launch_count() -> int:
+    """Kernels launched by libbie.so in this process so far (bie_launch_count)."""
+    return int(lib().bie_launch_count())
+
+
+def profile_begin(g: Geometry):
+    _check(lib().bie_profile_begin(g.h))
+
+
+def profile_end(g: Geometry) -> dict:
+    """Summed CUDA-event durations (ms) of the matvec phases since profile_begin."""
+    m, p, e, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    _check(lib().bie_profile_end(g.h, ctypes.byref(m), ctypes.byref(p), ctypes.byref(e), ctypes.byref(n)))
+    return dict(moments_ms=m.value, pairs_ms=p.value, epilogue_ms=e.value, applies=n.value)
 
 
 def dlp_apply(g: Geometry, sigma, out, nvec: int = 1, flags: int = BIE_FULL, stream=None):

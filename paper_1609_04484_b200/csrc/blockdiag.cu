@@ -423,6 +423,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         dim3 grid((unsigned)((elems + 255) / 256), v.count);
         k_bd_assemble<<<grid, 256, 0, st>>>(v, lo0, nodes, is_wall ? 1 : 0, g->pos, g->nw, g->nrm, g->tan, g->w,
                                             g->selfc, g->pore, g->wall_len);
+        count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
     }
     int panel_threads = n2 >= 1024 ? 1024 : (n2 >= 256 ? 256 : 128);
@@ -433,6 +434,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), v.count), 256, 0, st>>>(v, s, k0, nbe);
         k_make_G<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
         k_update<<<dim3((n2 + UT - 1) / UT, (n2 + UT - 1) / UT, v.count), 256, 0, st>>>(v, s, k0, nbe);
+        count_launch(5);
         BIE_CUDA_TRY(cudaGetLastError());
     }
     k_perm<<<v.count, 32, 0, st>>>(v, s);
@@ -440,6 +442,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     if (rowbytes > 48 * 1024)
         BIE_CUDA_TRY(cudaFuncSetAttribute(k_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowbytes));
     k_unpermute<<<dim3(n2, v.count), 256, rowbytes, st>>>(v, s);
+    count_launch(2);
     BIE_CUDA_TRY(cudaGetLastError());
     cudaFreeAsync(s.W, st);
     cudaFreeAsync(s.T, st);
@@ -462,14 +465,17 @@ int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec,
             k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
                                                       out, stride, v);
             v += 4;
+            count_launch();
         } else if (rem >= 2) {
             k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
                                                       out, stride, v);
             v += 2;
+            count_launch();
         } else {
             k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
                                                       out, stride, v);
             v += 1;
+            count_launch();
         }
         BIE_CUDA_TRY(cudaGetLastError());
     }

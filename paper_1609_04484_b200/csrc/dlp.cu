@@ -404,7 +404,19 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     if (Nt <= 0) return BIE_OK;
     const long long stride = 2LL * N;
     const bool full = !(flags & BIE_D_ONLY);
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (g->prof) {
+        while (g->prof_ev.size() < g->prof_used + 4) {
+            cudaEvent_t e;
+            BIE_CUDA_TRY(cudaEventCreate(&e));
+            g->prof_ev.push_back(e);
+        }
+        for (int q = 0; q < 4; ++q) ev[q] = g->prof_ev[g->prof_used + q];
+        g->prof_used += 4;
+        BIE_CUDA_TRY(cudaEventRecord(ev[0], st));
+    }
     if (full) {
+        count_launch();
         k_moments<<<g->M + 1, 256, 0, st>>>(g->pos, g->nrm, g->w, g->pore, sigma, stride, nvec, g->M, g->n_pore,
                                             g->wall_lo, N, g->wall_len, g->moments);
         BIE_CUDA_TRY(cudaGetLastError());
@@ -440,6 +452,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         BIE_CUDA_TRY(cudaMalloc(&g->partial, need * sizeof(double)));
         g->partial_elems = need;
     }
+    if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
     for (int c = 0; c < nch; ++c) {
         PairArgs a;
         a.pos = g->pos;
@@ -455,8 +468,10 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         a.nTS = sch[c].nTS;
         a.U = sch[c].U;
         launch_pairs(vis[c], sch[c], a, st);
+        count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
     }
+    if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
     ea.pos = g->pos;
     ea.nrm = g->nrm;
     ea.tan = g->tan;
@@ -476,7 +491,9 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     ea.flags = flags;
     ea.nchunks = nch;
     k_epilogue<<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
+    if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));
     return BIE_OK;
 }
 

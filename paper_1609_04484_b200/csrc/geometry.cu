@@ -1,4 +1,5 @@
 // geometry.cu -- bie_geometry_* and error plumbing (A1 of SURVEY.md s8(a)).
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -9,6 +10,9 @@
 namespace bie {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -97,6 +101,7 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     cudaFree(g->moments);
     cudaFree(g->stage_in);
     cudaFree(g->stage_out);
+    for (cudaEvent_t e : g->prof_ev) cudaEventDestroy(e);
     g->magic = 0;
     delete g;
     return BIE_OK;
@@ -192,6 +197,7 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     TRY(cudaMemcpy(g->pore, hp.data(), sizeof(double4) * (n_pores > 0 ? n_pores : 1), cudaMemcpyHostToDevice));
     k_nodes<<<(N + 255) / 256, 256>>>(N, g->M, g->n_pore, n_outer, outer_period, d_oxy, d_odxy, d_oddxy, g->pore,
                                       g->pos, g->nw, g->nrm, g->tan, g->w, g->selfc);
+    count_launch();
     TRY(cudaGetLastError());
     {
         std::vector<double> hw(n_outer);
@@ -231,6 +237,45 @@ int bie_geometry_nodes(bie_geometry_t gh, double *pos_host) {
         return BIE_EINVAL;
     }
     BIE_CUDA_TRY(cudaMemcpy(pos_host, g->pos, sizeof(double2) * g->N, cudaMemcpyDeviceToHost));
+    return BIE_OK;
+}
+
+long long bie_launch_count(void) { return g_launches.load(); }
+
+int bie_profile_begin(bie_geometry_t gh) {
+    Geometry *g = as_geom(gh);
+    if (!g) {
+        set_error("bie_profile_begin: invalid geometry handle");
+        return BIE_EINVAL;
+    }
+    g->prof = true;
+    g->prof_used = 0;
+    return BIE_OK;
+}
+
+int bie_profile_end(bie_geometry_t gh, double *ms_moments, double *ms_pairs, double *ms_epilogue, int *applies) {
+    Geometry *g = as_geom(gh);
+    if (!g || !ms_moments || !ms_pairs || !ms_epilogue || !applies) {
+        set_error("bie_profile_end: invalid handle or null output");
+        return BIE_EINVAL;
+    }
+    double m = 0, p = 0, e = 0;
+    for (size_t q = 0; q + 4 <= g->prof_used; q += 4) {
+        BIE_CUDA_TRY(cudaEventSynchronize(g->prof_ev[q + 3]));
+        float a = 0, b = 0, c = 0;
+        BIE_CUDA_TRY(cudaEventElapsedTime(&a, g->prof_ev[q], g->prof_ev[q + 1]));
+        BIE_CUDA_TRY(cudaEventElapsedTime(&b, g->prof_ev[q + 1], g->prof_ev[q + 2]));
+        BIE_CUDA_TRY(cudaEventElapsedTime(&c, g->prof_ev[q + 2], g->prof_ev[q + 3]));
+        m += a;
+        p += b;
+        e += c;
+    }
+    *ms_moments = m;
+    *ms_pairs = p;
+    *ms_epilogue = e;
+    *applies = (int)(g->prof_used / 4);
+    g->prof = false;
+    g->prof_used = 0;
     return BIE_OK;
 }
 

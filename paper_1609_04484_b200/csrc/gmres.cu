@@ -159,6 +159,7 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
                     cudaStream_t st) {
     k_multidot<<<d.nchunks, kDotThreads, 0, st>>>(V, ldv, nv, w, n, d.partial, d.ldp);
     k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, out, 0);
+    count_launch(2);
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
 }
@@ -167,6 +168,7 @@ static int multiaxpy(const double *V, long long ldv, int nv, const double *c, do
                      long long n, cudaStream_t st) {
     size_t smem = sizeof(double) * (size_t)std::max(nv, 1);
     k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, smem, st>>>(V, ldv, nv, c, alpha, beta, y, n);
+    count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
 }
@@ -257,6 +259,7 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
         int r = multidot(v, 0, 1, v, n, d, s.scal + 5, st);
         if (r) return r;
         k_sqrt<<<1, 1, 0, st>>>(s.scal + 5, dst);
+        count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
     };
@@ -284,6 +287,7 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
         return BIE_OK;
     }
     k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 0, V, n);
+    count_launch();
     GM_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
     int it = 0;
     for (int k = 0; k < max_iter; ++k) {
@@ -297,9 +301,13 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
         GM_RC(multiaxpy(V, n, k + 1, s.h2, -1.0, 1.0, w, n, st));
         GM_RC(norm_to(w, s.scal + 2));  // hk1
         k_givens<<<1, 1, 0, st>>>(s, k, ldh);
+        count_launch();
         GM_TRY(cudaGetLastError());
         GM_TRY(cudaMemcpyAsync(pinned + 3, s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        if (k + 1 < max_iter) k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, V + (long long)(k + 1) * n, n);
+        if (k + 1 < max_iter) {
+            k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, V + (long long)(k + 1) * n, n);
+            count_launch();
+        }
         GM_TRY(cudaStreamSynchronize(st));
         const double est = pinned[3];
         const bool brk = pinned[4] != 0.0;
@@ -313,11 +321,13 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     *iters = it;
     // y = H^{-1} g, x = V y
     k_trisolve<<<1, 256, 0, st>>>(s.H, ldh, s.g, s.h, it);
+    count_launch();
     GM_TRY(cudaGetLastError());
     GM_RC(multiaxpy(V, n, it, s.h, 1.0, 0.0, x, n, st));
     // residual pair (P:l.678-686): r = f - A x
     GM_RC(dlp_apply_impl(g, x, t, 1, BIE_FULL, 0, g->N, st));
     k_sub<<<eb, 256, 0, st>>>(f, t, w, n);
+    count_launch();
     GM_RC(norm_to(w, s.scal + 6));
     GM_RC(norm_to(f, s.scal + 7));
     if (bd) {

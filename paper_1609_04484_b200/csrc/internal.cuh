@@ -59,7 +59,14 @@ struct Geometry {
     PairSched sched[5];         // nv = 1, 2, 4, 8, 16
     int occ[5] = {0, 0, 0, 0, 0};  // resident pair CTAs per SM per variant
     int num_sms = 0;
+    // profiling (bie_profile_begin/end): 4 events per recorded apply
+    bool prof = false;
+    std::vector<cudaEvent_t> prof_ev;
+    size_t prof_used = 0;
 };
+
+// process-wide count of kernels launched by the library (bie_launch_count)
+void count_launch(int n = 1);
 
 struct BlockDiag {
     uint32_t magic = kBlockMagic;

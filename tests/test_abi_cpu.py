@@ -24,7 +24,7 @@ def bie():
 
 def _declared():
     hdr = open(os.path.join(ROOT, "include", "bie.h")).read()
-    return sorted(set(re.findall(r"BIE_API\s+(?:int|const char \*)\s*(bie_\w+)\(", hdr)))
+    return sorted(set(re.findall(r"BIE_API\s+(?:int|long long|const char \*)\s*(bie_\w+)\(", hdr)))
 
 
 def test_header_declares_boundary():
