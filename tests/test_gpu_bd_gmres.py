@@ -127,22 +127,60 @@ CASES = {
 
 
 @pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("pc", ["bd", "none"])
-def test_gmres_parity(bie, case, pc):
+def test_gmres_parity_bd(bie, case):
+    """BD-preconditioned histories are well conditioned (the oracle's own history
+    moves by ~2e-13 under 1e-15 perturbations of f): strict 1e-10 bar."""
     import torch
 
     mk, rhs = CASES[case]
     p = mk()
     c = _setup(bie, p)
     f = rhs(p)
-    ref = oracle.gmres(c["og"], f, _obd(c) if pc == "bd" else None, tol=1e-8, max_iter=1000)
+    ref = oracle.gmres(c["og"], f, _obd(c), tol=1e-8, max_iter=1000)
     x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
-    res = bie.gmres_solve(c["g"], c["bd"] if pc == "bd" else None, _t(f), x, tol=1e-8, max_iter=1000)
+    res = bie.gmres_solve(c["g"], c["bd"], _t(f), x, tol=1e-8, max_iter=1000)
     _cmp_gmres(res, ref)
     xs = x.cpu().numpy()
     assert np.abs(xs - ref["x"]).max() / np.abs(ref["x"]).max() < 1e-9
-    assert abs(res["res_true"] - ref["res_true"]) <= 1e-6 * ref["res_true"] + 1e-15
-    assert abs(res["res_pc"] - ref["res_pc"]) <= 1e-6 * ref["res_pc"] + 1e-15
+    assert abs(res["res_true"] - ref["res_true"]) <= 1e-6 * ref["res_true"] + 1e-13
+    assert abs(res["res_pc"] - ref["res_pc"]) <= 1e-6 * ref["res_pc"] + 1e-13
+
+
+def _oracle_envelope(og, f, n_runs=4, eps=1e-15):
+    """Oracle no-PC histories under 1e-15 relative perturbations of f (reading C23)."""
+    runs = []
+    for s in range(n_runs):
+        rng = np.random.default_rng(100 + s)
+        runs.append(oracle.gmres(og, f * (1 + eps * rng.standard_normal(f.size)), None, tol=1e-8, max_iter=1000))
+    return runs
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_gmres_parity_nopc(bie, case):
+    """No-PC histories are ill conditioned (reading C23: the oracle's own history
+    moves by up to 13% on config 2, and the off-centre tiny case changes its
+    iteration count, under 1e-15 perturbations of f).  The GPU history must
+    lie within 10x the oracle's own perturbation envelope (floor 1e-10), and
+    its iteration count within the perturbed oracle runs' range."""
+    import torch
+
+    mk, rhs = CASES[case]
+    p = mk()
+    c = _setup(bie, p, with_bd=False)
+    f = rhs(p)
+    ref = oracle.gmres(c["og"], f, None, tol=1e-8, max_iter=1000)
+    runs = _oracle_envelope(c["og"], f)
+    x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    res = bie.gmres_solve(c["g"], None, _t(f), x, tol=1e-8, max_iter=1000)
+    its = [r["iters"] for r in runs] + [ref["iters"]]
+    assert min(its) <= res["iters"] <= max(its), (res["iters"], its)
+    n = min([res["iters"]] + its) + 1
+    hr = ref["hist"][:n]
+    env = np.max([np.abs(r["hist"][:n] - hr) / hr for r in runs], axis=0)
+    big = hr > FLOOR
+    rel = np.abs(res["hist"][:n] - hr) / hr
+    assert np.all(rel[big] <= np.maximum(1e-10, 10 * env[big])), (rel.max(), env.max())
+    assert res["converged"] and res["res_true"] < 1e-7
 
 
 def test_gmres_single_body_one_iteration(bie):
