@@ -41,6 +41,8 @@ extern "C" {
 /* bie_dlp_apply flags */
 #define BIE_FULL 0u    /* -1/2 I + D + self term + N0 + pore completion (reading C5/C6) */
 #define BIE_D_ONLY 1u  /* PV trapezoid DLP sum + self term only (Gauss-identity pins) */
+#define BIE_ONE_SIDED 2u /* force the one-sided all-pairs kernel even where the symmetric
+                            (pair-reusing) kernel applies (A/B measurement; same result to rounding) */
 
 #define BIE_MAX_NVEC 16
 

@@ -233,9 +233,222 @@ __global__ void k_moments(const double2 *__restrict__ pos, const double2 *__rest
     }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric all-pairs path (nvec = 1, full rows).  Pair (i, j) and (j, i) share
+// r (up to sign), rho^2 and 1/rho^4.  With per-node quadratic forms
+//   Q_j = (nwx sx, nwx sy + nwy sx, nwy sy)   (nw = w n / pi, s = sigma)
+// (r.nw_j)(r.s_j) = Qxx rx^2 + Qxy rx ry + Qyy ry^2, so
+//   u_i += Q_j(r) r / rho^4      and      u_j -= Q_i(r) r / rho^4.
+// Each unordered pair is evaluated once: 22 FP64 instructions for both
+// directions (11 per directed pair vs 16).  Blocks of TB = 512 nodes; block A
+// pairs with every 32-node chunk after its end ("units"), handled by a
+// persistent grid over the triangular unit list.  Inside a warp the 32-source
+// chunk rotates through the lanes (__shfl) together with its accumulator, so
+// each source collects the contributions of the warp's 128 targets without a
+// reduction; the 4 warps' source sums are added in fixed order through shared
+// memory and stored as src_partial[A][j].  Target accumulators are flushed per
+// CTA segment (slot = CTA - first owner).  Pairs inside a block (A, A) are
+// done by k_dlp_diag with the one-sided kernel.  All sums have a fixed order.
+// ---------------------------------------------------------------------------
+constexpr int kSymR = 4;
+constexpr int kSymWarps = 4;
+constexpr int kSymTB = 32 * kSymR * kSymWarps;  // 512
+constexpr int kSymChunk = 32;
+
+__global__ void k_quad(const double2 *__restrict__ nw, const double *__restrict__ sigma, double4 *Q, int N) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const double2 a = nw[j];
+    const double2 b = reinterpret_cast<const double2 *>(sigma)[j];
+    Q[j] = make_double4(a.x * b.x, fma(a.x, b.y, a.y * b.x), a.y * b.y, 0.0);
+}
+
+struct SymArgs {
+    const double2 *pos;
+    const double4 *Q;
+    const long long *off;  // [nTB + 1] prefix of units per block
+    double *tgt_partial;   // [S][2N]
+    double *src_partial;   // [nTB][2N]
+    int N, nTB;
+    long long U;
+};
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+__global__ void __launch_bounds__(32 * kSymWarps) k_dlp_sym(SymArgs a) {
+    __shared__ double2 red[kSymWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int P = gridDim.x, p = blockIdx.x;
+    const long long U = a.U;
+    const long long u0 = ((long long)p * U) / P, u1 = ((long long)(p + 1) * U) / P;
+    if (u0 >= u1) return;
+    const int N = a.N;
+    // block containing u0: largest A with off[A] <= u0
+    int lo = 0, hi = a.nTB;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (a.off[mid] <= u0) lo = mid; else hi = mid;
+    }
+    int A = lo;
+    long long offA = a.off[A], offA1 = a.off[A + 1];
+
+    double tx[kSymR], ty[kSymR], tqa[kSymR], tqb[kSymR], tqc[kSymR], ax[kSymR], ay[kSymR];
+    auto load_targets = [&](int blk) {
+#pragma unroll
+        for (int r = 0; r < kSymR; ++r) {
+            const int i = blk * kSymTB + w * (32 * kSymR) + r * 32 + lane;
+            double2 x = make_double2(0.0, 0.0);
+            double4 q = make_double4(0.0, 0.0, 0.0, 0.0);
+            if (i < N) {
+                x = a.pos[i];
+                q = a.Q[i];
+            }
+            tx[r] = x.x;
+            ty[r] = x.y;
+            tqa[r] = q.x;
+            tqb[r] = q.y;
+            tqc[r] = q.z;
+            ax[r] = 0.0;
+            ay[r] = 0.0;
+        }
+    };
+    load_targets(A);
+    const int src_lane = (lane + 1) & 31;
+    for (long long u = u0; u < u1; ++u) {
+        const int c = (A + 1) * (kSymTB / kSymChunk) + (int)(u - offA);
+        const int j = c * kSymChunk + lane;
+        double sx = 0.0, sy = 0.0, sqa = 0.0, sqb = 0.0, sqc = 0.0, bx = 0.0, by = 0.0;
+        if (j < N) {
+            const double2 x = a.pos[j];
+            const double4 q = a.Q[j];
+            sx = x.x;
+            sy = x.y;
+            sqa = q.x;
+            sqb = q.y;
+            sqc = q.z;
+        }
+#pragma unroll 1
+        for (int t = 0; t < 32; ++t) {
+#pragma unroll
+            for (int r = 0; r < kSymR; ++r) {
+                const double rx = tx[r] - sx;
+                const double ry = ty[r] - sy;
+                const double rx2 = rx * rx;
+                const double rxy = rx * ry;
+                const double ry2 = fma(ry, ry, 1e-300);
+                const double rho2 = rx2 + ry2;
+                double inv = rcp_approx(rho2);
+                const double e = fma(-rho2, inv, 1.0);
+                inv = fma(inv, fma(e, e, e), inv);
+                const double inv2 = inv * inv;
+                const double cs = fma(sqa, rx2, fma(sqb, rxy, sqc * ry2)) * inv2;  // target <- source
+                const double ct = fma(tqa[r], rx2, fma(tqb[r], rxy, tqc[r] * ry2)) * inv2;  // source <- target
+                ax[r] = fma(cs, rx, ax[r]);
+                ay[r] = fma(cs, ry, ay[r]);
+                bx = fma(-ct, rx, bx);
+                by = fma(-ct, ry, by);
+            }
+            sx = shfl_d(sx, src_lane);
+            sy = shfl_d(sy, src_lane);
+            sqa = shfl_d(sqa, src_lane);
+            sqb = shfl_d(sqb, src_lane);
+            sqc = shfl_d(sqc, src_lane);
+            bx = shfl_d(bx, src_lane);
+            by = shfl_d(by, src_lane);
+        }
+        // after 32 rotations every source is back in its lane
+        red[w][lane] = make_double2(bx, by);
+        __syncthreads();
+        if (w == 0 && j < N) {
+            double2 s = red[0][lane];
+#pragma unroll
+            for (int q = 1; q < kSymWarps; ++q) {
+                s.x += red[q][lane].x;
+                s.y += red[q][lane].y;
+            }
+            reinterpret_cast<double2 *>(a.src_partial + (long long)A * 2LL * N)[j] = s;
+        }
+        __syncthreads();
+        if (u + 1 == u1 || u + 1 == offA1) {
+            const int slot = p - unit_owner(offA, U, P);
+#pragma unroll
+            for (int r = 0; r < kSymR; ++r) {
+                const int i = A * kSymTB + w * (32 * kSymR) + r * 32 + lane;
+                if (i < N)
+                    reinterpret_cast<double2 *>(a.tgt_partial + (long long)slot * 2LL * N)[i] =
+                        make_double2(ax[r], ay[r]);
+            }
+            if (u + 1 < u1) {
+                ++A;
+                offA = offA1;
+                offA1 = a.off[A + 1];
+                load_targets(A);
+            }
+        }
+    }
+}
+
+// Pairs inside one 512-node block (one-sided, all ordered pairs, self pair
+// zeroed by the rho^2 + 1e-300 rule).  One CTA per block, 128 threads x 4 targets.
+__global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ pos, const double2 *__restrict__ nw,
+                                                  const double *__restrict__ sigma, double *diag, int N) {
+    __shared__ double2 sp[3][kSymTB];
+    const int A = blockIdx.x, tid = threadIdx.x;
+    const int base = A * kSymTB;
+    for (int q = tid; q < kSymTB; q += 128) {
+        const int j = base + q;
+        const bool ok = j < N;
+        sp[0][q] = ok ? pos[j] : make_double2(0.0, 0.0);
+        sp[1][q] = ok ? nw[j] : make_double2(0.0, 0.0);
+        sp[2][q] = ok ? reinterpret_cast<const double2 *>(sigma)[j] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double tx[4], ty[4], ax[4], ay[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const double2 x = sp[0][r * 128 + tid];
+        tx[r] = x.x;
+        ty[r] = x.y;
+        ax[r] = 0.0;
+        ay[r] = 0.0;
+    }
+    const int nsrc = min(kSymTB, N - base);
+#pragma unroll 2
+    for (int jj = 0; jj < nsrc; ++jj) {
+        const double2 xj = sp[0][jj], nj = sp[1][jj], sj = sp[2][jj];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double rx = tx[r] - xj.x;
+            const double ry = ty[r] - xj.y;
+            const double rho2 = fma(rx, rx, fma(ry, ry, 1e-300));
+            const double rn = fma(rx, nj.x, ry * nj.y);
+            double inv = rcp_approx(rho2);
+            const double e = fma(-rho2, inv, 1.0);
+            inv = fma(inv, fma(e, e, e), inv);
+            const double c = ((rn * inv) * inv) * fma(rx, sj.x, ry * sj.y);
+            ax[r] = fma(c, rx, ax[r]);
+            ay[r] = fma(c, ry, ay[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int i = base + r * 128 + tid;
+        if (i < N) reinterpret_cast<double2 *>(diag)[i] = make_double2(ax[r], ay[r]);
+    }
+}
+
 struct Chunk {
     int v0, nv, TB, nTS, P;
     long long U;
+};
+struct SymEpi {
+    int on;                    // 1: partials come from the symmetric path (nvec = 1)
+    const double *tgt_partial; // [S][2N]
+    const double *src_partial; // [nTB][2N]
+    const double *diag;        // [2N]
+    const long long *off;      // [nTB + 1]
+    long long U;
+    int P;
 };
 struct EpiArgs {
     const double2 *pos, *nrm, *tan;
@@ -250,6 +463,7 @@ struct EpiArgs {
     unsigned flags;
     int nchunks;
     Chunk ch[5];
+    SymEpi sym;
 };
 
 // A4 + A5: reduce the split partials in fixed slot order, then add the local
@@ -264,6 +478,33 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
     const bool full = !(a.flags & BIE_D_ONLY);
     constexpr double k4pi = 1.0 / (4.0 * kPi);
     double2 u[BIE_MAX_NVEC];
+    if (a.sym.on) {
+        // fixed order: target-side slots, the in-block pairs, then source-side
+        // partials of every earlier block
+        const int B = i / kSymTB;
+        double2 acc = make_double2(0.0, 0.0);
+        const long long oB = a.sym.off[B], oB1 = a.sym.off[B + 1];
+        if (oB1 > oB) {
+            const int first = unit_owner(oB, a.sym.U, a.sym.P);
+            const int last = unit_owner(oB1 - 1, a.sym.U, a.sym.P);
+            for (int sl = 0; sl <= last - first; ++sl) {
+                const double2 pv = reinterpret_cast<const double2 *>(a.sym.tgt_partial + (long long)sl * 2LL * a.N)[i];
+                acc.x += pv.x;
+                acc.y += pv.y;
+            }
+        }
+        {
+            const double2 pv = reinterpret_cast<const double2 *>(a.sym.diag)[i];
+            acc.x += pv.x;
+            acc.y += pv.y;
+        }
+        for (int A = 0; A < B; ++A) {
+            const double2 pv = reinterpret_cast<const double2 *>(a.sym.src_partial + (long long)A * 2LL * a.N)[i];
+            acc.x += pv.x;
+            acc.y += pv.y;
+        }
+        u[0] = acc;
+    }
     for (int c = 0; c < a.nchunks; ++c) {
         const Chunk ch = a.ch[c];
         const int tb = it / ch.TB;
@@ -387,6 +628,51 @@ int build_schedules(Geometry *g) {
     return BIE_OK;
 }
 
+// Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only).
+// src_partial is [nTB][2N] doubles; above a 16 GiB cap the path is disabled and
+// the one-sided kernel is used instead.
+static int sym_prepare(Geometry *g) {
+    if (g->sym_state != 0) return BIE_OK;
+    const int N = g->N;
+    const int nTB = (N + kSymTB - 1) / kSymTB;
+    const long long nC = (N + kSymChunk - 1) / kSymChunk;
+    const size_t src_bytes = sizeof(double) * 2 * (size_t)N * nTB;
+    if (src_bytes > (16ull << 30)) {
+        g->sym_state = -1;
+        return BIE_OK;
+    }
+    std::vector<long long> off(nTB + 1, 0);
+    for (int A = 0; A < nTB; ++A) {
+        long long n = nC - (long long)(A + 1) * (kSymTB / kSymChunk);
+        off[A + 1] = off[A] + std::max(0LL, n);
+    }
+    const long long U = off[nTB];
+    int occ = 0;
+    BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dlp_sym, 32 * kSymWarps, 0));
+    const int P = (int)std::max<long long>(1, std::min<long long>((long long)g->num_sms * std::max(1, occ), U));
+    int S = 1;
+    for (int A = 0; A < nTB; ++A) {
+        if (off[A + 1] == off[A]) continue;
+        S = std::max(S, unit_owner(off[A + 1] - 1, U, P) - unit_owner(off[A], U, P) + 1);
+    }
+    g->sym_state = -1;  // stays -1 (one-sided fallback) if an allocation fails
+    if (cudaMalloc(&g->sym_Q, sizeof(double4) * (size_t)N) != cudaSuccess ||
+        cudaMalloc(&g->sym_off, sizeof(long long) * (size_t)(nTB + 1)) != cudaSuccess ||
+        cudaMalloc(&g->sym_tgt, sizeof(double) * 2 * (size_t)N * S) != cudaSuccess ||
+        cudaMalloc(&g->sym_src, src_bytes) != cudaSuccess ||
+        cudaMalloc(&g->sym_diag, sizeof(double) * 2 * (size_t)N) != cudaSuccess) {
+        (void)cudaGetLastError();  // clear the (non-sticky) allocation error
+        return BIE_OK;
+    }
+    BIE_CUDA_TRY(cudaMemcpy(g->sym_off, off.data(), sizeof(long long) * (size_t)(nTB + 1), cudaMemcpyHostToDevice));
+    g->sym_nTB = nTB;
+    g->sym_U = U;
+    g->sym_P = P;
+    g->sym_S = S;
+    g->sym_state = 1;
+    return BIE_OK;
+}
+
 static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStream_t st) {
     switch (vi) {
         case 0: k_dlp_pairs<1, 4, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
@@ -421,9 +707,26 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
                                             g->wall_lo, N, g->wall_len, g->moments);
         BIE_CUDA_TRY(cudaGetLastError());
     }
-    // decompose nvec into variant chunks (16, 8, 4, 2, 1)
     EpiArgs ea{};
-    int v = 0;
+    const bool sym = nvec == 1 && row_begin == 0 && row_end == N && !(flags & BIE_ONE_SIDED) &&
+                     sym_prepare(g) == BIE_OK && g->sym_state == 1;
+    if (sym) {
+        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+        count_launch();
+        if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
+        if (g->sym_U > 0) {
+            SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, g->sym_U};
+            k_dlp_sym<<<g->sym_P, 32 * kSymWarps, 0, st>>>(sa);
+            count_launch();
+        }
+        k_dlp_diag<<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+        count_launch();
+        BIE_CUDA_TRY(cudaGetLastError());
+        if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
+        ea.sym = SymEpi{1, g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, g->sym_U, g->sym_P};
+    }
+    // decompose nvec into variant chunks (16, 8, 4, 2, 1)
+    int v = sym ? nvec : 0;
     PairSched sch[5];
     int vis[5];
     int nch = 0;
@@ -452,7 +755,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         BIE_CUDA_TRY(cudaMalloc(&g->partial, need * sizeof(double)));
         g->partial_elems = need;
     }
-    if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
+    if (ev[1] && !sym) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
     for (int c = 0; c < nch; ++c) {
         PairArgs a;
         a.pos = g->pos;
@@ -471,7 +774,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
     }
-    if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
+    if (ev[2] && !sym) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
     ea.pos = g->pos;
     ea.nrm = g->nrm;
     ea.tan = g->tan;
@@ -516,11 +819,12 @@ static int check_apply_args(Geometry *g, const double *sigma, double *out, int n
         set_error(std::string(fn) + ": nvec must be in [1, 16]");
         return BIE_EINVAL;
     }
-    if (flags & ~BIE_D_ONLY) {
+    if (flags & ~(BIE_D_ONLY | BIE_ONE_SIDED)) {
         set_error(std::string(fn) + ": unknown flags");
         return BIE_EINVAL;
     }
     if ((const void *)sigma == (const void *)out) {
+        /* aliasing */
         set_error(std::string(fn) + ": out must not alias sigma");
         return BIE_EINVAL;
     }

@@ -102,6 +102,11 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     cudaFree(g->stage_in);
     cudaFree(g->stage_out);
     for (cudaEvent_t e : g->prof_ev) cudaEventDestroy(e);
+    cudaFree(g->sym_Q);
+    cudaFree(g->sym_off);
+    cudaFree(g->sym_tgt);
+    cudaFree(g->sym_src);
+    cudaFree(g->sym_diag);
     g->magic = 0;
     delete g;
     return BIE_OK;

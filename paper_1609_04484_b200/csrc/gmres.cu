@@ -198,6 +198,7 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     GmState s{};
     Dot d;
     double *pinned = nullptr;
+    cudaEvent_t evs[2] = {nullptr, nullptr};
     int rc = BIE_OK;
     d.nchunks = (int)((n + kChunk - 1) / kChunk);
     d.ldp = ldh;
@@ -214,6 +215,8 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
         cudaFree(s.scal);
         cudaFree(d.partial);
         cudaFreeHost(pinned);
+        if (evs[0]) cudaEventDestroy(evs[0]);
+        if (evs[1]) cudaEventDestroy(evs[1]);
     };
 #define GM_TRY(expr)                                       \
     do {                                                   \
@@ -243,7 +246,9 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     GM_TRY(cudaMalloc(&s.h2, sizeof(double) * ldh));
     GM_TRY(cudaMalloc(&s.scal, sizeof(double) * 8));
     GM_TRY(cudaMalloc(&d.partial, sizeof(double) * (size_t)d.nchunks * ldh));
-    GM_TRY(cudaMallocHost(&pinned, sizeof(double) * 8));
+    GM_TRY(cudaMallocHost(&pinned, sizeof(double) * 16));
+    GM_TRY(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
+    GM_TRY(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
     GM_TRY(cudaMemsetAsync(s.g, 0, sizeof(double) * ldh, st));
     GM_TRY(cudaMemsetAsync(s.H, 0, sizeof(double) * (size_t)ldh * max_iter, st));
 
@@ -289,8 +294,26 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 0, V, n);
     count_launch();
     GM_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    // One-iteration lookahead: iteration k is enqueued before the host reads the
+    // estimate of iteration k-1, so the device queue never drains on the
+    // per-iteration 16-byte D2H.  If k-1 converged, iteration k was speculative:
+    // it only touched H[:,k], g[k], g[k+1], cs/sn[k] and V[k+1], none of which the
+    // finish (columns 0..k-1) reads.
     int it = 0;
-    for (int k = 0; k < max_iter; ++k) {
+    bool done = false;
+    auto check = [&](int kk) -> int {  // read the estimate of iteration kk (its slot)
+        BIE_CUDA_TRY(cudaEventSynchronize(evs[kk & 1]));
+        const double est = pinned[8 + 2 * (kk & 1)];
+        const bool brk = pinned[9 + 2 * (kk & 1)] != 0.0;
+        hist_host[kk + 1] = est;
+        it = kk + 1;
+        if (est < tol || brk) {
+            *converged = 1;
+            done = true;
+        }
+        return BIE_OK;
+    };
+    for (int k = 0; k < max_iter && !done; ++k) {
         double *vk = V + (long long)k * n;
         GM_RC(apply_op(vk, w));
         GM_RC(norm_to(w, s.scal + 1));  // w0 = ||P^{-1} A v_k||
@@ -303,21 +326,16 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
         k_givens<<<1, 1, 0, st>>>(s, k, ldh);
         count_launch();
         GM_TRY(cudaGetLastError());
-        GM_TRY(cudaMemcpyAsync(pinned + 3, s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        GM_TRY(cudaMemcpyAsync(pinned + 8 + 2 * (k & 1), s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                               st));
+        GM_TRY(cudaEventRecord(evs[k & 1], st));
         if (k + 1 < max_iter) {
             k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, V + (long long)(k + 1) * n, n);
             count_launch();
         }
-        GM_TRY(cudaStreamSynchronize(st));
-        const double est = pinned[3];
-        const bool brk = pinned[4] != 0.0;
-        hist_host[k + 1] = est;
-        it = k + 1;
-        if (est < tol || brk) {
-            *converged = 1;
-            break;
-        }
+        if (k >= 1) GM_RC(check(k - 1));
     }
+    if (!done && it < max_iter) GM_RC(check(it));  // the last enqueued iteration
     *iters = it;
     // y = H^{-1} g, x = V y
     k_trisolve<<<1, 256, 0, st>>>(s.H, ldh, s.g, s.h, it);

@@ -59,6 +59,15 @@ struct Geometry {
     PairSched sched[5];         // nv = 1, 2, 4, 8, 16
     int occ[5] = {0, 0, 0, 0, 0};  // resident pair CTAs per SM per variant
     int num_sms = 0;
+    // symmetric nvec = 1 path (lazily allocated; see dlp.cu)
+    int sym_state = 0;            // 0 = not prepared, 1 = ready, -1 = unavailable (memory cap)
+    double4 *sym_Q = nullptr;     // [N] per-node quadratic forms
+    long long *sym_off = nullptr; // [nTB + 1] unit prefix per 512-node block
+    double *sym_tgt = nullptr;    // [S][2N]
+    double *sym_src = nullptr;    // [nTB][2N]
+    double *sym_diag = nullptr;   // [2N]
+    int sym_nTB = 0, sym_P = 0, sym_S = 0;
+    long long sym_U = 0;
     // profiling (bie_profile_begin/end): 4 events per recorded apply
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;

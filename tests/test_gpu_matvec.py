@@ -176,3 +176,25 @@ def test_apply_errors(bie):
         bie.dlp_apply(g, x, y, 1, flags=7)
     with pytest.raises(ValueError):
         bie.dlp_apply(g, x.float(), y, 1)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_symmetric_vs_one_sided(bie, cid):
+    """The pair-reusing nvec=1 kernel and the one-sided kernel agree to rounding."""
+    p = make_problem(cid)
+    g, _ = _setup(bie, p)
+    s = density(p, nvec=1, vec_id=4)
+    a = _gpu_apply(bie, g, s, 1, 0)
+    b = _gpu_apply(bie, g, s, 1, 2)  # BIE_ONE_SIDED
+    assert _relerr(a[0], b[0]) <= 1e-13
+
+
+def test_symmetric_ragged_sizes(bie):
+    """Block/chunk edges: N not a multiple of 512 or 32, tiny N (no off-block units)."""
+    for p in (make_pipe(31, 6.0, 262, 7, (0.1, 0.3), 0.05, 18),
+              make_circle_problem(16, 1.0, (), 64, 50, "c16"),
+              make_pipe(32, 12.0, 1000, 9, (0.1, 0.3), 0.05, 66)):
+        g, og = _setup(bie, p)
+        s = density(p, nvec=1)
+        y = _gpu_apply(bie, g, s, 1)
+        assert _relerr(y[0], og.apply(s)[0]) <= TOL, p.name

@@ -23,7 +23,7 @@ for cid in [int(c) for c in sys.argv[1:]] or [3, 4]:
     p = make_problem(cid)
     g = bie.Geometry.from_problem(p); g._p = p
     for nvec in (1, 4, 16):
-        for flags in (1, 0):
+        for flags in ((1, 0, 2) if nvec == 1 else (1, 0)):
             t = time_apply(g, nvec, flags, reps=3 if cid == 5 else 5)
             pairs = p.N * p.N * nvec
             print(json.dumps(dict(cfg=cid, N=p.N, nvec=nvec, flags=flags, ms=t*1e3, gpairs_s=pairs/t/1e9,
