@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -275,8 +276,10 @@ struct SymArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-__global__ void __launch_bounds__(32 * kSymWarps) k_dlp_sym(SymArgs a) {
-    __shared__ double2 red[kSymWarps][32];
+template <int SR, int SW>
+__global__ void __launch_bounds__(32 * SW) k_dlp_sym(SymArgs a) {
+    static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
+    __shared__ double2 red[SW][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int P = gridDim.x, p = blockIdx.x;
     const long long U = a.U;
@@ -292,11 +295,11 @@ __global__ void __launch_bounds__(32 * kSymWarps) k_dlp_sym(SymArgs a) {
     int A = lo;
     long long offA = a.off[A], offA1 = a.off[A + 1];
 
-    double tx[kSymR], ty[kSymR], tqa[kSymR], tqb[kSymR], tqc[kSymR], ax[kSymR], ay[kSymR];
+    double tx[SR], ty[SR], tqa[SR], tqb[SR], tqc[SR], ax[SR], ay[SR];
     auto load_targets = [&](int blk) {
 #pragma unroll
-        for (int r = 0; r < kSymR; ++r) {
-            const int i = blk * kSymTB + w * (32 * kSymR) + r * 32 + lane;
+        for (int r = 0; r < SR; ++r) {
+            const int i = blk * kSymTB + w * (32 * SR) + r * 32 + lane;
             double2 x = make_double2(0.0, 0.0);
             double4 q = make_double4(0.0, 0.0, 0.0, 0.0);
             if (i < N) {
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(32 * kSymWarps) k_dlp_sym(SymArgs a) {
 #pragma unroll 1
         for (int t = 0; t < 32; ++t) {
 #pragma unroll
-            for (int r = 0; r < kSymR; ++r) {
+            for (int r = 0; r < SR; ++r) {
                 const double rx = tx[r] - sx;
                 const double ry = ty[r] - sy;
                 const double rx2 = rx * rx;
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(32 * kSymWarps) k_dlp_sym(SymArgs a) {
         if (w == 0 && j < N) {
             double2 s = red[0][lane];
 #pragma unroll
-            for (int q = 1; q < kSymWarps; ++q) {
+            for (int q = 1; q < SW; ++q) {
                 s.x += red[q][lane].x;
                 s.y += red[q][lane].y;
             }
@@ -372,8 +375,8 @@ __global__ void __launch_bounds__(32 * kSymWarps) k_dlp_sym(SymArgs a) {
         if (u + 1 == u1 || u + 1 == offA1) {
             const int slot = p - unit_owner(offA, U, P);
 #pragma unroll
-            for (int r = 0; r < kSymR; ++r) {
-                const int i = A * kSymTB + w * (32 * kSymR) + r * 32 + lane;
+            for (int r = 0; r < SR; ++r) {
+                const int i = A * kSymTB + w * (32 * SR) + r * 32 + lane;
                 if (i < N)
                     reinterpret_cast<double2 *>(a.tgt_partial + (long long)slot * 2LL * N)[i] =
                         make_double2(ax[r], ay[r]);
@@ -628,6 +631,26 @@ int build_schedules(Geometry *g) {
     return BIE_OK;
 }
 
+// (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
+static const int kSymVar[4][2] = {{4, 4}, {2, 8}, {8, 2}, {1, 16}};
+static void *sym_kernel(int v) {
+    switch (v) {
+        case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
+        case 2: return reinterpret_cast<void *>(&k_dlp_sym<8, 2>);
+        case 3: return reinterpret_cast<void *>(&k_dlp_sym<1, 16>);
+        default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
+    }
+}
+static int sym_warps(int v) { return kSymVar[v][1]; }
+static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
+    switch (v) {
+        case 1: k_dlp_sym<2, 8><<<P, 256, 0, st>>>(sa); break;
+        case 2: k_dlp_sym<8, 2><<<P, 64, 0, st>>>(sa); break;
+        case 3: k_dlp_sym<1, 16><<<P, 512, 0, st>>>(sa); break;
+        default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
+    }
+}
+
 // Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only).
 // src_partial is [nTB][2N] doubles; above a 16 GiB cap the path is disabled and
 // the one-sided kernel is used instead.
@@ -637,6 +660,7 @@ static int sym_prepare(Geometry *g) {
     const int nTB = (N + kSymTB - 1) / kSymTB;
     const long long nC = (N + kSymChunk - 1) / kSymChunk;
     const size_t src_bytes = sizeof(double) * 2 * (size_t)N * nTB;
+    if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(3, atoi(e)));  // tuning knob
     if (src_bytes > (16ull << 30)) {
         g->sym_state = -1;
         return BIE_OK;
@@ -648,7 +672,7 @@ static int sym_prepare(Geometry *g) {
     }
     const long long U = off[nTB];
     int occ = 0;
-    BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dlp_sym, 32 * kSymWarps, 0));
+    BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel(g->sym_variant), 32 * sym_warps(g->sym_variant), 0));
     const int P = (int)std::max<long long>(1, std::min<long long>((long long)g->num_sms * std::max(1, occ), U));
     int S = 1;
     for (int A = 0; A < nTB; ++A) {
@@ -716,7 +740,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
         if (g->sym_U > 0) {
             SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, g->sym_U};
-            k_dlp_sym<<<g->sym_P, 32 * kSymWarps, 0, st>>>(sa);
+            launch_sym(g->sym_variant, g->sym_P, sa, st);
             count_launch();
         }
         k_dlp_diag<<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
