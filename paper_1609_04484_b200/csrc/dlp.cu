@@ -471,16 +471,20 @@ struct EpiArgs {
 
 // A4 + A5: reduce the split partials in fixed slot order, then add the local
 // terms and the completion field of every pore.
+// NVC > 0: nvec is the compile-time constant NVC (accumulators stay in
+// registers); NVC == 0: generic nvec.
+template <int NVC>
 __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (it >= a.Nt) return;
+    const int nvec = NVC > 0 ? NVC : a.nvec;
     const int i = a.row_begin + it;
     const double2 xi = a.pos[i];
     const double2 ti = a.tan[i];
     const double sc = a.selfc[i];
     const bool full = !(a.flags & BIE_D_ONLY);
     constexpr double k4pi = 1.0 / (4.0 * kPi);
-    double2 u[BIE_MAX_NVEC];
+    double2 u[NVC > 0 ? NVC : BIE_MAX_NVEC];
     if (a.sym.on) {
         // fixed order: target-side slots, the in-block pairs, then source-side
         // partials of every earlier block
@@ -513,18 +517,20 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         const int tb = it / ch.TB;
         const int first = unit_owner((long long)tb * ch.nTS, ch.U, ch.P);
         const int last = unit_owner((long long)(tb + 1) * ch.nTS - 1, ch.U, ch.P);
-        for (int v = ch.v0; v < ch.v0 + ch.nv; ++v) {
+        const int nv = NVC == 1 ? 1 : ch.nv;
+        for (int vv = 0; vv < nv; ++vv) {
+            const int v = NVC == 1 ? 0 : ch.v0 + vv;  // nvec == 1 -> a single chunk at v0 = 0
             double2 acc = make_double2(0.0, 0.0);
             for (int sl = 0; sl <= last - first; ++sl) {
                 const double2 pv = reinterpret_cast<const double2 *>(
-                    a.partial + ((long long)sl * a.nvec + v) * 2LL * a.Nt)[it];
+                    a.partial + ((long long)sl * nvec + v) * 2LL * a.Nt)[it];
                 acc.x += pv.x;
                 acc.y += pv.y;
             }
             u[v] = acc;
         }
     }
-    for (int v = 0; v < a.nvec; ++v) {
+    for (int v = 0; v < nvec; ++v) {
         const double2 si = reinterpret_cast<const double2 *>(a.sigma + (long long)v * a.sig_stride)[i];
         const double ts = sc * (ti.x * si.x + ti.y * si.y);
         u[v].x += ts * ti.x;
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             u[v].x += -0.5 * si.x;
             u[v].y += -0.5 * si.y;
             if (i >= a.wall_lo) {
-                const double nu = a.moments[(long long)a.nvec * a.M * 3 + v];
+                const double nu = a.moments[(long long)nvec * a.M * 3 + v];
                 const double2 ni = a.nrm[i];
                 u[v].x += nu * ni.x;
                 u[v].y += nu * ni.y;
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             const double ir = 1.0 / rho2;
             const double lg = 0.5 * log(rho2);
             const double rk = pk.z * ir;
-            for (int v = 0; v < a.nvec; ++v) {
+            for (int v = 0; v < nvec; ++v) {
                 const double *m = a.moments + ((long long)v * a.M + k) * 3;
                 const double lx = m[0], ly = m[1], mu = m[2];
                 const double rl = (rx * lx + ry * ly) * ir;
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             }
         }
     }
-    for (int v = 0; v < a.nvec; ++v)
+    for (int v = 0; v < nvec; ++v)
         reinterpret_cast<double2 *>(a.out + (long long)v * 2LL * a.Nt)[it] = u[v];
 }
 
@@ -817,7 +823,10 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     ea.Nt = Nt;
     ea.flags = flags;
     ea.nchunks = nch;
-    k_epilogue<<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    if (nvec == 1)
+        k_epilogue<1><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    else
+        k_epilogue<0><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));

@@ -178,6 +178,7 @@ def test_gmres_parity_nopc(bie, case):
     n = min([res["iters"]] + its) + 1
     hr = ref["hist"][:n]
     env = np.max([np.abs(r["hist"][:n] - hr) / hr for r in runs], axis=0)
+    env = np.maximum.accumulate(env)  # a chaotic divergence only grows
     big = hr > FLOOR
     rel = np.abs(res["hist"][:n] - hr) / hr
     assert np.all(rel[big] <= np.maximum(1e-10, 10 * env[big])), (rel.max(), env.max())
