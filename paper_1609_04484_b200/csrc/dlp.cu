@@ -330,35 +330,56 @@ __global__ void __launch_bounds__(32 * SW) k_dlp_sym(SymArgs a) {
             sqb = q.y;
             sqc = q.z;
         }
+        // Two pair chains are written stage by stage in lockstep (targets r, r+1)
+        // and the source accumulator is split in two, so ptxas keeps two
+        // independent dependency chains per warp in flight (a single chain per
+        // warp left the FP64 pipe idle on DFMA latency: 72% active).  The next
+        // source is fetched by __shfl at the start of the step.
+        double bx1 = 0.0, by1 = 0.0;
 #pragma unroll 1
         for (int t = 0; t < 32; ++t) {
+            const double nsx = shfl_d(sx, src_lane), nsy = shfl_d(sy, src_lane);
+            const double nqa = shfl_d(sqa, src_lane), nqb = shfl_d(sqb, src_lane), nqc = shfl_d(sqc, src_lane);
 #pragma unroll
-            for (int r = 0; r < SR; ++r) {
-                const double rx = tx[r] - sx;
-                const double ry = ty[r] - sy;
-                const double rx2 = rx * rx;
-                const double rxy = rx * ry;
-                const double ry2 = fma(ry, ry, 1e-300);
-                const double rho2 = rx2 + ry2;
-                double inv = rcp_approx(rho2);
-                const double e = fma(-rho2, inv, 1.0);
-                inv = fma(inv, fma(e, e, e), inv);
-                const double inv2 = inv * inv;
-                const double cs = fma(sqa, rx2, fma(sqb, rxy, sqc * ry2)) * inv2;  // target <- source
-                const double ct = fma(tqa[r], rx2, fma(tqb[r], rxy, tqc[r] * ry2)) * inv2;  // source <- target
-                ax[r] = fma(cs, rx, ax[r]);
-                ay[r] = fma(cs, ry, ay[r]);
-                bx = fma(-ct, rx, bx);
-                by = fma(-ct, ry, by);
+            for (int r = 0; r < SR; r += 2) {
+                const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
+                const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
+                const double xx0 = rx0 * rx0, xx1 = rx1 * rx1;
+                const double yy0 = fma(ry0, ry0, 1e-300), yy1 = fma(ry1, ry1, 1e-300);
+                const double xy0 = rx0 * ry0, xy1 = rx1 * ry1;
+                const double d0 = xx0 + yy0, d1 = xx1 + yy1;
+                double i0 = rcp_approx(d0), i1 = rcp_approx(d1);
+                const double cs0 = fma(sqa, xx0, fma(sqb, xy0, sqc * yy0));  // target <- source
+                const double cs1 = fma(sqa, xx1, fma(sqb, xy1, sqc * yy1));
+                const double ct0 = fma(tqa[r], xx0, fma(tqb[r], xy0, tqc[r] * yy0));  // source <- target
+                const double ct1 = fma(tqa[r + 1], xx1, fma(tqb[r + 1], xy1, tqc[r + 1] * yy1));
+                const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
+                i0 = fma(i0, fma(e0, e0, e0), i0);
+                i1 = fma(i1, fma(e1, e1, e1), i1);
+                const double q0 = i0 * i0, q1 = i1 * i1;
+                const double a0 = cs0 * q0, a1 = cs1 * q1;
+                const double b0 = ct0 * q0, b1 = ct1 * q1;
+                ax[r] = fma(a0, rx0, ax[r]);
+                ay[r] = fma(a0, ry0, ay[r]);
+                ax[r + 1] = fma(a1, rx1, ax[r + 1]);
+                ay[r + 1] = fma(a1, ry1, ay[r + 1]);
+                bx = fma(-b0, rx0, bx);
+                by = fma(-b0, ry0, by);
+                bx1 = fma(-b1, rx1, bx1);
+                by1 = fma(-b1, ry1, by1);
             }
-            sx = shfl_d(sx, src_lane);
-            sy = shfl_d(sy, src_lane);
-            sqa = shfl_d(sqa, src_lane);
-            sqb = shfl_d(sqb, src_lane);
-            sqc = shfl_d(sqc, src_lane);
+            sx = nsx;
+            sy = nsy;
+            sqa = nqa;
+            sqb = nqb;
+            sqc = nqc;
             bx = shfl_d(bx, src_lane);
             by = shfl_d(by, src_lane);
+            bx1 = shfl_d(bx1, src_lane);
+            by1 = shfl_d(by1, src_lane);
         }
+        bx += bx1;
+        by += by1;
         // after 32 rotations every source is back in its lane
         red[w][lane] = make_double2(bx, by);
         __syncthreads();
