@@ -659,12 +659,11 @@ int build_schedules(Geometry *g) {
 }
 
 // (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
-static const int kSymVar[4][2] = {{4, 4}, {2, 8}, {8, 2}, {1, 16}};
+static const int kSymVar[3][2] = {{4, 4}, {2, 8}, {8, 2}};  // R even (two interleaved chains)
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
         case 2: return reinterpret_cast<void *>(&k_dlp_sym<8, 2>);
-        case 3: return reinterpret_cast<void *>(&k_dlp_sym<1, 16>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -673,7 +672,6 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
         case 1: k_dlp_sym<2, 8><<<P, 256, 0, st>>>(sa); break;
         case 2: k_dlp_sym<8, 2><<<P, 64, 0, st>>>(sa); break;
-        case 3: k_dlp_sym<1, 16><<<P, 512, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
@@ -687,7 +685,7 @@ static int sym_prepare(Geometry *g) {
     const int nTB = (N + kSymTB - 1) / kSymTB;
     const long long nC = (N + kSymChunk - 1) / kSymChunk;
     const size_t src_bytes = sizeof(double) * 2 * (size_t)N * nTB;
-    if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(3, atoi(e)));  // tuning knob
+    if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(2, atoi(e)));  // tuning knob
     if (src_bytes > (16ull << 30)) {
         g->sym_state = -1;
         return BIE_OK;

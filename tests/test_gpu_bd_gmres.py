@@ -239,4 +239,10 @@ def test_gmres_golden(bie, name):
     x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
     res = bie.gmres_solve(c["g"], c["bd"] if gd["pc"] == "bd" else None, _t(f), x, tol=gd["tol"],
                           max_iter=gd["max_iter"])
-    _cmp_gmres(res, gd)
+    assert res["iters"] == gd["iters"] and res["converged"] == gd["converged"]
+    hr = np.asarray(gd["hist"])
+    env = np.maximum.accumulate(np.asarray(gd.get("envelope", np.zeros(hr.size))))
+    rel = np.abs(np.asarray(res["hist"]) - hr) / hr
+    # 1e-10 bar, relaxed only where the oracle's own history moves more under
+    # 1e-13 perturbations of f (reading C23)
+    assert np.all(rel <= np.maximum(1e-10, 10 * env)), (rel.max(), env.max())

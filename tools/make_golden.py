@@ -13,7 +13,7 @@ from bie_inputs import make_problem, rhs_pipe
 
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
 CASES = {
-    "config3_bd_pipe": dict(config=3, pc="bd", tol=1e-8, max_iter=1000),
+    "config3_bd_pipe": dict(config=3, pc="bd", tol=1e-8, max_iter=1000, env_runs=2),
     "config4_none_pipe_prefix": dict(config=4, pc="none", tol=1e-8, max_iter=6),
 }
 for name in (sys.argv[1:] or list(CASES)):
@@ -25,8 +25,19 @@ for name in (sys.argv[1:] or list(CASES)):
     t1 = time.time()
     r = oracle.gmres(g, f, bd, tol=c["tol"], max_iter=c["max_iter"])
     t2 = time.time()
+    # self-sensitivity envelope (reading C23): the oracle's own history
+    # under 1e-13 relative perturbations of f, at the GPU/oracle matvec agreement level
+    env = np.zeros(len(r["hist"]))
+    env_iters = []
+    for s in range(c.get("env_runs", 0)):
+        rng = np.random.default_rng(300 + s)
+        rp = oracle.gmres(g, f * (1 + 1e-13 * rng.standard_normal(f.size)), bd, tol=c["tol"], max_iter=c["max_iter"])
+        n = min(len(r["hist"]), len(rp["hist"]))
+        env[:n] = np.maximum(env[:n], np.abs(rp["hist"][:n] - r["hist"][:n]) / r["hist"][:n])
+        env_iters.append(rp["iters"])
     rec = dict(name=name, **c, f_norm=float(np.linalg.norm(f)), iters=r["iters"], converged=r["converged"],
                hist=[float(h) for h in r["hist"]], res_pc=r["res_pc"], res_true=r["res_true"],
+               envelope=[float(e) for e in env], envelope_iters=env_iters, envelope_eps=1e-13,
                oracle_build_s=t1 - t0, oracle_gmres_s=t2 - t1,
                source="oracle/bie_oracle.c via tools/make_golden.py; inputs bie_inputs seeded config",
                omp_threads=os.environ.get("OMP_NUM_THREADS", str(os.cpu_count())))
