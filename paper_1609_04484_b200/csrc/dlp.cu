@@ -279,7 +279,10 @@ __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync
 template <int SR, int SW>
 __global__ void __launch_bounds__(32 * SW) k_dlp_sym(SymArgs a) {
     static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
+    static_assert(SR % 2 == 0, "two interleaved chains");
     __shared__ double2 red[SW][32];
+    __shared__ double2 s_xy[SW][32], s_ab[SW][32];
+    __shared__ double s_c[SW][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int P = gridDim.x, p = blockIdx.x;
     const long long U = a.U;
@@ -336,10 +339,24 @@ __global__ void __launch_bounds__(32 * SW) k_dlp_sym(SymArgs a) {
         // warp left the FP64 pipe idle on DFMA latency: 72% active).  The next
         // source is fetched by __shfl at the start of the step.
         double bx1 = 0.0, by1 = 0.0;
+        // the chunk's sources sit in this warp's shared-memory slice; at step t
+        // lane l reads source (l + t) mod 32 (conflict-free), so the source data
+        // carry no loop dependency -- only the accumulators rotate by __shfl
+        s_xy[w][lane] = make_double2(sx, sy);
+        s_ab[w][lane] = make_double2(sqa, sqb);
+        s_c[w][lane] = sqc;
+        __syncwarp();
 #pragma unroll 1
         for (int t = 0; t < 32; ++t) {
-            const double nsx = shfl_d(sx, src_lane), nsy = shfl_d(sy, src_lane);
-            const double nqa = shfl_d(sqa, src_lane), nqb = shfl_d(sqb, src_lane), nqc = shfl_d(sqc, src_lane);
+            {
+                const int sl = (lane + t) & 31;
+                const double2 xy = s_xy[w][sl], ab = s_ab[w][sl];
+                sx = xy.x;
+                sy = xy.y;
+                sqa = ab.x;
+                sqb = ab.y;
+                sqc = s_c[w][sl];
+            }
 #pragma unroll
             for (int r = 0; r < SR; r += 2) {
                 const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
@@ -368,11 +385,6 @@ __global__ void __launch_bounds__(32 * SW) k_dlp_sym(SymArgs a) {
                 bx1 = fma(-b1, rx1, bx1);
                 by1 = fma(-b1, ry1, by1);
             }
-            sx = nsx;
-            sy = nsy;
-            sqa = nqa;
-            sqb = nqb;
-            sqc = nqc;
             bx = shfl_d(bx, src_lane);
             by = shfl_d(by, src_lane);
             bx1 = shfl_d(bx1, src_lane);
