@@ -119,17 +119,20 @@ __global__ void __launch_bounds__(1024) k_panel(BDView v, BDScratch s, int k0, i
     const int m = blockIdx.x;
     const int n2 = v.n2;
     const double *M = v.mat + (long long)m * v.mstride;
-    double *W = s.W + (long long)m * n2 * NB;  // W[r][c], r = row index (global), c < NB
+    // W column-major: W[c * n2 + r] (coalesced over rows r)
+    double *W = s.W + (long long)m * n2 * NB;
+#define WI(r, c) ((long long)(c) * n2 + (r))
     int *piv = s.piv + (long long)m * n2;
     __shared__ double red_v[32];
     __shared__ int red_i[32];
     __shared__ int s_p;
     __shared__ double s_d;
+    __shared__ double s_row[NB];
     __shared__ double L11[NB][NB + 1], U11[NB][NB + 1];
     const int tid = threadIdx.x, nt = blockDim.x;
     for (long long q = tid; q < (long long)(n2 - k0) * nbe; q += nt) {
         int r = k0 + (int)(q / nbe), c = (int)(q % nbe);
-        W[(long long)r * NB + c] = M[(long long)r * n2 + k0 + c];
+        W[WI(r, c)] = M[(long long)r * n2 + k0 + c];
     }
     __syncthreads();
     for (int c = 0; c < nbe; ++c) {
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(1024) k_panel(BDView v, BDScratch s, int k0, i
         double best = -1.0;
         int bi = n2;
         for (int r = k + tid; r < n2; r += nt) {
-            double a = fabs(W[(long long)r * NB + c]);
+            double a = fabs(W[WI(r, c)]);
             if (a > best) { best = a; bi = r; }
         }
         // warp argmax (lowest index on ties)
@@ -168,34 +171,35 @@ __global__ void __launch_bounds__(1024) k_panel(BDView v, BDScratch s, int k0, i
         }
         __syncthreads();
         const int p = s_p;
-        if (p != k && tid < nbe) {
-            double t = W[(long long)k * NB + tid];
-            W[(long long)k * NB + tid] = W[(long long)p * NB + tid];
-            W[(long long)p * NB + tid] = t;
+        if (tid < nbe) {
+            double t = W[WI(k, tid)];
+            if (p != k) {
+                double o = W[WI(p, tid)];
+                W[WI(k, tid)] = o;
+                W[WI(p, tid)] = t;
+                t = o;
+            }
+            s_row[tid] = t;  // pivot row after the swap
         }
         __syncthreads();
         if (tid == 0) {
-            double d = W[(long long)k * NB + c];
+            double d = s_row[c];
             s_d = (d != 0.0) ? d : 1.0;
         }
         __syncthreads();
         const double d = s_d;
-        // L column and trailing panel update (rows > k)
-        for (long long q = tid; q < (long long)(n2 - k - 1) * (nbe - c); q += nt) {
-            int r = k + 1 + (int)(q / (nbe - c));
-            int cc = c + (int)(q % (nbe - c));
-            if (cc == c) continue;
-            double l = W[(long long)r * NB + c] / d;
-            W[(long long)r * NB + cc] -= l * W[(long long)k * NB + cc];
+        // L column and trailing panel update, one thread per row below k
+        for (int r = k + 1 + tid; r < n2; r += nt) {
+            const double l = W[WI(r, c)] / d;
+            W[WI(r, c)] = l;
+            for (int cc = c + 1; cc < nbe; ++cc) W[WI(r, cc)] -= l * s_row[cc];
         }
-        __syncthreads();
-        for (int r = k + 1 + tid; r < n2; r += nt) W[(long long)r * NB + c] /= d;
         __syncthreads();
     }
     // A11 = L11 U11 (rows k0..k0+nbe); A11^{-1} by solving A11 X = I (column per thread)
     for (int q = tid; q < nbe * nbe; q += nt) {
         int r = q / nbe, c = q % nbe;
-        double val = W[(long long)(k0 + r) * NB + c];
+        double val = W[WI(k0 + r, c)];
         L11[r][c] = (c < r) ? val : (c == r ? 1.0 : 0.0);
         U11[r][c] = (c >= r) ? val : 0.0;
     }
@@ -217,6 +221,7 @@ __global__ void __launch_bounds__(1024) k_panel(BDView v, BDScratch s, int k0, i
         double *Ai = s.A11i + (long long)m * NB * NB;
         for (int r = 0; r < nbe; ++r) Ai[r * NB + col] = z[r];
     }
+#undef WI
 }
 
 // Apply the panel's row swaps to all columns of M (sequential in k, parallel over columns).
