@@ -37,6 +37,15 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 
+def _ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "round1", "k_dlp_sym_traffic.json")))[
+            "traffic_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -316,10 +325,12 @@ def run_gpu(args):
                    "N": N, "unknowns": 2 * N, "gmres_iters_per_step": GMRES_ITERS,
                    "matvecs_per_step": GMRES_ITERS + 1, "parallelism": f"replicas{ws}" if ws > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write); BD inverses (2.67 GB) exceed L2 each step"},
-        "roofline": {"kernel": "k_dlp_pairs<1,4,256>", "bound": "alu", "achieved": achieved_tflops,
+        "roofline": {"kernel": "all-pairs phase: k_dlp_sym<8,2> + k_dlp_diag (nvec=1 symmetric path)",
+                     "bound": "alu", "achieved": achieved_tflops,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
-                     "traffic": None, "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
+                     "traffic": _ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
                      "kernel_share_of_step": pairs_share,
+                     "executed_flop_per_pair": 17,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
         "e2e": {"value": ws * args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
                 "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8)},

@@ -508,8 +508,9 @@ struct EpiArgs {
 // registers); NVC == 0: generic nvec.
 template <int NVC>
 __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= a.Nt) return;
+    const int it_raw = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = it_raw < a.Nt;  // inactive threads still join the block barriers
+    const int it = active ? it_raw : a.Nt - 1;
     const int nvec = NVC > 0 ? NVC : a.nvec;
     const int i = a.row_begin + it;
     const double2 xi = a.pos[i];
@@ -579,7 +580,36 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             }
         }
     }
-    if (full) {
+    if (full && NVC == 1) {
+        // nvec = 1: pore records (c, r, lambda, mu) staged through shared memory
+        // in tiles of 128 (warp-broadcast reads); 1/rho^2 by seed + cubic Newton.
+        __shared__ double4 s_pc[128];  // (cx, cy, r, -)
+        __shared__ double4 s_pm[128];  // (lambda_x, lambda_y, mu, -)
+        for (int k0 = 0; k0 < a.M; k0 += 128) {
+            const int nk = min(128, a.M - k0);
+            __syncthreads();
+            if ((int)threadIdx.x < nk) {
+                const int k = k0 + threadIdx.x;
+                s_pc[threadIdx.x] = a.pore[k];
+                const double *m = a.moments + (long long)k * 3;
+                s_pm[threadIdx.x] = make_double4(m[0], m[1], m[2], 0.0);
+            }
+            __syncthreads();
+            for (int q = 0; q < nk; ++q) {
+                const double4 pk = s_pc[q], pm = s_pm[q];
+                const double rx = xi.x - pk.x, ry = xi.y - pk.y;
+                const double rho2 = fma(rx, rx, ry * ry);
+                double ir = rcp_approx(rho2);
+                const double e = fma(-rho2, ir, 1.0);
+                ir = fma(ir, fma(e, e, e), ir);
+                const double lg = 0.5 * log(rho2);
+                const double rk = pk.z * ir;
+                const double rl = (rx * pm.x + ry * pm.y) * ir;
+                u[0].x += k4pi * (-lg * pm.x + rx * rl) + rk * ry * pm.z;
+                u[0].y += k4pi * (-lg * pm.y + ry * rl) - rk * rx * pm.z;
+            }
+        }
+    } else if (full) {
         for (int k = 0; k < a.M; ++k) {
             const double4 pk = a.pore[k];
             const double rx = xi.x - pk.x, ry = xi.y - pk.y;
@@ -596,6 +626,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             }
         }
     }
+    if (!active) return;
     for (int v = 0; v < nvec; ++v)
         reinterpret_cast<double2 *>(a.out + (long long)v * 2LL * a.Nt)[it] = u[v];
 }
