@@ -276,8 +276,8 @@ struct SymArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int SR, int SW>
-__global__ void __launch_bounds__(32 * SW) k_dlp_sym(SymArgs a) {
+template <int SR, int SW, int MINB = 1>
+__global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
     static_assert(SR % 2 == 0, "two interleaved chains");
     __shared__ double2 red[SW][32];
@@ -702,11 +702,16 @@ int build_schedules(Geometry *g) {
 }
 
 // (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
-static const int kSymVar[3][2] = {{4, 4}, {2, 8}, {8, 2}};  // R even (two interleaved chains)
+// variants 3..5 add a minimum-blocks launch bound (register cap -> more warps)
+static const int kNumSymVar = 6;
+static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
         case 2: return reinterpret_cast<void *>(&k_dlp_sym<8, 2>);
+        case 3: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5>);
+        case 4: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 6>);
+        case 5: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -715,12 +720,16 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
         case 1: k_dlp_sym<2, 8><<<P, 256, 0, st>>>(sa); break;
         case 2: k_dlp_sym<8, 2><<<P, 64, 0, st>>>(sa); break;
+        case 3: k_dlp_sym<8, 2, 5><<<P, 64, 0, st>>>(sa); break;
+        case 4: k_dlp_sym<8, 2, 6><<<P, 64, 0, st>>>(sa); break;
+        case 5: k_dlp_sym<4, 4, 3><<<P, 128, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
 
 // Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only).
-// src_partial is [nTB][2N] doubles; above a 16 GiB cap the path is disabled and
+// src_partial is [nTB][2N] doubles; above a 48 GiB cap (or without 8 GiB of
+// free headroom) the path is disabled and
 // the one-sided kernel is used instead.
 static int sym_prepare(Geometry *g) {
     if (g->sym_state != 0) return BIE_OK;
@@ -728,10 +737,15 @@ static int sym_prepare(Geometry *g) {
     const int nTB = (N + kSymTB - 1) / kSymTB;
     const long long nC = (N + kSymChunk - 1) / kSymChunk;
     const size_t src_bytes = sizeof(double) * 2 * (size_t)N * nTB;
-    if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(2, atoi(e)));  // tuning knob
-    if (src_bytes > (16ull << 30)) {
-        g->sym_state = -1;
-        return BIE_OK;
+    if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(kNumSymVar - 1, atoi(e)));  // tuning knob
+    {
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        // cap: 48 GiB and leave 8 GiB of headroom (config 5 needs 35 GB)
+        if (src_bytes > (48ull << 30) || src_bytes + (8ull << 30) > free_b) {
+            g->sym_state = -1;
+            return BIE_OK;
+        }
     }
     std::vector<long long> off(nTB + 1, 0);
     for (int A = 0; A < nTB; ++A) {
