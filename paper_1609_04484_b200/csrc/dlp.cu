@@ -281,8 +281,7 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
     static_assert(SR % 2 == 0, "two interleaved chains");
     __shared__ double2 red[SW][32];
-    __shared__ double2 s_xy[SW][32], s_ab[SW][32];
-    __shared__ double s_c[SW][32];
+    __shared__ __align__(16) double2 s_src[2][SW][3][32];  // [buf][warp][(x,y) | (qa,qb) | (qc,-)][lane]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int P = gridDim.x, p = blockIdx.x;
     const long long U = a.U;
@@ -320,42 +319,52 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     };
     load_targets(A);
     const int src_lane = (lane + 1) & 31;
+    // The chunk's sources sit in this warp's shared-memory slice (double
+    // buffered; the next unit's chunk is fetched by cp.async while this one is
+    // computed).  At step t lane l reads source (l + t) mod 32 (conflict-free),
+    // so the source data carry no loop dependency -- only the accumulators
+    // rotate by __shfl.
+    auto fetch = [&](int buf, int blk, long long uoff) {  // chunk of unit uoff within block blk
+        const int cc = (blk + 1) * (kSymTB / kSymChunk) + (int)uoff;
+        const int jj = cc * kSymChunk + lane;
+        const bool ok = jj < N;
+        const double2 *q2 = reinterpret_cast<const double2 *>(a.Q + (ok ? jj : 0));
+        cp_async16(&s_src[buf][w][0][lane], a.pos + (ok ? jj : 0), ok ? 16 : 0);
+        cp_async16(&s_src[buf][w][1][lane], q2, ok ? 16 : 0);
+        cp_async16(&s_src[buf][w][2][lane], q2 + 1, ok ? 16 : 0);
+        cp_async_commit();
+    };
+    fetch(0, A, u0 - offA);
     for (long long u = u0; u < u1; ++u) {
+        const int buf = (int)((u - u0) & 1);
         const int c = (A + 1) * (kSymTB / kSymChunk) + (int)(u - offA);
         const int j = c * kSymChunk + lane;
-        double sx = 0.0, sy = 0.0, sqa = 0.0, sqb = 0.0, sqc = 0.0, bx = 0.0, by = 0.0;
-        if (j < N) {
-            const double2 x = a.pos[j];
-            const double4 q = a.Q[j];
-            sx = x.x;
-            sy = x.y;
-            sqa = q.x;
-            sqb = q.y;
-            sqc = q.z;
+        if (u + 1 < u1) {
+            if (u + 1 == offA1)
+                fetch(buf ^ 1, A + 1, 0);
+            else
+                fetch(buf ^ 1, A, u + 1 - offA);
+        } else {
+            cp_async_commit();
         }
+        cp_async_wait<1>();
+        __syncwarp();
+        double sx, sy, sqa, sqb, sqc, bx = 0.0, by = 0.0;
         // Two pair chains are written stage by stage in lockstep (targets r, r+1)
         // and the source accumulator is split in two, so ptxas keeps two
         // independent dependency chains per warp in flight (a single chain per
-        // warp left the FP64 pipe idle on DFMA latency: 72% active).  The next
-        // source is fetched by __shfl at the start of the step.
+        // warp left the FP64 pipe idle on DFMA latency: 72% active).
         double bx1 = 0.0, by1 = 0.0;
-        // the chunk's sources sit in this warp's shared-memory slice; at step t
-        // lane l reads source (l + t) mod 32 (conflict-free), so the source data
-        // carry no loop dependency -- only the accumulators rotate by __shfl
-        s_xy[w][lane] = make_double2(sx, sy);
-        s_ab[w][lane] = make_double2(sqa, sqb);
-        s_c[w][lane] = sqc;
-        __syncwarp();
 #pragma unroll 1
         for (int t = 0; t < 32; ++t) {
             {
                 const int sl = (lane + t) & 31;
-                const double2 xy = s_xy[w][sl], ab = s_ab[w][sl];
+                const double2 xy = s_src[buf][w][0][sl], ab = s_src[buf][w][1][sl];
                 sx = xy.x;
                 sy = xy.y;
                 sqa = ab.x;
                 sqb = ab.y;
-                sqc = s_c[w][sl];
+                sqc = s_src[buf][w][2][sl].x;
             }
 #pragma unroll
             for (int r = 0; r < SR; r += 2) {

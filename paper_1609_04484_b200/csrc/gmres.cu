@@ -24,31 +24,31 @@ namespace bie {
 constexpr int kChunk = 4096;      // elements of the 2N dimension per multidot CTA
 constexpr int kDotThreads = 256;
 
-// partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv)
+// partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv).
+// Grid (chunks, ceil(nv / 8)); each of the 8 warps owns one basis vector j and
+// reduces the whole 4096-element chunk (fixed lane order -> deterministic).
 __global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restrict__ V, long long ldv, int nv,
                                                           const double *__restrict__ w, long long n,
                                                           double *partial, int ldp) {
     __shared__ double ws[kChunk];
-    __shared__ double red[kDotThreads / 32];
     const long long e0 = (long long)blockIdx.x * kChunk;
     const int len = (int)std::min<long long>(kChunk, n - e0);
     for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j = 0; j < nv; ++j) {
-        const double *vj = V + (long long)j * ldv + e0;
-        double acc = 0.0;
-        for (int q = threadIdx.x; q < len; q += kDotThreads) acc = fma(vj[q], ws[q], acc);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) red[wid] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int q = 0; q < kDotThreads / 32; ++q) t += red[q];
-            partial[(long long)blockIdx.x * ldp + j] = t;
-        }
-        __syncthreads();
+    const int j = blockIdx.y * (kDotThreads / 32) + wid;
+    if (j >= nv) return;
+    const double *vj = V + (long long)j * ldv + e0;
+    double acc0 = 0.0, acc1 = 0.0;
+    int q = lane;
+    for (; q + 32 < len; q += 64) {
+        acc0 = fma(vj[q], ws[q], acc0);
+        acc1 = fma(vj[q + 32], ws[q + 32], acc1);
     }
+    if (q < len) acc0 = fma(vj[q], ws[q], acc0);
+    double acc = acc0 + acc1;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) partial[(long long)blockIdx.x * ldp + j] = acc;
 }
 
 // out[j] = (accumulate ? out[j] : 0) + sum_c partial[c * ldp + j]  (fixed order)
@@ -157,7 +157,8 @@ struct Dot {
 // out[0..nv) = V[0..nv)^T w (deterministic)
 static int multidot(const double *V, long long ldv, int nv, const double *w, long long n, Dot &d, double *out,
                     cudaStream_t st) {
-    k_multidot<<<d.nchunks, kDotThreads, 0, st>>>(V, ldv, nv, w, n, d.partial, d.ldp);
+    k_multidot<<<dim3(d.nchunks, (nv + kDotThreads / 32 - 1) / (kDotThreads / 32)), kDotThreads, 0, st>>>(
+        V, ldv, nv, w, n, d.partial, d.ldp);
     k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, out, 0);
     count_launch(2);
     BIE_CUDA_TRY(cudaGetLastError());
