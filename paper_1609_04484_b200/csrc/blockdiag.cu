@@ -16,6 +16,7 @@
 // After the last panel, columns are unpermuted (A^{-1} = M P).  Batched over
 // all blocks of one size class (pores share one size; Gamma_0 is its own class).
 // Apply: one warp per row of the explicit inverses (HBM-bound batched GEMV).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,6 +24,8 @@
 #include <vector>
 
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace bie {
 
@@ -224,6 +227,214 @@ __global__ void __launch_bounds__(1024) k_panel(BDView v, BDScratch s, int k0, i
 #undef WI
 }
 
+// Shared helper: A11^{-1} (nbe x nbe) from the LU'd pivot rows A (row-major,
+// stride NB: strict lower = L (unit diagonal), upper = U), one thread per column.
+__device__ void a11_inverse(const double *A, int nbe, double *Ai) {
+    const int col = threadIdx.x;
+    if (col >= nbe) return;
+    double z[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+        if (r < nbe) {
+            double acc = (r == col) ? 1.0 : 0.0;
+            for (int q = 0; q < r; ++q) acc -= A[r * NB + q] * z[q];
+            z[r] = acc;
+        }
+    }
+#pragma unroll
+    for (int r = NB - 1; r >= 0; --r) {
+        if (r < nbe) {
+            double acc = z[r];
+            for (int q = r + 1; q < nbe; ++q) acc -= A[r * NB + q] * z[q];
+            z[r] = acc / A[r * NB + r];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r)
+        if (r < nbe) Ai[r * NB + col] = z[r];
+}
+
+// Small matrices (rows n2 - k0 <= kSmemPanelRows): the panel LU runs entirely in
+// shared memory (column-major, rows k0..n2-1), one CTA per matrix.
+constexpr int kSmemPanelRows = 768;
+__global__ void __launch_bounds__(256) k_panel_smem(BDView v, BDScratch s, int k0, int nbe) {
+    extern __shared__ double Ws[];  // [NB][R]
+    __shared__ double red_v[8];
+    __shared__ int red_i[8];
+    __shared__ int s_p;
+    __shared__ double s_row[NB];
+    __shared__ double s_A[NB * NB];
+    const int m = blockIdx.x;
+    const int n2 = v.n2;
+    const int R = n2 - k0;
+    const double *M = v.mat + (long long)m * v.mstride;
+    int *piv = s.piv + (long long)m * n2;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int q = tid; q < R * nbe; q += nt) {
+        const int r = q / nbe, c = q % nbe;
+        Ws[c * R + r] = M[(long long)(k0 + r) * n2 + k0 + c];
+    }
+    __syncthreads();
+    for (int c = 0; c < nbe; ++c) {
+        double best = -1.0;
+        int bi = R;
+        for (int r = c + tid; r < R; r += nt) {
+            const double a = fabs(Ws[c * R + r]);
+            if (a > best) { best = a; bi = r; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_down_sync(0xffffffffu, best, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+            best = red_v[0];
+            bi = red_i[0];
+            for (int q = 1; q < nt / 32; ++q)
+                if (red_v[q] > best || (red_v[q] == best && red_i[q] < bi)) { best = red_v[q]; bi = red_i[q]; }
+            if (!(best > 0.0) || bi >= R) {
+                s.flag[m] = 1;
+                bi = c;
+            }
+            s_p = bi;
+            piv[k0 + c] = k0 + bi;
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (tid < nbe) {
+            double t = Ws[tid * R + c];
+            if (p != c) {
+                const double o = Ws[tid * R + p];
+                Ws[tid * R + c] = o;
+                Ws[tid * R + p] = t;
+                t = o;
+            }
+            s_row[tid] = t;
+        }
+        __syncthreads();
+        const double d = s_row[c] != 0.0 ? s_row[c] : 1.0;
+        for (int r = c + 1 + tid; r < R; r += nt) {
+            const double l = Ws[c * R + r] / d;
+            Ws[c * R + r] = l;
+            for (int cc = c + 1; cc < nbe; ++cc) Ws[cc * R + r] -= l * s_row[cc];
+        }
+        __syncthreads();
+    }
+    for (int q = tid; q < nbe * nbe; q += nt) s_A[(q / nbe) * NB + (q % nbe)] = Ws[(q % nbe) * R + q / nbe];
+    __syncthreads();
+    a11_inverse(s_A, nbe, s.A11i + (long long)m * NB * NB);
+}
+
+// Large matrix: cooperative panel LU over G CTAs of 128 threads; thread owns one
+// panel row in registers.  Per column: local argmax -> grid sync -> global pivot,
+// pivot/displaced rows exchanged through global buffers -> grid sync -> elimination.
+struct CoopScratch {
+    double *cand_v;  // [G]
+    int *cand_i;     // [G]
+    double *pbuf;    // [NB] new pivot row
+    double *kbuf;    // [NB] displaced row k
+    double *A;       // [NB][NB] LU'd pivot rows
+};
+__global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopScratch cs, int k0, int nbe) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red_v[4];
+    __shared__ int red_i[4];
+    __shared__ int s_p;
+    const int n2 = v.n2;
+    const double *M = v.mat;  // one matrix per class launch
+    const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+    const int r = k0 + g * 128 + tid;  // this thread's panel row
+    const bool own = r < n2;
+    double w[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) w[c] = (own && c < nbe) ? M[(long long)r * n2 + k0 + c] : 0.0;
+#pragma unroll 1
+    for (int c = 0; c < nbe; ++c) {
+        const int k = k0 + c;
+        double wc = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+            if (q == c) wc = w[q];
+        double best = (own && r >= k) ? fabs(wc) : -1.0;
+        int bi = (own && r >= k) ? r : n2;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_down_sync(0xffffffffu, best, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+            best = red_v[0];
+            bi = red_i[0];
+            for (int q = 1; q < 4; ++q)
+                if (red_v[q] > best || (red_v[q] == best && red_i[q] < bi)) { best = red_v[q]; bi = red_i[q]; }
+            cs.cand_v[g] = best;
+            cs.cand_i[g] = bi;
+        }
+        grid.sync();
+        if (tid == 0) {
+            best = -1.0;
+            bi = n2;
+            for (int q = 0; q < G; ++q) {
+                const double cv = cs.cand_v[q];
+                const int ci = cs.cand_i[q];
+                if (cv > best || (cv == best && ci < bi)) { best = cv; bi = ci; }
+            }
+            if (!(best > 0.0) || bi >= n2) {
+                if (g == 0) s.flag[0] = 1;
+                bi = k;
+            }
+            s_p = bi;
+            if (g == 0) s.piv[k] = bi;
+        }
+        __syncthreads();
+        const int p = s_p;
+        if (own && r == p) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) cs.pbuf[q] = w[q];
+        }
+        if (own && r == k) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) cs.kbuf[q] = w[q];
+        }
+        grid.sync();
+        if (own && r == k) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) w[q] = cs.pbuf[q];
+        } else if (own && r == p) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) w[q] = cs.kbuf[q];
+        }
+        if (own && r > k) {
+            double pr[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) pr[q] = cs.pbuf[q];
+            double dd = 1.0;
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+                if (q == c) dd = pr[q];
+            if (dd == 0.0) dd = 1.0;
+            double l = 0.0;
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+                if (q == c) { l = w[q] / dd; w[q] = l; }
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+                if (q > c && q < nbe) w[q] -= l * pr[q];
+        }
+        // the next column's pbuf/kbuf writes happen only after its first grid.sync
+    }
+    if (own && r < k0 + nbe) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) cs.A[(r - k0) * NB + q] = w[q];
+    }
+    grid.sync();
+    if (g == 0) a11_inverse(cs.A, nbe, s.A11i);
+}
+
 // Apply the panel's row swaps to all columns of M (sequential in k, parallel over columns).
 __global__ void k_swap(BDView v, BDScratch s, int k0, int nbe) {
     const int m = blockIdx.y;
@@ -341,6 +552,78 @@ __global__ void __launch_bounds__(256) k_update(BDView v, BDScratch s, int k0, i
     }
 }
 
+// The sweep, v2: 128x128 output tile per CTA, 256 threads, 8x8 outputs per
+// thread (rows tr + 16a, columns 2tc + 32b + {0,1}); T staged transposed and G
+// row-wise in shared memory (12 shared loads per 64 DFMA per panel column).
+constexpr int UT2 = 128;
+constexpr int UT2P = UT2 + 2;  // padding keeps double2 alignment and spreads banks
+__global__ void __launch_bounds__(256) k_update2(BDView v, BDScratch s, int k0, int nbe) {
+    extern __shared__ double sm2[];
+    double *Ts = sm2;              // [NB][UT2P]  Ts[c][i] = T[i0 + i][c]
+    double *Gs = sm2 + NB * UT2P;  // [NB][UT2P]  Gs[c][j] = G[c][j0 + j]
+    const int m = blockIdx.z;
+    const int n2 = v.n2;
+    const int i0 = blockIdx.y * UT2, j0 = blockIdx.x * UT2;
+    const double *T = s.T + (long long)m * n2 * NB;
+    const double *G = s.G + (long long)m * NB * n2;
+    double *M = v.mat + (long long)m * v.mstride;
+    const int tid = threadIdx.x;
+    for (int q = tid; q < UT2 * NB; q += 256) {
+        const int i = q / NB, c = q % NB;
+        Ts[c * UT2P + i] = (i0 + i < n2) ? T[(long long)(i0 + i) * NB + c] : 0.0;
+    }
+    for (int q = tid; q < NB * UT2; q += 256) {
+        const int c = q / UT2, j = q % UT2;
+        Gs[c * UT2P + j] = (j0 + j < n2) ? G[(long long)c * n2 + j0 + j] : 0.0;
+    }
+    __syncthreads();
+    const int tr = tid >> 4, tc = tid & 15;
+    double acc[8][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < NB; ++c) {
+        double ta[8], gb[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) ta[a] = Ts[c * UT2P + tr + 16 * a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double2 g2 = *reinterpret_cast<const double2 *>(&Gs[c * UT2P + 2 * tc + 32 * b]);
+            gb[2 * b] = g2.x;
+            gb[2 * b + 1] = g2.y;
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = fma(ta[a], gb[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int gi = i0 + tr + 16 * a;
+        if (gi >= n2) continue;
+        const bool rowK = gi >= k0 && gi < k0 + nbe;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int jj = 2 * tc + 32 * b;
+            const int gj = j0 + jj;
+            if (gj >= n2) continue;  // n2 even, gj even -> gj + 1 < n2 too
+            double2 *dst = reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj);
+            double2 o;
+            if (rowK) {
+                o = *reinterpret_cast<const double2 *>(&Gs[(gi - k0) * UT2P + jj]);
+            } else {
+                double2 base = *dst;
+                if (gj >= k0 && gj < k0 + nbe) base.x = 0.0;
+                if (gj + 1 >= k0 && gj + 1 < k0 + nbe) base.y = 0.0;
+                o = make_double2(base.x - acc[a][2 * b], base.y - acc[a][2 * b + 1]);
+            }
+            *dst = o;
+        }
+    }
+}
+
 // Column unpermutation: A^{-1}[:, q[r]] = M[:, r], q = row order after all swaps.
 __global__ void k_perm(BDView v, BDScratch s) {
     const int m = blockIdx.x;
@@ -431,16 +714,55 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
     }
-    int panel_threads = n2 >= 1024 ? 1024 : (n2 >= 256 ? 256 : 128);
+    // panel strategy: shared-memory panel (one CTA per matrix) while the panel fits,
+    // cooperative multi-CTA panel for the single large block (Gamma_0 of configs 2-5)
+    const bool coop = n2 > kSmemPanelRows && v.count == 1;
+    CoopScratch cs{};
+    if (coop) {
+        const int Gmax = (n2 + 127) / 128;
+        int per_sm = 0, dev = 0, coop_ok = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
+        BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_panel_coop, 128, 0));
+        if (!coop_ok || (long long)per_sm * g->num_sms < Gmax) {
+            set_error("bie_blockdiag_factor: cooperative launch unavailable for the panel factorisation");
+            return BIE_ECUDA;
+        }
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.cand_v, sizeof(double) * Gmax, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.cand_i, sizeof(int) * Gmax, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.pbuf, sizeof(double) * NB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.kbuf, sizeof(double) * NB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.A, sizeof(double) * NB * NB, st));
+    }
+    const size_t upd_smem = sizeof(double) * 2 * NB * UT2P;
+    BIE_CUDA_TRY(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
+    BIE_CUDA_TRY(cudaFuncSetAttribute(k_panel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(double) * NB * kSmemPanelRows)));
     for (int k0 = 0; k0 < n2; k0 += NB) {
         int nbe = std::min(NB, n2 - k0);
-        k_panel<<<v.count, panel_threads, 0, st>>>(v, s, k0, nbe);
+        if (coop) {
+            int G = (n2 - k0 + 127) / 128;
+            void *args[] = {&v, &s, &cs, &k0, &nbe};
+            BIE_CUDA_TRY(cudaLaunchCooperativeKernel((void *)k_panel_coop, G, 128, args, 0, st));
+        } else if (n2 - k0 <= kSmemPanelRows) {
+            k_panel_smem<<<v.count, 256, sizeof(double) * NB * (n2 - k0), st>>>(v, s, k0, nbe);
+        } else {
+            int panel_threads = n2 >= 1024 ? 1024 : 256;
+            k_panel<<<v.count, panel_threads, 0, st>>>(v, s, k0, nbe);
+        }
         k_swap<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
         k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), v.count), 256, 0, st>>>(v, s, k0, nbe);
         k_make_G<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
-        k_update<<<dim3((n2 + UT - 1) / UT, (n2 + UT - 1) / UT, v.count), 256, 0, st>>>(v, s, k0, nbe);
+        k_update2<<<dim3((n2 + UT2 - 1) / UT2, (n2 + UT2 - 1) / UT2, v.count), 256, upd_smem, st>>>(v, s, k0, nbe);
         count_launch(5);
         BIE_CUDA_TRY(cudaGetLastError());
+    }
+    if (coop) {
+        cudaFreeAsync(cs.cand_v, st);
+        cudaFreeAsync(cs.cand_i, st);
+        cudaFreeAsync(cs.pbuf, st);
+        cudaFreeAsync(cs.kbuf, st);
+        cudaFreeAsync(cs.A, st);
     }
     k_perm<<<v.count, 32, 0, st>>>(v, s);
     size_t rowbytes = sizeof(double) * (size_t)n2;
