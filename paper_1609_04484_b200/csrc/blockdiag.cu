@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -624,6 +625,83 @@ __global__ void __launch_bounds__(256) k_update2(BDView v, BDScratch s, int k0, 
     }
 }
 
+// The sweep, v3, on the FP64 tensor cores: out = base - T G is a rank-32 dense
+// update, i.e. a GEMM with K = 32, computed with mma.sync.m8n8k4.f64 (DMMA).
+// CTA tile 64x64, 4 warps in 2x2, each warp 32x32 = 4x4 DMMA tiles; T (64x32)
+// and G (32x64) staged in shared memory; fragments:
+//   A (8x4, row): lane t holds A[t>>2][t&3];  B (4x8, col): lane t holds B[t&3][t>>2];
+//   C (8x8): lane t holds C[t>>2][2(t&3)], C[t>>2][2(t&3)+1].
+__device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+constexpr int UT3 = 64;
+__global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, int nbe) {
+    __shared__ double Ts[UT3][NB + 1];  // Ts[i][c] = T[i0 + i][c]
+    __shared__ double Gs[NB][UT3 + 1];  // Gs[c][j] = G[c][j0 + j]
+    const int m = blockIdx.z;
+    const int n2 = v.n2;
+    const int i0 = blockIdx.y * UT3, j0 = blockIdx.x * UT3;
+    const double *T = s.T + (long long)m * n2 * NB;
+    const double *G = s.G + (long long)m * NB * n2;
+    double *M = v.mat + (long long)m * v.mstride;
+    const int tid = threadIdx.x;
+    for (int q = tid; q < UT3 * NB; q += 128) {
+        const int i = q / NB, c = q % NB;
+        Ts[i][c] = (i0 + i < n2) ? T[(long long)(i0 + i) * NB + c] : 0.0;
+    }
+    for (int q = tid; q < NB * UT3; q += 128) {
+        const int c = q / UT3, j = q % UT3;
+        Gs[c][j] = (j0 + j < n2) ? G[(long long)c * n2 + j0 + j] : 0.0;
+    }
+    __syncthreads();
+    const int lane = tid & 31, wid = tid >> 5;
+    const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
+    const int gr = lane >> 2, gq = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NB / 4; ++kk) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = Ts[wr + 8 * i + gr][kk * 4 + gq];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Gs[kk * 4 + gq][wc + 8 * j + gr];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int li = wr + 8 * i + gr;
+        const int gi = i0 + li;
+        if (gi >= n2) continue;
+        const bool rowK = gi >= k0 && gi < k0 + nbe;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int lj = wc + 8 * j + 2 * gq;
+            const int gj = j0 + lj;
+            if (gj >= n2) continue;  // n2 even, gj even
+            double2 *dst = reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj);
+            double2 o;
+            if (rowK) {
+                o = make_double2(Gs[gi - k0][lj], Gs[gi - k0][lj + 1]);
+            } else {
+                double2 base = *dst;
+                if (gj >= k0 && gj < k0 + nbe) base.x = 0.0;
+                if (gj + 1 >= k0 && gj + 1 < k0 + nbe) base.y = 0.0;
+                o = make_double2(base.x - acc[i][j][0], base.y - acc[i][j][1]);
+            }
+            *dst = o;
+        }
+    }
+}
+
 // Column unpermutation: A^{-1}[:, q[r]] = M[:, r], q = row order after all swaps.
 __global__ void k_perm(BDView v, BDScratch s) {
     const int m = blockIdx.x;
@@ -735,6 +813,9 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         BIE_CUDA_TRY(cudaMallocAsync(&cs.A, sizeof(double) * NB * NB, st));
     }
     const size_t upd_smem = sizeof(double) * 2 * NB * UT2P;
+    // sweep kernel: 0 = DMMA tensor-core tiles (default), 1 = 64x64 DFMA, 2 = 128x128 DFMA (tuning knob)
+    int upd_variant = 0;
+    if (const char *e = getenv("BIE_BD_UPDATE")) upd_variant = std::max(0, std::min(2, atoi(e)));
     BIE_CUDA_TRY(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
     BIE_CUDA_TRY(cudaFuncSetAttribute(k_panel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(double) * NB * kSmemPanelRows)));
@@ -753,7 +834,13 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         k_swap<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
         k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), v.count), 256, 0, st>>>(v, s, k0, nbe);
         k_make_G<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
-        k_update2<<<dim3((n2 + UT2 - 1) / UT2, (n2 + UT2 - 1) / UT2, v.count), 256, upd_smem, st>>>(v, s, k0, nbe);
+        if (upd_variant == 2)
+            k_update2<<<dim3((n2 + UT2 - 1) / UT2, (n2 + UT2 - 1) / UT2, v.count), 256, upd_smem, st>>>(v, s, k0,
+                                                                                                       nbe);
+        else if (upd_variant == 1)
+            k_update<<<dim3((n2 + UT - 1) / UT, (n2 + UT - 1) / UT, v.count), 256, 0, st>>>(v, s, k0, nbe);
+        else
+            k_update3<<<dim3((n2 + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3, v.count), 128, 0, st>>>(v, s, k0, nbe);
         count_launch(5);
         BIE_CUDA_TRY(cudaGetLastError());
     }
