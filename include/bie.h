@@ -116,6 +116,20 @@ BIE_API int bie_dlp_apply_host(bie_geometry_t g, const double *sigma_host, doubl
                        void *stream);
 
 /*
+ * bie_field_eval -- SURVEY s8(f) NEXT-2: off-surface velocity from a density,
+ *   u(x) = sum_j (w_j/pi)(r.n_j)(r.sigma_j) r / rho^4                 (P:l.243-246 kernel,
+ *        + sum_k Stokeslet(x-c_k) lambda_k + r_k rotlet(x-c_k) mu_k     trapezoid rule P:l.346-354,
+ *   r = x - x_j                                                         completion C5)
+ * i.e. the representation whose boundary limit bie_dlp_apply discretises (no
+ * jump, no self term, no N0).  Spectrally accurate for d(x, Gamma) > sqrt(ds)
+ * (P:l.356-358 footnote); no near-field correction (C18).
+ * sigma : device [2N];  targets : device [ntgt][2];  out : device [ntgt][2].
+ * Async on stream.  Errors: BIE_EINVAL (null, ntgt < 0, out aliasing sigma), BIE_ECUDA.
+ */
+BIE_API int bie_field_eval(bie_geometry_t g, const double *sigma, const double *targets, int ntgt, double *out,
+                           void *stream);
+
+/*
  * bie_blockdiag_factor -- A6: block-diagonal preconditioner, P:l.651-657
  * ("diagonal blocks corresponding to the self-interactions of the individual
  * pores and the outer boundary ... assembled, factorized, and inverted

@@ -18,6 +18,7 @@ from ._bie import (  # noqa: F401
     dlp_apply,
     dlp_apply_host,
     dlp_apply_rows,
+    field_eval,
     gmres_solve,
     launch_count,
     profile_begin,

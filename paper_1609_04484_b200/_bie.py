@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "bie_dlp_apply", "bie_dlp_apply_rows", "bie_dlp_apply_host",
     "bie_blockdiag_factor", "bie_blockdiag_apply", "bie_blockdiag_destroy", "bie_blockdiag_block_inverse",
     "bie_gmres_solve", "bie_last_error", "bie_profile_begin", "bie_profile_end", "bie_launch_count",
+    "bie_field_eval",
 )
 
 
@@ -66,6 +67,7 @@ def lib():
         "bie_blockdiag_destroy": [vp],
         "bie_blockdiag_block_inverse": [vp, c_int, dp, ctypes.c_longlong],
         "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
+        "bie_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_profile_begin": [vp],
         "bie_profile_end": [vp, dp, dp, dp, ip],
     }
@@ -174,6 +176,14 @@ def dlp_apply(g: Geometry, sigma, out, nvec: int = 1, flags: int = BIE_FULL, str
     n = nvec * 2 * g.N
     _check(lib().bie_dlp_apply(g.h, _dev_ptr(sigma, "sigma", n), _dev_ptr(out, "out", n), nvec, flags,
                                _stream_ptr(stream)))
+    return out
+
+
+def field_eval(g: Geometry, sigma, targets, out, stream=None):
+    """Off-surface velocity u(x) at targets [P,2] from density sigma [2N] (bie_field_eval)."""
+    ntgt = targets.numel() // 2
+    _check(lib().bie_field_eval(g.h, _dev_ptr(sigma, "sigma", 2 * g.N), _dev_ptr(targets, "targets", 2 * ntgt),
+                                ntgt, _dev_ptr(out, "out", 2 * ntgt), _stream_ptr(stream)))
     return out
 
 

@@ -50,7 +50,8 @@ __host__ __device__ __forceinline__ int unit_owner(long long u, long long U, int
 }
 
 struct PairArgs {
-    const double2 *pos;   // [N] source (and target) positions
+    const double2 *tpos;  // [Nt] target positions (pos + row_begin, or off-surface points)
+    const double2 *pos;   // [N] source positions
     const double2 *nw;    // [N] w n / pi
     const double *sigma;  // first vector of this chunk; vector v at sigma + v * sig_stride
     long long sig_stride; // 2N
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
         for (int r = 0; r < R; ++r) {
             int it = tb * TB + r * NT + tid;
             double2 x = make_double2(0.0, 0.0);
-            if (it < a.Nt) x = a.pos[a.row_begin + it];
+            if (it < a.Nt) x = a.tpos[it];
             tx[r] = x.x;
             ty[r] = x.y;
 #pragma unroll
@@ -873,6 +874,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     if (ev[1] && !sym) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
     for (int c = 0; c < nch; ++c) {
         PairArgs a;
+        a.tpos = g->pos + row_begin;
         a.pos = g->pos;
         a.nw = g->nw;
         a.sigma = sigma + (long long)ea.ch[c].v0 * stride;
@@ -915,6 +917,89 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));
+    return BIE_OK;
+}
+
+// NEXT-2 field evaluation epilogue: fixed-order slot sum + completion field.
+__global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restrict__ tgt, const double *partial,
+                                                        int Nt, Chunk ch, const double4 *__restrict__ pore,
+                                                        const double *__restrict__ moments, int M, double *out) {
+    __shared__ double4 s_pc[128], s_pm[128];
+    const int it_raw = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = it_raw < Nt;
+    const int it = active ? it_raw : Nt - 1;
+    const double2 xi = tgt[it];
+    const int tb = it / ch.TB;
+    const int first = unit_owner((long long)tb * ch.nTS, ch.U, ch.P);
+    const int last = unit_owner((long long)(tb + 1) * ch.nTS - 1, ch.U, ch.P);
+    double2 u = make_double2(0.0, 0.0);
+    for (int sl = 0; sl <= last - first; ++sl) {
+        const double2 pv = reinterpret_cast<const double2 *>(partial + (long long)sl * 2LL * Nt)[it];
+        u.x += pv.x;
+        u.y += pv.y;
+    }
+    constexpr double k4pi = 1.0 / (4.0 * kPi);
+    for (int k0 = 0; k0 < M; k0 += 128) {
+        const int nk = min(128, M - k0);
+        __syncthreads();
+        if ((int)threadIdx.x < nk) {
+            const int k = k0 + threadIdx.x;
+            s_pc[threadIdx.x] = pore[k];
+            s_pm[threadIdx.x] = make_double4(moments[3 * k], moments[3 * k + 1], moments[3 * k + 2], 0.0);
+        }
+        __syncthreads();
+        for (int q = 0; q < nk; ++q) {
+            const double4 pk = s_pc[q], pm = s_pm[q];
+            const double rx = xi.x - pk.x, ry = xi.y - pk.y;
+            const double rho2 = fma(rx, rx, ry * ry);
+            const double ir = 1.0 / rho2;
+            const double lg = 0.5 * log(rho2);
+            const double rk = pk.z * ir;
+            const double rl = (rx * pm.x + ry * pm.y) * ir;
+            u.x += k4pi * (-lg * pm.x + rx * rl) + rk * ry * pm.z;
+            u.y += k4pi * (-lg * pm.y + ry * rl) - rk * rx * pm.z;
+        }
+    }
+    if (active) reinterpret_cast<double2 *>(out)[it] = u;
+}
+
+int field_eval_impl(Geometry *g, const double *sigma, const double2 *targets, int ntgt, double *out, cudaStream_t st) {
+    if (ntgt == 0) return BIE_OK;
+    const int N = g->N;
+    k_moments<<<g->M + 1, 256, 0, st>>>(g->pos, g->nrm, g->w, g->pore, sigma, 2LL * N, 1, g->M, g->n_pore,
+                                        g->wall_lo, N, g->wall_len, g->moments);
+    count_launch();
+    PairSched s;
+    make_sched(g, 0, ntgt, s);
+    const size_t need = (size_t)s.S * 2 * (size_t)ntgt;
+    if (need > g->partial_elems) {
+        BIE_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaFree(g->partial);
+        g->partial = nullptr;
+        g->partial_elems = 0;
+        BIE_CUDA_TRY(cudaMalloc(&g->partial, need * sizeof(double)));
+        g->partial_elems = need;
+    }
+    PairArgs a;
+    a.tpos = targets;
+    a.pos = g->pos;
+    a.nw = g->nw;
+    a.sigma = sigma;
+    a.sig_stride = 2LL * N;
+    a.partial = g->partial;
+    a.nvec_total = 1;
+    a.v0 = 0;
+    a.N = N;
+    a.row_begin = 0;
+    a.Nt = ntgt;
+    a.nTS = s.nTS;
+    a.U = s.U;
+    launch_pairs(0, s, a, st);
+    count_launch();
+    k_field_epilogue<<<(ntgt + 127) / 128, 128, 0, st>>>(targets, g->partial, ntgt, Chunk{0, 1, s.TB, s.nTS, s.P, s.U},
+                                                         g->pore, g->moments, g->M, out);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
 }
 
@@ -966,6 +1051,16 @@ int bie_dlp_apply_rows(bie_geometry_t gh, const double *sigma, double *out, int 
         return BIE_EINVAL;
     }
     return dlp_apply_impl(g, sigma, out, nvec, flags, row_begin, row_end, (cudaStream_t)stream);
+}
+
+int bie_field_eval(bie_geometry_t gh, const double *sigma, const double *targets, int ntgt, double *out,
+                   void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !sigma || (ntgt > 0 && (!targets || !out)) || ntgt < 0 || (const void *)out == (const void *)sigma) {
+        set_error("bie_field_eval: invalid handle, null pointer, ntgt < 0 or out aliasing sigma");
+        return BIE_EINVAL;
+    }
+    return field_eval_impl(g, sigma, reinterpret_cast<const double2 *>(targets), ntgt, out, (cudaStream_t)stream);
 }
 
 int bie_dlp_apply_host(bie_geometry_t gh, const double *sigma_host, double *out_host, int nvec, unsigned flags,
