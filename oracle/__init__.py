@@ -68,6 +68,15 @@ def lib():
         L.ora_bd_free.argtypes = [ctypes.c_void_p]
         L.ora_gmres_dense.restype = ctypes.c_int
         L.ora_gmres_dense.argtypes = [ctypes.c_int, dp, dp, dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
+        L.ora_bdlu_factor.restype = ctypes.c_void_p
+        L.ora_bdlu_factor.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp, ip]
+        L.ora_bdlu_apply.restype = None
+        L.ora_bdlu_apply.argtypes = [ctypes.c_void_p, dp, dp]
+        L.ora_bdlu_free.restype = None
+        L.ora_bdlu_free.argtypes = [ctypes.c_void_p]
+        L.ora_gmres_bdlu.restype = ctypes.c_int
+        L.ora_gmres_bdlu.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp,
+                                     ctypes.c_void_p, dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
         L.ora_gmres.restype = ctypes.c_int
         L.ora_gmres.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp,
                                 ctypes.c_void_p, dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
@@ -184,6 +193,42 @@ class OracleBD:
         if getattr(self, "h", None):
             lib().ora_bd_free(self.h)
             self.h = None
+
+
+class OracleBDLU:
+    """The BD preconditioner in LU form (forward/back substitution per apply) --
+    the same operator as OracleBD without forming explicit inverses."""
+
+    def __init__(self, geom: OracleGeometry):
+        bad = ctypes.c_int(0)
+        self.geom = geom
+        self.h = lib().ora_bdlu_factor(*geom._geo(), ctypes.byref(bad))
+        if not self.h:
+            raise MemoryError("oracle BD-LU allocation failed")
+        if bad.value:
+            lib().ora_bdlu_free(self.h)
+            self.h = None
+            raise np.linalg.LinAlgError(f"singular BD block for body {bad.value - 1}")
+
+    def apply(self, v):
+        v = _c(v)
+        out = np.zeros_like(v)
+        lib().ora_bdlu_apply(self.h, _d(v), _d(out))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ora_bdlu_free(self.h)
+            self.h = None
+
+
+def gmres_bdlu(geom: OracleGeometry, f, bdlu: OracleBDLU, tol=1e-8, max_iter=1000):
+    x = np.zeros(2 * geom.N)
+    hist, rp, rt, conv = _gmres_out(max_iter)
+    it = lib().ora_gmres_bdlu(*geom._geo(), bdlu.h, _d(_c(f)), _d(x), tol, max_iter, _d(hist), ctypes.byref(rp),
+                              ctypes.byref(rt), ctypes.byref(conv))
+    return dict(x=x, iters=it, hist=hist[: it + 1].copy(), res_pc=rp.value, res_true=rt.value,
+                converged=bool(conv.value))
 
 
 def lu(A):

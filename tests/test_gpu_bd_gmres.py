@@ -223,9 +223,10 @@ def test_gmres_deterministic(bie):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_none_pipe_prefix"])
+@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_none_pipe_prefix", "config4_bd_pipe_prefix"])
 def test_gmres_golden(bie, name):
-    """Large configs: histories produced by tools/make_golden.py (oracle only)."""
+    """Large configs: histories produced by tools/make_golden.py (oracle only;
+    config 4's BD uses the oracle's LU-solve form of the same operator)."""
     import torch
 
     path = os.path.join(GOLDEN, f"gmres_{name}.json")
@@ -233,12 +234,12 @@ def test_gmres_golden(bie, name):
         pytest.skip(f"golden {path} not generated")
     gd = json.load(open(path))
     p = make_problem(gd["config"])
-    c = _setup(bie, p, with_bd=gd["pc"] == "bd")
+    use_bd = gd["pc"] in ("bd", "bdlu")
+    c = _setup(bie, p, with_bd=use_bd)
     f = rhs_pipe(p)
     assert abs(np.linalg.norm(f) - gd["f_norm"]) < 1e-12 * gd["f_norm"]
     x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
-    res = bie.gmres_solve(c["g"], c["bd"] if gd["pc"] == "bd" else None, _t(f), x, tol=gd["tol"],
-                          max_iter=gd["max_iter"])
+    res = bie.gmres_solve(c["g"], c["bd"] if use_bd else None, _t(f), x, tol=gd["tol"], max_iter=gd["max_iter"])
     assert res["iters"] == gd["iters"] and res["converged"] == gd["converged"]
     hr = np.asarray(gd["hist"])
     env = np.maximum.accumulate(np.asarray(gd.get("envelope", np.zeros(hr.size))))

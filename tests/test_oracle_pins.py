@@ -405,3 +405,17 @@ def test_V10_pore_block_universality(g2, bd2):
     C = np.linalg.inv(np.eye(2) - alpha * E.T @ Ai @ E)
     Bbi = Ai + alpha * Ai @ E @ C @ E.T @ Ai
     assert np.abs(Bbi - bd2.block_inverse(b)).max() < 1e-12
+
+
+def test_bd_lu_form_equals_explicit_inverse(g2, bd2):
+    """The LU-solve form of the BD preconditioner (used for config 4's golden
+    history) is the same operator as the explicit inverses."""
+    bdlu = oracle.OracleBDLU(g2)
+    v = density(g2.problem, vec_id=7)[0]
+    a, b = bd2.apply(v), bdlu.apply(v)
+    assert np.abs(a - b).max() / np.abs(a).max() < 1e-13
+    f = rhs_pipe(g2.problem)
+    r1 = oracle.gmres(g2, f, bd2, tol=1e-8, max_iter=200)
+    r2 = oracle.gmres_bdlu(g2, f, bdlu, tol=1e-8, max_iter=200)
+    assert r1["iters"] == r2["iters"]
+    assert (np.abs(r1["hist"] - r2["hist"]) / r1["hist"]).max() < 1e-10

@@ -15,15 +15,21 @@ OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 CASES = {
     "config3_bd_pipe": dict(config=3, pc="bd", tol=1e-8, max_iter=1000, env_runs=2),
     "config4_none_pipe_prefix": dict(config=4, pc="none", tol=1e-8, max_iter=6),
+    "config4_bd_pipe_prefix": dict(config=4, pc="bdlu", tol=1e-8, max_iter=8),
 }
 for name in (sys.argv[1:] or list(CASES)):
     c = CASES[name]
     p = make_problem(c["config"]); g = oracle.OracleGeometry(p)
     f = rhs_pipe(p)
     t0 = time.time()
-    bd = oracle.OracleBD(g) if c["pc"] == "bd" else None
-    t1 = time.time()
-    r = oracle.gmres(g, f, bd, tol=c["tol"], max_iter=c["max_iter"])
+    if c["pc"] == "bdlu":  # LU-solve form of the same BD operator (wall block too large to invert in plain C)
+        bd = oracle.OracleBDLU(g)
+        t1 = time.time()
+        r = oracle.gmres_bdlu(g, f, bd, tol=c["tol"], max_iter=c["max_iter"])
+    else:
+        bd = oracle.OracleBD(g) if c["pc"] == "bd" else None
+        t1 = time.time()
+        r = oracle.gmres(g, f, bd, tol=c["tol"], max_iter=c["max_iter"])
     t2 = time.time()
     # self-sensitivity envelope (reading C23): the oracle's own history
     # under 1e-13 relative perturbations of f, at the GPU/oracle matvec agreement level
