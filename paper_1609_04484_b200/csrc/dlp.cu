@@ -149,11 +149,22 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
                 const double e = fma(-rho2, inv, 1.0);
                 inv = fma(inv, fma(e, e, e), inv);
                 const double q = (rn * inv) * inv;  // (r.nw)/rho^4
+                if constexpr (NV >= 8) {
+                    // tensor form: P = q r r^T once per pair (5 ops), 4 DFMA per vector
+                    const double qx = q * rx;
+                    const double pxx = qx * rx, pxy = qx * ry, pyy = (q * ry) * ry;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const double c = q * fma(rx, sj[v].x, ry * sj[v].y);
-                    acc[r][v].x = fma(c, rx, acc[r][v].x);
-                    acc[r][v].y = fma(c, ry, acc[r][v].y);
+                    for (int v = 0; v < NV; ++v) {
+                        acc[r][v].x = fma(pxx, sj[v].x, fma(pxy, sj[v].y, acc[r][v].x));
+                        acc[r][v].y = fma(pxy, sj[v].x, fma(pyy, sj[v].y, acc[r][v].y));
+                    }
+                } else {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double c = q * fma(rx, sj[v].x, ry * sj[v].y);
+                        acc[r][v].x = fma(c, rx, acc[r][v].x);
+                        acc[r][v].y = fma(c, ry, acc[r][v].y);
+                    }
                 }
             }
         }
@@ -561,9 +572,11 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         const int tb = it / ch.TB;
         const int first = unit_owner((long long)tb * ch.nTS, ch.U, ch.P);
         const int last = unit_owner((long long)(tb + 1) * ch.nTS - 1, ch.U, ch.P);
-        const int nv = NVC == 1 ? 1 : ch.nv;
+        // NVC in {1, 4, 16}: nvec is one variant size -> a single chunk at v0 = 0
+        const int nv = NVC > 0 ? NVC : ch.nv;
+#pragma unroll
         for (int vv = 0; vv < nv; ++vv) {
-            const int v = NVC == 1 ? 0 : ch.v0 + vv;  // nvec == 1 -> a single chunk at v0 = 0
+            const int v = NVC > 0 ? vv : ch.v0 + vv;
             double2 acc = make_double2(0.0, 0.0);
             for (int sl = 0; sl <= last - first; ++sl) {
                 const double2 pv = reinterpret_cast<const double2 *>(
@@ -912,6 +925,10 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     ea.nchunks = nch;
     if (nvec == 1)
         k_epilogue<1><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    else if (nvec == 4)
+        k_epilogue<4><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    else if (nvec == 16)
+        k_epilogue<16><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
     else
         k_epilogue<0><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
     count_launch();
