@@ -167,6 +167,23 @@ BIE_API int bie_gmres_solve(bie_geometry_t g, bie_blockdiag_t bd, const double *
                     double *hist_host, int *iters, double *res_pc, double *res_true, int *converged,
                     void *stream);
 
+/*
+ * bie_gmres_solve_batch -- SURVEY s8(f) NEXT-3: nrhs independent left-
+ * preconditioned GMRES solves (same algorithm and stopping rule as
+ * bie_gmres_solve, one Krylov basis per right-hand side) whose operator
+ * applications are batched: every iteration applies A and P^{-1} to the
+ * current basis vectors of all still-active systems in one nvec-wide call
+ * (BIE_MAX_NVEC per chunk).  A system leaves the batch when it converges.
+ *   F, X      : device [nrhs][2N].
+ *   hist_host : host [nrhs][max_iter+1];  iters, converged : host [nrhs];
+ *   res_pc, res_true : host [nrhs].
+ * nrhs in [1, 64].  Device memory: nrhs (max_iter+1) 2N doubles for the bases.
+ * Errors: as bie_gmres_solve.
+ */
+BIE_API int bie_gmres_solve_batch(bie_geometry_t g, bie_blockdiag_t bd, const double *F, double *X, int nrhs,
+                                  double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                                  double *res_true, int *converged, void *stream);
+
 BIE_API const char *bie_last_error(void);
 
 /*

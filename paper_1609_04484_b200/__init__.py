@@ -20,6 +20,7 @@ from ._bie import (  # noqa: F401
     dlp_apply_rows,
     field_eval,
     gmres_solve,
+    gmres_solve_batch,
     launch_count,
     profile_begin,
     profile_end,

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "bie_dlp_apply", "bie_dlp_apply_rows", "bie_dlp_apply_host",
     "bie_blockdiag_factor", "bie_blockdiag_apply", "bie_blockdiag_destroy", "bie_blockdiag_block_inverse",
     "bie_gmres_solve", "bie_last_error", "bie_profile_begin", "bie_profile_end", "bie_launch_count",
-    "bie_field_eval",
+    "bie_field_eval", "bie_gmres_solve_batch",
 )
 
 
@@ -68,6 +68,7 @@ def lib():
         "bie_blockdiag_block_inverse": [vp, c_int, dp, ctypes.c_longlong],
         "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_field_eval": [vp, vp, vp, c_int, vp, vp],
+        "bie_gmres_solve_batch": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_profile_begin": [vp],
         "bie_profile_end": [vp, dp, dp, dp, ip],
     }
@@ -250,6 +251,24 @@ def blockdiag_apply(bd: BlockDiag, inp, out, nvec: int = 1, stream=None):
     _check(lib().bie_blockdiag_apply(bd.h, _dev_ptr(inp, "in", n), _dev_ptr(out, "out", n), nvec,
                                      _stream_ptr(stream)))
     return out
+
+
+def gmres_solve_batch(g: Geometry, bd: BlockDiag | None, F, X, nrhs: int, tol: float = 1e-8, max_iter: int = 1000,
+                      stream=None):
+    """bie_gmres_solve_batch: nrhs independent solves with batched operator applications.
+    F, X: float64 CUDA [nrhs * 2N].  Returns a list of per-system dicts."""
+    hist = np.zeros(nrhs * (max_iter + 1))
+    it = np.zeros(nrhs, dtype=np.int32)
+    conv = np.zeros(nrhs, dtype=np.int32)
+    rp, rt = np.zeros(nrhs), np.zeros(nrhs)
+    ip_ = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))  # noqa: E731
+    n = nrhs * 2 * g.N
+    _check(lib().bie_gmres_solve_batch(g.h, None if bd is None else bd.h, _dev_ptr(F, "F", n), _dev_ptr(X, "X", n),
+                                       int(nrhs), float(tol), int(max_iter), _dp(hist), ip_(it), _dp(rp), _dp(rt),
+                                       ip_(conv), _stream_ptr(stream)))
+    hist = hist.reshape(nrhs, max_iter + 1)
+    return [dict(iters=int(it[r]), hist=hist[r, : it[r] + 1].copy(), res_pc=float(rp[r]), res_true=float(rt[r]),
+                 converged=bool(conv[r])) for r in range(nrhs)]
 
 
 def gmres_solve(g: Geometry, bd: BlockDiag | None, f, x, tol: float = 1e-8, max_iter: int = 1000, stream=None):

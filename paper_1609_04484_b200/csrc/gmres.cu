@@ -364,3 +364,209 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     cleanup();
     return BIE_OK;
 }
+
+// ---------------------------------------------------------------------------
+// NEXT-3: batched multi-RHS GMRES.  Identical per-system algorithm (reading
+// C13); the operator applications of all active systems share one nvec-wide
+// bie_dlp_apply / bie_blockdiag_apply per iteration (chunks of 16).
+// ---------------------------------------------------------------------------
+namespace bie {
+static int batched_op(Geometry *g, BlockDiag *bd, const double *in, double *tmp, double *out, int nv,
+                      cudaStream_t st) {
+    const long long n = 2LL * g->N;
+    for (int v0 = 0; v0 < nv; v0 += BIE_MAX_NVEC) {
+        const int c = std::min(BIE_MAX_NVEC, nv - v0);
+        if (bd) {
+            int rc = dlp_apply_impl(g, in + v0 * n, tmp + v0 * n, c, BIE_FULL, 0, g->N, st);
+            if (rc) return rc;
+            rc = blockdiag_apply_impl(bd, tmp + v0 * n, out + v0 * n, c, st);
+            if (rc) return rc;
+        } else {
+            int rc = dlp_apply_impl(g, in + v0 * n, out + v0 * n, c, BIE_FULL, 0, g->N, st);
+            if (rc) return rc;
+        }
+    }
+    return BIE_OK;
+}
+}  // namespace bie
+
+extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, const double *F, double *X, int nrhs,
+                                     double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                                     double *res_true, int *converged, void *stream) {
+    Geometry *g = as_geom(gh);
+    BlockDiag *bd = bdh ? as_bd(bdh) : nullptr;
+    if (!g || (bdh && !bd) || !F || !X || !hist_host || !iters || !res_pc || !res_true || !converged ||
+        max_iter < 1 || !(tol > 0.0) || F == X || nrhs < 1 || nrhs > 64) {
+        set_error("bie_gmres_solve_batch: invalid handle, null pointer, F == X, nrhs not in [1,64], max_iter < 1 "
+                  "or tol <= 0");
+        return BIE_EINVAL;
+    }
+    if (bd && bd->g != g) {
+        set_error("bie_gmres_solve_batch: blockdiag was built from another geometry");
+        return BIE_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = 2LL * g->N;
+    const int ldh = max_iter + 1;
+    const unsigned eb = (unsigned)((n + 255) / 256);
+    double *V = nullptr, *Win = nullptr, *Wt = nullptr, *Wout = nullptr, *H = nullptr, *small = nullptr;
+    double *pinned = nullptr;
+    Dot d;
+    d.nchunks = (int)((n + kChunk - 1) / kChunk);
+    d.ldp = ldh;
+    int rc = BIE_OK;
+    auto cleanup = [&]() {
+        cudaFree(V);
+        cudaFree(Win);
+        cudaFree(Wt);
+        cudaFree(Wout);
+        cudaFree(H);
+        cudaFree(small);
+        cudaFree(d.partial);
+        cudaFreeHost(pinned);
+    };
+#define GB_TRY(expr)                   \
+    do {                               \
+        cudaError_t _e = (expr);       \
+        if (_e != cudaSuccess) {       \
+            rc = cuda_fail(_e, #expr); \
+            cleanup();                 \
+            return rc;                 \
+        }                              \
+    } while (0)
+#define GB_RC(expr)          \
+    do {                     \
+        rc = (expr);         \
+        if (rc != BIE_OK) {  \
+            cleanup();       \
+            return rc;       \
+        }                    \
+    } while (0)
+    // per-system small state: cs, sn, g, h, h2 [ldh each] + scal [8]
+    const long long smallper = 5LL * ldh + 8;
+    GB_TRY(cudaMalloc(&V, sizeof(double) * (size_t)nrhs * ldh * n));
+    GB_TRY(cudaMalloc(&Win, sizeof(double) * (size_t)nrhs * n));
+    GB_TRY(cudaMalloc(&Wt, sizeof(double) * (size_t)nrhs * n));
+    GB_TRY(cudaMalloc(&Wout, sizeof(double) * (size_t)nrhs * n));
+    GB_TRY(cudaMalloc(&H, sizeof(double) * (size_t)nrhs * ldh * max_iter));
+    GB_TRY(cudaMalloc(&small, sizeof(double) * (size_t)nrhs * smallper));
+    GB_TRY(cudaMalloc(&d.partial, sizeof(double) * (size_t)d.nchunks * ldh));
+    GB_TRY(cudaMallocHost(&pinned, sizeof(double) * (size_t)nrhs * 8));
+    GB_TRY(cudaMemsetAsync(H, 0, sizeof(double) * (size_t)nrhs * ldh * max_iter, st));
+    GB_TRY(cudaMemsetAsync(small, 0, sizeof(double) * (size_t)nrhs * smallper, st));
+    std::vector<GmState> S(nrhs);
+    for (int r = 0; r < nrhs; ++r) {
+        double *b = small + r * smallper;
+        S[r] = GmState{H + (size_t)r * ldh * max_iter, b, b + ldh, b + 2 * ldh, b + 3 * ldh, b + 4 * ldh, b + 5 * ldh};
+    }
+    auto Vr = [&](int r, int k) { return V + ((size_t)r * ldh + k) * n; };
+    auto norm_to = [&](const double *v, double *tmp, double *dst) -> int {
+        int q = multidot(v, 0, 1, v, n, d, tmp, st);
+        if (q) return q;
+        k_sqrt<<<1, 1, 0, st>>>(tmp, dst);
+        count_launch();
+        BIE_CUDA_TRY(cudaGetLastError());
+        return BIE_OK;
+    };
+    // r0 = P^{-1} f for all systems at once
+    if (bd) {
+        for (int v0 = 0; v0 < nrhs; v0 += BIE_MAX_NVEC)
+            GB_RC(blockdiag_apply_impl(bd, F + v0 * n, Wout + v0 * n, std::min(BIE_MAX_NVEC, nrhs - v0), st));
+    } else {
+        GB_TRY(cudaMemcpyAsync(Wout, F, sizeof(double) * (size_t)nrhs * n, cudaMemcpyDeviceToDevice, st));
+    }
+    for (int r = 0; r < nrhs; ++r) GB_RC(norm_to(Wout + r * n, S[r].scal + 5, S[r].scal + 0));
+    for (int r = 0; r < nrhs; ++r)
+        GB_TRY(cudaMemcpyAsync(pinned + 8 * r, S[r].scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+    GB_TRY(cudaStreamSynchronize(st));
+    GB_TRY(cudaMemsetAsync(X, 0, sizeof(double) * (size_t)nrhs * n, st));
+    std::vector<double> beta(nrhs);
+    std::vector<int> it(nrhs, 0), active;
+    for (int r = 0; r < nrhs; ++r) {
+        beta[r] = pinned[8 * r];
+        hist_host[(size_t)r * ldh] = 1.0;
+        converged[r] = 0;
+        iters[r] = 0;
+        res_pc[r] = res_true[r] = 0.0;
+        if (beta[r] == 0.0) {
+            converged[r] = 1;
+            continue;
+        }
+        active.push_back(r);
+        k_scale_div<<<eb, 256, 0, st>>>(Wout + r * n, S[r].scal + 0, Vr(r, 0), n);
+        count_launch();
+        GB_TRY(cudaMemcpyAsync(S[r].g, S[r].scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    for (int k = 0; k < max_iter && !active.empty(); ++k) {
+        const int na = (int)active.size();
+        for (int q = 0; q < na; ++q)
+            GB_TRY(cudaMemcpyAsync(Win + q * n, Vr(active[q], k), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        GB_RC(batched_op(g, bd, Win, Wt, Wout, na, st));
+        for (int q = 0; q < na; ++q) {
+            const int r = active[q];
+            GmState &s = S[r];
+            double *w = Wout + q * n;
+            double *Vb = Vr(r, 0);
+            GB_RC(norm_to(w, s.scal + 5, s.scal + 1));
+            GB_RC(multidot(Vb, n, k + 1, w, n, d, s.h, st));
+            GB_RC(multiaxpy(Vb, n, k + 1, s.h, -1.0, 1.0, w, n, st));
+            GB_RC(multidot(Vb, n, k + 1, w, n, d, s.h2, st));
+            GB_RC(multiaxpy(Vb, n, k + 1, s.h2, -1.0, 1.0, w, n, st));
+            GB_RC(norm_to(w, s.scal + 5, s.scal + 2));
+            k_givens<<<1, 1, 0, st>>>(s, k, ldh);
+            count_launch();
+            GB_TRY(cudaMemcpyAsync(pinned + 8 * r + 3, s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (k + 1 < max_iter) {
+                k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, Vr(r, k + 1), n);
+                count_launch();
+            }
+        }
+        GB_TRY(cudaStreamSynchronize(st));
+        std::vector<int> next;
+        for (int q = 0; q < na; ++q) {
+            const int r = active[q];
+            const double est = pinned[8 * r + 3];
+            const bool brk = pinned[8 * r + 4] != 0.0;
+            hist_host[(size_t)r * ldh + k + 1] = est;
+            it[r] = k + 1;
+            if (est < tol || brk)
+                converged[r] = 1;
+            else
+                next.push_back(r);
+        }
+        active.swap(next);
+    }
+    // finish: y = H^{-1} g, x = V y per system; residual pair with batched operators
+    for (int r = 0; r < nrhs; ++r) {
+        iters[r] = it[r];
+        if (it[r] == 0) continue;
+        k_trisolve<<<1, 256, 0, st>>>(S[r].H, ldh, S[r].g, S[r].h, it[r]);
+        count_launch();
+        GB_RC(multiaxpy(Vr(r, 0), n, it[r], S[r].h, 1.0, 0.0, X + r * n, n, st));
+    }
+    for (int v0 = 0; v0 < nrhs; v0 += BIE_MAX_NVEC)
+        GB_RC(dlp_apply_impl(g, X + v0 * n, Wt + v0 * n, std::min(BIE_MAX_NVEC, nrhs - v0), BIE_FULL, 0, g->N, st));
+    for (int r = 0; r < nrhs; ++r) {
+        k_sub<<<eb, 256, 0, st>>>(F + r * n, Wt + r * n, Win + r * n, n);
+        count_launch();
+    }
+    if (bd)
+        for (int v0 = 0; v0 < nrhs; v0 += BIE_MAX_NVEC)
+            GB_RC(blockdiag_apply_impl(bd, Win + v0 * n, Wout + v0 * n, std::min(BIE_MAX_NVEC, nrhs - v0), st));
+    for (int r = 0; r < nrhs; ++r) {
+        GB_RC(norm_to(Win + r * n, S[r].scal + 5, S[r].scal + 6));
+        GB_RC(norm_to(F + r * n, S[r].scal + 5, S[r].scal + 7));
+        if (bd) GB_RC(norm_to(Wout + r * n, S[r].scal + 4, S[r].scal + 5));
+        GB_TRY(cudaMemcpyAsync(pinned + 8 * r + 5, S[r].scal + 5, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    GB_TRY(cudaStreamSynchronize(st));
+    for (int r = 0; r < nrhs; ++r) {
+        if (beta[r] == 0.0) continue;
+        res_true[r] = pinned[8 * r + 6] / pinned[8 * r + 7];
+        res_pc[r] = bd ? pinned[8 * r + 5] / beta[r] : res_true[r];
+    }
+#undef GB_TRY
+#undef GB_RC
+    cleanup();
+    return BIE_OK;
+}
