@@ -647,6 +647,23 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
     const double *G = s.G + (long long)m * NB * n2;
     double *M = v.mat + (long long)m * v.mstride;
     const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
+    const int gr = lane >> 2, gq = lane & 3;
+    // issue this thread's 16 double2 reads of M first: the DRAM traffic of the
+    // sweep (read + write of the whole matrix per panel) overlaps the staging
+    // and the DMMA work instead of following it
+    double2 base[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gi = i0 + wr + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gj = j0 + wc + 8 * j + 2 * gq;
+            base[i][j] = (gi < n2 && gj < n2) ? *reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj)
+                                              : make_double2(0.0, 0.0);
+        }
+    }
     for (int q = tid; q < UT3 * NB; q += 128) {
         const int i = q / NB, c = q % NB;
         Ts[i][c] = (i0 + i < n2) ? T[(long long)(i0 + i) * NB + c] : 0.0;
@@ -656,9 +673,6 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
         Gs[c][j] = (j0 + j < n2) ? G[(long long)c * n2 + j0 + j] : 0.0;
     }
     __syncthreads();
-    const int lane = tid & 31, wid = tid >> 5;
-    const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
-    const int gr = lane >> 2, gq = lane & 3;
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -692,10 +706,10 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
             if (rowK) {
                 o = make_double2(Gs[gi - k0][lj], Gs[gi - k0][lj + 1]);
             } else {
-                double2 base = *dst;
-                if (gj >= k0 && gj < k0 + nbe) base.x = 0.0;
-                if (gj + 1 >= k0 && gj + 1 < k0 + nbe) base.y = 0.0;
-                o = make_double2(base.x - acc[i][j][0], base.y - acc[i][j][1]);
+                double2 b = base[i][j];
+                if (gj >= k0 && gj < k0 + nbe) b.x = 0.0;
+                if (gj + 1 >= k0 && gj + 1 < k0 + nbe) b.y = 0.0;
+                o = make_double2(b.x - acc[i][j][0], b.y - acc[i][j][1]);
             }
             *dst = o;
         }

@@ -198,3 +198,36 @@ def test_symmetric_ragged_sizes(bie):
         s = density(p, nvec=1)
         y = _gpu_apply(bie, g, s, 1)
         assert _relerr(y[0], og.apply(s)[0]) <= TOL, p.name
+
+
+def test_d_only_symmetric_path_large(bie):
+    """BIE_D_ONLY at nvec = 1 takes the symmetric kernel: sampled rows of config 4."""
+    p = make_problem(4)
+    g, og = _setup(bie, p)
+    s = density(p, nvec=1, vec_id=2)
+    y = _gpu_apply(bie, g, s, 1, flags=1).reshape(-1, 2)
+    rows = _rows(p.N, 512)
+    ref = og.apply(s, flags=1, rows=rows).reshape(-1, 2)
+    assert np.abs(y[rows] - ref).max() / np.abs(ref).max() <= TOL
+
+
+def test_side_stream_and_profile_hooks(bie):
+    """Async on a caller stream; profiling hooks and the launch counter."""
+    import torch
+
+    p = make_problem(2)
+    g, og = _setup(bie, p)
+    s = density(p, nvec=1)
+    sig = torch.from_numpy(s.reshape(-1).copy()).cuda()
+    out = torch.zeros_like(sig)
+    st = torch.cuda.Stream()
+    n0 = bie.launch_count()
+    bie.profile_begin(g)
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            bie.dlp_apply(g, sig, out, 1, stream=st)
+    st.synchronize()
+    pr = bie.profile_end(g)
+    assert pr["applies"] == 3 and pr["pairs_ms"] > 0 and pr["epilogue_ms"] > 0
+    assert bie.launch_count() - n0 >= 3 * 4  # moments, quad, sym, diag, epilogue per apply
+    assert _relerr(out.cpu().numpy(), og.apply(s)[0]) <= TOL
