@@ -175,6 +175,45 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def config5_sweep(bie, dev, stream):
+    """BASELINE.json configs[4]: N = 1,064,960 matvec sweep over nvec in {1, 4, 16}
+    (bie_dlp_apply, BIE_FULL), plus the oracle on a 4096-row subsample
+    extrapolated as O(N^2)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from bie_inputs import density, make_problem
+
+    p = make_problem(5)
+    g = bie.Geometry.from_problem(p)
+    res = {"N": p.N}
+    for nvec in (1, 4, 16):
+        s = torch.from_numpy(density(p, nvec=nvec).reshape(-1)).to(dev)
+        o = torch.zeros_like(s)
+        bie.dlp_apply(g, s, o, nvec)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        bie.dlp_apply(g, s, o, nvec)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        res[f"nvec{nvec}"] = {"ms": ms, "pairs_per_s": nvec * p.N * p.N / (ms * 1e-3),
+                              "alg_tflops": (11 + 8 * nvec) * p.N * p.N / (ms * 1e-3) / 1e12}
+        del s, o
+    og = oracle.OracleGeometry(p)
+    rows = np.linspace(0, p.N - 1, 4096).astype(np.int32)
+    s0 = density(p)[0]
+    t0 = time.perf_counter()
+    og.apply(s0, rows=rows)
+    t = time.perf_counter() - t0
+    res["oracle_4096_rows"] = {"seconds": t, "pairs_per_s": 4096 * p.N / t,
+                               "extrapolated_full_matvec_s": t * p.N / 4096,
+                               "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))}
+    g.close()
+    return res
+
+
 def run_gpu(args):
     import numpy as np
     import torch
@@ -308,6 +347,8 @@ def run_gpu(args):
                                    "iters": rr["iters"], "converged": rr["converged"], "max_iter": mi,
                                    "res_pc": rr["res_pc"], "res_true": rr["res_true"], "tol": 1e-8}
         extra["gmres_solve"] = sol
+        if not args.no_config5:
+            extra["config5_sweep"] = config5_sweep(bie, dev, stream)
 
     if rank != 0:
         if dist:
@@ -358,6 +399,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--gmres-cap", type=int, default=2000)
+    ap.add_argument("--no-config5", action="store_true", help="skip the config-5 (N = 1.06M) nvec sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -650,20 +650,6 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
     const int lane = tid & 31, wid = tid >> 5;
     const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
     const int gr = lane >> 2, gq = lane & 3;
-    // issue this thread's 16 double2 reads of M first: the DRAM traffic of the
-    // sweep (read + write of the whole matrix per panel) overlaps the staging
-    // and the DMMA work instead of following it
-    double2 base[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int gi = i0 + wr + 8 * i + gr;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gj = j0 + wc + 8 * j + 2 * gq;
-            base[i][j] = (gi < n2 && gj < n2) ? *reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj)
-                                              : make_double2(0.0, 0.0);
-        }
-    }
     for (int q = tid; q < UT3 * NB; q += 128) {
         const int i = q / NB, c = q % NB;
         Ts[i][c] = (i0 + i < n2) ? T[(long long)(i0 + i) * NB + c] : 0.0;
@@ -706,7 +692,7 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
             if (rowK) {
                 o = make_double2(Gs[gi - k0][lj], Gs[gi - k0][lj + 1]);
             } else {
-                double2 b = base[i][j];
+                double2 b = *dst;
                 if (gj >= k0 && gj < k0 + nbe) b.x = 0.0;
                 if (gj + 1 >= k0 && gj + 1 < k0 + nbe) b.y = 0.0;
                 o = make_double2(b.x - acc[i][j][0], b.y - acc[i][j][1]);
