@@ -288,8 +288,13 @@ struct SymArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int SR, int SW, int MINB = 1>
+template <int SR, int SW, int MINB = 1, bool QS = false>
 __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
+    // QS: keep the targets' quadratic forms in shared memory (lane-private
+    // slots) instead of registers, trading 3 shared loads per pair for 48
+    // registers (more resident warps)
+    __shared__ double2 s_tqab[QS ? SW : 1][QS ? SR : 1][32];
+    __shared__ double s_tqc[QS ? SW : 1][QS ? SR : 1][32];
     static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
     static_assert(SR % 2 == 0, "two interleaved chains");
     __shared__ double2 red[SW][32];
@@ -322,9 +327,14 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
             }
             tx[r] = x.x;
             ty[r] = x.y;
-            tqa[r] = q.x;
-            tqb[r] = q.y;
-            tqc[r] = q.z;
+            if constexpr (QS) {
+                s_tqab[w][r][lane] = make_double2(q.x, q.y);
+                s_tqc[w][r][lane] = q.z;
+            } else {
+                tqa[r] = q.x;
+                tqb[r] = q.y;
+                tqc[r] = q.z;
+            }
             ax[r] = 0.0;
             ay[r] = 0.0;
         }
@@ -389,8 +399,25 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
                 double i0 = rcp_approx(d0), i1 = rcp_approx(d1);
                 const double cs0 = fma(sqa, xx0, fma(sqb, xy0, sqc * yy0));  // target <- source
                 const double cs1 = fma(sqa, xx1, fma(sqb, xy1, sqc * yy1));
-                const double ct0 = fma(tqa[r], xx0, fma(tqb[r], xy0, tqc[r] * yy0));  // source <- target
-                const double ct1 = fma(tqa[r + 1], xx1, fma(tqb[r + 1], xy1, tqc[r + 1] * yy1));
+                double qa0, qb0, qc0, qa1, qb1, qc1;
+                if constexpr (QS) {
+                    const double2 ab0 = s_tqab[w][r][lane], ab1 = s_tqab[w][r + 1][lane];
+                    qa0 = ab0.x;
+                    qb0 = ab0.y;
+                    qa1 = ab1.x;
+                    qb1 = ab1.y;
+                    qc0 = s_tqc[w][r][lane];
+                    qc1 = s_tqc[w][r + 1][lane];
+                } else {
+                    qa0 = tqa[r];
+                    qb0 = tqb[r];
+                    qc0 = tqc[r];
+                    qa1 = tqa[r + 1];
+                    qb1 = tqb[r + 1];
+                    qc1 = tqc[r + 1];
+                }
+                const double ct0 = fma(qa0, xx0, fma(qb0, xy0, qc0 * yy0));  // source <- target
+                const double ct1 = fma(qa1, xx1, fma(qb1, xy1, qc1 * yy1));
                 const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
                 i0 = fma(i0, fma(e0, e0, e0), i0);
                 i1 = fma(i1, fma(e1, e1, e1), i1);
@@ -726,8 +753,10 @@ int build_schedules(Geometry *g) {
 
 // (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
 // variants 3..5 add a minimum-blocks launch bound (register cap -> more warps)
-static const int kNumSymVar = 6;
-static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}};
+// variants 6..8 keep the target quadratic forms in shared memory (QS)
+static const int kNumSymVar = 9;
+static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2},
+                                           {4, 4}, {8, 2}, {8, 2}, {4, 4}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
@@ -735,6 +764,9 @@ static void *sym_kernel(int v) {
         case 3: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5>);
         case 4: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 6>);
         case 5: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3>);
+        case 6: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, true>);
+        case 7: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, true>);
+        case 8: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, true>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -746,6 +778,9 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 3: k_dlp_sym<8, 2, 5><<<P, 64, 0, st>>>(sa); break;
         case 4: k_dlp_sym<8, 2, 6><<<P, 64, 0, st>>>(sa); break;
         case 5: k_dlp_sym<4, 4, 3><<<P, 128, 0, st>>>(sa); break;
+        case 6: k_dlp_sym<8, 2, 1, true><<<P, 64, 0, st>>>(sa); break;
+        case 7: k_dlp_sym<8, 2, 5, true><<<P, 64, 0, st>>>(sa); break;
+        case 8: k_dlp_sym<4, 4, 3, true><<<P, 128, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
