@@ -754,9 +754,9 @@ int build_schedules(Geometry *g) {
 // (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
 // variants 3..5 add a minimum-blocks launch bound (register cap -> more warps)
 // variants 6..8 keep the target quadratic forms in shared memory (QS)
-static const int kNumSymVar = 9;
-static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2},
-                                           {4, 4}, {8, 2}, {8, 2}, {4, 4}};
+static const int kNumSymVar = 11;
+static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4},
+                                           {8, 2}, {8, 2}, {4, 4}, {4, 4}, {4, 4}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
@@ -767,6 +767,8 @@ static void *sym_kernel(int v) {
         case 6: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, true>);
         case 7: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, true>);
         case 8: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, true>);
+        case 9: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4>);
+        case 10: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, true>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -781,6 +783,8 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 6: k_dlp_sym<8, 2, 1, true><<<P, 64, 0, st>>>(sa); break;
         case 7: k_dlp_sym<8, 2, 5, true><<<P, 64, 0, st>>>(sa); break;
         case 8: k_dlp_sym<4, 4, 3, true><<<P, 128, 0, st>>>(sa); break;
+        case 9: k_dlp_sym<4, 4, 4><<<P, 128, 0, st>>>(sa); break;
+        case 10: k_dlp_sym<4, 4, 4, true><<<P, 128, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
