@@ -264,12 +264,14 @@ def run_gpu(args):
     launches0 = bie.launch_count()
     bie.profile_begin(g)
     with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects this region
         for k in range(args.steps):
             flush.fill_(float(k))
             ev[k][0].record(stream)
             step()
             ev[k][1].record(stream)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     prof = bie.profile_end(g)
     launches = bie.launch_count() - launches0
     if dist:

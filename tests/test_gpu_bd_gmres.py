@@ -247,3 +247,47 @@ def test_gmres_golden(bie, name):
     # 1e-10 bar, relaxed only where the oracle's own history moves more under
     # 1e-13 perturbations of f (reading C23)
     assert np.all(rel <= np.maximum(1e-10, 10 * env)), (rel.max(), env.max())
+
+
+def test_abi_handle_and_argument_errors(bie):
+    """Wrong-geometry blockdiag, bad nvec, aliasing, double destroy -> BIE_EINVAL."""
+    import ctypes
+
+    import torch
+
+    p1, p2 = make_problem(1), make_pipe(0, 10.0, 256, 0, (0.1, 0.2), 0.05, 16)
+    c1, c2 = _setup(bie, p1), _setup(bie, p2)
+    f = _t(rhs_rotation_outer(p1))
+    x = torch.zeros_like(f)
+    with pytest.raises(bie.BieError) as ei:
+        bie.gmres_solve(c1["g"], c2["bd"], f, x)
+    assert ei.value.code == -1 and "another geometry" in str(ei.value)
+    v = torch.zeros(17 * 2 * p1.N, dtype=torch.float64, device="cuda")
+    out = torch.zeros_like(v)
+    with pytest.raises(bie.BieError):
+        bie.dlp_apply(c1["g"], v, out, nvec=17)
+    with pytest.raises(bie.BieError):
+        bie.blockdiag_apply(c1["bd"], v, v, nvec=1)
+    with pytest.raises(bie.BieError):
+        bie.gmres_solve(c1["g"], c1["bd"], f, f)
+    # a blockdiag handle passed where a geometry is expected (handle-kind check)
+    assert bie.lib().bie_geometry_info(ctypes.c_void_p(c1["bd"].h.value), ctypes.byref(ctypes.c_int()),
+                                       ctypes.byref(ctypes.c_int())) == -1
+
+
+def test_pinned_host_end_to_end(bie):
+    """bie_dlp_apply_host with pinned torch buffers (the e2e path of bench.py)."""
+    import torch
+
+    from paper_1609_04484_b200._bie import dlp_apply_host_ptr
+
+    p = make_problem(2)
+    c = _setup(bie, p, with_bd=False)
+    s = density(p, nvec=4)
+    hs = torch.from_numpy(s.reshape(-1).copy()).pin_memory()
+    ho = torch.zeros_like(hs).pin_memory()
+    dlp_apply_host_ptr(c["g"], hs.data_ptr(), ho.data_ptr(), nvec=4)
+    ref = c["og"].apply(s)
+    y = ho.numpy().reshape(4, -1)
+    for v in range(4):
+        assert np.abs(y[v] - ref[v]).max() / np.abs(ref[v]).max() <= 1e-12
