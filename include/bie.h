@@ -184,6 +184,41 @@ BIE_API int bie_gmres_solve_batch(bie_geometry_t g, bie_blockdiag_t bd, const do
                                   double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
                                   double *res_true, int *converged, void *stream);
 
+/*
+ * Row sharding: a rank owns the nodes of a
+ * contiguous body range.  bie_blockdiag_factor_range factors only bodies
+ * [body_begin, body_end) (pores 0..M-1, wall M); its bie_blockdiag_apply then
+ * takes LOCAL vectors [nvec][2 (row_end - row_begin)] for the node range that
+ * bie_blockdiag_rows reports.  Such a handle is rejected by bie_gmres_solve*.
+ */
+BIE_API int bie_blockdiag_factor_range(bie_geometry_t g, int body_begin, int body_end, bie_blockdiag_t *out,
+                                       void *stream);
+BIE_API int bie_blockdiag_rows(bie_blockdiag_t bd, int *row_begin, int *row_end);
+
+/*
+ * Krylov building blocks for a row-sharded GMRES (the kernels bie_gmres_solve
+ * uses; a multi-rank driver adds only the collectives).  All device pointers,
+ * async on stream; reading C13 conventions:
+ *   dots     : out[j] = sum_e V[j*ldv + e] w[e], j < nv (local partial; fixed-order two-stage reduction)
+ *   axpy     : y = beta y + alpha sum_j c[j] V[j*ldv + .]   (c on the device)
+ *   scale    : y = x / s[0]                                  (s on the device, a norm)
+ *   sqrt     : out[i] = sqrt(in[i]), i < n
+ *   givens   : Hessenberg column k = h + h2 with H[k+1,k] = scal[2]; applies the previous
+ *              rotations, forms rotation k, updates g; scal[0] = beta, scal[1] = ||P^-1 A v_k||,
+ *              scal[2] = ||w|| after CGS2; writes scal[3] = |g[k+1]|/beta, scal[4] = breakdown flag.
+ *              H is column-major with leading dimension ldh.
+ *   trisolve : y = H[0:iters,0:iters]^{-1} g (upper triangular).
+ */
+BIE_API int bie_krylov_dots(const double *V, long long ldv, int nv, const double *w, long long n, double *out,
+                            void *stream);
+BIE_API int bie_krylov_axpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta,
+                            double *y, long long n, void *stream);
+BIE_API int bie_krylov_scale(const double *x, const double *s, double *y, long long n, void *stream);
+BIE_API int bie_krylov_sqrt(const double *in, double *out, int n, void *stream);
+BIE_API int bie_krylov_givens(double *H, int ldh, double *cs, double *sn, double *g, const double *h,
+                              const double *h2, int k, double *scal, void *stream);
+BIE_API int bie_krylov_trisolve(const double *H, int ldh, const double *g, double *y, int iters, void *stream);
+
 BIE_API const char *bie_last_error(void);
 
 /*

@@ -13,6 +13,7 @@ from ._bie import (  # noqa: F401
     BieError,
     BlockDiag,
     Geometry,
+    Krylov,
     blockdiag_apply,
     blockdiag_factor,
     dlp_apply,

@@ -27,7 +27,9 @@ EXPORTED_SYMBOLS = (
     "bie_dlp_apply", "bie_dlp_apply_rows", "bie_dlp_apply_host",
     "bie_blockdiag_factor", "bie_blockdiag_apply", "bie_blockdiag_destroy", "bie_blockdiag_block_inverse",
     "bie_gmres_solve", "bie_last_error", "bie_profile_begin", "bie_profile_end", "bie_launch_count",
-    "bie_field_eval", "bie_gmres_solve_batch",
+    "bie_field_eval", "bie_gmres_solve_batch", "bie_blockdiag_factor_range", "bie_blockdiag_rows",
+    "bie_krylov_dots", "bie_krylov_axpy", "bie_krylov_scale", "bie_krylov_sqrt", "bie_krylov_givens",
+    "bie_krylov_trisolve",
 )
 
 
@@ -69,6 +71,14 @@ def lib():
         "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_gmres_solve_batch": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
+        "bie_blockdiag_factor_range": [vp, c_int, c_int, ctypes.POINTER(vp), vp],
+        "bie_blockdiag_rows": [vp, ip, ip],
+        "bie_krylov_dots": [vp, ctypes.c_longlong, c_int, vp, ctypes.c_longlong, vp, vp],
+        "bie_krylov_axpy": [vp, ctypes.c_longlong, c_int, vp, c_double, c_double, vp, ctypes.c_longlong, vp],
+        "bie_krylov_scale": [vp, vp, vp, ctypes.c_longlong, vp],
+        "bie_krylov_sqrt": [vp, vp, c_int, vp],
+        "bie_krylov_givens": [vp, c_int, vp, vp, vp, vp, vp, c_int, vp, vp],
+        "bie_krylov_trisolve": [vp, c_int, vp, vp, c_int, vp],
         "bie_profile_begin": [vp],
         "bie_profile_end": [vp, dp, dp, dp, ip],
     }
@@ -215,13 +225,21 @@ def dlp_apply_host_ptr(g: Geometry, sigma_ptr: int, out_ptr: int, nvec: int = 1,
 
 
 class BlockDiag:
-    """bie_blockdiag_t: explicit per-body inverses (A6)."""
+    """bie_blockdiag_t: explicit per-body inverses (A6).  bodies=(b0, b1) factors
+    only that body range (row sharding); its apply takes local vectors."""
 
-    def __init__(self, g: Geometry, stream=None):
+    def __init__(self, g: Geometry, stream=None, bodies=None):
         h = ctypes.c_void_p()
-        _check(lib().bie_blockdiag_factor(g.h, ctypes.byref(h), _stream_ptr(stream)))
+        if bodies is None:
+            _check(lib().bie_blockdiag_factor(g.h, ctypes.byref(h), _stream_ptr(stream)))
+        else:
+            _check(lib().bie_blockdiag_factor_range(g.h, int(bodies[0]), int(bodies[1]), ctypes.byref(h),
+                                                    _stream_ptr(stream)))
         self.h = h
         self.g = g
+        rb, re_ = ctypes.c_int(), ctypes.c_int()
+        _check(lib().bie_blockdiag_rows(h, ctypes.byref(rb), ctypes.byref(re_)))
+        self.rows = (rb.value, re_.value)
 
     def block_inverse(self, body: int) -> np.ndarray:
         g = self.g
@@ -246,8 +264,41 @@ def blockdiag_factor(g: Geometry, stream=None) -> BlockDiag:
     return BlockDiag(g, stream)
 
 
+class Krylov:
+    """Thin wrappers of the bie_krylov_* building blocks (device tensors)."""
+
+    @staticmethod
+    def dots(V, ldv: int, nv: int, w, n: int, out, stream=None):
+        _check(lib().bie_krylov_dots(_dev_ptr(V, "V"), ldv, nv, _dev_ptr(w, "w"), n, _dev_ptr(out, "out", nv),
+                                     _stream_ptr(stream)))
+
+    @staticmethod
+    def axpy(V, ldv: int, nv: int, c, alpha: float, beta: float, y, n: int, stream=None):
+        _check(lib().bie_krylov_axpy(_dev_ptr(V, "V"), ldv, nv, _dev_ptr(c, "c"), float(alpha), float(beta),
+                                     _dev_ptr(y, "y"), n, _stream_ptr(stream)))
+
+    @staticmethod
+    def scale(x, s, y, n: int, stream=None):
+        _check(lib().bie_krylov_scale(_dev_ptr(x, "x"), _dev_ptr(s, "s"), _dev_ptr(y, "y"), n, _stream_ptr(stream)))
+
+    @staticmethod
+    def sqrt(inp, out, n: int, stream=None):
+        _check(lib().bie_krylov_sqrt(_dev_ptr(inp, "in"), _dev_ptr(out, "out"), n, _stream_ptr(stream)))
+
+    @staticmethod
+    def givens(H, ldh: int, cs, sn, g, h, h2, k: int, scal, stream=None):
+        _check(lib().bie_krylov_givens(_dev_ptr(H, "H"), ldh, _dev_ptr(cs, "cs"), _dev_ptr(sn, "sn"),
+                                       _dev_ptr(g, "g"), _dev_ptr(h, "h"), _dev_ptr(h2, "h2"), k,
+                                       _dev_ptr(scal, "scal"), _stream_ptr(stream)))
+
+    @staticmethod
+    def trisolve(H, ldh: int, g, y, iters: int, stream=None):
+        _check(lib().bie_krylov_trisolve(_dev_ptr(H, "H"), ldh, _dev_ptr(g, "g"), _dev_ptr(y, "y"), iters,
+                                         _stream_ptr(stream)))
+
+
 def blockdiag_apply(bd: BlockDiag, inp, out, nvec: int = 1, stream=None):
-    n = nvec * 2 * bd.g.N
+    n = nvec * 2 * (bd.rows[1] - bd.rows[0])
     _check(lib().bie_blockdiag_apply(bd.h, _dev_ptr(inp, "in", n), _dev_ptr(out, "out", n), nvec,
                                      _stream_ptr(stream)))
     return out

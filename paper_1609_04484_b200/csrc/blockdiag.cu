@@ -732,27 +732,30 @@ __global__ void k_unpermute(BDView v, BDScratch s) {
 
 // ------------------------------------------------------------------ apply (A7)
 // One warp per row of the explicit inverse; NVA vectors per pass.
+// Vectors are local to the handle's body range: local row 0 is node row_lo.
 template <int NVA>
 __global__ void __launch_bounds__(256) k_bd_apply(const double *__restrict__ inv, const long long *__restrict__ off,
-                                                  int wall_lo, int n_pore, int nb, int N, const double *in,
-                                                  double *out, long long stride, int v0) {
+                                                  int wall_lo, int n_pore, int N, int b0, int row_lo, int rows_loc,
+                                                  const double *in, double *out, long long stride, int v0) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (warp >= 2 * N) return;
-    const int node = warp >> 1;
+    if (warp >= 2 * rows_loc) return;
+    const int node = row_lo + (warp >> 1);
     int b, lo, n;
     if (node < wall_lo) {
         b = node / n_pore;
         lo = b * n_pore;
         n = n_pore;
     } else {
-        b = nb - 1;
+        b = wall_lo / max(n_pore, 1);  // wall body index = M
+        if (n_pore == 0) b = 0;
         lo = wall_lo;
         n = N - wall_lo;
     }
     const int n2 = 2 * n;
-    const int lr = warp - 2 * lo;
-    const double2 *row = reinterpret_cast<const double2 *>(inv + off[b] + (long long)lr * n2);
+    const int lr = 2 * (node - lo) + (warp & 1);
+    const double2 *row = reinterpret_cast<const double2 *>(inv + off[b - b0] + (long long)lr * n2);
+    const int lo_loc = lo - row_lo;
     double acc[NVA];
 #pragma unroll
     for (int v = 0; v < NVA; ++v) acc[v] = 0.0;
@@ -760,7 +763,7 @@ __global__ void __launch_bounds__(256) k_bd_apply(const double *__restrict__ inv
         const double2 a = __ldcs(row + c);
 #pragma unroll
         for (int v = 0; v < NVA; ++v) {
-            const double2 x = reinterpret_cast<const double2 *>(in + (long long)(v0 + v) * stride + 2LL * lo)[c];
+            const double2 x = reinterpret_cast<const double2 *>(in + (long long)(v0 + v) * stride + 2LL * lo_loc)[c];
             acc[v] = fma(a.x, x.x, fma(a.y, x.y, acc[v]));
         }
     }
@@ -868,26 +871,27 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
 
 int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec, cudaStream_t st) {
     Geometry *g = bd->g;
-    const long long stride = 2LL * g->N;
-    const int rows = 2 * g->N;
+    const int rows_loc = bd->row_hi - bd->row_lo;
+    const long long stride = 2LL * rows_loc;
     const int threads = 256;
-    const int blocks = (int)(((long long)rows * 32 + threads - 1) / threads);
+    const int blocks = (int)(((long long)2 * rows_loc * 32 + threads - 1) / threads);
+    if (rows_loc == 0) return BIE_OK;
     int v = 0;
     while (v < nvec) {
         int rem = nvec - v;
         if (rem >= 4) {
-            k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
-                                                      out, stride, v);
+            k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, bd->b0,
+                                                      bd->row_lo, rows_loc, in, out, stride, v);
             v += 4;
             count_launch();
         } else if (rem >= 2) {
-            k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
-                                                      out, stride, v);
+            k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, bd->b0,
+                                                      bd->row_lo, rows_loc, in, out, stride, v);
             v += 2;
             count_launch();
         } else {
-            k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, bd->nb, g->N, in,
-                                                      out, stride, v);
+            k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, bd->b0,
+                                                      bd->row_lo, rows_loc, in, out, stride, v);
             v += 1;
             count_launch();
         }
@@ -915,19 +919,15 @@ int bie_blockdiag_destroy(bie_blockdiag_t h) {
     return BIE_OK;
 }
 
-int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) {
-    Geometry *g = as_geom(gh);
-    if (!g || !out) {
-        set_error("bie_blockdiag_factor: invalid geometry handle or null output");
-        return BIE_EINVAL;
-    }
+static int factor_range(Geometry *g, int b0, int b1, bie_blockdiag_t *out, cudaStream_t st) {
     *out = nullptr;
-    cudaStream_t st = (cudaStream_t)stream;
     BlockDiag *bd = new BlockDiag();
     bd->g = g;
-    bd->nb = g->M + 1;
+    bd->b0 = b0;
+    bd->b1 = b1;
+    bd->nb = b1 - b0;
     long long off = 0;
-    for (int b = 0; b < bd->nb; ++b) {
+    for (int b = b0; b < b1; ++b) {
         int lo = b < g->M ? b * g->n_pore : g->wall_lo;
         int n = b < g->M ? g->n_pore : g->n_outer;
         bd->lo.push_back(lo);
@@ -936,6 +936,8 @@ int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) 
         off += 4LL * n * n;
     }
     bd->off.push_back(off);
+    bd->row_lo = bd->lo.front();
+    bd->row_hi = bd->lo.back() + bd->n.back();
     int *d_flag = nullptr;
     auto fail = [&](int rc) {
         cudaFree(d_flag);
@@ -953,14 +955,15 @@ int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) 
     e = cudaMemsetAsync(d_flag, 0, sizeof(int) * (size_t)bd->nb, st);
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemsetAsync(flags)"));
     int rc;
-    if (g->M > 0) {
-        BDView pv{bd->inv, 4LL * g->n_pore * g->n_pore, 2 * g->n_pore, g->M, 0};
-        rc = factor_class(g, pv, 0, g->n_pore, false, st, d_flag);
+    const int np_hi = std::min(b1, g->M);
+    if (b0 < np_hi) {  // pores [b0, np_hi)
+        BDView pv{bd->inv, 4LL * g->n_pore * g->n_pore, 2 * g->n_pore, np_hi - b0, b0};
+        rc = factor_class(g, pv, b0 * g->n_pore, g->n_pore, false, st, d_flag);
         if (rc) return fail(rc);
     }
-    {
-        BDView wv{bd->inv + bd->off[g->M], 0, 2 * g->n_outer, 1, g->M};
-        rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + g->M);
+    if (b1 == g->M + 1) {  // the wall
+        BDView wv{bd->inv + bd->off[g->M - b0], 0, 2 * g->n_outer, 1, g->M};
+        rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + (g->M - b0));
         if (rc) return fail(rc);
     }
     std::vector<int> flags(bd->nb);
@@ -968,8 +971,9 @@ int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) 
     if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemcpyAsync(flags)"));
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(cuda_fail(e, "bie_blockdiag_factor (kernels)"));
-    for (int b = 0; b < bd->nb; ++b) {
-        if (flags[b]) {
+    for (int q = 0; q < bd->nb; ++q) {
+        if (flags[q]) {
+            const int b = b0 + q;
             set_error("bie_blockdiag_factor: block of body " + std::to_string(b) +
                       (b < g->M ? " (pore)" : " (outer wall)") + " is singular (zero pivot)");
             return fail(BIE_ESINGULAR);
@@ -977,6 +981,36 @@ int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) 
     }
     cudaFree(d_flag);
     *out = reinterpret_cast<bie_blockdiag_t>(bd);
+    return BIE_OK;
+}
+
+int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out) {
+        set_error("bie_blockdiag_factor: invalid geometry handle or null output");
+        return BIE_EINVAL;
+    }
+    return factor_range(g, 0, g->M + 1, out, (cudaStream_t)stream);
+}
+
+int bie_blockdiag_factor_range(bie_geometry_t gh, int body_begin, int body_end, bie_blockdiag_t *out,
+                               void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out || body_begin < 0 || body_end > g->M + 1 || body_begin >= body_end) {
+        set_error("bie_blockdiag_factor_range: invalid handle/output or body range not in [0, M+1]");
+        return BIE_EINVAL;
+    }
+    return factor_range(g, body_begin, body_end, out, (cudaStream_t)stream);
+}
+
+int bie_blockdiag_rows(bie_blockdiag_t h, int *row_begin, int *row_end) {
+    BlockDiag *bd = as_bd(h);
+    if (!bd || !row_begin || !row_end) {
+        set_error("bie_blockdiag_rows: invalid handle or null output");
+        return BIE_EINVAL;
+    }
+    *row_begin = bd->row_lo;
+    *row_end = bd->row_hi;
     return BIE_OK;
 }
 
@@ -991,10 +1025,11 @@ int bie_blockdiag_apply(bie_blockdiag_t h, const double *in, double *out, int nv
 
 int bie_blockdiag_block_inverse(bie_blockdiag_t h, int body, double *host, long long host_len) {
     BlockDiag *bd = as_bd(h);
-    if (!bd || !host || body < 0 || body >= bd->nb) {
-        set_error("bie_blockdiag_block_inverse: invalid handle, body or buffer");
+    if (!bd || !host || body < bd->b0 || body >= bd->b1) {
+        set_error("bie_blockdiag_block_inverse: invalid handle, body not in the handle's range, or buffer");
         return BIE_EINVAL;
     }
+    body -= bd->b0;
     long long n = bd->off[body + 1] - bd->off[body];
     if (host_len < n) {
         set_error("bie_blockdiag_block_inverse: host buffer too small");

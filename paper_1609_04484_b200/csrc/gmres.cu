@@ -174,9 +174,101 @@ static int multiaxpy(const double *V, long long ldv, int nv, const double *c, do
     return BIE_OK;
 }
 
+__global__ void k_sqrt_n(const double *in, double *out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = sqrt(in[i]);
+}
+
 }  // namespace bie
 
 using namespace bie;
+
+// ---------------------------------------------------------------------------
+// Krylov building blocks (row-sharded GMRES): the same kernels
+// bie_gmres_solve uses, exposed so a multi-rank driver keeps every vector
+// operation in this library and only adds the collectives.
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int bie_krylov_dots(const double *V, long long ldv, int nv, const double *w, long long n, double *out,
+                    void *stream) {
+    if (!V || !w || !out || nv < 1 || n < 0) {
+        set_error("bie_krylov_dots: null pointer, nv < 1 or n < 0");
+        return BIE_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) {
+        BIE_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * nv, st));
+        return BIE_OK;
+    }
+    Dot d;
+    d.nchunks = (int)((n + kChunk - 1) / kChunk);
+    d.ldp = nv;
+    BIE_CUDA_TRY(cudaMallocAsync(&d.partial, sizeof(double) * (size_t)d.nchunks * nv, st));
+    int rc = multidot(V, ldv, nv, w, n, d, out, st);
+    cudaFreeAsync(d.partial, st);
+    return rc;
+}
+
+int bie_krylov_axpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,
+                    long long n, void *stream) {
+    if (!V || !c || !y || nv < 0 || n < 0) {
+        set_error("bie_krylov_axpy: null pointer, nv < 0 or n < 0");
+        return BIE_EINVAL;
+    }
+    if (n == 0) return BIE_OK;
+    return multiaxpy(V, ldv, nv, c, alpha, beta, y, n, (cudaStream_t)stream);
+}
+
+int bie_krylov_scale(const double *x, const double *s, double *y, long long n, void *stream) {
+    if (!x || !s || !y || n < 0) {
+        set_error("bie_krylov_scale: null pointer or n < 0");
+        return BIE_EINVAL;
+    }
+    if (n == 0) return BIE_OK;
+    k_scale_div<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, s, y, n);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+int bie_krylov_sqrt(const double *in, double *out, int n, void *stream) {
+    if (!in || !out || n < 1) {
+        set_error("bie_krylov_sqrt: null pointer or n < 1");
+        return BIE_EINVAL;
+    }
+    k_sqrt_n<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(in, out, n);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+int bie_krylov_givens(double *H, int ldh, double *cs, double *sn, double *g, const double *h, const double *h2,
+                      int k, double *scal, void *stream) {
+    if (!H || !cs || !sn || !g || !h || !h2 || !scal || k < 0 || ldh < k + 2) {
+        set_error("bie_krylov_givens: null pointer or bad k / ldh");
+        return BIE_EINVAL;
+    }
+    GmState s{H, cs, sn, g, const_cast<double *>(h), const_cast<double *>(h2), scal};
+    k_givens<<<1, 1, 0, (cudaStream_t)stream>>>(s, k, ldh);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+int bie_krylov_trisolve(const double *H, int ldh, const double *g, double *y, int iters, void *stream) {
+    if (!H || !g || !y || iters < 0 || ldh < iters) {
+        set_error("bie_krylov_trisolve: null pointer or bad iters / ldh");
+        return BIE_EINVAL;
+    }
+    if (iters == 0) return BIE_OK;
+    k_trisolve<<<1, 256, 0, (cudaStream_t)stream>>>(H, ldh, g, y, iters);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+}  // extern "C"
 
 extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f, double *x, double tol,
                                int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
@@ -190,6 +282,10 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     }
     if (bd && bd->g != g) {
         set_error("bie_gmres_solve: blockdiag was built from another geometry");
+        return BIE_EINVAL;
+    }
+    if (bd && (bd->b0 != 0 || bd->b1 != g->M + 1)) {
+        set_error("bie_gmres_solve: blockdiag covers a body range, not the whole geometry");
         return BIE_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -403,6 +499,10 @@ extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, con
     }
     if (bd && bd->g != g) {
         set_error("bie_gmres_solve_batch: blockdiag was built from another geometry");
+        return BIE_EINVAL;
+    }
+    if (bd && (bd->b0 != 0 || bd->b1 != g->M + 1)) {
+        set_error("bie_gmres_solve_batch: blockdiag covers a body range, not the whole geometry");
         return BIE_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;

@@ -80,6 +80,8 @@ void count_launch(int n = 1);
 struct BlockDiag {
     uint32_t magic = kBlockMagic;
     Geometry *g = nullptr;
+    int b0 = 0, b1 = 0;             // body range [b0, b1) (pores 0..M-1, wall M)
+    int row_lo = 0, row_hi = 0;     // node range covered; apply vectors are local [2 (row_hi-row_lo)]
     int nb = 0;                     // number of bodies
     std::vector<int> lo, n;         // node range per body
     std::vector<long long> off;     // offset of body b's inverse (doubles)

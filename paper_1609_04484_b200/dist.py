@@ -1,0 +1,185 @@
+"""Row-sharded BD-GMRES over several ranks.
+
+Each rank owns the nodes of a contiguous body range (shard.partition_rows):
+  * matvec  : all-gather of the density shards, then bie_dlp_apply_rows on the
+              rank's rows (the one exchange step of the operator);
+  * BD      : body-local blocks (bie_blockdiag_factor_range) -> no communication;
+  * GMRES   : Krylov vectors sharded by rows; every inner product is a local
+              bie_krylov_dots followed by an all-reduce of k+1 doubles; the
+              Givens/Hessenberg work (bie_krylov_givens) is replicated on every
+              rank from identical all-reduced inputs.
+`dist_gmres` is backend-agnostic: `GpuBackend` runs every vector operation in
+libbie.so kernels with NCCL collectives; the CPU tests drive the same algorithm
+with a gloo backend built on the oracle (tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .shard import partition_rows
+
+
+def bodies_of_rows(row_begin: int, row_end: int, M: int, n_pore: int):
+    """Body range [b0, b1) covering node range [row_begin, row_end) (cut at body boundaries)."""
+    wall_lo = M * n_pore
+
+    def body(node):
+        return node // n_pore if node < wall_lo else M
+
+    b0 = body(row_begin)
+    b1 = body(row_end - 1) + 1
+    return b0, b1
+
+
+def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000):
+    """Left-preconditioned full GMRES (reading C13) on row-sharded vectors.
+
+    be must provide: n, zeros(len), pc(x, out), apply_pc_op(v, out), apply_op(v, out),
+    dots(V, ldv, nv, w, out), axpy(V, ldv, nv, c, alpha, beta, y), scale(x, s, y),
+    sqrt(inp, out, m), givens(H, ldh, cs, sn, g, h, h2, k, scal), trisolve(H, ldh, g, y, iters),
+    allreduce_(t), copy_(dst, src), sub(a, b, out), host(t) -> numpy.
+    Returns (x_loc, dict(iters, hist, res_pc, res_true, converged))."""
+    n = be.n
+    ldh = max_iter + 1
+    V = be.zeros(ldh * n)
+    H = be.zeros(ldh * max_iter)
+    cs, sn, g, h, h2, tmp = (be.zeros(ldh) for _ in range(6))
+    scal = be.zeros(8)
+    w, t = be.zeros(n), be.zeros(n)
+    x = be.zeros(n)
+
+    def vec(k):
+        return V[k * n:(k + 1) * n]
+
+    def norm_into(v, i):  # scal[i] = ||v|| over all ranks
+        be.dots(v, 0, 1, v, tmp[0:1])
+        be.allreduce_(tmp[0:1])
+        be.sqrt(tmp[0:1], scal[i:i + 1], 1)
+
+    be.pc(f_loc, w)
+    norm_into(w, 0)
+    beta = float(be.host(scal[0:1])[0])
+    hist = [1.0]
+    if beta == 0.0:
+        return x, dict(iters=0, hist=np.array(hist), res_pc=0.0, res_true=0.0, converged=True)
+    be.scale(w, scal[0:1], vec(0))
+    be.copy_(g[0:1], scal[0:1])
+    it, conv = 0, False
+    for k in range(max_iter):
+        be.apply_pc_op(vec(k), w)
+        norm_into(w, 1)
+        be.dots(V, n, k + 1, w, h[:k + 1])
+        be.allreduce_(h[:k + 1])
+        be.axpy(V, n, k + 1, h, -1.0, 1.0, w)
+        be.dots(V, n, k + 1, w, h2[:k + 1])
+        be.allreduce_(h2[:k + 1])
+        be.axpy(V, n, k + 1, h2, -1.0, 1.0, w)
+        norm_into(w, 2)
+        be.givens(H, ldh, cs, sn, g, h, h2, k, scal)
+        est, brk = be.host(scal[3:5])
+        hist.append(float(est))
+        it = k + 1
+        if est < tol or brk != 0.0:
+            conv = True
+            break
+        if k + 1 < max_iter:
+            be.scale(w, scal[2:3], vec(k + 1))
+    be.trisolve(H, ldh, g, tmp, it)
+    be.axpy(V, n, it, tmp, 1.0, 0.0, x)
+    # residual pair (P:l.678-686)
+    be.apply_op(x, t)
+    be.sub(f_loc, t, w)
+    norm_into(w, 6)
+    norm_into(f_loc, 7)
+    be.pc(w, t)
+    norm_into(t, 5)
+    r5, r6, r7 = be.host(scal[5:8])
+    return x, dict(iters=it, hist=np.array(hist), res_pc=float(r5 / beta), res_true=float(r6 / r7), converged=conv)
+
+
+class GpuBackend:
+    """libbie.so kernels + torch.distributed (NCCL) collectives for one rank."""
+
+    def __init__(self, g, rank: int, world: int, group=None, stream=None):
+        import torch
+
+        from . import _bie as B
+
+        self.torch, self.B = torch, B
+        self.g, self.rank, self.world, self.group = g, rank, world, group
+        self.stream = stream
+        self.ranges = partition_rows(g.N, g.M, g.n_pore, world)
+        self.rb, self.re = self.ranges[rank]
+        self.n = 2 * (self.re - self.rb)
+        b0, b1 = bodies_of_rows(self.rb, self.re, g.M, g.n_pore)
+        self.bd = B.BlockDiag(g, bodies=(b0, b1))
+        assert self.bd.rows == (self.rb, self.re)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        self.maxlen = max(2 * (e - b) for b, e in self.ranges)
+        self.pad = torch.zeros(self.maxlen, dtype=torch.float64, device=dev)
+        self.gath = torch.zeros(world * self.maxlen, dtype=torch.float64, device=dev)
+        self.full = torch.zeros(2 * g.N, dtype=torch.float64, device=dev)
+        self.rows_out = torch.zeros(self.n, dtype=torch.float64, device=dev)
+
+    def zeros(self, m):
+        return self.torch.zeros(m, dtype=self.torch.float64, device=self.dev)
+
+    def _gather_full(self, v):
+        if self.world == 1:
+            self.full.copy_(v)
+            return self.full
+        import torch.distributed as dist
+
+        self.pad[: v.numel()].copy_(v)
+        dist.all_gather_into_tensor(self.gath, self.pad, group=self.group)
+        for r, (b, e) in enumerate(self.ranges):
+            self.full[2 * b:2 * e].copy_(self.gath[r * self.maxlen: r * self.maxlen + 2 * (e - b)])
+        return self.full
+
+    def apply_op(self, v, out):
+        full = self._gather_full(v)
+        self.B.dlp_apply_rows(self.g, full, out, self.rb, self.re, stream=self.stream)
+
+    def pc(self, x, out):
+        self.B.blockdiag_apply(self.bd, x, out, stream=self.stream)
+
+    def apply_pc_op(self, v, out):
+        self.apply_op(v, self.rows_out)
+        self.pc(self.rows_out, out)
+
+    def dots(self, V, ldv, nv, w, out):
+        self.B.Krylov.dots(V, ldv, nv, w, self.n, out, self.stream)
+
+    def axpy(self, V, ldv, nv, c, alpha, beta, y):
+        self.B.Krylov.axpy(V, ldv, nv, c, alpha, beta, y, self.n, self.stream)
+
+    def scale(self, x, s, y):
+        self.B.Krylov.scale(x, s, y, self.n, self.stream)
+
+    def sqrt(self, inp, out, m):
+        self.B.Krylov.sqrt(inp, out, m, self.stream)
+
+    def givens(self, H, ldh, cs, sn, g, h, h2, k, scal):
+        self.B.Krylov.givens(H, ldh, cs, sn, g, h, h2, k, scal, self.stream)
+
+    def trisolve(self, H, ldh, g, y, iters):
+        self.B.Krylov.trisolve(H, ldh, g, y, iters, self.stream)
+
+    def allreduce_(self, t):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(t, group=self.group)
+
+    def copy_(self, dst, src):
+        dst.copy_(src)
+
+    def sub(self, a, b, out):  # out = a - b with the library's axpy kernel
+        if not hasattr(self, "_one"):
+            self._one = self.torch.ones(1, dtype=self.torch.float64, device=self.dev)
+        out.copy_(a)
+        self.B.Krylov.axpy(b, 0, 1, self._one, -1.0, 1.0, out, self.n, self.stream)
+
+    def host(self, t):
+        return t.cpu().numpy()
