@@ -9,8 +9,8 @@ Each rank owns the nodes of a contiguous body range (shard.partition_rows):
               Givens/Hessenberg work (bie_krylov_givens) is replicated on every
               rank from identical all-reduced inputs.
 `dist_gmres` is backend-agnostic: `GpuBackend` runs every vector operation in
-libbie.so kernels with NCCL collectives; the CPU tests drive the same algorithm
-with a gloo backend built on the oracle (tests/test_dist_gloo.py).
+libbie.so kernels with NCCL collectives; tests/test_dist_gloo.py drives the
+same algorithm with a CPU/gloo test backend.
 """
 from __future__ import annotations
 
