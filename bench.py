@@ -13,6 +13,11 @@ once before timing and is reported separately ("build PC", P:l.720).
 
 metric = DLP matvec pair-interactions/s (N^2 per matvec, self pairs included
 since the kernel evaluates them branch-free).
+
+N > 1 (torchrun): the SAME solve is row-sharded over the ranks
+(paper_1609_04484_b200.dist: body-range BD, all-gather of the density per
+matvec, all-reduced inner products over NCCL) -> strong scaling; value is the
+whole job's pair interactions over the max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -164,7 +169,7 @@ def run_reference(args):
         "impl": "reference", "metric": "DLP matvec pair-interactions/s", "value": value,
         "unit": "pair-interactions/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * pairs_per_step * p.N * p.N / value, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config4 pipe L=100 M=1000 N={p.N}: oracle completed DLP matvec rows "
                                f"(bounded sample per step; ms_per_step extrapolated to {pairs_per_step} matvecs)",
                    "N": p.N, "unknowns": 2 * p.N},
@@ -238,19 +243,34 @@ def run_gpu(args):
     torch.cuda.synchronize()
     t_geom = time.perf_counter() - t0
     t0 = time.perf_counter()
-    bd = bie.BlockDiag(g)
+    if ws == 1:
+        bd = bie.BlockDiag(g)
+        rb, re_ = 0, N
+    else:
+        # row-sharded solve: body-range BD on each rank,
+        # all-gather of the density per matvec, all-reduced inner products
+        from paper_1609_04484_b200.dist import GpuBackend, dist_gmres
+
+        be = GpuBackend(g, rank, ws)
+        rb, re_ = be.rb, be.re
     torch.cuda.synchronize()
     t_bd = time.perf_counter() - t0
 
-    f_host = torch.from_numpy(rhs_pipe(p)).pin_memory()
+    f_full = rhs_pipe(p)
+    f_host = torch.from_numpy(np.ascontiguousarray(f_full[2 * rb:2 * re_])).pin_memory()
     f = f_host.to(dev)
     x = torch.zeros_like(f)
     x_host = torch.zeros_like(f_host).pin_memory()
     flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.float64, device=dev)
+    # whole-job pair interactions per step (all ranks together)
     pairs_per_step = (GMRES_ITERS + 1) * N * N
 
     def step():
-        return bie.gmres_solve(g, bd, f, x, tol=1e-30, max_iter=GMRES_ITERS)
+        if ws == 1:
+            return bie.gmres_solve(g, bd, f, x, tol=1e-30, max_iter=GMRES_ITERS)
+        xx, rr = dist_gmres(be, f, tol=1e-30, max_iter=GMRES_ITERS)
+        x.copy_(xx)
+        return rr
 
     for _ in range(max(3, args.warmup)):
         r = step()
@@ -282,11 +302,12 @@ def run_gpu(args):
         tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total = tt.item()
-    value = ws * args.steps * pairs_per_step / t_total
+    # N = 1: one solve; N > 1: ONE solve sharded over the ranks (strong scaling)
+    value = args.steps * pairs_per_step / t_total
 
-    # ---- dominant kernel roofline (k_dlp_pairs, CUDA events on the launch stream)
+    # ---- dominant kernel roofline (all-pairs phase, CUDA events on the launch stream)
     pair_ms = prof["pairs_ms"] / max(1, prof["applies"])
-    achieved_tflops = FLOP_PER_PAIR * N * N / (pair_ms * 1e-3) / 1e12
+    achieved_tflops = FLOP_PER_PAIR * N * (re_ - rb) / (pair_ms * 1e-3) / 1e12  # this rank's rows
     pairs_share = prof["pairs_ms"] / sum(step_ms)
 
     # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
@@ -306,7 +327,7 @@ def run_gpu(args):
         e2e_s = tt.item()
 
     extra = {}
-    if rank == 0 and not args.quick:
+    if rank == 0 and ws == 1 and not args.quick:
         # matvec-only sweep (bie_dlp_apply, BIE_FULL) and full GMRES solves
         sweep = {}
         for nvec in (1, 4, 16):
@@ -361,21 +382,24 @@ def run_gpu(args):
     line = {
         "metric": "DLP matvec pair-interactions/s", "value": value, "unit": "pair-interactions/s", "n_gpus": ws,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": statistics.mean(step_ms),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config4 pipe L=100 M=1000 N={N} (2N={2 * N} unknowns), pipe BC; step = "
                                f"BD-preconditioned GMRES solve, fixed {GMRES_ITERS} iterations "
                                f"({GMRES_ITERS + 1} completed DLP matvecs + BD applies + CGS2)",
                    "N": N, "unknowns": 2 * N, "gmres_iters_per_step": GMRES_ITERS,
-                   "matvecs_per_step": GMRES_ITERS + 1, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "matvecs_per_step": GMRES_ITERS + 1,
+                   "parallelism": f"rows{ws} (row-sharded solve, all-gather + all-reduce over NCCL)" if ws > 1
+                   else "single",
                    "l2": "flushed between timed steps (256 MiB write); BD inverses (2.67 GB) exceed L2 each step"},
-        "roofline": {"kernel": "all-pairs phase: k_dlp_sym<8,2> + k_dlp_diag (nvec=1 symmetric path)",
+        "roofline": {"kernel": ("all-pairs phase: k_dlp_sym<8,2> + k_dlp_diag (nvec=1 symmetric path)" if ws == 1
+                                else "k_dlp_pairs<1,4,256> on this rank's rows (one-sided)"),
                      "bound": "alu", "achieved": achieved_tflops,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
                      "traffic": _ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
                      "kernel_share_of_step": pairs_share,
-                     "executed_flop_per_pair": 17,
+                     "executed_flop_per_pair": 17 if ws == 1 else 24,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
-        "e2e": {"value": ws * args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
+        "e2e": {"value": args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
                 "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8)},
         "gpu_launches": int(launches),
         "clocks": clocks,

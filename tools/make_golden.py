@@ -15,7 +15,7 @@ OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 CASES = {
     "config3_bd_pipe": dict(config=3, pc="bd", tol=1e-8, max_iter=1000, env_runs=2),
     "config4_none_pipe_prefix": dict(config=4, pc="none", tol=1e-8, max_iter=6),
-    "config4_bd_pipe_prefix": dict(config=4, pc="bdlu", tol=1e-8, max_iter=8),
+    "config4_bd_pipe_prefix": dict(config=4, pc="bdlu", tol=1e-8, max_iter=8, env_runs=2),
 }
 for name in (sys.argv[1:] or list(CASES)):
     c = CASES[name]
@@ -37,7 +37,11 @@ for name in (sys.argv[1:] or list(CASES)):
     env_iters = []
     for s in range(c.get("env_runs", 0)):
         rng = np.random.default_rng(300 + s)
-        rp = oracle.gmres(g, f * (1 + 1e-13 * rng.standard_normal(f.size)), bd, tol=c["tol"], max_iter=c["max_iter"])
+        fp = f * (1 + 1e-13 * rng.standard_normal(f.size))
+        if c["pc"] == "bdlu":
+            rp = oracle.gmres_bdlu(g, fp, bd, tol=c["tol"], max_iter=c["max_iter"])
+        else:
+            rp = oracle.gmres(g, fp, bd, tol=c["tol"], max_iter=c["max_iter"])
         n = min(len(r["hist"]), len(rp["hist"]))
         env[:n] = np.maximum(env[:n], np.abs(rp["hist"][:n] - r["hist"][:n]) / r["hist"][:n])
         env_iters.append(rp["iters"])
