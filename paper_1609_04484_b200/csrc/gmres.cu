@@ -39,14 +39,18 @@ __global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restri
     const int j = blockIdx.y * (kDotThreads / 32) + wid;
     if (j >= nv) return;
     const double *vj = V + (long long)j * ldv + e0;
-    double acc0 = 0.0, acc1 = 0.0;
+    // four independent streams per lane keep enough loads in flight for HBM
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     int q = lane;
-    for (; q + 32 < len; q += 64) {
-        acc0 = fma(vj[q], ws[q], acc0);
-        acc1 = fma(vj[q + 32], ws[q + 32], acc1);
+    for (; q + 96 < len; q += 128) {
+        const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64), a3 = __ldcs(vj + q + 96);
+        acc0 = fma(a0, ws[q], acc0);
+        acc1 = fma(a1, ws[q + 32], acc1);
+        acc2 = fma(a2, ws[q + 64], acc2);
+        acc3 = fma(a3, ws[q + 96], acc3);
     }
-    if (q < len) acc0 = fma(vj[q], ws[q], acc0);
-    double acc = acc0 + acc1;
+    for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
+    double acc = (acc0 + acc1) + (acc2 + acc3);
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) partial[(long long)blockIdx.x * ldp + j] = acc;
 }
