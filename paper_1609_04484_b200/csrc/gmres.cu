@@ -22,7 +22,7 @@
 namespace bie {
 
 constexpr int kChunk = 4096;      // elements of the 2N dimension per multidot CTA
-constexpr int kDotThreads = 256;
+constexpr int kDotThreads = 512;  // 16 basis vectors share one staged w chunk
 
 // partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv).
 // Grid (chunks, ceil(nv / 8)); each of the 8 warps owns one basis vector j and
