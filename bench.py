@@ -370,6 +370,26 @@ def run_gpu(args):
                                    "iters": rr["iters"], "converged": rr["converged"], "max_iter": mi,
                                    "res_pc": rr["res_pc"], "res_true": rr["res_true"], "tol": 1e-8}
         extra["gmres_solve"] = sol
+        # NEXT-3: 16 right-hand sides on config 3 -- batched solver vs 16 single solves
+        pp = make_problem(3)
+        gg = bie.Geometry.from_problem(pp)
+        bdd = bie.BlockDiag(gg)
+        F = torch.from_numpy(density(pp, nvec=16, vec_id=100).reshape(-1)).to(dev)
+        X = torch.zeros_like(F)
+        bie.gmres_solve_batch(gg, bdd, F, X, nrhs=16, tol=1e-8, max_iter=1000)  # warm-up
+        torch.cuda.synchronize()
+        tb = time.perf_counter()
+        rb_ = bie.gmres_solve_batch(gg, bdd, F, X, nrhs=16, tol=1e-8, max_iter=1000)
+        torch.cuda.synchronize()
+        tb = time.perf_counter() - tb
+        ts = time.perf_counter()
+        n2 = 2 * pp.N
+        for r in range(16):
+            bie.gmres_solve(gg, bdd, F[r * n2:(r + 1) * n2], X[r * n2:(r + 1) * n2], tol=1e-8, max_iter=1000)
+        torch.cuda.synchronize()
+        ts = time.perf_counter() - ts
+        extra["multi_rhs"] = {"config": 3, "nrhs": 16, "batched_s": tb, "sequential_s": ts,
+                              "iters": [r["iters"] for r in rb_], "all_converged": all(r["converged"] for r in rb_)}
         if not args.no_config5:
             extra["config5_sweep"] = config5_sweep(bie, dev, stream)
 
