@@ -196,6 +196,26 @@ BIE_API int bie_blockdiag_factor_range(bie_geometry_t g, int body_begin, int bod
 BIE_API int bie_blockdiag_rows(bie_blockdiag_t bd, int *row_begin, int *row_end);
 
 /*
+ * Sharded symmetric matvec, nvec = 1.  The all-pairs work of
+ * the symmetric kernel is a triangular list of `units` (512-node block x
+ * 32-node chunk after it) plus `blocks` in-block diagonal tiles
+ * (bie_dlp_sym_info).  bie_dlp_pairs_partial computes the pair sums
+ * sum_{j != i} (w_j/pi)(r.n_j)(r.sigma_j) r/rho^4 restricted to units
+ * [unit_begin, unit_end) and diagonal blocks [block_begin, block_end) into a
+ * FULL output out_full [2N] (both directions of every pair in the slice); the
+ * ranks' vectors sum (e.g. NCCL reduce-scatter) to the complete pair sum.
+ * bie_dlp_epilogue_rows then adds the local terms of the operator (jump, self,
+ * N0, completion -- BIE_FULL; self only -- BIE_D_ONLY) for rows
+ * [row_begin, row_end): out_rows = pairsum_rows + local terms, both [2 rows].
+ * sigma is the full density [2N].  Async on stream.
+ */
+BIE_API int bie_dlp_sym_info(bie_geometry_t g, long long *units, int *blocks);
+BIE_API int bie_dlp_pairs_partial(bie_geometry_t g, const double *sigma, double *out_full, long long unit_begin,
+                                  long long unit_end, int block_begin, int block_end, void *stream);
+BIE_API int bie_dlp_epilogue_rows(bie_geometry_t g, const double *sigma, const double *pairsum_rows,
+                                  double *out_rows, int row_begin, int row_end, unsigned flags, void *stream);
+
+/*
  * Krylov building blocks for a row-sharded GMRES (the kernels bie_gmres_solve
  * uses; a multi-rank driver adds only the collectives).  All device pointers,
  * async on stream; reading C13 conventions:

@@ -19,6 +19,9 @@ from ._bie import (  # noqa: F401
     dlp_apply,
     dlp_apply_host,
     dlp_apply_rows,
+    dlp_epilogue_rows,
+    dlp_pairs_partial,
+    dlp_sym_info,
     field_eval,
     gmres_solve,
     gmres_solve_batch,

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "bie_gmres_solve", "bie_last_error", "bie_profile_begin", "bie_profile_end", "bie_launch_count",
     "bie_field_eval", "bie_gmres_solve_batch", "bie_blockdiag_factor_range", "bie_blockdiag_rows",
     "bie_krylov_dots", "bie_krylov_axpy", "bie_krylov_scale", "bie_krylov_sqrt", "bie_krylov_givens",
-    "bie_krylov_trisolve",
+    "bie_krylov_trisolve", "bie_dlp_sym_info", "bie_dlp_pairs_partial", "bie_dlp_epilogue_rows",
 )
 
 
@@ -79,6 +79,9 @@ def lib():
         "bie_krylov_sqrt": [vp, vp, c_int, vp],
         "bie_krylov_givens": [vp, c_int, vp, vp, vp, vp, vp, c_int, vp, vp],
         "bie_krylov_trisolve": [vp, c_int, vp, vp, c_int, vp],
+        "bie_dlp_sym_info": [vp, ctypes.POINTER(ctypes.c_longlong), ip],
+        "bie_dlp_pairs_partial": [vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong, c_int, c_int, vp],
+        "bie_dlp_epilogue_rows": [vp, vp, vp, vp, c_int, c_int, c_uint, vp],
         "bie_profile_begin": [vp],
         "bie_profile_end": [vp, dp, dp, dp, ip],
     }
@@ -188,6 +191,30 @@ def dlp_apply(g: Geometry, sigma, out, nvec: int = 1, flags: int = BIE_FULL, str
     _check(lib().bie_dlp_apply(g.h, _dev_ptr(sigma, "sigma", n), _dev_ptr(out, "out", n), nvec, flags,
                                _stream_ptr(stream)))
     return out
+
+
+def dlp_sym_info(g: Geometry):
+    """(units, blocks) of the symmetric all-pairs work list (bie_dlp_sym_info)."""
+    u, b = ctypes.c_longlong(), ctypes.c_int()
+    _check(lib().bie_dlp_sym_info(g.h, ctypes.byref(u), ctypes.byref(b)))
+    return u.value, b.value
+
+
+def dlp_pairs_partial(g: Geometry, sigma, out_full, units, blocks, stream=None):
+    """Pair sums of a slice of the symmetric work into a full [2N] vector (bie_dlp_pairs_partial)."""
+    _check(lib().bie_dlp_pairs_partial(g.h, _dev_ptr(sigma, "sigma", 2 * g.N), _dev_ptr(out_full, "out", 2 * g.N),
+                                       int(units[0]), int(units[1]), int(blocks[0]), int(blocks[1]),
+                                       _stream_ptr(stream)))
+    return out_full
+
+
+def dlp_epilogue_rows(g: Geometry, sigma, pairsum_rows, out_rows, row_begin: int, row_end: int,
+                      flags: int = BIE_FULL, stream=None):
+    """out_rows = pairsum_rows + local operator terms on [row_begin, row_end) (bie_dlp_epilogue_rows)."""
+    n = 2 * (row_end - row_begin)
+    _check(lib().bie_dlp_epilogue_rows(g.h, _dev_ptr(sigma, "sigma", 2 * g.N), _dev_ptr(pairsum_rows, "pairsum", n),
+                                       _dev_ptr(out_rows, "out", n), row_begin, row_end, flags, _stream_ptr(stream)))
+    return out_rows
 
 
 def field_eval(g: Geometry, sigma, targets, out, stream=None):

@@ -283,7 +283,8 @@ struct SymArgs {
     double *tgt_partial;   // [S][2N]
     double *src_partial;   // [nTB][2N]
     int N, nTB;
-    long long U;
+    long long U;           // units in this launch's slice [ub, ub + U) of the triangular list
+    long long ub;          // 0 for the single-GPU matvec; a rank's slice start when sharded
 };
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int P = gridDim.x, p = blockIdx.x;
     const long long U = a.U;
-    const long long u0 = ((long long)p * U) / P, u1 = ((long long)(p + 1) * U) / P;
+    const long long u0 = a.ub + ((long long)p * U) / P, u1 = a.ub + ((long long)(p + 1) * U) / P;
     if (u0 >= u1) return;
     const int N = a.N;
     // block containing u0: largest A with off[A] <= u0
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
         }
         __syncthreads();
         if (u + 1 == u1 || u + 1 == offA1) {
-            const int slot = p - unit_owner(offA, U, P);
+            const int slot = p - unit_owner(std::max(offA, a.ub) - a.ub, U, P);
 #pragma unroll
             for (int r = 0; r < SR; ++r) {
                 const int i = A * kSymTB + w * (32 * SR) + r * 32 + lane;
@@ -475,9 +476,10 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
 // Pairs inside one 512-node block (one-sided, all ordered pairs, self pair
 // zeroed by the rho^2 + 1e-300 rule).  One CTA per block, 128 threads x 4 targets.
 __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ pos, const double2 *__restrict__ nw,
-                                                  const double *__restrict__ sigma, double *diag, int N) {
+                                                  const double *__restrict__ sigma, double *diag, int N,
+                                                  int blk0 = 0) {
     __shared__ double2 sp[3][kSymTB];
-    const int A = blockIdx.x, tid = threadIdx.x;
+    const int A = blk0 + blockIdx.x, tid = threadIdx.x;
     const int base = A * kSymTB;
     for (int q = tid; q < kSymTB; q += 128) {
         const int j = base + q;
@@ -548,6 +550,7 @@ struct EpiArgs {
     int nchunks;
     Chunk ch[5];
     SymEpi sym;
+    const double *presum;  // nvec = 1: pair sums already reduced (sharded path), local rows [2 Nt]
 };
 
 // A4 + A5: reduce the split partials in fixed slot order, then add the local
@@ -567,6 +570,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
     const bool full = !(a.flags & BIE_D_ONLY);
     constexpr double k4pi = 1.0 / (4.0 * kPi);
     double2 u[NVC > 0 ? NVC : BIE_MAX_NVEC];
+    if (a.presum) u[0] = reinterpret_cast<const double2 *>(a.presum)[it];
     if (a.sym.on) {
         // fixed order: target-side slots, the in-block pairs, then source-side
         // partials of every earlier block
@@ -883,7 +887,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         count_launch();
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
         if (g->sym_U > 0) {
-            SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, g->sym_U};
+            SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, g->sym_U, 0};
             launch_sym(g->sym_variant, g->sym_P, sa, st);
             count_launch();
         }
@@ -1019,6 +1023,130 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
     if (active) reinterpret_cast<double2 *>(out)[it] = u;
 }
 
+// ---------------------------------------------------------------------------
+// Sharded symmetric path: a rank computes the pair sums of a
+// slice [ub, ue) of the triangular unit list plus the in-block pairs of blocks
+// [blk0, blk1) into a full-size vector; the ranks' vectors are reduce-scattered
+// and each rank finishes its rows with bie_dlp_epilogue_rows.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sym_gather(const double *__restrict__ tgt, const double *__restrict__ src,
+                                                    const double *__restrict__ diag, const long long *__restrict__ off,
+                                                    int N, long long ub, long long U, int P, int blk0, int blk1,
+                                                    double *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int B = i / kSymTB;
+    double2 acc = make_double2(0.0, 0.0);
+    const long long lo = max(off[B], ub), hi = min(off[B + 1], ub + U);
+    if (hi > lo) {
+        const int first = unit_owner(lo - ub, U, P), last = unit_owner(hi - 1 - ub, U, P);
+        for (int sl = 0; sl <= last - first; ++sl) {
+            const double2 pv = reinterpret_cast<const double2 *>(tgt + (long long)sl * 2LL * N)[i];
+            acc.x += pv.x;
+            acc.y += pv.y;
+        }
+    }
+    if (B >= blk0 && B < blk1) {
+        const double2 pv = reinterpret_cast<const double2 *>(diag)[i];
+        acc.x += pv.x;
+        acc.y += pv.y;
+    }
+    const int c = i / kSymChunk;
+    for (int A = 0; A < B; ++A) {
+        const long long u = off[A] + (c - (A + 1) * (kSymTB / kSymChunk));
+        if (u >= ub && u < ub + U) {
+            const double2 pv = reinterpret_cast<const double2 *>(src + (long long)A * 2LL * N)[i];
+            acc.x += pv.x;
+            acc.y += pv.y;
+        }
+    }
+    reinterpret_cast<double2 *>(out)[i] = acc;
+}
+
+int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long long ub, long long ue, int blk0,
+                       int blk1, cudaStream_t st) {
+    int rc = sym_prepare(g);
+    if (rc) return rc;
+    if (g->sym_state != 1) {
+        set_error("bie_dlp_pairs_partial: symmetric path unavailable (memory cap)");
+        return BIE_ENOMEM;
+    }
+    const int N = g->N;
+    const long long U = ue - ub;
+    k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+    count_launch();
+    int P = 1;
+    if (U > 0) {
+        // slots needed for this slice
+        std::vector<long long> off(g->sym_nTB + 1);
+        BIE_CUDA_TRY(cudaMemcpy(off.data(), g->sym_off, sizeof(long long) * off.size(), cudaMemcpyDeviceToHost));
+        int occ = 0;
+        BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel(g->sym_variant),
+                                                                   32 * sym_warps(g->sym_variant), 0));
+        P = (int)std::max<long long>(1, std::min<long long>((long long)g->num_sms * std::max(1, occ), U));
+        int S = 1;
+        for (int A = 0; A < g->sym_nTB; ++A) {
+            const long long lo = std::max(off[A], ub), hi = std::min(off[A + 1], ue);
+            if (hi > lo) S = std::max(S, unit_owner(hi - 1 - ub, U, P) - unit_owner(lo - ub, U, P) + 1);
+        }
+        if (S > g->sym_S) {
+            BIE_CUDA_TRY(cudaStreamSynchronize(st));
+            cudaFree(g->sym_tgt);
+            g->sym_tgt = nullptr;
+            BIE_CUDA_TRY(cudaMalloc(&g->sym_tgt, sizeof(double) * 2 * (size_t)N * S));
+            g->sym_S = S;
+        }
+        SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, U, ub};
+        launch_sym(g->sym_variant, P, sa, st);
+        count_launch();
+    }
+    if (blk1 > blk0) {
+        k_dlp_diag<<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
+        count_launch();
+    }
+    k_sym_gather<<<(N + 255) / 256, 256, 0, st>>>(g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, N, ub, U, P, blk0,
+                                                  blk1, out_full);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
+int epilogue_rows_impl(Geometry *g, const double *sigma, const double *presum, double *out, int rb, int re,
+                       unsigned flags, cudaStream_t st) {
+    const int N = g->N;
+    const int Nt = re - rb;
+    if (Nt <= 0) return BIE_OK;
+    if (!(flags & BIE_D_ONLY)) {
+        k_moments<<<g->M + 1, 256, 0, st>>>(g->pos, g->nrm, g->w, g->pore, sigma, 2LL * N, 1, g->M, g->n_pore,
+                                            g->wall_lo, N, g->wall_len, g->moments);
+        count_launch();
+    }
+    EpiArgs ea{};
+    ea.pos = g->pos;
+    ea.nrm = g->nrm;
+    ea.tan = g->tan;
+    ea.selfc = g->selfc;
+    ea.pore = g->pore;
+    ea.sigma = sigma;
+    ea.sig_stride = 2LL * N;
+    ea.partial = nullptr;
+    ea.moments = g->moments;
+    ea.out = out;
+    ea.nvec = 1;
+    ea.N = N;
+    ea.M = g->M;
+    ea.wall_lo = g->wall_lo;
+    ea.row_begin = rb;
+    ea.Nt = Nt;
+    ea.flags = flags;
+    ea.nchunks = 0;
+    ea.presum = presum;
+    k_epilogue<1><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
 int field_eval_impl(Geometry *g, const double *sigma, const double2 *targets, int ntgt, double *out, cudaStream_t st) {
     if (ntgt == 0) return BIE_OK;
     const int N = g->N;
@@ -1107,6 +1235,51 @@ int bie_dlp_apply_rows(bie_geometry_t gh, const double *sigma, double *out, int 
         return BIE_EINVAL;
     }
     return dlp_apply_impl(g, sigma, out, nvec, flags, row_begin, row_end, (cudaStream_t)stream);
+}
+
+int bie_dlp_sym_info(bie_geometry_t gh, long long *units, int *blocks) {
+    Geometry *g = as_geom(gh);
+    if (!g || !units || !blocks) {
+        set_error("bie_dlp_sym_info: invalid handle or null output");
+        return BIE_EINVAL;
+    }
+    int rc = sym_prepare(g);
+    if (rc) return rc;
+    if (g->sym_state != 1) {
+        set_error("bie_dlp_sym_info: symmetric path unavailable (memory cap)");
+        return BIE_ENOMEM;
+    }
+    *units = g->sym_U;
+    *blocks = g->sym_nTB;
+    return BIE_OK;
+}
+
+int bie_dlp_pairs_partial(bie_geometry_t gh, const double *sigma, double *out_full, long long unit_begin,
+                          long long unit_end, int block_begin, int block_end, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !sigma || !out_full || sigma == out_full) {
+        set_error("bie_dlp_pairs_partial: invalid handle, null pointer or aliasing");
+        return BIE_EINVAL;
+    }
+    int rc = sym_prepare(g);
+    if (rc) return rc;
+    if (unit_begin < 0 || unit_end > g->sym_U || unit_begin > unit_end || block_begin < 0 ||
+        block_end > g->sym_nTB || block_begin > block_end) {
+        set_error("bie_dlp_pairs_partial: unit or block range out of bounds (see bie_dlp_sym_info)");
+        return BIE_EINVAL;
+    }
+    return pairs_partial_impl(g, sigma, out_full, unit_begin, unit_end, block_begin, block_end, (cudaStream_t)stream);
+}
+
+int bie_dlp_epilogue_rows(bie_geometry_t gh, const double *sigma, const double *pairsum_rows, double *out_rows,
+                          int row_begin, int row_end, unsigned flags, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !sigma || !pairsum_rows || !out_rows || (flags & ~BIE_D_ONLY) || row_begin < 0 || row_end > g->N ||
+        row_begin > row_end) {
+        set_error("bie_dlp_epilogue_rows: invalid handle, pointer, flags or row range");
+        return BIE_EINVAL;
+    }
+    return epilogue_rows_impl(g, sigma, pairsum_rows, out_rows, row_begin, row_end, flags, (cudaStream_t)stream);
 }
 
 int bie_field_eval(bie_geometry_t gh, const double *sigma, const double *targets, int ntgt, double *out,

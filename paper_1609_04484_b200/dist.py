@@ -98,9 +98,16 @@ def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000):
 
 
 class GpuBackend:
-    """libbie.so kernels + torch.distributed (NCCL) collectives for one rank."""
+    """libbie.so kernels + torch.distributed (NCCL) collectives for one rank.
 
-    def __init__(self, g, rank: int, world: int, group=None, stream=None):
+    mode "sym" (default): every rank computes a slice of the symmetric kernel's
+    work list into a full-size vector, the vectors are reduce-scattered to the
+    row owners, and each rank adds the local terms of its rows
+    (bie_dlp_pairs_partial -> reduce-scatter -> bie_dlp_epilogue_rows): the
+    11-instruction pair kernel is kept at N > 1.
+    mode "rows": each rank evaluates its rows one-sidedly (bie_dlp_apply_rows)."""
+
+    def __init__(self, g, rank: int, world: int, group=None, stream=None, mode: str = "sym"):
         import torch
 
         from . import _bie as B
@@ -121,6 +128,14 @@ class GpuBackend:
         self.gath = torch.zeros(world * self.maxlen, dtype=torch.float64, device=dev)
         self.full = torch.zeros(2 * g.N, dtype=torch.float64, device=dev)
         self.rows_out = torch.zeros(self.n, dtype=torch.float64, device=dev)
+        self.mode = mode
+        if mode == "sym":
+            U, nblk = B.dlp_sym_info(g)
+            self.units = (U * rank // world, U * (rank + 1) // world)
+            self.blocks = (nblk * rank // world, nblk * (rank + 1) // world)
+            self.part_full = torch.zeros(2 * g.N, dtype=torch.float64, device=dev)
+            self.send = torch.zeros(world * self.maxlen, dtype=torch.float64, device=dev)
+            self.recv = torch.zeros(self.maxlen, dtype=torch.float64, device=dev)
 
     def zeros(self, m):
         return self.torch.zeros(m, dtype=self.torch.float64, device=self.dev)
@@ -139,7 +154,20 @@ class GpuBackend:
 
     def apply_op(self, v, out):
         full = self._gather_full(v)
-        self.B.dlp_apply_rows(self.g, full, out, self.rb, self.re, stream=self.stream)
+        if self.mode == "rows":
+            self.B.dlp_apply_rows(self.g, full, out, self.rb, self.re, stream=self.stream)
+            return
+        self.B.dlp_pairs_partial(self.g, full, self.part_full, self.units, self.blocks, stream=self.stream)
+        if self.world == 1:
+            rows = self.part_full
+        else:
+            import torch.distributed as dist
+
+            for r, (b, e) in enumerate(self.ranges):
+                self.send[r * self.maxlen: r * self.maxlen + 2 * (e - b)].copy_(self.part_full[2 * b:2 * e])
+            dist.reduce_scatter_tensor(self.recv, self.send, group=self.group)
+            rows = self.recv[: self.n]
+        self.B.dlp_epilogue_rows(self.g, full, rows, out, self.rb, self.re, stream=self.stream)
 
     def pc(self, x, out):
         self.B.blockdiag_apply(self.bd, x, out, stream=self.stream)
