@@ -307,7 +307,8 @@ def run_gpu(args):
 
     # ---- dominant kernel roofline (all-pairs phase, CUDA events on the launch stream)
     pair_ms = prof["pairs_ms"] / max(1, prof["applies"])
-    achieved_tflops = FLOP_PER_PAIR * N * (re_ - rb) / (pair_ms * 1e-3) / 1e12  # this rank's rows
+    # the rank's share of the N^2 pair interactions (units and diagonal blocks split evenly)
+    achieved_tflops = FLOP_PER_PAIR * N * N / ws / (pair_ms * 1e-3) / 1e12
     pairs_share = prof["pairs_ms"] / sum(step_ms)
 
     # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
@@ -412,12 +413,12 @@ def run_gpu(args):
                    else "single",
                    "l2": "flushed between timed steps (256 MiB write); BD inverses (2.67 GB) exceed L2 each step"},
         "roofline": {"kernel": ("all-pairs phase: k_dlp_sym<8,2> + k_dlp_diag (nvec=1 symmetric path)" if ws == 1
-                                else "k_dlp_pairs<1,4,256> on this rank's rows (one-sided)"),
+                                else "all-pairs phase on this rank's slice of the symmetric work list"),
                      "bound": "alu", "achieved": achieved_tflops,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
                      "traffic": _ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
                      "kernel_share_of_step": pairs_share,
-                     "executed_flop_per_pair": 17 if ws == 1 else 24,
+                     "executed_flop_per_pair": 17,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
         "e2e": {"value": args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
                 "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8)},

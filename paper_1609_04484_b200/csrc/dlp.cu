@@ -1073,8 +1073,20 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
     }
     const int N = g->N;
     const long long U = ue - ub;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (g->prof) {  // same phase events as dlp_apply_impl (moments slot unused)
+        while (g->prof_ev.size() < g->prof_used + 4) {
+            cudaEvent_t e;
+            BIE_CUDA_TRY(cudaEventCreate(&e));
+            g->prof_ev.push_back(e);
+        }
+        for (int q = 0; q < 4; ++q) ev[q] = g->prof_ev[g->prof_used + q];
+        g->prof_used += 4;
+        BIE_CUDA_TRY(cudaEventRecord(ev[0], st));
+    }
     k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
     count_launch();
+    if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
     int P = 1;
     if (U > 0) {
         // slots needed for this slice
@@ -1104,10 +1116,12 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         k_dlp_diag<<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
         count_launch();
     }
+    if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
     k_sym_gather<<<(N + 255) / 256, 256, 0, st>>>(g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, N, ub, U, P, blk0,
                                                   blk1, out_full);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
+    if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));
     return BIE_OK;
 }
 
