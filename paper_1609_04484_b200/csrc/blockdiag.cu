@@ -650,13 +650,29 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
     const int lane = tid & 31, wid = tid >> 5;
     const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
     const int gr = lane >> 2, gq = lane & 3;
-    for (int q = tid; q < UT3 * NB; q += 128) {
-        const int i = q / NB, c = q % NB;
-        Ts[i][c] = (i0 + i < n2) ? T[(long long)(i0 + i) * NB + c] : 0.0;
-    }
-    for (int q = tid; q < NB * UT3; q += 128) {
-        const int c = q / UT3, j = q % UT3;
-        Gs[c][j] = (j0 + j < n2) ? G[(long long)c * n2 + j0 + j] : 0.0;
+    // staging: all 32 loads of a thread are issued before any shared store
+    // (latency-bound otherwise: ncu showed long-scoreboard stalls dominating)
+    {
+        constexpr int PER = UT3 * NB / 128;  // 16
+        double tv[PER], gv[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int q = tid + 128 * r;
+            const int i = q / NB, c = q % NB;
+            tv[r] = (i0 + i < n2) ? T[(long long)(i0 + i) * NB + c] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int q = tid + 128 * r;
+            const int c = q / UT3, j = q % UT3;
+            gv[r] = (j0 + j < n2) ? G[(long long)c * n2 + j0 + j] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int q = tid + 128 * r;
+            Ts[q / NB][q % NB] = tv[r];
+            Gs[q / UT3][q % UT3] = gv[r];
+        }
     }
     __syncthreads();
     double acc[4][4][2];
@@ -676,6 +692,18 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
 #pragma unroll
             for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    // epilogue: the 16 double2 reads of M are issued together, then the writes
+    double2 base[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gi = i0 + wr + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gj = j0 + wc + 8 * j + 2 * gq;
+            base[i][j] = (gi < n2 && gj < n2) ? __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj))
+                                              : make_double2(0.0, 0.0);
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int li = wr + 8 * i + gr;
@@ -692,12 +720,12 @@ __global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, 
             if (rowK) {
                 o = make_double2(Gs[gi - k0][lj], Gs[gi - k0][lj + 1]);
             } else {
-                double2 b = *dst;
+                double2 b = base[i][j];
                 if (gj >= k0 && gj < k0 + nbe) b.x = 0.0;
                 if (gj + 1 >= k0 && gj + 1 < k0 + nbe) b.y = 0.0;
                 o = make_double2(b.x - acc[i][j][0], b.y - acc[i][j][1]);
             }
-            *dst = o;
+            __stcs(dst, o);
         }
     }
 }
