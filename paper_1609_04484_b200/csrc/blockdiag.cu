@@ -637,7 +637,7 @@ __device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, do
                  : "d"(a), "d"(b));
 }
 constexpr int UT3 = 64;
-__global__ void __launch_bounds__(128) k_update3(BDView v, BDScratch s, int k0, int nbe) {
+__global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k0, int nbe) {
     __shared__ double Ts[UT3][NB + 1];  // Ts[i][c] = T[i0 + i][c]
     __shared__ double Gs[NB][UT3 + 1];  // Gs[c][j] = G[c][j0 + j]
     const int m = blockIdx.z;
