@@ -329,20 +329,24 @@ __global__ void __launch_bounds__(256) k_panel_smem(BDView v, BDScratch s, int k
 }
 
 // Large matrix: cooperative panel LU over G CTAs of 128 threads; thread owns one
-// panel row in registers.  Per column: local argmax -> grid sync -> global pivot,
-// pivot/displaced rows exchanged through global buffers -> grid sync -> elimination.
+// panel row in registers.  One grid sync per column: before it every CTA publishes
+// its local argmax AND that candidate's whole row, and the owner of row k publishes
+// row k; after it every CTA picks the global pivot and reads the pivot row straight
+// from the winning CTA's slot.  All exchange buffers are double-buffered by column
+// parity: a CTA can only overwrite parity c&1 again after passing column c+1's sync,
+// which every CTA reaches only after finishing its reads of column c.
 struct CoopScratch {
-    double *cand_v;  // [G]
-    int *cand_i;     // [G]
-    double *pbuf;    // [NB] new pivot row
-    double *kbuf;    // [NB] displaced row k
+    double *cand_v;  // [2][G]
+    int *cand_i;     // [2][G]
+    double *crow;    // [2][G][NB] candidate rows
+    double *kbuf;    // [2][NB] row k before the swap
     double *A;       // [NB][NB] LU'd pivot rows
 };
 __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopScratch cs, int k0, int nbe) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double red_v[4];
     __shared__ int red_i[4];
-    __shared__ int s_p;
+    __shared__ int s_p, s_src, s_bi;
     const int n2 = v.n2;
     const double *M = v.mat;  // one matrix per class launch
     const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
@@ -353,7 +357,11 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
     for (int c = 0; c < NB; ++c) w[c] = (own && c < nbe) ? M[(long long)r * n2 + k0 + c] : 0.0;
 #pragma unroll 1
     for (int c = 0; c < nbe; ++c) {
-        const int k = k0 + c;
+        const int k = k0 + c, par = c & 1;
+        double *cv_ = cs.cand_v + par * G;
+        int *ci_ = cs.cand_i + par * G;
+        double *crow = cs.crow + (long long)par * G * NB;
+        double *kb = cs.kbuf + par * NB;
         double wc = 0.0;
 #pragma unroll
         for (int q = 0; q < NB; ++q)
@@ -372,47 +380,62 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
             bi = red_i[0];
             for (int q = 1; q < 4; ++q)
                 if (red_v[q] > best || (red_v[q] == best && red_i[q] < bi)) { best = red_v[q]; bi = red_i[q]; }
-            cs.cand_v[g] = best;
-            cs.cand_i[g] = bi;
+            cv_[g] = best;
+            ci_[g] = bi;
+            s_bi = bi;
+        }
+        __syncthreads();
+        if (own && r == s_bi) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) crow[(long long)g * NB + q] = w[q];
+        }
+        if (own && r == k) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) kb[q] = w[q];
         }
         grid.sync();
-        if (tid == 0) {
+        int src = -1;
+        if (tid < 32) {
+            // warp 0 reduces the G candidates: lanes load in parallel (one L2
+            // round trip instead of G serial ones), then a shuffle tree
             best = -1.0;
             bi = n2;
-            for (int q = 0; q < G; ++q) {
-                const double cv = cs.cand_v[q];
-                const int ci = cs.cand_i[q];
-                if (cv > best || (cv == best && ci < bi)) { best = cv; bi = ci; }
+            for (int q = tid; q < G; q += 32) {
+                const double cv = __ldcg(cv_ + q);
+                const int ci = __ldcg(ci_ + q);
+                if (cv > best || (cv == best && ci < bi)) { best = cv; bi = ci; src = q; }
             }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_down_sync(0xffffffffu, best, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                const int os = __shfl_down_sync(0xffffffffu, src, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; src = os; }
+            }
+        }
+        if (tid == 0) {
             if (!(best > 0.0) || bi >= n2) {
                 if (g == 0) s.flag[0] = 1;
                 bi = k;
+                src = -1;  // no usable pivot: keep row k (read back from kbuf)
             }
             s_p = bi;
+            s_src = src;
             if (g == 0) s.piv[k] = bi;
         }
         __syncthreads();
         const int p = s_p;
-        if (own && r == p) {
-#pragma unroll
-            for (int q = 0; q < NB; ++q) cs.pbuf[q] = w[q];
-        }
+        const double *prow = s_src >= 0 ? crow + (long long)s_src * NB : kb;
         if (own && r == k) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) cs.kbuf[q] = w[q];
-        }
-        grid.sync();
-        if (own && r == k) {
-#pragma unroll
-            for (int q = 0; q < NB; ++q) w[q] = cs.pbuf[q];
+            for (int q = 0; q < NB; ++q) w[q] = prow[q];
         } else if (own && r == p) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) w[q] = cs.kbuf[q];
+            for (int q = 0; q < NB; ++q) w[q] = kb[q];
         }
         if (own && r > k) {
             double pr[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) pr[q] = cs.pbuf[q];
+            for (int q = 0; q < NB; ++q) pr[q] = prow[q];
             double dd = 1.0;
 #pragma unroll
             for (int q = 0; q < NB; ++q)
@@ -426,7 +449,6 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
             for (int q = 0; q < NB; ++q)
                 if (q > c && q < nbe) w[q] -= l * pr[q];
         }
-        // the next column's pbuf/kbuf writes happen only after its first grid.sync
     }
     if (own && r < k0 + nbe) {
 #pragma unroll
@@ -837,10 +859,10 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
             set_error("bie_blockdiag_factor: cooperative launch unavailable for the panel factorisation");
             return BIE_ECUDA;
         }
-        BIE_CUDA_TRY(cudaMallocAsync(&cs.cand_v, sizeof(double) * Gmax, st));
-        BIE_CUDA_TRY(cudaMallocAsync(&cs.cand_i, sizeof(int) * Gmax, st));
-        BIE_CUDA_TRY(cudaMallocAsync(&cs.pbuf, sizeof(double) * NB, st));
-        BIE_CUDA_TRY(cudaMallocAsync(&cs.kbuf, sizeof(double) * NB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.cand_v, sizeof(double) * 2 * Gmax, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.cand_i, sizeof(int) * 2 * Gmax, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.crow, sizeof(double) * 2 * Gmax * NB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&cs.kbuf, sizeof(double) * 2 * NB, st));
         BIE_CUDA_TRY(cudaMallocAsync(&cs.A, sizeof(double) * NB * NB, st));
     }
     const size_t upd_smem = sizeof(double) * 2 * NB * UT2P;
@@ -878,7 +900,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     if (coop) {
         cudaFreeAsync(cs.cand_v, st);
         cudaFreeAsync(cs.cand_i, st);
-        cudaFreeAsync(cs.pbuf, st);
+        cudaFreeAsync(cs.crow, st);
         cudaFreeAsync(cs.kbuf, st);
         cudaFreeAsync(cs.A, st);
     }
