@@ -289,8 +289,11 @@ struct SymArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int SR, int SW, int MINB = 1, bool QS = false>
+template <int SR, int SW, int MINB = 1, bool QS = false, int TP = 0>
 __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
+    // TP: source-step pipelining.  0: none; 1: the next step's source is read
+    // from shared memory one step ahead (hides the LDS latency at the loop
+    // head); 2: the step loop is unrolled by two.
     // QS: keep the targets' quadratic forms in shared memory (lane-private
     // slots) instead of registers, trading 3 shared loads per pair for 48
     // registers (more resident warps)
@@ -378,9 +381,26 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
         // independent dependency chains per warp in flight (a single chain per
         // warp left the FP64 pipe idle on DFMA latency: 72% active).
         double bx1 = 0.0, by1 = 0.0;
-#pragma unroll 1
+        double2 nxy, nab;
+        double nc;
+        if constexpr (TP == 1) {
+            nxy = s_src[buf][w][0][lane];
+            nab = s_src[buf][w][1][lane];
+            nc = s_src[buf][w][2][lane].x;
+        }
+#pragma unroll(TP == 2 ? 2 : 1)
         for (int t = 0; t < 32; ++t) {
-            {
+            if constexpr (TP == 1) {
+                sx = nxy.x;
+                sy = nxy.y;
+                sqa = nab.x;
+                sqb = nab.y;
+                sqc = nc;
+                const int sl = (lane + t + 1) & 31;
+                nxy = s_src[buf][w][0][sl];
+                nab = s_src[buf][w][1][sl];
+                nc = s_src[buf][w][2][sl].x;
+            } else {
                 const int sl = (lane + t) & 31;
                 const double2 xy = s_src[buf][w][0][sl], ab = s_src[buf][w][1][sl];
                 sx = xy.x;
@@ -758,9 +778,10 @@ int build_schedules(Geometry *g) {
 // (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
 // variants 3..5 add a minimum-blocks launch bound (register cap -> more warps)
 // variants 6..8 keep the target quadratic forms in shared memory (QS)
-static const int kNumSymVar = 11;
-static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4},
-                                           {8, 2}, {8, 2}, {4, 4}, {4, 4}, {4, 4}};
+// variants 11..14 pipeline the source steps (TP = 1: loads one step ahead; 2: unroll 2)
+static const int kNumSymVar = 15;
+static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2}, {8, 2},
+                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4}, {4, 4}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
@@ -773,6 +794,10 @@ static void *sym_kernel(int v) {
         case 8: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, true>);
         case 9: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4>);
         case 10: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, true>);
+        case 11: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 1>);
+        case 12: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 2>);
+        case 13: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, false, 1>);
+        case 14: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, false, 1>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -789,6 +814,10 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 8: k_dlp_sym<4, 4, 3, true><<<P, 128, 0, st>>>(sa); break;
         case 9: k_dlp_sym<4, 4, 4><<<P, 128, 0, st>>>(sa); break;
         case 10: k_dlp_sym<4, 4, 4, true><<<P, 128, 0, st>>>(sa); break;
+        case 11: k_dlp_sym<8, 2, 1, false, 1><<<P, 64, 0, st>>>(sa); break;
+        case 12: k_dlp_sym<8, 2, 1, false, 2><<<P, 64, 0, st>>>(sa); break;
+        case 13: k_dlp_sym<4, 4, 4, false, 1><<<P, 128, 0, st>>>(sa); break;
+        case 14: k_dlp_sym<4, 4, 3, false, 1><<<P, 128, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
