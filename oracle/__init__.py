@@ -1,8 +1,10 @@
 """CPU oracle -- TEST INFRASTRUCTURE ONLY.
 
 Python (ctypes) front-end of oracle/bie_oracle.c, the plain-C definition of the
-completed double-layer operator, the block-diagonal preconditioner and GMRES
-(see that file's header for citations and pins).  Only tests/,
+completed double-layer operator, the single-layer operator with Kapur-Rokhlin
+corrections (NEXT-1), the block-diagonal preconditioner and GMRES (see that
+file's header for citations and pins), plus kr_weights(), the Kapur-Rokhlin
+correction weights computed here in 40-digit decimal arithmetic.  Only tests/,
 __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
 import this package.  It shares no code with paper_1609_04484_b200 and the
 product path never imports it.
@@ -10,8 +12,10 @@ product path never imports it.
 from __future__ import annotations
 
 import ctypes
+import decimal
 import os
 import subprocess
+from fractions import Fraction
 
 import numpy as np
 
@@ -77,6 +81,20 @@ def lib():
         L.ora_gmres_bdlu.restype = ctypes.c_int
         L.ora_gmres_bdlu.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp,
                                      ctypes.c_void_p, dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
+        L.ora_slp_apply.restype = None
+        L.ora_slp_apply.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, ctypes.c_int, ip,
+                                    ctypes.c_int]
+        L.ora_slp_field.restype = None
+        L.ora_slp_field.argtypes = [ctypes.c_int, dp, dp, dp, dp, ctypes.c_int, dp]
+        L.ora_slp_block.restype = None
+        L.ora_slp_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, ctypes.c_int, dp]
+        L.ora_slp_bd_factor.restype = ctypes.c_void_p
+        L.ora_slp_bd_factor.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, ip]
+        L.ora_slp_bdlu_factor.restype = ctypes.c_void_p
+        L.ora_slp_bdlu_factor.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, ip]
+        L.ora_slp_gmres.restype = ctypes.c_int
+        L.ora_slp_gmres.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, ctypes.c_void_p, ctypes.c_int,
+                                    dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
         L.ora_gmres.restype = ctypes.c_int
         L.ora_gmres.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp,
                                 ctypes.c_void_p, dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
@@ -161,6 +179,36 @@ class OracleGeometry:
             return b * self.n_pore, (b + 1) * self.n_pore
         return self.M * self.n_pore, self.N
 
+    # --- NEXT-1: single-layer operator with Kapur-Rokhlin corrections ---
+    def _slp(self):
+        if not hasattr(self, "_gam"):
+            self._gam = kr_weights()
+        return self.N, self.M, self.n_pore, _d(self.x), _d(self.w), _d(self._gam)
+
+    def slp_apply(self, sigma, rows=None):
+        """out = A_SLP sigma (P:l.310-330): sigma (2N,) or (nvec, 2N); optional target rows."""
+        s = _c(sigma)
+        squeeze = s.ndim == 1
+        s = s.reshape(-1, 2 * self.N)
+        r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+        nr = self.N if r is None else r.shape[0]
+        out = np.zeros((s.shape[0], 2 * nr))
+        lib().ora_slp_apply(*self._slp(), _d(s), _d(out), s.shape[0], _i(r), 0 if r is None else nr)
+        return out[0] if squeeze else out
+
+    def slp_field(self, sigma, targets):
+        """Off-surface u(x) = sum_j w_j G(x, x_j) sigma_j (P:l.346-354) at targets (P, 2)."""
+        t = _c(targets).reshape(-1)
+        out = np.zeros(t.shape[0])
+        lib().ora_slp_field(self.N, _d(self.x), _d(self.w), _d(_c(sigma)), _d(t), t.shape[0] // 2, _d(out))
+        return out.reshape(-1, 2)
+
+    def slp_block(self, b: int):
+        lo, hi = self.body_range(b)
+        B = np.zeros((2 * (hi - lo), 2 * (hi - lo)))
+        lib().ora_slp_block(*self._slp(), b, _d(B))
+        return B
+
 
 class OracleBD:
     """Explicit per-body inverses (A6); apply is A7."""
@@ -220,6 +268,135 @@ class OracleBDLU:
         if getattr(self, "h", None):
             lib().ora_bdlu_free(self.h)
             self.h = None
+
+
+class OracleSLPBD(OracleBD):
+    """Explicit per-body inverses of the SLP blocks (NEXT-1, P:l.651-657)."""
+
+    def __init__(self, geom: OracleGeometry):
+        bad = ctypes.c_int(0)
+        self.geom = geom
+        self.h = lib().ora_slp_bd_factor(*geom._slp(), ctypes.byref(bad))
+        if not self.h:
+            raise MemoryError("oracle SLP BD allocation failed")
+        if bad.value:
+            lib().ora_bd_free(self.h)
+            self.h = None
+            raise np.linalg.LinAlgError(f"singular SLP BD block for body {bad.value - 1}")
+
+
+class OracleSLPBDLU(OracleBDLU):
+    """The SLP BD preconditioner in LU form."""
+
+    def __init__(self, geom: OracleGeometry):
+        bad = ctypes.c_int(0)
+        self.geom = geom
+        self.h = lib().ora_slp_bdlu_factor(*geom._slp(), ctypes.byref(bad))
+        if not self.h:
+            raise MemoryError("oracle SLP BD-LU allocation failed")
+        if bad.value:
+            lib().ora_bdlu_free(self.h)
+            self.h = None
+            raise np.linalg.LinAlgError(f"singular SLP BD block for body {bad.value - 1}")
+
+
+def slp_gmres(geom: OracleGeometry, f, pc=None, tol=1e-8, max_iter=1000):
+    """Left-preconditioned GMRES on the SLP system (pc: None, OracleSLPBD or OracleSLPBDLU)."""
+    kind = 0 if pc is None else 2 if isinstance(pc, OracleBDLU) else 1
+    x = np.zeros(2 * geom.N)
+    hist, rp, rt, conv = _gmres_out(max_iter)
+    it = lib().ora_slp_gmres(*geom._slp(), None if pc is None else pc.h, kind, _d(_c(f)), _d(x), tol, max_iter,
+                             _d(hist), ctypes.byref(rp), ctypes.byref(rt), ctypes.byref(conv))
+    return dict(x=x, iters=it, hist=hist[: it + 1].copy(), res_pc=rp.value, res_true=rt.value,
+                converged=bool(conv.value))
+
+
+# ---------------------------------------------------------------------------
+# Kapur-Rokhlin sixth-order correction weights (P:l.321-330; reading C24 of
+# DESIGN.md).  The rule  h sum_{j != 0} f(jh) + h sum_{0<|k|<=6} gamma_|k| f(kh)
+# for f = phi(x) log|x| + psi(x) (periodic, singular node excluded) is exact
+# to O(h^7 log h) when, with Navot's generalised Euler-Maclaurin expansion of
+# the punctured trapezoid sum,
+#     I - T'_h = h phi(0)(log h - log 2 pi) + 2 sum_{l>=1} zeta'(-2l) h^{2l+1} phi^(2l)(0)/(2l)!,
+#   2 sum_k gamma_k k^(2l)        = [l == 0]          l = 0, 1, 2   (smooth part psi)
+#   2 sum_k gamma_k k^(2l) log k  = 2 zeta'(-2l)      l = 0, 1, 2   (log part phi)
+# with zeta'(0) = -log(2 pi)/2 and zeta'(-2l) = (-1)^l (2l)! zeta(2l+1) / (2 (2 pi)^(2l)).
+# Everything below is plain 40-digit decimal arithmetic (Euler-Maclaurin for
+# zeta(3), zeta(5); Machin for pi; Gauss-Jordan for the 6 x 6 system).
+# ---------------------------------------------------------------------------
+_KR_DIGITS = 40
+
+
+def _bernoulli(n):
+    """B_0..B_n as Fractions (B_1 = -1/2) from sum_{k<m} C(m+1, k) B_k = -(m+1) B_m."""
+    B = [Fraction(0)] * (n + 1)
+    B[0] = Fraction(1)
+    for m in range(1, n + 1):
+        acc = Fraction(0)
+        c = 1  # C(m+1, k)
+        for k in range(m):
+            acc += c * B[k]
+            c = c * (m + 1 - k) // (k + 1)
+        B[m] = -acc / (m + 1)
+    return B
+
+
+def _zeta(s, D):
+    """zeta(s), integer s >= 2: sum_{n<Nz} n^-s + Euler-Maclaurin tail at Nz = 40."""
+    Nz, K = 40, 12
+    total = sum(D(1) / D(n) ** s for n in range(1, Nz))
+    total += D(Nz) ** (1 - s) / (s - 1) + D(1) / (2 * D(Nz) ** s)
+    B = _bernoulli(2 * K)
+    rising = D(s)  # s (s+1) ... (s + 2k - 2)
+    fact = D(2)    # (2k)!
+    for k in range(1, K + 1):
+        b = D(B[2 * k].numerator) / D(B[2 * k].denominator)
+        total += b / fact * rising / D(Nz) ** (s + 2 * k - 1)
+        rising *= D(s + 2 * k - 1) * D(s + 2 * k)
+        fact *= D(2 * k + 1) * D(2 * k + 2)
+    return total
+
+
+def _atan_inv(n, D):
+    """atan(1/n) by its Taylor series."""
+    x = D(1) / D(n)
+    x2 = x * x
+    term, total, k = x, D(0), 0
+    eps = D(10) ** (-(_KR_DIGITS + 5))
+    while abs(term) > eps:
+        total += term / (2 * k + 1) if k % 2 == 0 else -term / (2 * k + 1)
+        term *= x2
+        k += 1
+    return total
+
+
+def kr_weights(order: int = 6):
+    """gamma_1..gamma_6 of the sixth-order Kapur-Rokhlin log correction (float64)."""
+    assert order == 6
+    with decimal.localcontext() as ctx:
+        ctx.prec = _KR_DIGITS + 10
+        D = decimal.Decimal
+        pi = 16 * _atan_inv(5, D) - 4 * _atan_inv(239, D)
+        two_pi = 2 * pi
+        zeta_p = [-(two_pi.ln()) / 2,
+                  -D(2) * _zeta(3, D) / (2 * two_pi ** 2),
+                  D(24) * _zeta(5, D) / (2 * two_pi ** 4)]
+        rows = []
+        for l in range(3):
+            rows.append([2 * D(k) ** (2 * l) for k in range(1, 7)] + [D(1) if l == 0 else D(0)])
+        for l in range(3):
+            rows.append([2 * D(k) ** (2 * l) * D(k).ln() for k in range(1, 7)] + [2 * zeta_p[l]])
+        n = 6
+        for c in range(n):  # Gauss-Jordan, partial pivoting
+            p = max(range(c, n), key=lambda r: abs(rows[r][c]))
+            rows[c], rows[p] = rows[p], rows[c]
+            piv = rows[c][c]
+            rows[c] = [v / piv for v in rows[c]]
+            for r in range(n):
+                if r != c and rows[r][c] != 0:
+                    f = rows[r][c]
+                    rows[r] = [a - f * b for a, b in zip(rows[r], rows[c])]
+        return np.array([float(rows[k][n]) for k in range(n)])
 
 
 def gmres_bdlu(geom: OracleGeometry, f, bdlu: OracleBDLU, tol=1e-8, max_iter=1000):

@@ -17,6 +17,11 @@
  * Citations: P:l.N = /root/reference/PAPER.md line N; readings C1..C19 are
  * listed in DESIGN.md s3 (taken from SURVEY.md s8(c)).
  *
+ * It also holds the paper's own single-layer operator with the Kapur-Rokhlin
+ * correction (NEXT-1; readings C24-C26), pinned by tests/test_oracle_slp.py
+ * (periodic log integral, sixth-order convergence against Bessel closed
+ * forms, circle closed forms, the normal null space, an exact Stokes flow).
+ *
  * Parity pins (tests/test_oracle_*.py): Gauss identities (V1), Bessel circle
  * integral (V2), null space of the bare operator (V3), completion closed forms
  * (V4), Couette flow (V5), the paper's Stokeslet/rotlet exact solution (V6),
@@ -91,7 +96,12 @@ typedef struct {
     int N, M, n_pore;
     const double *x, *nrm, *w, *tan, *kn; /* from ora_nodes */
     const double *pc, *pr;                /* pore centres (2M), radii (M) */
+    int op;                               /* 0: completed DLP; 1: SLP + Kapur-Rokhlin (NEXT-1) */
+    const double *gam;                    /* op 1: KR corrections gamma_1..gamma_6 */
 } ora_geom;
+
+#define ORA_OP_SLP 1
+static void ora_slp_row(const ora_geom *g, const double *sig, int i, double *yo);
 
 /* ---------------------------------------------------------------------------
  * A2: moments of the completion (reading C5), per density vector.
@@ -193,13 +203,16 @@ static void ora_apply_g(const ora_geom *g, const double *sig, double *out, unsig
     double *lam = (double *)calloc(2 * (size_t)(g->M > 0 ? g->M : 1), sizeof(double));
     double *mu = (double *)calloc((size_t)(g->M > 0 ? g->M : 1), sizeof(double));
     double nu = 0.0;
-    if (!(flags & ORA_D_ONLY))
+    if (!(flags & ORA_D_ONLY) && g->op != ORA_OP_SLP)
         ora_moments(g, sig, lam, mu, &nu);
     int n = rows ? nrows : g->N;
 #pragma omp parallel for schedule(dynamic, 16)
     for (int q = 0; q < n; ++q) {
         int i = rows ? rows[q] : q;
-        ora_row(g, sig, lam, mu, nu, flags, i, out + 2 * (size_t)q);
+        if (g->op == ORA_OP_SLP)
+            ora_slp_row(g, sig, i, out + 2 * (size_t)q);
+        else
+            ora_row(g, sig, lam, mu, nu, flags, i, out + 2 * (size_t)q);
     }
     free(lam);
     free(mu);
@@ -210,7 +223,7 @@ void ora_apply(int N, int M, int n_pore, const double *x, const double *nrm, con
                const double *tan, const double *kn, const double *pc, const double *pr,
                const double *sigma, double *out, int nvec, unsigned flags, const int *rows, int nrows)
 {
-    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr};
+    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr, 0, NULL};
     int n = rows ? nrows : N;
     for (int v = 0; v < nvec; ++v)
         ora_apply_g(&g, sigma + (size_t)v * 2 * N, out + (size_t)v * 2 * n, flags, rows, nrows);
@@ -226,7 +239,7 @@ void ora_field(int N, int M, int n_pore, const double *x, const double *nrm, con
                const double *pc, const double *pr, const double *sig,
                const double *tgt, int ntgt, double *u)
 {
-    ora_geom g = {N, M, n_pore, x, nrm, w, NULL, NULL, pc, pr};
+    ora_geom g = {N, M, n_pore, x, nrm, w, NULL, NULL, pc, pr, 0, NULL};
     double *lam = (double *)calloc(2 * (size_t)(M > 0 ? M : 1), sizeof(double));
     double *mu = (double *)calloc((size_t)(M > 0 ? M : 1), sizeof(double));
     double nu = 0.0;
@@ -263,6 +276,147 @@ void ora_field(int N, int M, int n_pore, const double *x, const double *nrm, con
     free(mu);
 }
 
+
+/* ---------------------------------------------------------------------------
+ * NEXT-1: the paper's own operator -- the Stokes single-layer
+ * potential with the Kapur-Rokhlin sixth-order correction.
+ *   P:l.270-276 (eq. stokesSLP):  G(x, y) = (1/4pi)(-log rho I + r r^T/rho^2),
+ *   P:l.310-319 (eq. dense):      f_i = sum_j w_j G(x_i, x_j) sigma_j,
+ *   P:l.321-330: "identical to the trapezoid rule, except that the weights are
+ *   modified at the six nodes to the left and right of the singularity".
+ * Weights (readings C24-C25): for target i on closed curve Gamma
+ * (a pore or Gamma_0, n nodes, periodic local index),
+ *   W_ii = 0;  W_ij = w_j (1 + gamma_k) if j is on Gamma at periodic offset
+ *   +-k, 1 <= k <= 6;  W_ij = w_j otherwise (other offsets, other curves).
+ * gamma_1..gamma_6 are passed in (oracle/__init__.py: kr_weights()).
+ * ------------------------------------------------------------------------- */
+static void ora_curve(const ora_geom *g, int i, int *lo, int *n)
+{
+    if (i < g->M * g->n_pore) {
+        *lo = (i / g->n_pore) * g->n_pore;
+        *n = g->n_pore;
+    } else {
+        *lo = g->M * g->n_pore;
+        *n = g->N - *lo;
+    }
+}
+
+static double ora_slp_weight(const ora_geom *g, int i, int j)
+{
+    if (j == i)
+        return 0.0;
+    int lo_i, n_i, lo_j, n_j;
+    ora_curve(g, i, &lo_i, &n_i);
+    ora_curve(g, j, &lo_j, &n_j);
+    if (lo_i != lo_j)
+        return g->w[j];
+    int d = ((j - i) % n_i + n_i) % n_i; /* periodic offset on the curve */
+    int k = d < n_i - d ? d : n_i - d;
+    if (k <= 6)
+        return g->w[j] * (1.0 + g->gam[k - 1]);
+    return g->w[j];
+}
+
+/* G(x, y) sigma with the 1/4pi factor; r = x - y. */
+static void ora_slp_kernel(double rx, double ry, double sx, double sy, double *gx, double *gy)
+{
+    double rho2 = rx * rx + ry * ry;
+    double lg = 0.5 * log(rho2); /* log rho */
+    double rs = rx * sx + ry * sy;
+    *gx = (1.0 / (4.0 * ORA_PI)) * (-lg * sx + rx * rs / rho2);
+    *gy = (1.0 / (4.0 * ORA_PI)) * (-lg * sy + ry * rs / rho2);
+}
+
+static void ora_slp_row(const ora_geom *g, const double *sig, int i, double *yo)
+{
+    double xi = g->x[2 * i], yi = g->x[2 * i + 1];
+    double ux = 0.0, uy = 0.0;
+    for (int j = 0; j < g->N; ++j) {
+        if (j == i)
+            continue;
+        double W = ora_slp_weight(g, i, j);
+        double gx, gy;
+        ora_slp_kernel(xi - g->x[2 * j], yi - g->x[2 * j + 1], sig[2 * j], sig[2 * j + 1], &gx, &gy);
+        ux += W * gx;
+        uy += W * gy;
+    }
+    yo[0] = ux;
+    yo[1] = uy;
+}
+
+/* out = A_SLP sigma for nvec densities ([nvec][2N] -> [nvec][2*nrows]). */
+void ora_slp_apply(int N, int M, int n_pore, const double *x, const double *w, const double *gam,
+                   const double *sigma, double *out, int nvec, const int *rows, int nrows)
+{
+    ora_geom g = {N, M, n_pore, x, NULL, w, NULL, NULL, NULL, NULL, ORA_OP_SLP, gam};
+    int n = rows ? nrows : N;
+    for (int v = 0; v < nvec; ++v)
+        ora_apply_g(&g, sigma + (size_t)v * 2 * N, out + (size_t)v * 2 * n, 0u, rows, nrows);
+}
+
+/* Off-surface velocity u(x) = sum_j w_j G(x, x_j) sigma_j: the trapezoid rule
+ * of P:l.346-354 (eq. stokesSLP_discretized), no correction. */
+void ora_slp_field(int N, const double *x, const double *w, const double *sig, const double *tgt, int ntgt,
+                   double *u)
+{
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int q = 0; q < ntgt; ++q) {
+        double ux = 0.0, uy = 0.0;
+        for (int j = 0; j < N; ++j) {
+            double gx, gy;
+            ora_slp_kernel(tgt[2 * q] - x[2 * j], tgt[2 * q + 1] - x[2 * j + 1], sig[2 * j], sig[2 * j + 1],
+                           &gx, &gy);
+            ux += w[j] * gx;
+            uy += w[j] * gy;
+        }
+        u[2 * q] = ux;
+        u[2 * q + 1] = uy;
+    }
+}
+
+/* BD block of the SLP operator for body b: entries W_ij G(x_i, x_j) for i, j
+ * on body b (2x2 node blocks, zero for i == j). */
+static void ora_slp_block_g(const ora_geom *g, int b, double *B)
+{
+    int lo, hi;
+    if (b < g->M) {
+        lo = b * g->n_pore;
+        hi = lo + g->n_pore;
+    } else {
+        lo = g->M * g->n_pore;
+        hi = g->N;
+    }
+    int n2 = 2 * (hi - lo);
+    for (int i = lo; i < hi; ++i) {
+        for (int j = lo; j < hi; ++j) {
+            double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;
+            if (j != i) {
+                double W = ora_slp_weight(g, i, j);
+                double gx, gy;
+                double rx = g->x[2 * i] - g->x[2 * j], ry = g->x[2 * i + 1] - g->x[2 * j + 1];
+                ora_slp_kernel(rx, ry, W, 0.0, &gx, &gy); /* column for sigma = (1, 0) */
+                e00 = gx;
+                e10 = gy;
+                ora_slp_kernel(rx, ry, 0.0, W, &gx, &gy); /* column for sigma = (0, 1) */
+                e01 = gx;
+                e11 = gy;
+            }
+            size_t r0 = (size_t)(2 * (i - lo)), c0 = (size_t)(2 * (j - lo));
+            B[r0 * n2 + c0] = e00;
+            B[r0 * n2 + c0 + 1] = e01;
+            B[(r0 + 1) * n2 + c0] = e10;
+            B[(r0 + 1) * n2 + c0 + 1] = e11;
+        }
+    }
+}
+
+void ora_slp_block(int N, int M, int n_pore, const double *x, const double *w, const double *gam, int b,
+                   double *B)
+{
+    ora_geom g = {N, M, n_pore, x, NULL, w, NULL, NULL, NULL, NULL, ORA_OP_SLP, gam};
+    ora_slp_block_g(&g, b, B);
+}
+
 /* ---------------------------------------------------------------------------
  * A6: BD blocks.  P:l.651-657: "diagonal blocks corresponding to the
  * self-interactions of the individual pores and the outer boundary ...
@@ -290,6 +444,10 @@ static void ora_body_range(const ora_geom *g, int b, int *lo, int *hi)
 
 static void ora_bd_block_g(const ora_geom *g, int b, double *B)
 {
+    if (g->op == ORA_OP_SLP) {
+        ora_slp_block_g(g, b, B);
+        return;
+    }
     int lo, hi;
     ora_body_range(g, b, &lo, &hi);
     int n = hi - lo, n2 = 2 * n;
@@ -352,7 +510,7 @@ static void ora_bd_block_g(const ora_geom *g, int b, double *B)
 void ora_bd_block(int N, int M, int n_pore, const double *x, const double *nrm, const double *w,
                   const double *tan, const double *kn, const double *pc, const double *pr, int b, double *B)
 {
-    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr};
+    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr, 0, NULL};
     ora_bd_block_g(&g, b, B);
 }
 
@@ -438,10 +596,10 @@ typedef struct {
 } ora_bd;
 
 /* Returns NULL on allocation failure; *bad = body index + 1 if singular. */
-void *ora_bd_factor(int N, int M, int n_pore, const double *x, const double *nrm, const double *w,
-                    const double *tan, const double *kn, const double *pc, const double *pr, int *bad)
+static void *ora_bd_factor_g(const ora_geom *gp, int *bad)
 {
-    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr};
+    const ora_geom g = *gp;
+    int N = g.N, M = g.M, n_pore = g.n_pore;
     ora_bd *bd = (ora_bd *)calloc(1, sizeof(ora_bd));
     int nb = M + (N > M * n_pore ? 1 : 0);
     bd->N = N;
@@ -495,6 +653,21 @@ void *ora_bd_factor(int N, int M, int n_pore, const double *x, const double *nrm
     return bd;
 }
 
+void *ora_bd_factor(int N, int M, int n_pore, const double *x, const double *nrm, const double *w,
+                    const double *tan, const double *kn, const double *pc, const double *pr, int *bad)
+{
+    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr, 0, NULL};
+    return ora_bd_factor_g(&g, bad);
+}
+
+/* BD of the SLP operator (NEXT-1): the same exact per-body inverses of the
+ * SLP blocks (P:l.651-657 footnote). */
+void *ora_slp_bd_factor(int N, int M, int n_pore, const double *x, const double *w, const double *gam, int *bad)
+{
+    ora_geom g = {N, M, n_pore, x, NULL, w, NULL, NULL, NULL, NULL, ORA_OP_SLP, gam};
+    return ora_bd_factor_g(&g, bad);
+}
+
 /* Solve with stored LU factors (Doolittle, partial pivoting): z = A^{-1} v. */
 static void ora_lu_solve(int n, const double *LU, const int *piv, const double *v, double *z)
 {
@@ -534,10 +707,10 @@ typedef struct {
     int *piv; /* piv of block b at 2*lo[b] */
 } ora_bdlu;
 
-void *ora_bdlu_factor(int N, int M, int n_pore, const double *x, const double *nrm, const double *w,
-                      const double *tan, const double *kn, const double *pc, const double *pr, int *bad)
+static void *ora_bdlu_factor_g(const ora_geom *gp, int *bad)
 {
-    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr};
+    const ora_geom g = *gp;
+    int N = g.N, M = g.M, n_pore = g.n_pore;
     ora_bdlu *bd = (ora_bdlu *)calloc(1, sizeof(ora_bdlu));
     int nb = M + (N > M * n_pore ? 1 : 0);
     bd->N = N;
@@ -573,6 +746,19 @@ void *ora_bdlu_factor(int N, int M, int n_pore, const double *x, const double *n
             *bad = b + 1;
     }
     return bd;
+}
+
+void *ora_bdlu_factor(int N, int M, int n_pore, const double *x, const double *nrm, const double *w,
+                      const double *tan, const double *kn, const double *pc, const double *pr, int *bad)
+{
+    ora_geom g = {N, M, n_pore, x, nrm, w, tan, kn, pc, pr, 0, NULL};
+    return ora_bdlu_factor_g(&g, bad);
+}
+
+void *ora_slp_bdlu_factor(int N, int M, int n_pore, const double *x, const double *w, const double *gam, int *bad)
+{
+    ora_geom g = {N, M, n_pore, x, NULL, w, NULL, NULL, NULL, NULL, ORA_OP_SLP, gam};
+    return ora_bdlu_factor_g(&g, bad);
 }
 
 void ora_bdlu_apply(void *h, const double *in, double *out)
@@ -828,7 +1014,7 @@ typedef struct {
 static void ora_op_apply(void *ctx, const double *in, double *out)
 {
     ora_opctx *c = (ora_opctx *)ctx;
-    ora_apply_g(&c->g, in, out, 0u, NULL, 0);
+    ora_apply_g(&c->g, in, out, 0u, NULL, 0); /* op 0: completed DLP, op 1: SLP */
 }
 
 static void ora_op_bd(void *ctx, const double *in, double *out)
@@ -846,7 +1032,7 @@ int ora_gmres_bdlu(int N, int M, int n_pore, const double *x, const double *nrm,
                    const double *kn, const double *pc, const double *pr, void *bdlu, const double *f, double *sol,
                    double tol, int max_iter, double *hist, double *res_pc, double *res_true, int *converged)
 {
-    ora_opctx c = {{N, M, n_pore, x, nrm, w, tan, kn, pc, pr}};
+    ora_opctx c = {{N, M, n_pore, x, nrm, w, tan, kn, pc, pr, 0, NULL}};
     return ora_gmres_core(2 * N, ora_op_apply, &c, ora_op_bdlu, bdlu, f, sol, tol, max_iter, hist, res_pc,
                           res_true, converged);
 }
@@ -855,7 +1041,19 @@ int ora_gmres(int N, int M, int n_pore, const double *x, const double *nrm, cons
               const double *kn, const double *pc, const double *pr, void *bd, const double *f, double *sol,
               double tol, int max_iter, double *hist, double *res_pc, double *res_true, int *converged)
 {
-    ora_opctx c = {{N, M, n_pore, x, nrm, w, tan, kn, pc, pr}};
+    ora_opctx c = {{N, M, n_pore, x, nrm, w, tan, kn, pc, pr, 0, NULL}};
     return ora_gmres_core(2 * N, ora_op_apply, &c, bd ? ora_op_bd : NULL, bd, f, sol, tol, max_iter, hist,
                           res_pc, res_true, converged);
+}
+
+/* GMRES on the SLP operator (NEXT-1); pc_kind 0: none, 1: explicit-inverse BD
+ * (ora_slp_bd_factor), 2: LU-form BD (ora_slp_bdlu_factor). */
+int ora_slp_gmres(int N, int M, int n_pore, const double *x, const double *w, const double *gam, void *pc,
+                  int pc_kind, const double *f, double *sol, double tol, int max_iter, double *hist, double *res_pc,
+                  double *res_true, int *converged)
+{
+    ora_opctx c = {{N, M, n_pore, x, NULL, w, NULL, NULL, NULL, NULL, ORA_OP_SLP, gam}};
+    ora_op P = pc_kind == 1 ? ora_op_bd : pc_kind == 2 ? ora_op_bdlu : NULL;
+    return ora_gmres_core(2 * N, ora_op_apply, &c, P, pc, f, sol, tol, max_iter, hist, res_pc, res_true,
+                          converged);
 }
