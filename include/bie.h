@@ -255,6 +255,64 @@ BIE_API int bie_profile_end(bie_geometry_t g, double *ms_moments, double *ms_pai
                             int *applies);
 BIE_API long long bie_launch_count(void);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-1: the paper's own operator, the Stokes single-layer
+ * potential with the sixth-order Kapur-Rokhlin correction (P:l.270-330):
+ *   (A sigma)_i = sum_{j != i} W_ij G(x_i, x_j) sigma_j,
+ *   G(x, y) = (1/4pi)(-log rho I + r r^T / rho^2),  r = x - y    (eq. stokesSLP, eq. dense)
+ *   W_ij = w_j (1 + gamma_k) for j on i's own closed curve at periodic offset
+ *   +-k, 1 <= k <= 6 ("weights modified at the six nodes to the left and right
+ *   of the singularity", P:l.321-325); W_ij = w_j otherwise (readings C24-C26).
+ * The same handles, layouts, stream semantics and error codes as the DLP calls.
+ * ------------------------------------------------------------------------- */
+
+/* gamma_1..gamma_6 of the Kapur-Rokhlin rule as this library computes them
+ * (host, long double; reading C24).  gamma: host double[6].  BIE_EINVAL if null. */
+BIE_API int bie_kr_weights(double *gamma);
+
+/*
+ * bie_slp_apply -- out = A_SLP sigma.  sigma, out: device [nvec][2N], out must
+ * not alias sigma; nvec in [1, BIE_MAX_NVEC]; flags: 0 or BIE_ONE_SIDED
+ * (BIE_D_ONLY is rejected).  Async, never synchronises.
+ * Errors: BIE_EINVAL (null, nvec, aliasing, flags), BIE_ECUDA, BIE_ENOMEM.
+ */
+BIE_API int bie_slp_apply(bie_geometry_t g, const double *sigma, double *out, int nvec, unsigned flags, void *stream);
+
+/* Same operator for target rows [row_begin, row_end): out is [nvec][2*(row_end-row_begin)]. */
+BIE_API int bie_slp_apply_rows(bie_geometry_t g, const double *sigma, double *out, int nvec, int row_begin,
+                               int row_end, void *stream);
+
+/*
+ * bie_slp_field_eval -- off-surface velocity u(x) = sum_j w_j G(x, x_j) sigma_j,
+ * the trapezoid rule of P:l.346-354 (eq. stokesSLP_discretized), no correction
+ * (accurate for d(x, Gamma) > sqrt(ds), P:l.356-358 footnote).
+ * sigma: device [2N]; targets: device [ntgt][2]; out: device [ntgt][2]. Async.
+ * Errors: BIE_EINVAL (null, ntgt < 0, out aliasing sigma), BIE_ECUDA.
+ */
+BIE_API int bie_slp_field_eval(bie_geometry_t g, const double *sigma, const double *targets, int ntgt, double *out,
+                               void *stream);
+
+/*
+ * bie_blockdiag_factor_slp -- the BD preconditioner of the SLP system: exact
+ * inverses of the per-body SLP blocks (P:l.651-657 footnote), same object and
+ * apply as bie_blockdiag_factor.  The blocks are nearly singular (S n_b = 0,
+ * reading C26) but invertible; a zero pivot still raises BIE_ESINGULAR.
+ */
+BIE_API int bie_blockdiag_factor_slp(bie_geometry_t g, bie_blockdiag_t *out, void *stream);
+
+/*
+ * bie_gmres_solve_slp / bie_gmres_solve_batch_slp -- bie_gmres_solve and
+ * bie_gmres_solve_batch on the SLP system A_SLP sigma = f (P:l.596-601,
+ * 661-663).  bd must be NULL or come from bie_blockdiag_factor_slp on g
+ * (BIE_EINVAL otherwise).
+ */
+BIE_API int bie_gmres_solve_slp(bie_geometry_t g, bie_blockdiag_t bd, const double *f, double *x, double tol,
+                                int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
+                                int *converged, void *stream);
+BIE_API int bie_gmres_solve_batch_slp(bie_geometry_t g, bie_blockdiag_t bd, const double *F, double *X, int nrhs,
+                                      double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                                      double *res_true, int *converged, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,9 +25,15 @@ from ._bie import (  # noqa: F401
     field_eval,
     gmres_solve,
     gmres_solve_batch,
+    gmres_solve_batch_slp,
+    gmres_solve_slp,
+    kr_weights,
     launch_count,
     profile_begin,
     profile_end,
+    slp_apply,
+    slp_apply_rows,
+    slp_field_eval,
     lib,
     lib_path,
     EXPORTED_SYMBOLS,

@@ -30,6 +30,8 @@ EXPORTED_SYMBOLS = (
     "bie_field_eval", "bie_gmres_solve_batch", "bie_blockdiag_factor_range", "bie_blockdiag_rows",
     "bie_krylov_dots", "bie_krylov_axpy", "bie_krylov_scale", "bie_krylov_sqrt", "bie_krylov_givens",
     "bie_krylov_trisolve", "bie_dlp_sym_info", "bie_dlp_pairs_partial", "bie_dlp_epilogue_rows",
+    "bie_kr_weights", "bie_slp_apply", "bie_slp_apply_rows", "bie_slp_field_eval", "bie_blockdiag_factor_slp",
+    "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp",
 )
 
 
@@ -82,6 +84,13 @@ def lib():
         "bie_dlp_sym_info": [vp, ctypes.POINTER(ctypes.c_longlong), ip],
         "bie_dlp_pairs_partial": [vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong, c_int, c_int, vp],
         "bie_dlp_epilogue_rows": [vp, vp, vp, vp, c_int, c_int, c_uint, vp],
+        "bie_kr_weights": [dp],
+        "bie_slp_apply": [vp, vp, vp, c_int, c_uint, vp],
+        "bie_slp_apply_rows": [vp, vp, vp, c_int, c_int, c_int, vp],
+        "bie_slp_field_eval": [vp, vp, vp, c_int, vp, vp],
+        "bie_blockdiag_factor_slp": [vp, ctypes.POINTER(vp), vp],
+        "bie_gmres_solve_slp": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
+        "bie_gmres_solve_batch_slp": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_profile_begin": [vp],
         "bie_profile_end": [vp, dp, dp, dp, ip],
     }
@@ -253,11 +262,17 @@ def dlp_apply_host_ptr(g: Geometry, sigma_ptr: int, out_ptr: int, nvec: int = 1,
 
 class BlockDiag:
     """bie_blockdiag_t: explicit per-body inverses (A6).  bodies=(b0, b1) factors
-    only that body range (row sharding); its apply takes local vectors."""
+    only that body range (row sharding); its apply takes local vectors.
+    op="slp": blocks of the single-layer operator (bie_blockdiag_factor_slp)."""
 
-    def __init__(self, g: Geometry, stream=None, bodies=None):
+    def __init__(self, g: Geometry, stream=None, bodies=None, op: str = "dlp"):
         h = ctypes.c_void_p()
-        if bodies is None:
+        self.op = op
+        if op == "slp":
+            if bodies is not None:
+                raise ValueError("the SLP block-diagonal preconditioner covers the whole geometry")
+            _check(lib().bie_blockdiag_factor_slp(g.h, ctypes.byref(h), _stream_ptr(stream)))
+        elif bodies is None:
             _check(lib().bie_blockdiag_factor(g.h, ctypes.byref(h), _stream_ptr(stream)))
         else:
             _check(lib().bie_blockdiag_factor_range(g.h, int(bodies[0]), int(bodies[1]), ctypes.byref(h),
@@ -359,3 +374,64 @@ def gmres_solve(g: Geometry, bd: BlockDiag | None, f, x, tol: float = 1e-8, max_
                                  ctypes.byref(rp), ctypes.byref(rt), ctypes.byref(conv), _stream_ptr(stream)))
     return dict(iters=it.value, hist=hist[: it.value + 1].copy(), res_pc=rp.value, res_true=rt.value,
                 converged=bool(conv.value))
+
+
+# --- NEXT-1: single-layer operator with the Kapur-Rokhlin correction ---------
+def kr_weights() -> np.ndarray:
+    """gamma_1..gamma_6 as libbie.so computes them (bie_kr_weights)."""
+    out = np.zeros(6)
+    _check(lib().bie_kr_weights(_dp(out)))
+    return out
+
+
+def slp_apply(g: Geometry, sigma, out, nvec: int = 1, flags: int = 0, stream=None):
+    """out = A_SLP sigma on the device (bie_slp_apply); flags 0 or BIE_ONE_SIDED (2)."""
+    n = nvec * 2 * g.N
+    _check(lib().bie_slp_apply(g.h, _dev_ptr(sigma, "sigma", n), _dev_ptr(out, "out", n), nvec, flags,
+                               _stream_ptr(stream)))
+    return out
+
+
+def slp_apply_rows(g: Geometry, sigma, out, row_begin: int, row_end: int, nvec: int = 1, stream=None):
+    _check(lib().bie_slp_apply_rows(g.h, _dev_ptr(sigma, "sigma", nvec * 2 * g.N),
+                                    _dev_ptr(out, "out", nvec * 2 * (row_end - row_begin)), nvec, row_begin, row_end,
+                                    _stream_ptr(stream)))
+    return out
+
+
+def slp_field_eval(g: Geometry, sigma, targets, out, stream=None):
+    """Off-surface SLP velocity at targets [P,2] (bie_slp_field_eval)."""
+    ntgt = targets.numel() // 2
+    _check(lib().bie_slp_field_eval(g.h, _dev_ptr(sigma, "sigma", 2 * g.N), _dev_ptr(targets, "targets", 2 * ntgt),
+                                    ntgt, _dev_ptr(out, "out", 2 * ntgt), _stream_ptr(stream)))
+    return out
+
+
+def gmres_solve_slp(g: Geometry, bd: BlockDiag | None, f, x, tol: float = 1e-8, max_iter: int = 1000, stream=None):
+    """bie_gmres_solve_slp; bd from BlockDiag(g, op="slp") or None."""
+    hist = np.zeros(max_iter + 1)
+    it, conv = ctypes.c_int(0), ctypes.c_int(0)
+    rp, rt = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().bie_gmres_solve_slp(g.h, None if bd is None else bd.h, _dev_ptr(f, "f", 2 * g.N),
+                                     _dev_ptr(x, "x", 2 * g.N), float(tol), int(max_iter), _dp(hist),
+                                     ctypes.byref(it), ctypes.byref(rp), ctypes.byref(rt), ctypes.byref(conv),
+                                     _stream_ptr(stream)))
+    return dict(iters=it.value, hist=hist[: it.value + 1].copy(), res_pc=rp.value, res_true=rt.value,
+                converged=bool(conv.value))
+
+
+def gmres_solve_batch_slp(g: Geometry, bd: BlockDiag | None, F, X, nrhs: int, tol: float = 1e-8,
+                          max_iter: int = 1000, stream=None):
+    hist = np.zeros(nrhs * (max_iter + 1))
+    it = np.zeros(nrhs, dtype=np.int32)
+    conv = np.zeros(nrhs, dtype=np.int32)
+    rp, rt = np.zeros(nrhs), np.zeros(nrhs)
+    ip_ = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))  # noqa: E731
+    n = nrhs * 2 * g.N
+    _check(lib().bie_gmres_solve_batch_slp(g.h, None if bd is None else bd.h, _dev_ptr(F, "F", n),
+                                           _dev_ptr(X, "X", n), int(nrhs), float(tol), int(max_iter), _dp(hist),
+                                           ip_(it), _dp(rp), _dp(rt), ip_(conv), _stream_ptr(stream)))
+    hist = hist.reshape(nrhs, max_iter + 1)
+    return [dict(iters=int(it[r]), hist=hist[r, : it[r] + 1].copy(), res_pc=float(rp[r]), res_true=float(rt[r]),
+                 converged=bool(conv[r])) for r in range(nrhs)]
+

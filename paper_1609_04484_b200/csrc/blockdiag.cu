@@ -116,6 +116,43 @@ __global__ void k_bd_assemble(BDView v, int lo0, int nodes, int is_wall, const d
     M[(2LL * li + 1) * n2 + 2 * lj + 1] = e11;
 }
 
+// SLP blocks (NEXT-1; reading C25): node pair (i, j) of one closed curve of
+// `nodes` nodes carries W_ij G(x_i, x_j) with G = (1/4pi)(-log rho I + r r^T/rho^2),
+// W_ii = 0, W_ij = w_j (1 + gamma_k) at periodic offset +-k (k <= 6), else w_j.
+struct KRWeights {
+    double g[6];
+};
+__global__ void k_bd_assemble_slp(BDView v, int lo0, int nodes, const double2 *__restrict__ pos,
+                                  const double *__restrict__ w, KRWeights kr) {
+    const int m = blockIdx.y;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)nodes * nodes) return;
+    const int li = (int)(e / nodes), lj = (int)(e % nodes);
+    const int lo = lo0 + m * nodes;
+    double e00 = 0.0, e01 = 0.0, e11 = 0.0;
+    if (li != lj) {
+        int d = lj - li;
+        d = d < 0 ? d + nodes : d;
+        const int k = min(d, nodes - d);
+        double W = w[lo + lj];
+        if (k <= 6) W *= 1.0 + kr.g[k - 1];
+        const double2 xi = pos[lo + li], xj = pos[lo + lj];
+        const double rx = xi.x - xj.x, ry = xi.y - xj.y;
+        const double rho2 = rx * rx + ry * ry;
+        const double lg = 0.5 * log(rho2);
+        const double f = W * (1.0 / (4.0 * kPi));
+        e00 = f * (-lg + rx * rx / rho2);
+        e01 = f * (rx * ry / rho2);
+        e11 = f * (-lg + ry * ry / rho2);
+    }
+    double *M = v.mat + (long long)m * v.mstride;
+    const long long n2 = v.n2;
+    M[(2LL * li) * n2 + 2 * lj] = e00;
+    M[(2LL * li) * n2 + 2 * lj + 1] = e01;
+    M[(2LL * li + 1) * n2 + 2 * lj] = e01;
+    M[(2LL * li + 1) * n2 + 2 * lj + 1] = e11;
+}
+
 // ------------------------------------------------------------------ panel LU
 // One CTA per matrix.  Rows [k0, n2) of panel columns [k0, k0+nbe).
 // Pivot = max |value|, lowest row index on ties (as the oracle).
@@ -826,7 +863,7 @@ __global__ void __launch_bounds__(256) k_bd_apply(const double *__restrict__ inv
 }
 
 static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall, cudaStream_t st,
-                        int *d_flag) {
+                        int *d_flag, int op) {
     if (v.count == 0) return BIE_OK;
     const int n2 = v.n2;
     BDScratch s{};
@@ -840,8 +877,14 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     {
         long long elems = (long long)nodes * nodes;
         dim3 grid((unsigned)((elems + 255) / 256), v.count);
-        k_bd_assemble<<<grid, 256, 0, st>>>(v, lo0, nodes, is_wall ? 1 : 0, g->pos, g->nw, g->nrm, g->tan, g->w,
-                                            g->selfc, g->pore, g->wall_len);
+        if (op) {
+            KRWeights kr;
+            for (int k = 0; k < 6; ++k) kr.g[k] = g->kr[k];
+            k_bd_assemble_slp<<<grid, 256, 0, st>>>(v, lo0, nodes, g->pos, g->w, kr);
+        } else {
+            k_bd_assemble<<<grid, 256, 0, st>>>(v, lo0, nodes, is_wall ? 1 : 0, g->pos, g->nw, g->nrm, g->tan,
+                                                g->w, g->selfc, g->pore, g->wall_len);
+        }
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
     }
@@ -969,10 +1012,11 @@ int bie_blockdiag_destroy(bie_blockdiag_t h) {
     return BIE_OK;
 }
 
-static int factor_range(Geometry *g, int b0, int b1, bie_blockdiag_t *out, cudaStream_t st) {
+static int factor_range(Geometry *g, int b0, int b1, bie_blockdiag_t *out, cudaStream_t st, int op = 0) {
     *out = nullptr;
     BlockDiag *bd = new BlockDiag();
     bd->g = g;
+    bd->op = op;
     bd->b0 = b0;
     bd->b1 = b1;
     bd->nb = b1 - b0;
@@ -1008,12 +1052,12 @@ static int factor_range(Geometry *g, int b0, int b1, bie_blockdiag_t *out, cudaS
     const int np_hi = std::min(b1, g->M);
     if (b0 < np_hi) {  // pores [b0, np_hi)
         BDView pv{bd->inv, 4LL * g->n_pore * g->n_pore, 2 * g->n_pore, np_hi - b0, b0};
-        rc = factor_class(g, pv, b0 * g->n_pore, g->n_pore, false, st, d_flag);
+        rc = factor_class(g, pv, b0 * g->n_pore, g->n_pore, false, st, d_flag, op);
         if (rc) return fail(rc);
     }
     if (b1 == g->M + 1) {  // the wall
         BDView wv{bd->inv + bd->off[g->M - b0], 0, 2 * g->n_outer, 1, g->M};
-        rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + (g->M - b0));
+        rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + (g->M - b0), op);
         if (rc) return fail(rc);
     }
     std::vector<int> flags(bd->nb);
@@ -1041,6 +1085,15 @@ int bie_blockdiag_factor(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) 
         return BIE_EINVAL;
     }
     return factor_range(g, 0, g->M + 1, out, (cudaStream_t)stream);
+}
+
+int bie_blockdiag_factor_slp(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out) {
+        set_error("bie_blockdiag_factor_slp: invalid geometry handle or null output");
+        return BIE_EINVAL;
+    }
+    return factor_range(g, 0, g->M + 1, out, (cudaStream_t)stream, 1);
 }
 
 int bie_blockdiag_factor_range(bie_geometry_t gh, int body_begin, int body_end, bie_blockdiag_t *out,

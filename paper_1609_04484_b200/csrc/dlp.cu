@@ -34,6 +34,51 @@ __device__ __forceinline__ double rcp_approx(double x) {
     return r;
 }
 
+// Single-layer pair factor (NEXT-1; P:l.270-276): for r = x_i - x_j returns
+// hl = -1/2 log rho^2 and inv = 1/rho^2, so that
+//   G(x_i, x_j) (w_j sigma_j) = hl S_j + (r . S_j) inv r,   S_j = w_j sigma_j / (4 pi).
+// r = 0 (the self pair, or zero-padded slots that coincide) maps rho^2 -> 1:
+// hl = 0 and the dyadic term vanishes with r, so no branch is needed.
+// Branch-free natural log for the pair loop (d > 0 and normal; pair distances
+// are never denormal).  d = 2^e m with m in [1/sqrt2, sqrt2) by integer ops,
+// s = (m - 1)/(m + 1) (|s| <= 0.1716) by seed + cubic Newton reciprocal, and
+// log m = 2 atanh s = s (2 + z (2/3 + 2/5 z + ... + 2/19 z^8)), z = s^2:
+// truncation <= 2 s^21 / 21 < 1e-17.  The library log() carries special-case
+// branches that keep ptxas from interleaving the independent pairs.
+__device__ __forceinline__ double log_pair(double d) {
+    const int hi = __double2hiint(d), lo = __double2loint(d);
+    const int mh = hi & 0x000fffff;
+    const int big = mh >= 0x6a09e;  // mantissa >= sqrt 2: use m / 2
+    const int e = (hi >> 20) - 1023 + big;
+    const double m = __hiloint2double(mh | (big ? 0x3fe00000 : 0x3ff00000), lo);
+    const double den = m + 1.0;
+    double i = rcp_approx(den);
+    const double ee = fma(-den, i, 1.0);
+    i = fma(i, fma(ee, ee, ee), i);
+    const double s = (m - 1.0) * i;
+    const double z = s * s;
+    double p = 2.0 / 19.0;
+    p = fma(p, z, 2.0 / 17.0);
+    p = fma(p, z, 2.0 / 15.0);
+    p = fma(p, z, 2.0 / 13.0);
+    p = fma(p, z, 2.0 / 11.0);
+    p = fma(p, z, 2.0 / 9.0);
+    p = fma(p, z, 2.0 / 7.0);
+    p = fma(p, z, 2.0 / 5.0);
+    p = fma(p, z, 2.0 / 3.0);
+    const double lm = s * fma(z, p, 2.0);
+    return fma((double)e, 0.69314718055994530942, lm);
+}
+
+__device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, double &inv) {
+    double d = fma(rx, rx, ry * ry);
+    d = d == 0.0 ? 1.0 : d;
+    double i = rcp_approx(d);
+    const double e = fma(-d, i, 1.0);
+    inv = fma(i, fma(e, e, e), i);
+    hl = -0.5 * log_pair(d);
+}
+
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src, int src_bytes) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem_src), "r"(src_bytes));
@@ -69,7 +114,9 @@ struct PairArgs {
 // (r = 0) needs no branch: rho^2 gets +1e-300 (below one ulp of any real
 // pair distance), so 1/rho^2 stays finite and r.nw = 0 zeroes the term.
 // 1/rho^2: MUFU.RCP64H seed + one cubic Newton step (3 DFMA, rel. err ~2^-60).
-template <int NV, int R, int TS>
+// OP = 1: the single-layer operator instead (NEXT-1).  sigma then holds the
+// pre-scaled S_j = w_j sigma_j / (4 pi) and nw is unused.
+template <int NV, int R, int TS, int OP = 0>
 __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
     extern __shared__ double2 smem[];  // [2][(2 + NV) * TS]
     constexpr int NT = kPairThreads;
@@ -141,6 +188,19 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
             for (int v = 0; v < NV; ++v) sj[v] = sp[(2 + v) * TS + j];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
+                if constexpr (OP == 1) {
+                    const double rx = tx[r] - xj.x;
+                    const double ry = ty[r] - xj.y;
+                    double hl, inv;
+                    slp_factors(rx, ry, hl, inv);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double c = inv * fma(rx, sj[v].x, ry * sj[v].y);
+                        acc[r][v].x = fma(c, rx, fma(hl, sj[v].x, acc[r][v].x));
+                        acc[r][v].y = fma(c, ry, fma(hl, sj[v].y, acc[r][v].y));
+                    }
+                    continue;
+                }
                 const double rx = tx[r] - xj.x;
                 const double ry = ty[r] - xj.y;
                 const double rho2 = fma(rx, rx, fma(ry, ry, 1e-300));
@@ -289,8 +349,11 @@ struct SymArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int SR, int SW, int MINB = 1, bool QS = false, int TP = 0>
+template <int SR, int SW, int MINB = 1, bool QS = false, int TP = 0, int OP = 0>
 __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
+    // OP = 1: single-layer operator (NEXT-1).  Q holds (S_x, S_y, 0, 0) with
+    // S = w sigma / (4 pi); G is even in r, so both directions get
+    //   u += hl S + (r . S) r / rho^2   with the shared hl = -1/2 log rho^2, 1/rho^2.
     // TP: source-step pipelining.  0: none; 1: the next step's source is read
     // from shared memory one step ahead (hides the LDS latency at the loop
     // head); 2: the step loop is unrolled by two.
@@ -411,6 +474,25 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
             }
 #pragma unroll
             for (int r = 0; r < SR; r += 2) {
+                if constexpr (OP == 1) {
+                    const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
+                    const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
+                    double hl0, hl1, i0, i1;
+                    slp_factors(rx0, ry0, hl0, i0);
+                    slp_factors(rx1, ry1, hl1, i1);
+                    const double ct0 = i0 * fma(rx0, sqa, ry0 * sqb), ct1 = i1 * fma(rx1, sqa, ry1 * sqb);
+                    const double cs0 = i0 * fma(rx0, tqa[r], ry0 * tqb[r]);
+                    const double cs1 = i1 * fma(rx1, tqa[r + 1], ry1 * tqb[r + 1]);
+                    ax[r] = fma(ct0, rx0, fma(hl0, sqa, ax[r]));
+                    ay[r] = fma(ct0, ry0, fma(hl0, sqb, ay[r]));
+                    ax[r + 1] = fma(ct1, rx1, fma(hl1, sqa, ax[r + 1]));
+                    ay[r + 1] = fma(ct1, ry1, fma(hl1, sqb, ay[r + 1]));
+                    bx = fma(cs0, rx0, fma(hl0, tqa[r], bx));
+                    by = fma(cs0, ry0, fma(hl0, tqb[r], by));
+                    bx1 = fma(cs1, rx1, fma(hl1, tqa[r + 1], bx1));
+                    by1 = fma(cs1, ry1, fma(hl1, tqb[r + 1], by1));
+                    continue;
+                }
                 const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
                 const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
                 const double xx0 = rx0 * rx0, xx1 = rx1 * rx1;
@@ -495,6 +577,9 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
 
 // Pairs inside one 512-node block (one-sided, all ordered pairs, self pair
 // zeroed by the rho^2 + 1e-300 rule).  One CTA per block, 128 threads x 4 targets.
+// OP = 1: single-layer pairs (sigma = pre-scaled S, nw unused; the self pair
+// vanishes through slp_factors).
+template <int OP = 0>
 __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ pos, const double2 *__restrict__ nw,
                                                   const double *__restrict__ sigma, double *diag, int N,
                                                   int blk0 = 0) {
@@ -505,7 +590,7 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
         const int j = base + q;
         const bool ok = j < N;
         sp[0][q] = ok ? pos[j] : make_double2(0.0, 0.0);
-        sp[1][q] = ok ? nw[j] : make_double2(0.0, 0.0);
+        sp[1][q] = (ok && OP == 0) ? nw[j] : make_double2(0.0, 0.0);
         sp[2][q] = ok ? reinterpret_cast<const double2 *>(sigma)[j] : make_double2(0.0, 0.0);
     }
     __syncthreads();
@@ -524,6 +609,16 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
         const double2 xj = sp[0][jj], nj = sp[1][jj], sj = sp[2][jj];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
+            if constexpr (OP == 1) {
+                const double rx = tx[r] - xj.x;
+                const double ry = ty[r] - xj.y;
+                double hl, inv;
+                slp_factors(rx, ry, hl, inv);
+                const double c = inv * fma(rx, sj.x, ry * sj.y);
+                ax[r] = fma(c, rx, fma(hl, sj.x, ax[r]));
+                ay[r] = fma(c, ry, fma(hl, sj.y, ay[r]));
+                continue;
+            }
             const double rx = tx[r] - xj.x;
             const double ry = ty[r] - xj.y;
             const double rho2 = fma(rx, rx, fma(ry, ry, 1e-300));
@@ -571,6 +666,10 @@ struct EpiArgs {
     Chunk ch[5];
     SymEpi sym;
     const double *presum;  // nvec = 1: pair sums already reduced (sharded path), local rows [2 Nt]
+    int op;                // 0: completed DLP; 1: single-layer operator + Kapur-Rokhlin correction
+    int n_pore;
+    const double *slp_s;   // op 1: S = w sigma / (4 pi), [nvec][2N]
+    double kr[6];          // op 1: gamma_1..gamma_6
 };
 
 // A4 + A5: reduce the split partials in fixed slot order, then add the local
@@ -637,6 +736,43 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             }
             u[v] = acc;
         }
+    }
+    if (a.op == 1) {
+        // Kapur-Rokhlin correction (reading C25): the all-pairs sum used w_j for
+        // every j != i; the 12 periodic neighbours on i's own curve carry
+        // w_j (1 + gamma_k), i.e. + gamma_k G(x_i, x_j) (w_j sigma_j).
+        int lo, n;
+        if (i < a.wall_lo) {
+            lo = (i / a.n_pore) * a.n_pore;
+            n = a.n_pore;
+        } else {
+            lo = a.wall_lo;
+            n = a.N - a.wall_lo;
+        }
+        const int li = i - lo;
+#pragma unroll
+        for (int k = 1; k <= 6; ++k) {
+            const double gk = a.kr[k - 1];
+            for (int sg = 0; sg < 2; ++sg) {
+                int lj = sg == 0 ? li + k : li - k;
+                lj = lj >= n ? lj - n : (lj < 0 ? lj + n : lj);
+                const int j = lo + lj;
+                const double2 xj = a.pos[j];
+                const double rx = xi.x - xj.x, ry = xi.y - xj.y;
+                const double d = rx * rx + ry * ry;
+                const double hl = -0.5 * log(d), inv = 1.0 / d;
+                for (int v = 0; v < nvec; ++v) {
+                    const double2 sj = reinterpret_cast<const double2 *>(a.slp_s + (long long)v * 2LL * a.N)[j];
+                    const double c = inv * (rx * sj.x + ry * sj.y);
+                    u[v].x += gk * (hl * sj.x + c * rx);
+                    u[v].y += gk * (hl * sj.y + c * ry);
+                }
+            }
+        }
+        if (!active) return;
+        for (int v = 0; v < nvec; ++v)
+            reinterpret_cast<double2 *>(a.out + (long long)v * 2LL * a.Nt)[it] = u[v];
+        return;
     }
     for (int v = 0; v < nvec; ++v) {
         const double2 si = reinterpret_cast<const double2 *>(a.sigma + (long long)v * a.sig_stride)[i];
@@ -706,17 +842,18 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
 }
 
 template <int NV, int R, int TS>
-static void *pair_kernel_ptr() {
-    return reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS>);
+static void *pair_kernel_ptr(int op) {
+    return op ? reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS, 1>)
+              : reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS, 0>);
 }
 
-static void *variant_kernel(int idx) {
+static void *variant_kernel(int idx, int op = 0) {
     switch (idx) {
-        case 0: return pair_kernel_ptr<1, 4, 256>();
-        case 1: return pair_kernel_ptr<2, 2, 256>();
-        case 2: return pair_kernel_ptr<4, 2, 256>();
-        case 3: return pair_kernel_ptr<8, 1, 128>();
-        default: return pair_kernel_ptr<16, 1, 64>();
+        case 0: return pair_kernel_ptr<1, 4, 256>(op);
+        case 1: return pair_kernel_ptr<2, 2, 256>(op);
+        case 2: return pair_kernel_ptr<4, 2, 256>(op);
+        case 3: return pair_kernel_ptr<8, 1, 128>(op);
+        default: return pair_kernel_ptr<16, 1, 64>(op);
     }
 }
 
@@ -731,7 +868,7 @@ static int variant_index(int nv) {
 }
 
 // Fill the schedule of one variant for Nt targets and N sources.
-static void make_sched(const Geometry *g, int vi, int Nt, PairSched &s) {
+static void make_sched(const Geometry *g, int vi, int Nt, PairSched &s, int op = 0) {
     const Variant &V = kVariants[vi];
     s.nv = V.nv;
     s.R = V.R;
@@ -741,7 +878,7 @@ static void make_sched(const Geometry *g, int vi, int Nt, PairSched &s) {
     s.nTS = (g->N + s.TS - 1) / s.TS;
     s.U = (long long)s.nTB * s.nTS;
     s.smem = 2 * (2 + V.nv) * V.TS * (int)sizeof(double2);
-    long long Pmax = (long long)g->num_sms * std::max(1, g->occ[vi]);
+    long long Pmax = (long long)g->num_sms * std::max(1, op ? g->occ_slp[vi] : g->occ[vi]);
     s.P = (int)std::min<long long>(Pmax, s.U);
     // max slots per target block: ceil(P / nTB) + 1 bounds it; compute exactly
     int S = 1;
@@ -758,16 +895,19 @@ int build_schedules(Geometry *g) {
     for (int vi = 0; vi < 5; ++vi) {
         const Variant &V = kVariants[vi];
         int smem = 2 * (2 + V.nv) * V.TS * (int)sizeof(double2);
-        cudaError_t e = cudaFuncSetAttribute(variant_kernel(vi), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_dlp_pairs)");
-        int occ = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, variant_kernel(vi), kPairThreads, smem);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-        g->occ[vi] = std::max(1, occ);
-        PairSched s;
-        make_sched(g, vi, g->N, s);
-        g->sched[vi] = s;
-        need = std::max(need, (size_t)s.S * BIE_MAX_NVEC * 2 * (size_t)g->N);
+        for (int op = 0; op < 2; ++op) {  // completed DLP, single-layer (NEXT-1)
+            cudaError_t e =
+                cudaFuncSetAttribute(variant_kernel(vi, op), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(k_dlp_pairs)");
+            int occ = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, variant_kernel(vi, op), kPairThreads, smem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+            (op ? g->occ_slp : g->occ)[vi] = std::max(1, occ);
+            PairSched s;
+            make_sched(g, vi, g->N, s, op);
+            (op ? g->sched_slp : g->sched)[vi] = s;
+            need = std::max(need, (size_t)s.S * BIE_MAX_NVEC * 2 * (size_t)g->N);
+        }
     }
     cudaError_t e = cudaMalloc(&g->partial, need * sizeof(double));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(partial)");
@@ -874,7 +1014,17 @@ static int sym_prepare(Geometry *g) {
     return BIE_OK;
 }
 
-static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStream_t st) {
+static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStream_t st, int op = 0) {
+    if (op) {
+        switch (vi) {
+            case 0: k_dlp_pairs<1, 4, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+            case 1: k_dlp_pairs<2, 2, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+            case 2: k_dlp_pairs<4, 2, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+            case 3: k_dlp_pairs<8, 1, 128, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+            default: k_dlp_pairs<16, 1, 64, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        }
+        return;
+    }
     switch (vi) {
         case 0: k_dlp_pairs<1, 4, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         case 1: k_dlp_pairs<2, 2, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
@@ -884,13 +1034,40 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
     }
 }
 
+// NEXT-1: S = w sigma / (4 pi) for every vector (the single-layer source
+// strength), and for the symmetric path also the (S_x, S_y, 0, 0) records.
+__global__ void k_slp_scale(const double *__restrict__ w, const double *__restrict__ sigma, long long stride,
+                            int nvec, int N, double *S, double4 *Q) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    const double f = w[j] * (1.0 / (4.0 * kPi));
+    for (int v = 0; v < nvec; ++v) {
+        const double2 sj = reinterpret_cast<const double2 *>(sigma + (long long)v * stride)[j];
+        const double2 o = make_double2(f * sj.x, f * sj.y);
+        reinterpret_cast<double2 *>(S + (long long)v * 2LL * N)[j] = o;
+        if (Q && v == 0) Q[j] = make_double4(o.x, o.y, 0.0, 0.0);
+    }
+}
+
+static int slp_prepare(Geometry *g) {
+    if (g->slp_s) return BIE_OK;
+    BIE_CUDA_TRY(cudaMalloc(&g->slp_s, sizeof(double) * BIE_MAX_NVEC * 2 * (size_t)g->N));
+    return BIE_OK;
+}
+
 int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, int row_begin,
                    int row_end, cudaStream_t st) {
     const int N = g->N;
     const int Nt = row_end - row_begin;
     if (Nt <= 0) return BIE_OK;
     const long long stride = 2LL * N;
-    const bool full = !(flags & BIE_D_ONLY);
+    const int op = (flags & kOpSLP) ? 1 : 0;
+    const bool full = !(flags & BIE_D_ONLY) && !op;
+    const double *sigma_in = sigma;  // the caller's density (epilogue local terms)
+    if (op) {
+        int rc = slp_prepare(g);
+        if (rc != BIE_OK) return rc;
+    }
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     if (g->prof) {
         while (g->prof_ev.size() < g->prof_used + 4) {
@@ -911,16 +1088,30 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     EpiArgs ea{};
     const bool sym = nvec == 1 && row_begin == 0 && row_end == N && !(flags & BIE_ONE_SIDED) &&
                      sym_prepare(g) == BIE_OK && g->sym_state == 1;
-    if (sym) {
-        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+    if (op) {
+        k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, stride, nvec, N, g->slp_s,
+                                                     sym ? g->sym_Q : nullptr);
         count_launch();
+        sigma = g->slp_s;  // the pair kernels read S
+    }
+    if (sym) {
+        if (!op) {
+            k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+            count_launch();
+        }
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
         if (g->sym_U > 0) {
             SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, g->sym_U, 0};
-            launch_sym(g->sym_variant, g->sym_P, sa, st);
+            if (op)
+                k_dlp_sym<8, 2, 1, false, 1, 1><<<g->sym_P, 64, 0, st>>>(sa);
+            else
+                launch_sym(g->sym_variant, g->sym_P, sa, st);
             count_launch();
         }
-        k_dlp_diag<<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+        if (op)
+            k_dlp_diag<1><<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+        else
+            k_dlp_diag<0><<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -938,9 +1129,9 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         int vi = variant_index(nv);
         PairSched s;
         if (row_begin == 0 && row_end == N)
-            s = g->sched[vi];
+            s = op ? g->sched_slp[vi] : g->sched[vi];
         else
-            make_sched(g, vi, Nt, s);
+            make_sched(g, vi, Nt, s, op);
         need = std::max(need, (size_t)s.S * nvec * 2 * (size_t)Nt);
         sch[nch] = s;
         vis[nch] = vi;
@@ -972,7 +1163,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         a.Nt = Nt;
         a.nTS = sch[c].nTS;
         a.U = sch[c].U;
-        launch_pairs(vis[c], sch[c], a, st);
+        launch_pairs(vis[c], sch[c], a, st, op);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
     }
@@ -982,8 +1173,12 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     ea.tan = g->tan;
     ea.selfc = g->selfc;
     ea.pore = g->pore;
-    ea.sigma = sigma;
+    ea.sigma = sigma_in;
     ea.sig_stride = stride;
+    ea.op = op;
+    ea.n_pore = g->n_pore;
+    ea.slp_s = g->slp_s;
+    for (int k = 0; k < 6; ++k) ea.kr[k] = g->kr[k];
     ea.partial = g->partial;
     ea.moments = g->moments;
     ea.out = out;
@@ -1142,7 +1337,7 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         count_launch();
     }
     if (blk1 > blk0) {
-        k_dlp_diag<<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
+        k_dlp_diag<0><<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
         count_launch();
     }
     if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -1236,6 +1431,50 @@ using namespace bie;
 
 extern "C" {
 
+// NEXT-1 field evaluation with the single-layer density: the plain trapezoid
+// sum of P:l.346-354 (eq. stokesSLP_discretized), no correction.
+int slp_field_eval_impl(Geometry *g, const double *sigma, const double2 *targets, int ntgt, double *out,
+                        cudaStream_t st) {
+    if (ntgt == 0) return BIE_OK;
+    const int N = g->N;
+    int rc = slp_prepare(g);
+    if (rc != BIE_OK) return rc;
+    k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, 2LL * N, 1, N, g->slp_s, nullptr);
+    count_launch();
+    PairSched s;
+    make_sched(g, 0, ntgt, s, 1);
+    const size_t need = (size_t)s.S * 2 * (size_t)ntgt;
+    if (need > g->partial_elems) {
+        BIE_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaFree(g->partial);
+        g->partial = nullptr;
+        g->partial_elems = 0;
+        BIE_CUDA_TRY(cudaMalloc(&g->partial, need * sizeof(double)));
+        g->partial_elems = need;
+    }
+    PairArgs a;
+    a.tpos = targets;
+    a.pos = g->pos;
+    a.nw = g->nw;
+    a.sigma = g->slp_s;
+    a.sig_stride = 2LL * N;
+    a.partial = g->partial;
+    a.nvec_total = 1;
+    a.v0 = 0;
+    a.N = N;
+    a.row_begin = 0;
+    a.Nt = ntgt;
+    a.nTS = s.nTS;
+    a.U = s.U;
+    launch_pairs(0, s, a, st, 1);
+    count_launch();
+    k_field_epilogue<<<(ntgt + 127) / 128, 128, 0, st>>>(targets, g->partial, ntgt, Chunk{0, 1, s.TB, s.nTS, s.P, s.U},
+                                                         nullptr, nullptr, 0, out);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
+    return BIE_OK;
+}
+
 static int check_apply_args(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, const char *fn) {
     if (!g) {
         set_error(std::string(fn) + ": invalid geometry handle");
@@ -1323,6 +1562,40 @@ int bie_dlp_epilogue_rows(bie_geometry_t gh, const double *sigma, const double *
         return BIE_EINVAL;
     }
     return epilogue_rows_impl(g, sigma, pairsum_rows, out_rows, row_begin, row_end, flags, (cudaStream_t)stream);
+}
+
+int bie_slp_apply(bie_geometry_t gh, const double *sigma, double *out, int nvec, unsigned flags, void *stream) {
+    Geometry *g = as_geom(gh);
+    int rc = check_apply_args(g, sigma, out, nvec, flags, "bie_slp_apply");
+    if (rc) return rc;
+    if (flags & BIE_D_ONLY) {
+        set_error("bie_slp_apply: BIE_D_ONLY does not apply to the single-layer operator");
+        return BIE_EINVAL;
+    }
+    return dlp_apply_impl(g, sigma, out, nvec, flags | kOpSLP, 0, g->N, (cudaStream_t)stream);
+}
+
+int bie_slp_apply_rows(bie_geometry_t gh, const double *sigma, double *out, int nvec, int row_begin, int row_end,
+                       void *stream) {
+    Geometry *g = as_geom(gh);
+    int rc = check_apply_args(g, sigma, out, nvec, 0u, "bie_slp_apply_rows");
+    if (rc) return rc;
+    if (row_begin < 0 || row_end > g->N || row_begin > row_end) {
+        set_error("bie_slp_apply_rows: row range out of [0, N]");
+        return BIE_EINVAL;
+    }
+    return dlp_apply_impl(g, sigma, out, nvec, kOpSLP, row_begin, row_end, (cudaStream_t)stream);
+}
+
+int bie_slp_field_eval(bie_geometry_t gh, const double *sigma, const double *targets, int ntgt, double *out,
+                       void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !sigma || (ntgt > 0 && (!targets || !out)) || ntgt < 0 || (const void *)out == (const void *)sigma) {
+        set_error("bie_slp_field_eval: invalid handle, null pointer, ntgt < 0 or out aliasing sigma");
+        return BIE_EINVAL;
+    }
+    return slp_field_eval_impl(g, sigma, reinterpret_cast<const double2 *>(targets), ntgt, out,
+                               (cudaStream_t)stream);
 }
 
 int bie_field_eval(bie_geometry_t gh, const double *sigma, const double *targets, int ntgt, double *out,

@@ -1,4 +1,5 @@
 // geometry.cu -- bie_geometry_* and error plumbing (A1 of SURVEY.md s8(a)).
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -76,6 +77,58 @@ __global__ void k_nodes(int N, int M, int n_pore, int n_outer, double T, const d
     selfc[i] = wi * kn / (2.0 * kPi);
 }
 
+// Kapur-Rokhlin sixth-order log-correction weights (P:l.321-330; reading C24
+// of DESIGN.md).  gamma_1..gamma_6 solve, for l = 0, 1, 2,
+//   2 sum_k gamma_k k^(2l)          = [l == 0]
+//   2 sum_k gamma_k k^(2l) log k    = 2 zeta'(-2l),
+//   zeta'(0) = -log(2 pi)/2,  zeta'(-2l) = (-1)^l (2l)! zeta(2l+1) / (2 (2 pi)^(2l)),
+// computed here in long double: zeta(3), zeta(5) by direct summation to
+// n = 10^5 with the integral tail plus its first two Euler-Maclaurin terms,
+// then Gaussian elimination with partial pivoting.
+static long double zeta_ld(int s) {
+    const long n0 = 100000;
+    long double acc = 0.0L;
+    for (long n = n0 - 1; n >= 1; --n) acc += powl((long double)n, (long double)-s);  // small terms first
+    const long double N = (long double)n0;
+    acc += powl(N, (long double)(1 - s)) / (long double)(s - 1) + 0.5L * powl(N, (long double)-s) +
+           (long double)s / 12.0L * powl(N, (long double)(-s - 1));
+    return acc;
+}
+
+void kr_weights(double gamma[6]) {
+    const long double two_pi = 2.0L * acosl(-1.0L);
+    const long double zp[3] = {-0.5L * logl(two_pi), -2.0L * zeta_ld(3) / (2.0L * two_pi * two_pi),
+                               24.0L * zeta_ld(5) / (2.0L * powl(two_pi, 4))};
+    long double A[6][7];
+    for (int l = 0; l < 3; ++l)
+        for (int k = 1; k <= 6; ++k) {
+            const long double k2l = powl((long double)k, (long double)(2 * l));
+            A[l][k - 1] = 2.0L * k2l;
+            A[3 + l][k - 1] = 2.0L * k2l * logl((long double)k);
+        }
+    for (int l = 0; l < 3; ++l) {
+        A[l][6] = l == 0 ? 1.0L : 0.0L;
+        A[3 + l][6] = 2.0L * zp[l];
+    }
+    for (int c = 0; c < 6; ++c) {
+        int p = c;
+        for (int r = c + 1; r < 6; ++r)
+            if (fabsl(A[r][c]) > fabsl(A[p][c])) p = r;
+        for (int q = 0; q < 7; ++q) std::swap(A[c][q], A[p][q]);
+        for (int r = c + 1; r < 6; ++r) {
+            const long double f = A[r][c] / A[c][c];
+            for (int q = c; q < 7; ++q) A[r][q] -= f * A[c][q];
+        }
+    }
+    long double x[6];
+    for (int c = 5; c >= 0; --c) {
+        long double t = A[c][6];
+        for (int q = c + 1; q < 6; ++q) t -= A[c][q] * x[q];
+        x[c] = t / A[c][c];
+    }
+    for (int k = 0; k < 6; ++k) gamma[k] = (double)x[k];
+}
+
 }  // namespace bie
 
 using namespace bie;
@@ -102,6 +155,7 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     cudaFree(g->stage_in);
     cudaFree(g->stage_out);
     for (cudaEvent_t e : g->prof_ev) cudaEventDestroy(e);
+    cudaFree(g->slp_s);
     cudaFree(g->sym_Q);
     cudaFree(g->sym_off);
     cudaFree(g->sym_tgt);
@@ -215,6 +269,7 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     TRY(cudaMalloc(&g->stage_out, sizeof(double) * (size_t)BIE_MAX_NVEC * 2 * N));
     rc = build_schedules(g);
     if (rc != BIE_OK) return fail(rc);
+    kr_weights(g->kr);
     TRY(cudaDeviceSynchronize());
 #undef TRY
     cudaFree(d_oxy);
@@ -281,6 +336,15 @@ int bie_profile_end(bie_geometry_t gh, double *ms_moments, double *ms_pairs, dou
     *applies = (int)(g->prof_used / 4);
     g->prof = false;
     g->prof_used = 0;
+    return BIE_OK;
+}
+
+int bie_kr_weights(double *gamma) {
+    if (!gamma) {
+        set_error("bie_kr_weights: null output");
+        return BIE_EINVAL;
+    }
+    kr_weights(gamma);
     return BIE_OK;
 }
 

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <cmath>
 #include <vector>
 
@@ -274,22 +275,27 @@ int bie_krylov_trisolve(const double *H, int ldh, const double *g, double *y, in
 
 }  // extern "C"
 
-extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f, double *x, double tol,
-                               int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
-                               int *converged, void *stream) {
+// opf: BIE_FULL (the completed DLP) or kOpSLP (the single-layer operator, NEXT-1)
+static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie_blockdiag_t bdh, const double *f,
+                            double *x, double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                            double *res_true, int *converged, void *stream) {
     Geometry *g = as_geom(gh);
     BlockDiag *bd = bdh ? as_bd(bdh) : nullptr;
     if (!g || (bdh && !bd) || !f || !x || !hist_host || !iters || !res_pc || !res_true || !converged ||
         max_iter < 1 || !(tol > 0.0) || f == x) {
-        set_error("bie_gmres_solve: invalid handle, null pointer, f == x, max_iter < 1 or tol <= 0");
+        set_error(std::string(fn) + ": invalid handle, null pointer, f == x, max_iter < 1 or tol <= 0");
         return BIE_EINVAL;
     }
     if (bd && bd->g != g) {
-        set_error("bie_gmres_solve: blockdiag was built from another geometry");
+        set_error(std::string(fn) + ": blockdiag was built from another geometry");
         return BIE_EINVAL;
     }
     if (bd && (bd->b0 != 0 || bd->b1 != g->M + 1)) {
-        set_error("bie_gmres_solve: blockdiag covers a body range, not the whole geometry");
+        set_error(std::string(fn) + ": blockdiag covers a body range, not the whole geometry");
+        return BIE_EINVAL;
+    }
+    if (bd && bd->op != ((opf & kOpSLP) ? 1 : 0)) {
+        set_error(std::string(fn) + ": blockdiag was factored for the other operator (DLP vs SLP)");
         return BIE_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -355,11 +361,11 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
 
     auto apply_op = [&](const double *in, double *out) -> int {  // out = P^{-1} A in
         if (bd) {
-            int r = dlp_apply_impl(g, in, t, 1, BIE_FULL, 0, g->N, st);
+            int r = dlp_apply_impl(g, in, t, 1, opf, 0, g->N, st);
             if (r) return r;
             return blockdiag_apply_impl(bd, t, out, 1, st);
         }
-        return dlp_apply_impl(g, in, out, 1, BIE_FULL, 0, g->N, st);
+        return dlp_apply_impl(g, in, out, 1, opf, 0, g->N, st);
     };
     auto norm_to = [&](const double *v, double *dst) -> int {  // dst = ||v|| (device)
         int r = multidot(v, 0, 1, v, n, d, s.scal + 5, st);
@@ -444,7 +450,7 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     GM_TRY(cudaGetLastError());
     GM_RC(multiaxpy(V, n, it, s.h, 1.0, 0.0, x, n, st));
     // residual pair (P:l.678-686): r = f - A x
-    GM_RC(dlp_apply_impl(g, x, t, 1, BIE_FULL, 0, g->N, st));
+    GM_RC(dlp_apply_impl(g, x, t, 1, opf, 0, g->N, st));
     k_sub<<<eb, 256, 0, st>>>(f, t, w, n);
     count_launch();
     GM_RC(norm_to(w, s.scal + 6));
@@ -465,6 +471,20 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
     return BIE_OK;
 }
 
+extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f, double *x, double tol,
+                               int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
+                               int *converged, void *stream) {
+    return gmres_solve_impl("bie_gmres_solve", BIE_FULL, gh, bdh, f, x, tol, max_iter, hist_host, iters, res_pc,
+                            res_true, converged, stream);
+}
+
+extern "C" int bie_gmres_solve_slp(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f, double *x, double tol,
+                                   int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
+                                   int *converged, void *stream) {
+    return gmres_solve_impl("bie_gmres_solve_slp", kOpSLP, gh, bdh, f, x, tol, max_iter, hist_host, iters, res_pc,
+                            res_true, converged, stream);
+}
+
 // ---------------------------------------------------------------------------
 // NEXT-3: batched multi-RHS GMRES.  Identical per-system algorithm (reading
 // C13); the operator applications of all active systems share one nvec-wide
@@ -472,17 +492,17 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
 // ---------------------------------------------------------------------------
 namespace bie {
 static int batched_op(Geometry *g, BlockDiag *bd, const double *in, double *tmp, double *out, int nv,
-                      cudaStream_t st) {
+                      cudaStream_t st, unsigned opf) {
     const long long n = 2LL * g->N;
     for (int v0 = 0; v0 < nv; v0 += BIE_MAX_NVEC) {
         const int c = std::min(BIE_MAX_NVEC, nv - v0);
         if (bd) {
-            int rc = dlp_apply_impl(g, in + v0 * n, tmp + v0 * n, c, BIE_FULL, 0, g->N, st);
+            int rc = dlp_apply_impl(g, in + v0 * n, tmp + v0 * n, c, opf, 0, g->N, st);
             if (rc) return rc;
             rc = blockdiag_apply_impl(bd, tmp + v0 * n, out + v0 * n, c, st);
             if (rc) return rc;
         } else {
-            int rc = dlp_apply_impl(g, in + v0 * n, out + v0 * n, c, BIE_FULL, 0, g->N, st);
+            int rc = dlp_apply_impl(g, in + v0 * n, out + v0 * n, c, opf, 0, g->N, st);
             if (rc) return rc;
         }
     }
@@ -490,23 +510,27 @@ static int batched_op(Geometry *g, BlockDiag *bd, const double *in, double *tmp,
 }
 }  // namespace bie
 
-extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, const double *F, double *X, int nrhs,
-                                     double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
-                                     double *res_true, int *converged, void *stream) {
+static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie_blockdiag_t bdh, const double *F,
+                            double *X, int nrhs, double tol, int max_iter, double *hist_host, int *iters,
+                            double *res_pc, double *res_true, int *converged, void *stream) {
     Geometry *g = as_geom(gh);
     BlockDiag *bd = bdh ? as_bd(bdh) : nullptr;
     if (!g || (bdh && !bd) || !F || !X || !hist_host || !iters || !res_pc || !res_true || !converged ||
         max_iter < 1 || !(tol > 0.0) || F == X || nrhs < 1 || nrhs > 64) {
-        set_error("bie_gmres_solve_batch: invalid handle, null pointer, F == X, nrhs not in [1,64], max_iter < 1 "
-                  "or tol <= 0");
+        set_error(std::string(fn) + ": invalid handle, null pointer, F == X, nrhs not in [1,64], max_iter < 1 "
+                                    "or tol <= 0");
         return BIE_EINVAL;
     }
     if (bd && bd->g != g) {
-        set_error("bie_gmres_solve_batch: blockdiag was built from another geometry");
+        set_error(std::string(fn) + ": blockdiag was built from another geometry");
         return BIE_EINVAL;
     }
     if (bd && (bd->b0 != 0 || bd->b1 != g->M + 1)) {
-        set_error("bie_gmres_solve_batch: blockdiag covers a body range, not the whole geometry");
+        set_error(std::string(fn) + ": blockdiag covers a body range, not the whole geometry");
+        return BIE_EINVAL;
+    }
+    if (bd && bd->op != ((opf & kOpSLP) ? 1 : 0)) {
+        set_error(std::string(fn) + ": blockdiag was factored for the other operator (DLP vs SLP)");
         return BIE_EINVAL;
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -605,7 +629,7 @@ extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, con
         const int na = (int)active.size();
         for (int q = 0; q < na; ++q)
             GB_TRY(cudaMemcpyAsync(Win + q * n, Vr(active[q], k), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        GB_RC(batched_op(g, bd, Win, Wt, Wout, na, st));
+        GB_RC(batched_op(g, bd, Win, Wt, Wout, na, st, opf));
         for (int q = 0; q < na; ++q) {
             const int r = active[q];
             GmState &s = S[r];
@@ -649,7 +673,7 @@ extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, con
         GB_RC(multiaxpy(Vr(r, 0), n, it[r], S[r].h, 1.0, 0.0, X + r * n, n, st));
     }
     for (int v0 = 0; v0 < nrhs; v0 += BIE_MAX_NVEC)
-        GB_RC(dlp_apply_impl(g, X + v0 * n, Wt + v0 * n, std::min(BIE_MAX_NVEC, nrhs - v0), BIE_FULL, 0, g->N, st));
+        GB_RC(dlp_apply_impl(g, X + v0 * n, Wt + v0 * n, std::min(BIE_MAX_NVEC, nrhs - v0), opf, 0, g->N, st));
     for (int r = 0; r < nrhs; ++r) {
         k_sub<<<eb, 256, 0, st>>>(F + r * n, Wt + r * n, Win + r * n, n);
         count_launch();
@@ -673,4 +697,18 @@ extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, con
 #undef GB_RC
     cleanup();
     return BIE_OK;
+}
+
+extern "C" int bie_gmres_solve_batch(bie_geometry_t gh, bie_blockdiag_t bdh, const double *F, double *X, int nrhs,
+                                     double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                                     double *res_true, int *converged, void *stream) {
+    return gmres_batch_impl("bie_gmres_solve_batch", BIE_FULL, gh, bdh, F, X, nrhs, tol, max_iter, hist_host, iters,
+                            res_pc, res_true, converged, stream);
+}
+
+extern "C" int bie_gmres_solve_batch_slp(bie_geometry_t gh, bie_blockdiag_t bdh, const double *F, double *X,
+                                         int nrhs, double tol, int max_iter, double *hist_host, int *iters,
+                                         double *res_pc, double *res_true, int *converged, void *stream) {
+    return gmres_batch_impl("bie_gmres_solve_batch_slp", kOpSLP, gh, bdh, F, X, nrhs, tol, max_iter, hist_host,
+                            iters, res_pc, res_true, converged, stream);
 }

@@ -13,6 +13,9 @@ namespace bie {
 constexpr double kPi = 3.14159265358979323846;
 constexpr uint32_t kGeomMagic = 0x4745304du;   // "GEOM"
 constexpr uint32_t kBlockMagic = 0x424c4b44u;  // "BLKD"
+// internal operator bit of dlp_apply_impl's flags: the single-layer operator with
+// the Kapur-Rokhlin correction (NEXT-1) instead of the completed DLP
+constexpr unsigned kOpSLP = 1u << 16;
 
 void set_error(const std::string &msg);
 int cuda_fail(cudaError_t e, const char *what);
@@ -58,6 +61,11 @@ struct Geometry {
     double *stage_in = nullptr, *stage_out = nullptr;  // e2e staging [16][2N] each
     PairSched sched[5];         // nv = 1, 2, 4, 8, 16
     int occ[5] = {0, 0, 0, 0, 0};  // resident pair CTAs per SM per variant
+    // single-layer operator (NEXT-1)
+    PairSched sched_slp[5];
+    int occ_slp[5] = {0, 0, 0, 0, 0};
+    double kr[6] = {0, 0, 0, 0, 0, 0};  // Kapur-Rokhlin gamma_1..gamma_6 (reading C24)
+    double *slp_s = nullptr;             // [16][2N] S = w sigma / (4 pi) (lazy)
     int num_sms = 0;
     // symmetric nvec = 1 path (lazily allocated; see dlp.cu)
     int sym_state = 0;            // 0 = not prepared, 1 = ready, -1 = unavailable (memory cap)
@@ -81,6 +89,7 @@ struct BlockDiag {
     uint32_t magic = kBlockMagic;
     Geometry *g = nullptr;
     int b0 = 0, b1 = 0;             // body range [b0, b1) (pores 0..M-1, wall M)
+    int op = 0;                     // 0: blocks of the completed DLP; 1: of the SLP (NEXT-1)
     int row_lo = 0, row_hi = 0;     // node range covered; apply vectors are local [2 (row_hi-row_lo)]
     int nb = 0;                     // number of bodies
     std::vector<int> lo, n;         // node range per body
@@ -93,6 +102,8 @@ struct BlockDiag {
 Geometry *as_geom(bie_geometry_t g);
 BlockDiag *as_bd(bie_blockdiag_t b);
 
+// geometry.cu
+void kr_weights(double gamma[6]);
 // dlp.cu
 int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, int row_begin,
                    int row_end, cudaStream_t s);

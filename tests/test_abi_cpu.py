@@ -86,3 +86,21 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("no oracle", ""), f
+
+
+def test_kr_weights_library_matches_oracle(bie):
+    """bie_kr_weights needs no device: the library's long-double solve of the
+    C24 conditions agrees with the oracle's 40-digit one to a few ulp."""
+    import oracle
+
+    assert np.abs(bie.kr_weights() - oracle.kr_weights()).max() <= 4 * np.spacing(26.0)
+
+
+def test_slp_entry_points_validate_arguments(bie):
+    L = bie._bie.lib()
+    assert L.bie_slp_apply(None, None, None, 1, 0, None) == -1
+    assert L.bie_slp_apply_rows(None, None, None, 1, 0, 1, None) == -1
+    assert L.bie_slp_field_eval(None, None, None, 1, None, None) == -1
+    assert L.bie_blockdiag_factor_slp(None, None, None) == -1
+    assert L.bie_gmres_solve_slp(None, None, None, None, 1e-8, 10, None, None, None, None, None, None) == -1
+    assert L.bie_kr_weights(None) == -1
