@@ -391,6 +391,43 @@ def run_gpu(args):
         ts = time.perf_counter() - ts
         extra["multi_rhs"] = {"config": 3, "nrhs": 16, "batched_s": tb, "sequential_s": ts,
                               "iters": [r["iters"] for r in rb_], "all_converged": all(r["converged"] for r in rb_)}
+        # NEXT-1: the paper's own single-layer operator (KR-6 corrected) on the same
+        # geometry, and an SLP BD-GMRES solve on config 3
+        slp = {}
+        for nvec in (1, 16):
+            s = torch.from_numpy(density(p, nvec=nvec).reshape(-1)).to(dev)
+            o = torch.zeros_like(s)
+            for _ in range(2):
+                bie.slp_apply(g, s, o, nvec)
+            reps = 3 if nvec == 1 else 1
+            bie.profile_begin(g)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                bie.slp_apply(g, s, o, nvec)
+            b.record(stream)
+            torch.cuda.synchronize()
+            pr = bie.profile_end(g)
+            ms = a.elapsed_time(b) / reps
+            slp[f"matvec_config{CONFIG_ID}_nvec{nvec}"] = {
+                "ms": ms, "pairs_per_s": nvec * N * N / (ms * 1e-3),
+                "kernel_ms": pr["pairs_ms"] / max(1, pr["applies"])}
+            del s, o
+        pp = make_problem(3)
+        gg = bie.Geometry.from_problem(pp)
+        torch.cuda.synchronize()
+        tb = time.perf_counter()
+        bdd = bie.BlockDiag(gg, op="slp")
+        torch.cuda.synchronize()
+        tb = time.perf_counter() - tb
+        ff = torch.from_numpy(rhs_pipe(pp)).to(dev)
+        xx = torch.zeros_like(ff)
+        ts = time.perf_counter()
+        rr = bie.gmres_solve_slp(gg, bdd, ff, xx, tol=1e-8, max_iter=1000)
+        ts = time.perf_counter() - ts
+        slp["gmres_config3"] = {"build_pc_s": tb, "gmres_s": ts, "iters": rr["iters"], "converged": rr["converged"],
+                                "res_true": rr["res_true"], "tol": 1e-8}
+        extra["slp"] = slp
         if not args.no_config5:
             extra["config5_sweep"] = config5_sweep(bie, dev, stream)
 
