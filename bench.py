@@ -77,6 +77,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (NVML init, device enumeration) holds driver
+            # locks for ~100 ms; wait for its first sample so that cost lands
+            # before the timed region, not inside its first steps
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -440,6 +446,7 @@ def run_gpu(args):
     line = {
         "metric": "DLP matvec pair-interactions/s", "value": value, "unit": "pair-interactions/s", "n_gpus": ws,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": statistics.mean(step_ms),
+        "step_ms_each": [round(t, 3) for t in step_ms],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config4 pipe L=100 M=1000 N={N} (2N={2 * N} unknowns), pipe BC; step = "
                                f"BD-preconditioned GMRES solve, fixed {GMRES_ITERS} iterations "
