@@ -456,7 +456,7 @@ def run_gpu(args):
                    "parallelism": f"rows{ws} (row-sharded solve, all-gather + all-reduce over NCCL)" if ws > 1
                    else "single",
                    "l2": "flushed between timed steps (256 MiB write); BD inverses (2.67 GB) exceed L2 each step"},
-        "roofline": {"kernel": ("all-pairs phase: k_dlp_sym<8,2> + k_dlp_diag (nvec=1 symmetric path)" if ws == 1
+        "roofline": {"kernel": ("all-pairs phase: k_dlp_sym<8,2> dual-source + k_dlp_diag (nvec=1 symmetric path)" if ws == 1
                                 else "all-pairs phase on this rank's slice of the symmetric work list"),
                      "bound": "alu", "achieved": achieved_tflops,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,

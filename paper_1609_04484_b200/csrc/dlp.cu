@@ -336,6 +336,41 @@ __global__ void k_quad(const double2 *__restrict__ nw, const double *__restrict_
     Q[j] = make_double4(a.x * b.x, fma(a.x, b.y, a.y * b.x), a.y * b.y, 0.0);
 }
 
+// One unordered pair (target t, source s) of the symmetric kernels: the target
+// accumulates the source's contribution and vice versa (DLP: odd in r, so the
+// source side takes -b; SLP: even in r).
+__device__ __forceinline__ void dlp_pairpair(double tx, double ty, double tqa, double tqb, double tqc, double sx,
+                                             double sy, double sqa, double sqb, double sqc, double &ax, double &ay,
+                                             double &bx, double &by) {
+    const double rx = tx - sx, ry = ty - sy;
+    const double xx = rx * rx, yy = fma(ry, ry, 1e-300), xy = rx * ry;
+    const double d = xx + yy;
+    double i = rcp_approx(d);
+    const double cs = fma(sqa, xx, fma(sqb, xy, sqc * yy));  // target <- source
+    const double ct = fma(tqa, xx, fma(tqb, xy, tqc * yy));  // source <- target
+    const double e = fma(-d, i, 1.0);
+    i = fma(i, fma(e, e, e), i);
+    const double q = i * i;
+    const double a = cs * q, b = ct * q;
+    ax = fma(a, rx, ax);
+    ay = fma(a, ry, ay);
+    bx = fma(-b, rx, bx);
+    by = fma(-b, ry, by);
+}
+
+__device__ __forceinline__ void slp_pairpair(double tx, double ty, double tsx, double tsy, double sx, double sy,
+                                             double ssx, double ssy, double &ax, double &ay, double &bx,
+                                             double &by) {
+    const double rx = tx - sx, ry = ty - sy;
+    double hl, i;
+    slp_factors(rx, ry, hl, i);
+    const double ct = i * fma(rx, ssx, ry * ssy), cs = i * fma(rx, tsx, ry * tsy);
+    ax = fma(ct, rx, fma(hl, ssx, ax));
+    ay = fma(ct, ry, fma(hl, ssy, ay));
+    bx = fma(cs, rx, fma(hl, tsx, bx));
+    by = fma(cs, ry, fma(hl, tsy, by));
+}
+
 struct SymArgs {
     const double2 *pos;
     const double4 *Q;
@@ -349,8 +384,11 @@ struct SymArgs {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int SR, int SW, int MINB = 1, bool QS = false, int TP = 0, int OP = 0>
+template <int SR, int SW, int MINB = 1, bool QS = false, int TP = 0, int OP = 0, bool DS = false>
 __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
+    // DS: dual-source steps -- each of 16 steps pairs every target with sources
+    // (l + t) and (l + t + 16); two rotating source accumulators give the
+    // independent chains with half the target registers of SR = 8.
     // OP = 1: single-layer operator (NEXT-1).  Q holds (S_x, S_y, 0, 0) with
     // S = w sigma / (4 pi); G is even in r, so both directions get
     //   u += hl S + (r . S) r / rho^2   with the shared hl = -1/2 log rho^2, 1/rho^2.
@@ -446,13 +484,45 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
         double bx1 = 0.0, by1 = 0.0;
         double2 nxy, nab;
         double nc;
-        if constexpr (TP == 1) {
+        if constexpr (DS) {
+            double bxA = 0.0, byA = 0.0, bxB = 0.0, byB = 0.0;
+#pragma unroll 1
+            for (int t = 0; t < 16; ++t) {
+                const int la = (lane + t) & 31, lb = (lane + t + 16) & 31;
+                const double2 xa = s_src[buf][w][0][la], qa = s_src[buf][w][1][la];
+                const double2 xb = s_src[buf][w][0][lb], qb = s_src[buf][w][1][lb];
+                const double ca = s_src[buf][w][2][la].x, cb = s_src[buf][w][2][lb].x;
+#pragma unroll
+                for (int r = 0; r < SR; ++r) {
+                    if constexpr (OP == 1) {
+                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xa.x, xa.y, qa.x, qa.y, ax[r], ay[r], bxA, byA);
+                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xb.x, xb.y, qb.x, qb.y, ax[r], ay[r], bxB, byB);
+                    } else {
+                        dlp_pairpair(tx[r], ty[r], tqa[r], tqb[r], tqc[r], xa.x, xa.y, qa.x, qa.y, ca, ax[r], ay[r],
+                                     bxA, byA);
+                        dlp_pairpair(tx[r], ty[r], tqa[r], tqb[r], tqc[r], xb.x, xb.y, qb.x, qb.y, cb, ax[r], ay[r],
+                                     bxB, byB);
+                    }
+                }
+                bxA = shfl_d(bxA, src_lane);
+                byA = shfl_d(byA, src_lane);
+                bxB = shfl_d(bxB, src_lane);
+                byB = shfl_d(byB, src_lane);
+            }
+            // after 16 rotations source l's B-accumulator is back in lane l and
+            // its A-accumulator sits in lane l + 16
+            bx = bxB;
+            by = byB;
+            bx1 = __shfl_xor_sync(0xffffffffu, bxA, 16);
+            by1 = __shfl_xor_sync(0xffffffffu, byA, 16);
+        }
+        if constexpr (TP == 1 && !DS) {
             nxy = s_src[buf][w][0][lane];
             nab = s_src[buf][w][1][lane];
             nc = s_src[buf][w][2][lane].x;
         }
 #pragma unroll(TP == 2 ? 2 : 1)
-        for (int t = 0; t < 32; ++t) {
+        for (int t = 0; t < (DS ? 0 : 32); ++t) {
             if constexpr (TP == 1) {
                 sx = nxy.x;
                 sy = nxy.y;
@@ -919,9 +989,11 @@ int build_schedules(Geometry *g) {
 // variants 3..5 add a minimum-blocks launch bound (register cap -> more warps)
 // variants 6..8 keep the target quadratic forms in shared memory (QS)
 // variants 11..14 pipeline the source steps (TP = 1: loads one step ahead; 2: unroll 2)
-static const int kNumSymVar = 15;
-static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2}, {8, 2},
-                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4}, {4, 4}};
+// variants 15..18 use dual-source steps (DS)
+static const int kNumSymVar = 19;
+static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2},
+                                           {8, 2}, {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4},
+                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {2, 8}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
@@ -938,6 +1010,10 @@ static void *sym_kernel(int v) {
         case 12: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 2>);
         case 13: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, false, 1>);
         case 14: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, false, 1>);
+        case 15: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, false, 0, 0, true>);
+        case 16: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, false, 0, 0, true>);
+        case 17: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 0, 0, true>);
+        case 18: return reinterpret_cast<void *>(&k_dlp_sym<2, 8, 2, false, 0, 0, true>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -958,7 +1034,23 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 12: k_dlp_sym<8, 2, 1, false, 2><<<P, 64, 0, st>>>(sa); break;
         case 13: k_dlp_sym<4, 4, 4, false, 1><<<P, 128, 0, st>>>(sa); break;
         case 14: k_dlp_sym<4, 4, 3, false, 1><<<P, 128, 0, st>>>(sa); break;
+        case 15: k_dlp_sym<4, 4, 4, false, 0, 0, true><<<P, 128, 0, st>>>(sa); break;
+        case 16: k_dlp_sym<4, 4, 3, false, 0, 0, true><<<P, 128, 0, st>>>(sa); break;
+        case 17: k_dlp_sym<8, 2, 1, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
+        case 18: k_dlp_sym<2, 8, 2, false, 0, 0, true><<<P, 256, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
+    }
+}
+
+// Single-layer symmetric kernel variants (tuning knob BIE_SLP_SYM_VARIANT):
+// 0 = (8,2) with one-step-ahead source loads, 1 = (8,2) dual-source,
+// 2 = (4,4) dual-source at 3 CTAs/SM, 3 = (4,4) dual-source at 4 CTAs/SM.
+static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
+    switch (v) {
+        case 1: k_dlp_sym<8, 2, 1, false, 0, 1, true><<<P, 64, 0, st>>>(sa); break;
+        case 2: k_dlp_sym<4, 4, 3, false, 0, 1, true><<<P, 128, 0, st>>>(sa); break;
+        case 3: k_dlp_sym<4, 4, 4, false, 0, 1, true><<<P, 128, 0, st>>>(sa); break;
+        default: k_dlp_sym<8, 2, 1, false, 1, 1><<<P, 64, 0, st>>>(sa); break;
     }
 }
 
@@ -973,6 +1065,7 @@ static int sym_prepare(Geometry *g) {
     const long long nC = (N + kSymChunk - 1) / kSymChunk;
     const size_t src_bytes = sizeof(double) * 2 * (size_t)N * nTB;
     if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(kNumSymVar - 1, atoi(e)));  // tuning knob
+    if (const char *e = getenv("BIE_SLP_SYM_VARIANT")) g->slp_sym_variant = std::max(0, std::min(3, atoi(e)));
     {
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
@@ -1103,7 +1196,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         if (g->sym_U > 0) {
             SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, g->sym_U, 0};
             if (op)
-                k_dlp_sym<8, 2, 1, false, 1, 1><<<g->sym_P, 64, 0, st>>>(sa);
+                launch_sym_slp(g->slp_sym_variant, g->sym_P, sa, st);
             else
                 launch_sym(g->sym_variant, g->sym_P, sa, st);
             count_launch();

@@ -74,7 +74,8 @@ struct Geometry {
     double *sym_tgt = nullptr;    // [S][2N]
     double *sym_src = nullptr;    // [nTB][2N]
     double *sym_diag = nullptr;   // [2N]
-    int sym_nTB = 0, sym_P = 0, sym_S = 0, sym_variant = 2;  // (R, W) = (8, 2): fastest measured
+    int sym_nTB = 0, sym_P = 0, sym_S = 0, sym_variant = 17;  // (R, W) = (8, 2) dual-source: fastest measured
+    int slp_sym_variant = 0;
     long long sym_U = 0;
     // profiling (bie_profile_begin/end): 4 events per recorded apply
     bool prof = false;
