@@ -875,6 +875,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
                 s_pm[threadIdx.x] = make_double4(m[0], m[1], m[2], 0.0);
             }
             __syncthreads();
+#pragma unroll 4
             for (int q = 0; q < nk; ++q) {
                 const double4 pk = s_pc[q], pm = s_pm[q];
                 const double rx = xi.x - pk.x, ry = xi.y - pk.y;
@@ -882,7 +883,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
                 double ir = rcp_approx(rho2);
                 const double e = fma(-rho2, ir, 1.0);
                 ir = fma(ir, fma(e, e, e), ir);
-                const double lg = 0.5 * log(rho2);
+                const double lg = 0.5 * log_pair(rho2);
                 const double rk = pk.z * ir;
                 const double rl = (rx * pm.x + ry * pm.y) * ir;
                 u[0].x += k4pi * (-lg * pm.x + rx * rl) + rk * ry * pm.z;
@@ -895,7 +896,7 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             const double rx = xi.x - pk.x, ry = xi.y - pk.y;
             const double rho2 = rx * rx + ry * ry;
             const double ir = 1.0 / rho2;
-            const double lg = 0.5 * log(rho2);
+            const double lg = 0.5 * log_pair(rho2);
             const double rk = pk.z * ir;
             for (int v = 0; v < nvec; ++v) {
                 const double *m = a.moments + ((long long)v * a.M + k) * 3;
@@ -1330,7 +1331,7 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
             const double rx = xi.x - pk.x, ry = xi.y - pk.y;
             const double rho2 = fma(rx, rx, ry * ry);
             const double ir = 1.0 / rho2;
-            const double lg = 0.5 * log(rho2);
+            const double lg = 0.5 * log_pair(rho2);
             const double rk = pk.z * ir;
             const double rl = (rx * pm.x + ry * pm.y) * ir;
             u.x += k4pi * (-lg * pm.x + rx * rl) + rk * ry * pm.z;
