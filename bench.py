@@ -327,7 +327,8 @@ def run_gpu(args):
         x_host.copy_(x, non_blocking=True)
         e2e_ev[k][1].record(stream)
     torch.cuda.synchronize()
-    e2e_s = sum(a.elapsed_time(b) for a, b in e2e_ev) / 1e3
+    e2e_ms_each = [a.elapsed_time(b) for a, b in e2e_ev]
+    e2e_s = sum(e2e_ms_each) / 1e3
     if dist:
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -465,7 +466,8 @@ def run_gpu(args):
                      "executed_flop_per_pair": 17,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
         "e2e": {"value": args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
-                "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8)},
+                "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8),
+                "step_ms_each": [round(t, 3) for t in e2e_ms_each]},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "setup": {"geometry_s": t_geom, "build_pc_s": t_bd},

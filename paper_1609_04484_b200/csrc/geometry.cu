@@ -3,8 +3,10 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -155,7 +157,19 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     cudaFree(g->stage_in);
     cudaFree(g->stage_out);
     for (cudaEvent_t e : g->prof_ev) cudaEventDestroy(e);
+    if (g->sym_trace) {  // BIE_SYM_TRACE=<file>: dump the last symmetric launch's CTA start/end times
+        std::vector<unsigned long long> tr(2 * (size_t)g->sym_P);
+        if (cudaMemcpy(tr.data(), g->sym_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost) ==
+            cudaSuccess) {
+            if (FILE *f = fopen(getenv("BIE_SYM_TRACE"), "w")) {
+                for (size_t q = 0; q < tr.size(); q += 2) fprintf(f, "%llu %llu\n", tr[q], tr[q + 1]);
+                fclose(f);
+            }
+        }
+        cudaFree(g->sym_trace);
+    }
     cudaFree(g->slp_s);
+    cudaFree(g->sym_counter);
     cudaFree(g->sym_Q);
     cudaFree(g->sym_off);
     cudaFree(g->sym_tgt);

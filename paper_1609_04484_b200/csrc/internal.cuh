@@ -76,6 +76,9 @@ struct Geometry {
     double *sym_diag = nullptr;   // [2N]
     int sym_nTB = 0, sym_P = 0, sym_S = 0, sym_variant = 17;  // (R, W) = (8, 2) dual-source: fastest measured
     int slp_sym_variant = 0;
+    unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
+    unsigned long long *sym_counter = nullptr;  // dynamic segment counter of the symmetric kernel
+    long long sym_Useg = 1;                     // units per segment
     long long sym_U = 0;
     // profiling (bie_profile_begin/end): 4 events per recorded apply
     bool prof = false;
