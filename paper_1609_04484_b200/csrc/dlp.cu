@@ -1024,10 +1024,10 @@ int build_schedules(Geometry *g) {
 // variants 6..8 keep the target quadratic forms in shared memory (QS)
 // variants 11..14 pipeline the source steps (TP = 1: loads one step ahead; 2: unroll 2)
 // variants 15..18 use dual-source steps (DS)
-static const int kNumSymVar = 19;
+static const int kNumSymVar = 21;
 static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2},
                                            {8, 2}, {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4},
-                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {2, 8}};
+                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {2, 8}, {8, 2}, {8, 2}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
@@ -1048,6 +1048,8 @@ static void *sym_kernel(int v) {
         case 16: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, false, 0, 0, true>);
         case 17: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 0, 0, true>);
         case 18: return reinterpret_cast<void *>(&k_dlp_sym<2, 8, 2, false, 0, 0, true>);
+        case 19: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, false, 0, 0, true>);
+        case 20: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 6, false, 0, 0, true>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -1072,6 +1074,8 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 16: k_dlp_sym<4, 4, 3, false, 0, 0, true><<<P, 128, 0, st>>>(sa); break;
         case 17: k_dlp_sym<8, 2, 1, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
         case 18: k_dlp_sym<2, 8, 2, false, 0, 0, true><<<P, 256, 0, st>>>(sa); break;
+        case 19: k_dlp_sym<8, 2, 5, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
+        case 20: k_dlp_sym<8, 2, 6, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
