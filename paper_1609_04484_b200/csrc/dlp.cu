@@ -79,6 +79,40 @@ __device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, do
     hl = -0.5 * log_pair(d);
 }
 
+// Table-driven variant for the symmetric SLP kernel (Tang-style reduction):
+// d = 2^e m, m in [1, 2); k = top 6 mantissa bits; tab[k] = (rc_k, -1/2 log rc_k)
+// with rc_k = RN(1 / (1 + (k + 1/2)/64)).  r = m rc_k - 1 (one FMA, |r| < 2^-7),
+// log m = log1p(r) - log rc_k, log1p(r) = r (1 - r/2 + ... - r^7/8) (truncation
+// < 2^-63).  Returns hl = -1/2 log d directly (scaled coefficients): 11 FP64
+// instructions instead of 18 + 1, plus one shared-memory lookup.
+struct LogTab {
+    double2 e[64];
+};
+__device__ __forceinline__ void log_tab_init(LogTab &t, int tid, int nthreads) {
+    for (int k = tid; k < 64; k += nthreads) {
+        const double rc = 1.0 / (1.0 + (k + 0.5) / 64.0);
+        t.e[k] = make_double2(rc, 0.5 * log(rc));  // -1/2 log(1/rc) = 1/2 log rc
+    }
+}
+__device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
+    const int hi = __double2hiint(d), lo = __double2loint(d);
+    const int e = (hi >> 20) - 1023;
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double2 tk = t.e[(hi >> 14) & 63];
+    const double r = fma(m, tk.x, -1.0);
+    double q = 0.5 / 8.0;  // -1/2 (1 - r/2 + r^2/3 - ... - r^7/8)
+    q = fma(q, r, -0.5 / 7.0);
+    q = fma(q, r, 0.5 / 6.0);
+    q = fma(q, r, -0.5 / 5.0);
+    q = fma(q, r, 0.5 / 4.0);
+    q = fma(q, r, -0.5 / 3.0);
+    q = fma(q, r, 0.5 / 2.0);
+    q = fma(q, r, -0.5);
+    const double ed = (double)e;
+    const double base = fma(ed, -0.5 * 0.69314718055994528623, fma(ed, -0.5 * 2.3190468138462996e-17, tk.y));
+    return fma(r, q, base);
+}
+
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src, int src_bytes) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem_src), "r"(src_bytes));
@@ -360,10 +394,14 @@ __device__ __forceinline__ void dlp_pairpair(double tx, double ty, double tqa, d
 
 __device__ __forceinline__ void slp_pairpair(double tx, double ty, double tsx, double tsy, double sx, double sy,
                                              double ssx, double ssy, double &ax, double &ay, double &bx,
-                                             double &by) {
+                                             double &by, const LogTab &lt) {
     const double rx = tx - sx, ry = ty - sy;
-    double hl, i;
-    slp_factors(rx, ry, hl, i);
+    double d = fma(rx, rx, ry * ry);
+    d = d == 0.0 ? 1.0 : d;  // zero padding only (no self pairs here): hl = 0, r = 0
+    double i = rcp_approx(d);
+    const double ee = fma(-d, i, 1.0);
+    i = fma(i, fma(ee, ee, ee), i);
+    const double hl = neg_half_log_tab(d, lt);
     const double ct = i * fma(rx, ssx, ry * ssy), cs = i * fma(rx, tsx, ry * tsy);
     ax = fma(ct, rx, fma(hl, ssx, ax));
     ay = fma(ct, ry, fma(hl, ssy, ay));
@@ -420,6 +458,8 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     static_assert(SR % 2 == 0, "two interleaved chains");
     __shared__ double2 red[SW][32];
     __shared__ __align__(16) double2 s_src[2][SW][3][32];  // [buf][warp][(x,y) | (qa,qb) | (qc,-)][lane]
+    __shared__ LogTab s_log;  // OP = 1 only
+    if constexpr (OP == 1) log_tab_init(s_log, threadIdx.x, 32 * SW);  // visible after the first segment barrier
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int p = blockIdx.x;
     const long long U = a.U, Useg = a.Useg;
@@ -527,8 +567,10 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
 #pragma unroll
                 for (int r = 0; r < SR; ++r) {
                     if constexpr (OP == 1) {
-                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xa.x, xa.y, qa.x, qa.y, ax[r], ay[r], bxA, byA);
-                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xb.x, xb.y, qb.x, qb.y, ax[r], ay[r], bxB, byB);
+                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xa.x, xa.y, qa.x, qa.y, ax[r], ay[r], bxA, byA,
+                                     s_log);
+                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xb.x, xb.y, qb.x, qb.y, ax[r], ay[r], bxB, byB,
+                                     s_log);
                     } else {
                         dlp_pairpair(tx[r], ty[r], tqa[r], tqb[r], tqc[r], xa.x, xa.y, qa.x, qa.y, ca, ax[r], ay[r],
                                      bxA, byA);
@@ -580,8 +622,18 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
                     const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
                     const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
                     double hl0, hl1, i0, i1;
-                    slp_factors(rx0, ry0, hl0, i0);
-                    slp_factors(rx1, ry1, hl1, i1);
+                    {
+                        double d0 = fma(rx0, rx0, ry0 * ry0), d1 = fma(rx1, rx1, ry1 * ry1);
+                        d0 = d0 == 0.0 ? 1.0 : d0;
+                        d1 = d1 == 0.0 ? 1.0 : d1;
+                        i0 = rcp_approx(d0);
+                        i1 = rcp_approx(d1);
+                        const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
+                        i0 = fma(i0, fma(e0, e0, e0), i0);
+                        i1 = fma(i1, fma(e1, e1, e1), i1);
+                        hl0 = neg_half_log_tab(d0, s_log);
+                        hl1 = neg_half_log_tab(d1, s_log);
+                    }
                     const double ct0 = i0 * fma(rx0, sqa, ry0 * sqb), ct1 = i1 * fma(rx1, sqa, ry1 * sqb);
                     const double cs0 = i0 * fma(rx0, tqa[r], ry0 * tqb[r]);
                     const double cs1 = i1 * fma(rx1, tqa[r + 1], ry1 * tqb[r + 1]);
@@ -1081,7 +1133,7 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
 }
 
 // Single-layer symmetric kernel variants (tuning knob BIE_SLP_SYM_VARIANT):
-// 0 = (8,2) with one-step-ahead source loads, 1 = (8,2) dual-source,
+// 0 = (8,2) with one-step-ahead source loads, 1 = (8,2) dual-source (default),
 // 2 = (4,4) dual-source at 3 CTAs/SM, 3 = (4,4) dual-source at 4 CTAs/SM.
 static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {

@@ -75,7 +75,7 @@ struct Geometry {
     double *sym_src = nullptr;    // [nTB][2N]
     double *sym_diag = nullptr;   // [2N]
     int sym_nTB = 0, sym_P = 0, sym_S = 0, sym_variant = 17;  // (R, W) = (8, 2) dual-source: fastest measured
-    int slp_sym_variant = 0;
+    int slp_sym_variant = 1;  // (8,2) dual-source: fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
     unsigned long long *sym_counter = nullptr;  // dynamic segment counter of the symmetric kernel
     long long sym_Useg = 1;                     // units per segment
