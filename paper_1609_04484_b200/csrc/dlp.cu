@@ -346,8 +346,8 @@ __global__ void k_moments(const double2 *__restrict__ pos, const double2 *__rest
 //   Q_j = (nwx sx, nwx sy + nwy sx, nwy sy)   (nw = w n / pi, s = sigma)
 // (r.nw_j)(r.s_j) = Qxx rx^2 + Qxy rx ry + Qyy ry^2, so
 //   u_i += Q_j(r) r / rho^4      and      u_j -= Q_i(r) r / rho^4.
-// Each unordered pair is evaluated once: 22 FP64 instructions for both
-// directions (11 per directed pair vs 16).  Blocks of TB = 512 nodes; block A
+// Each unordered pair is evaluated once: 21 FP64 instructions for both
+// directions (10.5 per directed pair vs 16; see k_quad for the Q' form).  Blocks of TB = 512 nodes; block A
 // pairs with every 32-node chunk after its end ("units"), handled by a
 // persistent grid over the triangular unit list.  Inside a warp the 32-source
 // chunk rotates through the lanes (__shfl) together with its accumulator, so
@@ -367,7 +367,11 @@ __global__ void k_quad(const double2 *__restrict__ nw, const double *__restrict_
     if (j >= N) return;
     const double2 a = nw[j];
     const double2 b = reinterpret_cast<const double2 *>(sigma)[j];
-    Q[j] = make_double4(a.x * b.x, fma(a.x, b.y, a.y * b.x), a.y * b.y, 0.0);
+    // (Qxx, Qxy, Qyy - Qxx): with d = rx^2 + ry^2,
+    //   Qxx rx^2 + Qxy rx ry + Qyy ry^2 = Qxx d + Qxy rx ry + (Qyy - Qxx) ry^2,
+    // so the pair loop never forms rx^2 (21 instead of 22 FP64 instructions)
+    const double qxx = a.x * b.x;
+    Q[j] = make_double4(qxx, fma(a.x, b.y, a.y * b.x), fma(a.y, b.y, -qxx), 0.0);
 }
 
 // One unordered pair (target t, source s) of the symmetric kernels: the target
@@ -377,11 +381,11 @@ __device__ __forceinline__ void dlp_pairpair(double tx, double ty, double tqa, d
                                              double sy, double sqa, double sqb, double sqc, double &ax, double &ay,
                                              double &bx, double &by) {
     const double rx = tx - sx, ry = ty - sy;
-    const double xx = rx * rx, yy = fma(ry, ry, 1e-300), xy = rx * ry;
-    const double d = xx + yy;
+    const double yy = fma(ry, ry, 1e-300), xy = rx * ry;
+    const double d = fma(rx, rx, yy);
     double i = rcp_approx(d);
-    const double cs = fma(sqa, xx, fma(sqb, xy, sqc * yy));  // target <- source
-    const double ct = fma(tqa, xx, fma(tqb, xy, tqc * yy));  // source <- target
+    const double cs = fma(sqa, d, fma(sqb, xy, sqc * yy));  // target <- source (Q' form, k_quad)
+    const double ct = fma(tqa, d, fma(tqb, xy, tqc * yy));  // source <- target
     const double e = fma(-d, i, 1.0);
     i = fma(i, fma(e, e, e), i);
     const double q = i * i;
@@ -649,13 +653,12 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
                 }
                 const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
                 const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
-                const double xx0 = rx0 * rx0, xx1 = rx1 * rx1;
                 const double yy0 = fma(ry0, ry0, 1e-300), yy1 = fma(ry1, ry1, 1e-300);
                 const double xy0 = rx0 * ry0, xy1 = rx1 * ry1;
-                const double d0 = xx0 + yy0, d1 = xx1 + yy1;
+                const double d0 = fma(rx0, rx0, yy0), d1 = fma(rx1, rx1, yy1);
                 double i0 = rcp_approx(d0), i1 = rcp_approx(d1);
-                const double cs0 = fma(sqa, xx0, fma(sqb, xy0, sqc * yy0));  // target <- source
-                const double cs1 = fma(sqa, xx1, fma(sqb, xy1, sqc * yy1));
+                const double cs0 = fma(sqa, d0, fma(sqb, xy0, sqc * yy0));  // target <- source (Q' form)
+                const double cs1 = fma(sqa, d1, fma(sqb, xy1, sqc * yy1));
                 double qa0, qb0, qc0, qa1, qb1, qc1;
                 if constexpr (QS) {
                     const double2 ab0 = s_tqab[w][r][lane], ab1 = s_tqab[w][r + 1][lane];
@@ -673,8 +676,8 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
                     qb1 = tqb[r + 1];
                     qc1 = tqc[r + 1];
                 }
-                const double ct0 = fma(qa0, xx0, fma(qb0, xy0, qc0 * yy0));  // source <- target
-                const double ct1 = fma(qa1, xx1, fma(qb1, xy1, qc1 * yy1));
+                const double ct0 = fma(qa0, d0, fma(qb0, xy0, qc0 * yy0));  // source <- target
+                const double ct1 = fma(qa1, d1, fma(qb1, xy1, qc1 * yy1));
                 const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
                 i0 = fma(i0, fma(e0, e0, e0), i0);
                 i1 = fma(i1, fma(e1, e1, e1), i1);
