@@ -283,3 +283,37 @@ def test_slp_abi_errors(bie):
     slp_bd = bie.BlockDiag(g, op="slp")
     with pytest.raises(bie.BieError):
         bie.gmres_solve(g, slp_bd, s, o, 1e-8, 10)
+
+
+@pytest.mark.parametrize("n", [64, 100, 16])
+def test_single_curve_no_pores(bie, n):
+    """Edge case: a geometry with no pores (M = 0), node counts below one
+    512-block and not a multiple of the 32-node chunk; DLP and SLP parity."""
+    p = make_circle_problem(n_outer=n, R=1.3, pores=())
+    g = bie.Geometry.from_problem(p)
+    og = oracle.OracleGeometry(p)
+    s = density(p, nvec=2, vec_id=1)
+    y = _gpu_slp(bie, g, s, 2)
+    ref = og.slp_apply(s)
+    for v in range(2):
+        assert _relerr(y[v], ref[v]) <= TOL
+    import torch
+
+    sig = _t(s)
+    out = torch.full_like(sig, float("nan"))
+    bie.dlp_apply(g, sig, out, 2)
+    torch.cuda.synchronize()
+    yd = out.cpu().numpy().reshape(2, -1)
+    refd = og.apply(s)
+    for v in range(2):
+        assert _relerr(yd[v], refd[v]) <= TOL
+
+
+def test_slp_one_sided_sampled_config3(bie):
+    p = make_problem(3)
+    g, og = _setup(bie, p)
+    s = density(p, nvec=1, vec_id=5)
+    y = _gpu_slp(bie, g, s, 1, 2)[0].reshape(-1, 2)
+    rows = _rows(p, 512)
+    ref = og.slp_apply(s[0], rows=rows).reshape(-1, 2)
+    assert np.abs(y[rows] - ref).max() / np.abs(ref).max() <= TOL
