@@ -797,6 +797,28 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
     }
 }
 
+// acc += sum_{q < n} p[q * stride + 2i .. 2i+1] in order q = 0, 1, ..., with
+// the loads issued 8 at a time (the adds stay sequential, so the order and the
+// result are unchanged; the loop was latency-bound on one load per add).
+__device__ __forceinline__ void sum_strided(double2 &acc, const double *p, long long stride, int n, int i) {
+    int q = 0;
+    for (; q + 8 <= n; q += 8) {
+        double2 v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = reinterpret_cast<const double2 *>(p + (long long)(q + t) * stride)[i];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            acc.x += v[t].x;
+            acc.y += v[t].y;
+        }
+    }
+    for (; q < n; ++q) {
+        const double2 v = reinterpret_cast<const double2 *>(p + (long long)q * stride)[i];
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+}
+
 struct Chunk {
     int v0, nv, TB, nTS, P;
     long long U;
@@ -857,22 +879,14 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         if (oB1 > oB) {
             const int first = (int)seg_of(oB, 0, a.sym.Useg);
             const int last = (int)seg_of(oB1 - 1, 0, a.sym.Useg);
-            for (int sl = 0; sl <= last - first; ++sl) {
-                const double2 pv = reinterpret_cast<const double2 *>(a.sym.tgt_partial + (long long)sl * 2LL * a.N)[i];
-                acc.x += pv.x;
-                acc.y += pv.y;
-            }
+            sum_strided(acc, a.sym.tgt_partial, 2LL * a.N, last - first + 1, i);
         }
         {
             const double2 pv = reinterpret_cast<const double2 *>(a.sym.diag)[i];
             acc.x += pv.x;
             acc.y += pv.y;
         }
-        for (int A = 0; A < B; ++A) {
-            const double2 pv = reinterpret_cast<const double2 *>(a.sym.src_partial + (long long)A * 2LL * a.N)[i];
-            acc.x += pv.x;
-            acc.y += pv.y;
-        }
+        sum_strided(acc, a.sym.src_partial, 2LL * a.N, B, i);
         u[0] = acc;
     }
     for (int c = 0; c < a.nchunks; ++c) {
@@ -953,31 +967,45 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         // in tiles of 128 (warp-broadcast reads); 1/rho^2 by seed + cubic Newton.
         __shared__ double4 s_pc[128];  // (cx, cy, r, -)
         __shared__ double4 s_pm[128];  // (lambda_x, lambda_y, mu, -)
+        __shared__ LogTab s_log;       // table log (visible after the first tile barrier)
+        log_tab_init(s_log, threadIdx.x, blockDim.x);
+        // staged per pore: (cx, cy) and (lambda/4pi, r_k mu); two accumulator
+        // pairs (even / odd pores) break the serial add chain
+        double2 c0 = make_double2(0.0, 0.0), c1 = make_double2(0.0, 0.0);
         for (int k0 = 0; k0 < a.M; k0 += 128) {
             const int nk = min(128, a.M - k0);
             __syncthreads();
             if ((int)threadIdx.x < nk) {
                 const int k = k0 + threadIdx.x;
-                s_pc[threadIdx.x] = a.pore[k];
+                const double4 pk = a.pore[k];
+                s_pc[threadIdx.x] = pk;
                 const double *m = a.moments + (long long)k * 3;
-                s_pm[threadIdx.x] = make_double4(m[0], m[1], m[2], 0.0);
+                s_pm[threadIdx.x] = make_double4(k4pi * m[0], k4pi * m[1], pk.z * m[2], 0.0);
             }
             __syncthreads();
-#pragma unroll 4
-            for (int q = 0; q < nk; ++q) {
+            auto pore_term = [&](int q, double2 &c) {
                 const double4 pk = s_pc[q], pm = s_pm[q];
                 const double rx = xi.x - pk.x, ry = xi.y - pk.y;
                 const double rho2 = fma(rx, rx, ry * ry);
                 double ir = rcp_approx(rho2);
                 const double e = fma(-rho2, ir, 1.0);
                 ir = fma(ir, fma(e, e, e), ir);
-                const double lg = 0.5 * log_pair(rho2);
-                const double rk = pk.z * ir;
-                const double rl = (rx * pm.x + ry * pm.y) * ir;
-                u[0].x += k4pi * (-lg * pm.x + rx * rl) + rk * ry * pm.z;
-                u[0].y += k4pi * (-lg * pm.y + ry * rl) - rk * rx * pm.z;
+                const double nlg = neg_half_log_tab(rho2, s_log);  // -log rho
+                const double rl = fma(rx, pm.x, ry * pm.y) * ir;     // (r . lambda/4pi) / rho^2
+                const double mr = pm.z * ir;                          // r_k mu / rho^2
+                c.x += fma(nlg, pm.x, fma(rl, rx, mr * ry));
+                c.y += fma(nlg, pm.y, fma(rl, ry, -mr * rx));
+            };
+            int q = 0;
+#pragma unroll 2
+            for (; q + 2 <= nk; q += 2) {
+                pore_term(q, c0);
+                pore_term(q + 1, c1);
             }
+            if (q < nk) pore_term(q, c0);
         }
+        u[0].x += c0.x + c1.x;
+        u[0].y += c0.y + c1.y;
     } else if (full) {
         for (int k = 0; k < a.M; ++k) {
             const double4 pk = a.pore[k];
