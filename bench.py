@@ -250,7 +250,7 @@ def run_gpu(args):
     t_geom = time.perf_counter() - t0
     t0 = time.perf_counter()
     if ws == 1:
-        bd = bie.BlockDiag(g)
+        bd = bie.BlockDiag(g, structured=True)  # pores: one inverse + rank-2 Woodbury terms (NEXT-4)
         rb, re_ = 0, N
     else:
         # row-sharded solve: body-range BD on each rank,
@@ -366,7 +366,7 @@ def run_gpu(args):
             gg = g if cid == CONFIG_ID else bie.Geometry.from_problem(pp)
             torch.cuda.synchronize()
             tb = time.perf_counter()
-            bdd = bd if cid == CONFIG_ID else bie.BlockDiag(gg)
+            bdd = bd if cid == CONFIG_ID else bie.BlockDiag(gg, structured=True)
             torch.cuda.synchronize()
             tb = time.perf_counter() - tb
             ff = torch.from_numpy(rhs_pipe(pp)).to(dev)
@@ -381,7 +381,7 @@ def run_gpu(args):
         # NEXT-3: 16 right-hand sides on config 3 -- batched solver vs 16 single solves
         pp = make_problem(3)
         gg = bie.Geometry.from_problem(pp)
-        bdd = bie.BlockDiag(gg)
+        bdd = bie.BlockDiag(gg, structured=True)
         F = torch.from_numpy(density(pp, nvec=16, vec_id=100).reshape(-1)).to(dev)
         X = torch.zeros_like(F)
         bie.gmres_solve_batch(gg, bdd, F, X, nrhs=16, tol=1e-8, max_iter=1000)  # warm-up

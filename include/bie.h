@@ -7,7 +7,7 @@
  *   left-preconditioned full GMRES       -> bie_gmres_solve
  *
  * Citations: P:l.N = PAPER.md line N (arxiv 1609.04484 LaTeX body); readings
- * C1..C19 are listed in DESIGN.md s3.
+ * C1..C26 are listed in DESIGN.md s3.
  *
  * Conventions for every call:
  *  - Returns BIE_OK (0) or a negative BIE_E* code; bie_last_error() returns a
@@ -254,6 +254,22 @@ BIE_API int bie_profile_begin(bie_geometry_t g);
 BIE_API int bie_profile_end(bie_geometry_t g, double *ms_moments, double *ms_pairs, double *ms_epilogue,
                             int *applies);
 BIE_API long long bie_launch_count(void);
+
+/*
+ * bie_blockdiag_factor_structured -- NEXT-4: the same BD
+ * preconditioner as bie_blockdiag_factor with structured pore blocks.  For
+ * equispaced circular pores of equal n_p the completed-DLP blocks differ only
+ * by the Stokeslet's -log r_k term (pin V10):
+ *   B_k = B_0 + c_k (1 1^T (x) I_2),  c_k = (log r_0 - log r_k) / (4 pi n_p),
+ * so one exact inverse X = B_0^-1 plus a rank-2 Woodbury term per pore gives
+ * every B_k^-1 (P:l.655-657 footnote: the pore blocks need not be factorised
+ * one by one).  The wall block is inverted exactly as before.  Apply is one
+ * GEMM over all pores plus the rank-2 corrections; block_inverse materialises
+ * X - W M_k Z on the host.  Same handle semantics and errors as
+ * bie_blockdiag_factor (BIE_ESINGULAR for a zero pivot or a singular 2x2
+ * Woodbury capacitance, naming the body).
+ */
+BIE_API int bie_blockdiag_factor_structured(bie_geometry_t g, bie_blockdiag_t *out, void *stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT-1: the paper's own operator, the Stokes single-layer

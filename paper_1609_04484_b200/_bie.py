@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "bie_krylov_dots", "bie_krylov_axpy", "bie_krylov_scale", "bie_krylov_sqrt", "bie_krylov_givens",
     "bie_krylov_trisolve", "bie_dlp_sym_info", "bie_dlp_pairs_partial", "bie_dlp_epilogue_rows",
     "bie_kr_weights", "bie_slp_apply", "bie_slp_apply_rows", "bie_slp_field_eval", "bie_blockdiag_factor_slp",
-    "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp",
+    "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp", "bie_blockdiag_factor_structured",
 )
 
 
@@ -89,6 +89,7 @@ def lib():
         "bie_slp_apply_rows": [vp, vp, vp, c_int, c_int, c_int, vp],
         "bie_slp_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_blockdiag_factor_slp": [vp, ctypes.POINTER(vp), vp],
+        "bie_blockdiag_factor_structured": [vp, ctypes.POINTER(vp), vp],
         "bie_gmres_solve_slp": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_gmres_solve_batch_slp": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_profile_begin": [vp],
@@ -263,12 +264,18 @@ def dlp_apply_host_ptr(g: Geometry, sigma_ptr: int, out_ptr: int, nvec: int = 1,
 class BlockDiag:
     """bie_blockdiag_t: explicit per-body inverses (A6).  bodies=(b0, b1) factors
     only that body range (row sharding); its apply takes local vectors.
-    op="slp": blocks of the single-layer operator (bie_blockdiag_factor_slp)."""
+    op="slp": blocks of the single-layer operator (bie_blockdiag_factor_slp).
+    structured=True: pore blocks from one reference inverse + rank-2 Woodbury
+    terms (bie_blockdiag_factor_structured; DLP only)."""
 
-    def __init__(self, g: Geometry, stream=None, bodies=None, op: str = "dlp"):
+    def __init__(self, g: Geometry, stream=None, bodies=None, op: str = "dlp", structured: bool = False):
         h = ctypes.c_void_p()
         self.op = op
-        if op == "slp":
+        if structured:
+            if op != "dlp" or bodies is not None:
+                raise ValueError("the structured pore BD is built for the whole geometry and the DLP operator")
+            _check(lib().bie_blockdiag_factor_structured(g.h, ctypes.byref(h), _stream_ptr(stream)))
+        elif op == "slp":
             if bodies is not None:
                 raise ValueError("the SLP block-diagonal preconditioner covers the whole geometry")
             _check(lib().bie_blockdiag_factor_slp(g.h, ctypes.byref(h), _stream_ptr(stream)))

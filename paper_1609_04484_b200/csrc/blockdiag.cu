@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -962,29 +963,134 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     return BIE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Structured pore blocks (NEXT-4; pin V10 of DESIGN.md).  Equispaced circular
+// pores with equal n_p have completed-DLP blocks
+//   B_k = B_ref + c_k E,  E = 1 1^T (x) I_2 = U U^T,  c_k = (log r_ref - log r_k) / (4 pi n_p)
+// (only the Stokeslet's -log r_k term of the completion depends on the radius),
+// so by Woodbury  B_k^-1 = X - c_k W (I_2 + c_k G)^-1 Z  with X = B_ref^-1,
+// W = X U, Z = U^T X, G = U^T X U.  Apply: Y = X [v_1 .. v_M] (one GEMM over
+// all pores), s_k = U^T y_k, y_k -= W M_k s_k with M_k = c_k (I + c_k G)^-1.
+// ---------------------------------------------------------------------------
+__global__ void k_struct_WG(const double *__restrict__ X, int n2, double *W, double *G) {
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        double w0 = 0.0, w1 = 0.0;
+        for (int j = 0; j < n2; j += 2) {
+            w0 += X[(long long)i * n2 + j];
+            w1 += X[(long long)i * n2 + j + 1];
+        }
+        W[2 * i] = w0;
+        W[2 * i + 1] = w1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int a = threadIdx.x >> 1, c = threadIdx.x & 1;  // G[a][c] = sum_i W[2i + a][c]
+        double g = 0.0;
+        for (int i = 0; i < n2 / 2; ++i) g += W[2 * (2 * i + a) + c];
+        G[threadIdx.x] = g;
+    }
+}
+
+// Y[:, col] = X V[:, col] for col < ncols; column col is vector col / M,
+// pore col % M, at base + (col / M) * stride + n2 * (col % M).  32 x 32 tiles.
+__global__ void __launch_bounds__(256) k_struct_gemm(const double *__restrict__ X, int n2, int M, int ncols,
+                                                     const double *__restrict__ in, double *out, long long stride) {
+    __shared__ double Xs[32][33];
+    __shared__ double Vs[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 8 row groups of 4 rows
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    const int col = c0 + tx;
+    const long long cbase = col < ncols ? (long long)(col / M) * stride + (long long)n2 * (col % M) : 0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < n2; k0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int rr = ty * 4 + q;  // X tile row, V tile k
+            Xs[rr][tx] = (r0 + rr < n2 && k0 + tx < n2) ? X[(long long)(r0 + rr) * n2 + k0 + tx] : 0.0;
+            Vs[rr][tx] = (col < ncols && k0 + rr < n2) ? in[cbase + k0 + rr] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            const double v = Vs[kk][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(Xs[ty * 4 + q][kk], v, acc[q]);
+        }
+        __syncthreads();
+    }
+    if (col < ncols) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = r0 + ty * 4 + q;
+            if (r < n2) out[cbase + r] = acc[q];
+        }
+    }
+}
+
+// Rank-2 Woodbury correction, one warp per column (fixed-order sums).
+__global__ void k_struct_corr(const double *__restrict__ W, const double *__restrict__ Mk, int n2, int M, int ncols,
+                              double *out, long long stride) {
+    const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (col >= ncols) return;
+    const int k = col % M;
+    double *y = out + (long long)(col / M) * stride + (long long)n2 * k;
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = 2 * lane; i < n2; i += 64) {
+        s0 += y[i];
+        s1 += y[i + 1];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    const double m0 = Mk[4 * k] * s0 + Mk[4 * k + 1] * s1;
+    const double m1 = Mk[4 * k + 2] * s0 + Mk[4 * k + 3] * s1;
+    for (int i = lane; i < n2; i += 32) y[i] -= W[2 * i] * m0 + W[2 * i + 1] * m1;
+}
+
 int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec, cudaStream_t st) {
     Geometry *g = bd->g;
     const int rows_loc = bd->row_hi - bd->row_lo;
     const long long stride = 2LL * rows_loc;
     const int threads = 256;
-    const int blocks = (int)(((long long)2 * rows_loc * 32 + threads - 1) / threads);
+    int blocks = (int)(((long long)2 * rows_loc * 32 + threads - 1) / threads);
     if (rows_loc == 0) return BIE_OK;
+    int row_lo = bd->row_lo, rows_k = rows_loc, kb0 = bd->b0;
+    if (bd->structured) {
+        const int M = g->M, n2 = 2 * g->n_pore, ncols = nvec * M;
+        if (M > 0) {
+            dim3 grid((unsigned)((ncols + 31) / 32), (unsigned)((n2 + 31) / 32));
+            k_struct_gemm<<<grid, 256, 0, st>>>(bd->sX, n2, M, ncols, in, out, stride);
+            k_struct_corr<<<(ncols * 32 + 255) / 256, 256, 0, st>>>(bd->sW, bd->sM, n2, M, ncols, out, stride);
+            count_launch(2);
+            BIE_CUDA_TRY(cudaGetLastError());
+        }
+        // the wall through the explicit-inverse kernel (rows [wall_lo, N), body M)
+        row_lo = g->wall_lo;
+        rows_k = g->N - g->wall_lo;
+        kb0 = M;
+        in += 2LL * g->wall_lo;
+        out += 2LL * g->wall_lo;
+        blocks = (int)(((long long)2 * rows_k * 32 + threads - 1) / threads);
+        if (rows_k == 0) return BIE_OK;
+    }
     int v = 0;
     while (v < nvec) {
         int rem = nvec - v;
         if (rem >= 4) {
-            k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, bd->b0,
-                                                      bd->row_lo, rows_loc, in, out, stride, v);
+            k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, kb0,
+                                                      row_lo, rows_k, in, out, stride, v);
             v += 4;
             count_launch();
         } else if (rem >= 2) {
-            k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, bd->b0,
-                                                      bd->row_lo, rows_loc, in, out, stride, v);
+            k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, kb0,
+                                                      row_lo, rows_k, in, out, stride, v);
             v += 2;
             count_launch();
         } else {
-            k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, bd->b0,
-                                                      bd->row_lo, rows_loc, in, out, stride, v);
+            k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, kb0,
+                                                      row_lo, rows_k, in, out, stride, v);
             v += 1;
             count_launch();
         }
@@ -1007,6 +1113,10 @@ int bie_blockdiag_destroy(bie_blockdiag_t h) {
     }
     cudaFree(bd->inv);
     cudaFree(bd->d_off);
+    cudaFree(bd->sX);
+    cudaFree(bd->sW);
+    cudaFree(bd->sG);
+    cudaFree(bd->sM);
     bd->magic = 0;
     delete bd;
     return BIE_OK;
@@ -1096,6 +1206,99 @@ int bie_blockdiag_factor_slp(bie_geometry_t gh, bie_blockdiag_t *out, void *stre
     return factor_range(g, 0, g->M + 1, out, (cudaStream_t)stream, 1);
 }
 
+int bie_blockdiag_factor_structured(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out) {
+        set_error("bie_blockdiag_factor_structured: invalid geometry handle or null output");
+        return BIE_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    *out = nullptr;
+    BlockDiag *bd = new BlockDiag();
+    bd->g = g;
+    bd->b0 = 0;
+    bd->b1 = g->M + 1;
+    bd->nb = g->M + 1;
+    bd->structured = 1;
+    for (int b = 0; b <= g->M; ++b) {
+        bd->lo.push_back(b < g->M ? b * g->n_pore : g->wall_lo);
+        bd->n.push_back(b < g->M ? g->n_pore : g->n_outer);
+    }
+    const long long wsz = 4LL * g->n_outer * g->n_outer;
+    bd->off = {0, wsz};  // explicit storage: the wall only
+    bd->row_lo = 0;
+    bd->row_hi = g->N;
+    int *d_flag = nullptr;
+    auto fail = [&](int rc) {
+        cudaFree(d_flag);
+        bie_blockdiag_destroy(reinterpret_cast<bie_blockdiag_t>(bd));
+        return rc;
+    };
+    cudaError_t e = cudaMalloc(&bd->inv, sizeof(double) * (size_t)wsz);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(wall inverse)"));
+    e = cudaMalloc(&bd->d_off, sizeof(long long) * 2);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(offsets)"));
+    e = cudaMemcpy(bd->d_off, bd->off.data(), sizeof(long long) * 2, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemcpy(offsets)"));
+    e = cudaMalloc(&d_flag, sizeof(int) * 2);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(flags)"));
+    e = cudaMemsetAsync(d_flag, 0, sizeof(int) * 2, st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemsetAsync(flags)"));
+    const int n2 = 2 * g->n_pore;
+    if (g->M > 0) {  // the reference pore (pore 0): one exact inverse
+        e = cudaMalloc(&bd->sX, sizeof(double) * (size_t)n2 * n2);
+        if (e == cudaSuccess) e = cudaMalloc(&bd->sW, sizeof(double) * 2 * (size_t)n2);
+        if (e == cudaSuccess) e = cudaMalloc(&bd->sG, sizeof(double) * 4);
+        if (e == cudaSuccess) e = cudaMalloc(&bd->sM, sizeof(double) * 4 * (size_t)g->M);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(structured pore blocks)"));
+        BDView pv{bd->sX, 0, n2, 1, 0};
+        int rc = factor_class(g, pv, 0, g->n_pore, false, st, d_flag, 0);
+        if (rc) return fail(rc);
+        k_struct_WG<<<1, 256, 0, st>>>(bd->sX, n2, bd->sW, bd->sG);
+        count_launch();
+    }
+    {
+        BDView wv{bd->inv, 0, 2 * g->n_outer, 1, g->M};
+        int rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + 1, 0);
+        if (rc) return fail(rc);
+    }
+    int flags[2] = {0, 0};
+    double G[4] = {0, 0, 0, 0};
+    e = cudaMemcpyAsync(flags, d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && g->M > 0) e = cudaMemcpyAsync(G, bd->sG, sizeof(double) * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "bie_blockdiag_factor_structured (kernels)"));
+    if (flags[0] || flags[1]) {
+        set_error(std::string("bie_blockdiag_factor_structured: block of body ") +
+                  (flags[0] ? "0 (reference pore)" : std::to_string(g->M) + " (outer wall)") +
+                  " is singular (zero pivot)");
+        return fail(BIE_ESINGULAR);
+    }
+    if (g->M > 0) {
+        bd->h_M.resize(4 * (size_t)g->M);
+        const double r0 = g->h_pore_r[0];
+        for (int k = 0; k < g->M; ++k) {
+            const double c = (std::log(r0) - std::log(g->h_pore_r[k])) / (4.0 * kPi * g->n_pore);
+            const double a00 = 1.0 + c * G[0], a01 = c * G[1], a10 = c * G[2], a11 = 1.0 + c * G[3];
+            const double det = a00 * a11 - a01 * a10;
+            if (!(std::fabs(det) > 1e-13 * (std::fabs(a00 * a11) + std::fabs(a01 * a10)))) {
+                set_error("bie_blockdiag_factor_structured: block of body " + std::to_string(k) +
+                          " (pore) is singular (Woodbury capacitance)");
+                return fail(BIE_ESINGULAR);
+            }
+            bd->h_M[4 * k] = c * a11 / det;
+            bd->h_M[4 * k + 1] = -c * a01 / det;
+            bd->h_M[4 * k + 2] = -c * a10 / det;
+            bd->h_M[4 * k + 3] = c * a00 / det;
+        }
+        e = cudaMemcpy(bd->sM, bd->h_M.data(), sizeof(double) * bd->h_M.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemcpy(M_k)"));
+    }
+    cudaFree(d_flag);
+    *out = reinterpret_cast<bie_blockdiag_t>(bd);
+    return BIE_OK;
+}
+
 int bie_blockdiag_factor_range(bie_geometry_t gh, int body_begin, int body_end, bie_blockdiag_t *out,
                                void *stream) {
     Geometry *g = as_geom(gh);
@@ -1131,6 +1334,36 @@ int bie_blockdiag_block_inverse(bie_blockdiag_t h, int body, double *host, long 
     if (!bd || !host || body < bd->b0 || body >= bd->b1) {
         set_error("bie_blockdiag_block_inverse: invalid handle, body not in the handle's range, or buffer");
         return BIE_EINVAL;
+    }
+    if (bd->structured) {
+        Geometry *g = bd->g;
+        if (body == g->M) {
+            const long long n = bd->off[1];
+            if (host_len < n) {
+                set_error("bie_blockdiag_block_inverse: host buffer too small");
+                return BIE_EINVAL;
+            }
+            BIE_CUDA_TRY(cudaMemcpy(host, bd->inv, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
+            return BIE_OK;
+        }
+        // B_k^-1 = X - W M_k Z, Z = U^T X (materialised on the host for inspection)
+        const int n2 = 2 * g->n_pore;
+        if (host_len < (long long)n2 * n2) {
+            set_error("bie_blockdiag_block_inverse: host buffer too small");
+            return BIE_EINVAL;
+        }
+        std::vector<double> W(2 * (size_t)n2), Z(2 * (size_t)n2, 0.0);
+        BIE_CUDA_TRY(cudaMemcpy(host, bd->sX, sizeof(double) * (size_t)n2 * n2, cudaMemcpyDeviceToHost));
+        BIE_CUDA_TRY(cudaMemcpy(W.data(), bd->sW, sizeof(double) * W.size(), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < n2; ++i)
+            for (int c = 0; c < n2; ++c) Z[(size_t)(i & 1) * n2 + c] += host[(size_t)i * n2 + c];
+        const double *Mk = bd->h_M.data() + 4 * (size_t)body;
+        for (int i = 0; i < n2; ++i) {
+            const double p0 = W[2 * i] * Mk[0] + W[2 * i + 1] * Mk[2];
+            const double p1 = W[2 * i] * Mk[1] + W[2 * i + 1] * Mk[3];
+            for (int c = 0; c < n2; ++c) host[(size_t)i * n2 + c] -= p0 * Z[c] + p1 * Z[(size_t)n2 + c];
+        }
+        return BIE_OK;
     }
     body -= bd->b0;
     long long n = bd->off[body + 1] - bd->off[body];

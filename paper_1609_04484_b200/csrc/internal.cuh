@@ -101,6 +101,14 @@ struct BlockDiag {
     double *inv = nullptr;          // explicit inverses, row-major [2n_b][2n_b]
     long long *d_off = nullptr;
     int *d_lo = nullptr, *d_n = nullptr;
+    // structured pore blocks (NEXT-4, bie_blockdiag_factor_structured): inv/off then
+    // hold only the wall; pores use X = B_ref^-1 plus a rank-2 Woodbury term each
+    int structured = 0;
+    double *sX = nullptr;           // [2n_p][2n_p] inverse of the reference pore block
+    double *sW = nullptr;           // [2n_p][2]   W = X U
+    double *sG = nullptr;           // [4]         G = U^T X U
+    double *sM = nullptr;           // [M][4]      M_k = c_k (I + c_k G)^-1
+    std::vector<double> h_M;        // host copy of M_k
 };
 
 Geometry *as_geom(bie_geometry_t g);

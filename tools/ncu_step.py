@@ -18,7 +18,7 @@ p = make_problem(cid)
 g = bie.Geometry.from_problem(p)
 dev = torch.device("cuda", 0)
 if mode == "step":
-    bd = bie.BlockDiag(g)
+    bd = bie.BlockDiag(g, structured=True)
     f = torch.from_numpy(rhs_pipe(p)).to(dev)
     x = torch.zeros_like(f)
     bie.gmres_solve(g, bd, f, x, tol=1e-30, max_iter=50)
