@@ -100,7 +100,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -111,10 +111,15 @@ class ClockSampler:
                 smax = float(f[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[2]))
+            except ValueError:
+                pass
             for n, v in zip(names, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "sm_mhz_min": min(sm) if sm else None, "power_w_max": max(pw) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -319,14 +324,15 @@ def run_gpu(args):
 
     # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.fill_(float(k))
-        e2e_ev[k][0].record(stream)
-        f.copy_(f_host, non_blocking=True)
-        step()
-        x_host.copy_(x, non_blocking=True)
-        e2e_ev[k][1].record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clk_e2e:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            e2e_ev[k][0].record(stream)
+            f.copy_(f_host, non_blocking=True)
+            step()
+            x_host.copy_(x, non_blocking=True)
+            e2e_ev[k][1].record(stream)
+        torch.cuda.synchronize()
     e2e_ms_each = [a.elapsed_time(b) for a, b in e2e_ev]
     e2e_s = sum(e2e_ms_each) / 1e3
     if dist:
@@ -467,7 +473,7 @@ def run_gpu(args):
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
         "e2e": {"value": args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
                 "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8),
-                "step_ms_each": [round(t, 3) for t in e2e_ms_each]},
+                "step_ms_each": [round(t, 3) for t in e2e_ms_each], "clocks": clk_e2e.summary()},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "setup": {"geometry_s": t_geom, "build_pc_s": t_bd},

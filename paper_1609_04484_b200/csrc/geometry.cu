@@ -170,6 +170,15 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     }
     cudaFree(g->slp_s);
     cudaFree(g->sym_counter);
+    cudaFree(g->gm.V);
+    cudaFree(g->gm.w);
+    cudaFree(g->gm.t);
+    cudaFree(g->gm.H);
+    cudaFree(g->gm.small);
+    cudaFree(g->gm.partial);
+    if (g->gm.pinned) cudaFreeHost(g->gm.pinned);
+    for (auto &ev : g->gm.evs)
+        if (ev) cudaEventDestroy(ev);
     cudaFree(g->sym_Q);
     cudaFree(g->sym_off);
     cudaFree(g->sym_tgt);

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <cmath>
 #include <vector>
@@ -301,30 +302,16 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     cudaStream_t st = (cudaStream_t)stream;
     const long long n = 2LL * g->N;
     const int ldh = max_iter + 1;
-    double *V = nullptr, *w = nullptr, *t = nullptr;
     GmState s{};
     Dot d;
-    double *pinned = nullptr;
-    cudaEvent_t evs[2] = {nullptr, nullptr};
+    constexpr int kMaxLook = 7;
+    int kLook = 3;                     // iterations enqueued ahead of the host's convergence check
+    if (const char *e = getenv("BIE_GMRES_LOOKAHEAD")) kLook = std::max(1, std::min(kMaxLook, atoi(e)));
+    const int kRing = kLook + 1;       // estimate slots / events in flight
     int rc = BIE_OK;
     d.nchunks = (int)((n + kChunk - 1) / kChunk);
     d.ldp = ldh;
-    auto cleanup = [&]() {
-        cudaFree(V);
-        cudaFree(w);
-        cudaFree(t);
-        cudaFree(s.H);
-        cudaFree(s.cs);
-        cudaFree(s.sn);
-        cudaFree(s.g);
-        cudaFree(s.h);
-        cudaFree(s.h2);
-        cudaFree(s.scal);
-        cudaFree(d.partial);
-        cudaFreeHost(pinned);
-        if (evs[0]) cudaEventDestroy(evs[0]);
-        if (evs[1]) cudaEventDestroy(evs[1]);
-    };
+    auto cleanup = [&]() {};           // the workspace stays cached on the geometry
 #define GM_TRY(expr)                                       \
     do {                                                   \
         cudaError_t _e = (expr);                           \
@@ -342,20 +329,35 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
             return rc;                                     \
         }                                                  \
     } while (0)
-    GM_TRY(cudaMalloc(&V, sizeof(double) * (size_t)ldh * n));
-    GM_TRY(cudaMalloc(&w, sizeof(double) * n));
-    GM_TRY(cudaMalloc(&t, sizeof(double) * n));
-    GM_TRY(cudaMalloc(&s.H, sizeof(double) * (size_t)ldh * max_iter));
-    GM_TRY(cudaMalloc(&s.cs, sizeof(double) * max_iter));
-    GM_TRY(cudaMalloc(&s.sn, sizeof(double) * max_iter));
-    GM_TRY(cudaMalloc(&s.g, sizeof(double) * ldh));
-    GM_TRY(cudaMalloc(&s.h, sizeof(double) * ldh));
-    GM_TRY(cudaMalloc(&s.h2, sizeof(double) * ldh));
-    GM_TRY(cudaMalloc(&s.scal, sizeof(double) * 8));
-    GM_TRY(cudaMalloc(&d.partial, sizeof(double) * (size_t)d.nchunks * ldh));
-    GM_TRY(cudaMallocHost(&pinned, sizeof(double) * 16));
-    GM_TRY(cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming));
-    GM_TRY(cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming));
+    GmresWork &ws = g->gm;
+    auto ensure = [&](double *&ptr, size_t &cap, size_t need) -> cudaError_t {
+        if (need <= cap) return cudaSuccess;
+        cudaFree(ptr);  // synchronises the device: no work in flight uses the old buffer
+        ptr = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&ptr, sizeof(double) * need);
+        if (e == cudaSuccess) cap = need;
+        return e;
+    };
+    GM_TRY(ensure(ws.V, ws.V_cap, (size_t)ldh * n));
+    GM_TRY(ensure(ws.w, ws.n_cap, 2 * (size_t)n));  // w and t = w + n
+    GM_TRY(ensure(ws.H, ws.H_cap, (size_t)ldh * max_iter));
+    GM_TRY(ensure(ws.small, ws.small_cap, 5 * (size_t)ldh + 8));
+    GM_TRY(ensure(ws.partial, ws.partial_cap, (size_t)d.nchunks * ldh));
+    if (!ws.pinned) GM_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * (8 + 2 * (kMaxLook + 1))));
+    for (int q = 0; q < kRing; ++q)
+        if (!ws.evs[q]) GM_TRY(cudaEventCreateWithFlags(&ws.evs[q], cudaEventDisableTiming));
+    double *V = ws.V, *w = ws.w, *t = ws.w + n;
+    double *pinned = ws.pinned;
+    cudaEvent_t *evs = ws.evs;
+    s.H = ws.H;
+    s.cs = ws.small;
+    s.sn = ws.small + ldh;
+    s.g = ws.small + 2 * ldh;
+    s.h = ws.small + 3 * ldh;
+    s.h2 = ws.small + 4 * ldh;
+    s.scal = ws.small + 5 * ldh;
+    d.partial = ws.partial;
     GM_TRY(cudaMemsetAsync(s.g, 0, sizeof(double) * ldh, st));
     GM_TRY(cudaMemsetAsync(s.H, 0, sizeof(double) * (size_t)ldh * max_iter, st));
 
@@ -401,17 +403,19 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 0, V, n);
     count_launch();
     GM_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
-    // One-iteration lookahead: iteration k is enqueued before the host reads the
-    // estimate of iteration k-1, so the device queue never drains on the
-    // per-iteration 16-byte D2H.  If k-1 converged, iteration k was speculative:
-    // it only touched H[:,k], g[k], g[k+1], cs/sn[k] and V[k+1], none of which the
-    // finish (columns 0..k-1) reads.
+    // kLook-iteration lookahead: iteration k is enqueued before the host reads
+    // the estimate of iteration k - kLook, so the device queue holds ~kLook
+    // matvecs of work and a late host thread (descheduled, or waiting on a
+    // driver lock) does not idle the GPU.  Iterations after the converged one
+    // are speculative: iteration k only touches H[:,k], g[k], g[k+1], cs/sn[k]
+    // and V[k+1], none of which the finish (columns 0..it-1) reads; after a
+    // happy breakdown they may compute NaNs in those unused entries only.
     int it = 0;
     bool done = false;
     auto check = [&](int kk) -> int {  // read the estimate of iteration kk (its slot)
-        BIE_CUDA_TRY(cudaEventSynchronize(evs[kk & 1]));
-        const double est = pinned[8 + 2 * (kk & 1)];
-        const bool brk = pinned[9 + 2 * (kk & 1)] != 0.0;
+        BIE_CUDA_TRY(cudaEventSynchronize(evs[kk % kRing]));
+        const double est = pinned[8 + 2 * (kk % kRing)];
+        const bool brk = pinned[9 + 2 * (kk % kRing)] != 0.0;
         hist_host[kk + 1] = est;
         it = kk + 1;
         if (est < tol || brk) {
@@ -433,16 +437,16 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
         k_givens<<<1, 1, 0, st>>>(s, k, ldh);
         count_launch();
         GM_TRY(cudaGetLastError());
-        GM_TRY(cudaMemcpyAsync(pinned + 8 + 2 * (k & 1), s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost,
-                               st));
-        GM_TRY(cudaEventRecord(evs[k & 1], st));
+        GM_TRY(cudaMemcpyAsync(pinned + 8 + 2 * (k % kRing), s.scal + 3, 2 * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+        GM_TRY(cudaEventRecord(evs[k % kRing], st));
         if (k + 1 < max_iter) {
             k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, V + (long long)(k + 1) * n, n);
             count_launch();
         }
-        if (k >= 1) GM_RC(check(k - 1));
+        if (k >= kLook) GM_RC(check(k - kLook));
     }
-    if (!done && it < max_iter) GM_RC(check(it));  // the last enqueued iteration
+    while (!done && it < max_iter) GM_RC(check(it));  // the iterations still in flight
     *iters = it;
     // y = H^{-1} g, x = V y
     k_trisolve<<<1, 256, 0, st>>>(s.H, ldh, s.g, s.h, it);

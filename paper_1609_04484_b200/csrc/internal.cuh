@@ -39,6 +39,15 @@ struct PairSched {
     int smem = 0;
 };
 
+// GMRES workspace cached on the geometry (grow-only): per-call cudaMalloc /
+// cudaMallocHost left the device idle for up to ~1 s in some steps.
+struct GmresWork {
+    double *V = nullptr, *w = nullptr, *t = nullptr, *H = nullptr, *small = nullptr, *partial = nullptr;
+    size_t V_cap = 0, n_cap = 0, H_cap = 0, small_cap = 0, partial_cap = 0;
+    double *pinned = nullptr;  // 8 + 2 * 8 doubles
+    cudaEvent_t evs[8] = {};
+};
+
 struct Geometry {
     uint32_t magic = kGeomMagic;
     int N = 0, M = 0, n_pore = 0, n_outer = 0;
@@ -80,6 +89,7 @@ struct Geometry {
     unsigned long long *sym_counter = nullptr;  // dynamic segment counter of the symmetric kernel
     long long sym_Useg = 1;                     // units per segment
     long long sym_U = 0;
+    GmresWork gm;               // bie_gmres_solve* workspace
     // profiling (bie_profile_begin/end): 4 events per recorded apply
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;
