@@ -179,6 +179,12 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     if (g->gm.pinned) cudaFreeHost(g->gm.pinned);
     for (auto &ev : g->gm.evs)
         if (ev) cudaEventDestroy(ev);
+    cudaFree(g->gmb.V);
+    cudaFree(g->gmb.w);
+    cudaFree(g->gmb.H);
+    cudaFree(g->gmb.small);
+    cudaFree(g->gmb.partial);
+    if (g->gmb.pinned) cudaFreeHost(g->gmb.pinned);
     cudaFree(g->sym_Q);
     cudaFree(g->sym_off);
     cudaFree(g->sym_tgt);

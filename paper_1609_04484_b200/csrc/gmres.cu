@@ -541,22 +541,11 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     const long long n = 2LL * g->N;
     const int ldh = max_iter + 1;
     const unsigned eb = (unsigned)((n + 255) / 256);
-    double *V = nullptr, *Win = nullptr, *Wt = nullptr, *Wout = nullptr, *H = nullptr, *small = nullptr;
-    double *pinned = nullptr;
     Dot d;
     d.nchunks = (int)((n + kChunk - 1) / kChunk);
     d.ldp = ldh;
     int rc = BIE_OK;
-    auto cleanup = [&]() {
-        cudaFree(V);
-        cudaFree(Win);
-        cudaFree(Wt);
-        cudaFree(Wout);
-        cudaFree(H);
-        cudaFree(small);
-        cudaFree(d.partial);
-        cudaFreeHost(pinned);
-    };
+    auto cleanup = [&]() {};  // the workspace stays cached on the geometry
 #define GB_TRY(expr)                   \
     do {                               \
         cudaError_t _e = (expr);       \
@@ -576,14 +565,25 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     } while (0)
     // per-system small state: cs, sn, g, h, h2 [ldh each] + scal [8]
     const long long smallper = 5LL * ldh + 8;
-    GB_TRY(cudaMalloc(&V, sizeof(double) * (size_t)nrhs * ldh * n));
-    GB_TRY(cudaMalloc(&Win, sizeof(double) * (size_t)nrhs * n));
-    GB_TRY(cudaMalloc(&Wt, sizeof(double) * (size_t)nrhs * n));
-    GB_TRY(cudaMalloc(&Wout, sizeof(double) * (size_t)nrhs * n));
-    GB_TRY(cudaMalloc(&H, sizeof(double) * (size_t)nrhs * ldh * max_iter));
-    GB_TRY(cudaMalloc(&small, sizeof(double) * (size_t)nrhs * smallper));
-    GB_TRY(cudaMalloc(&d.partial, sizeof(double) * (size_t)d.nchunks * ldh));
-    GB_TRY(cudaMallocHost(&pinned, sizeof(double) * (size_t)nrhs * 8));
+    GmresWork &ws = g->gmb;
+    auto ensure = [&](double *&ptr, size_t &cap, size_t need) -> cudaError_t {
+        if (need <= cap) return cudaSuccess;
+        cudaFree(ptr);  // synchronises the device: no work in flight uses the old buffer
+        ptr = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&ptr, sizeof(double) * need);
+        if (e == cudaSuccess) cap = need;
+        return e;
+    };
+    GB_TRY(ensure(ws.V, ws.V_cap, (size_t)nrhs * ldh * n));
+    GB_TRY(ensure(ws.w, ws.n_cap, 3 * (size_t)nrhs * n));
+    GB_TRY(ensure(ws.H, ws.H_cap, (size_t)nrhs * ldh * max_iter));
+    GB_TRY(ensure(ws.small, ws.small_cap, (size_t)nrhs * smallper));
+    GB_TRY(ensure(ws.partial, ws.partial_cap, (size_t)d.nchunks * ldh));
+    if (!ws.pinned) GB_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * 64 * 8));  // nrhs <= 64
+    double *V = ws.V, *Win = ws.w, *Wt = ws.w + (size_t)nrhs * n, *Wout = ws.w + 2 * (size_t)nrhs * n;
+    double *H = ws.H, *small = ws.small, *pinned = ws.pinned;
+    d.partial = ws.partial;
     GB_TRY(cudaMemsetAsync(H, 0, sizeof(double) * (size_t)nrhs * ldh * max_iter, st));
     GB_TRY(cudaMemsetAsync(small, 0, sizeof(double) * (size_t)nrhs * smallper, st));
     std::vector<GmState> S(nrhs);

@@ -90,6 +90,7 @@ struct Geometry {
     long long sym_Useg = 1;                     // units per segment
     long long sym_U = 0;
     GmresWork gm;               // bie_gmres_solve* workspace
+    GmresWork gmb;              // bie_gmres_solve_batch* workspace (w holds Win | Wt | Wout)
     // profiling (bie_profile_begin/end): 4 events per recorded apply
     bool prof = false;
     std::vector<cudaEvent_t> prof_ev;
