@@ -97,6 +97,22 @@ def test_matvec_config5_sampled_rows(bie):
     assert np.abs(y[rows] - ref).max() / np.abs(ref).max() <= TOL
 
 
+@pytest.mark.parametrize("cid,nvec", [(4, 16), (5, 4), (5, 16)])
+def test_matvec_multivector_sampled_rows_large(bie, cid, nvec):
+    """The bench's matvec sweeps (config 4 nvec 16; config 5 nvec 4/16, the
+    one-sided multi-vector kernels at full size) on strided sampled rows."""
+    p = make_problem(cid)
+    g, og = _setup(bie, p)
+    s = density(p, nvec=nvec, vec_id=40)
+    y = _gpu_apply(bie, g, s, nvec)
+    rows = _rows(p.N, 128)
+    ref = og.apply(s, rows=rows)
+    for v in range(nvec):
+        yv = y[v].reshape(-1, 2)[rows]
+        rv = ref[v].reshape(-1, 2)
+        assert np.abs(yv - rv).max() / np.abs(rv).max() <= TOL
+
+
 def test_gauss_identity_on_gpu(bie):
     """Property at any size (V1): D_ONLY of a constant density = -1/2 e.
     Config 4 tolerance: the trapezoid near-field error at its closest pore
