@@ -140,14 +140,39 @@ class GpuBackend:
     def zeros(self, m):
         return self.torch.zeros(m, dtype=self.torch.float64, device=self.dev)
 
+    # Collectives: NCCL on device tensors.  Other backends (gloo, used by the
+    # world-size-2 correctness test on a single GPU) stage through host memory.
+    def _nccl(self):
+        import torch.distributed as dist
+
+        return dist.get_backend(self.group) == "nccl"
+
+    def _all_gather(self, out, inp):
+        import torch.distributed as dist
+
+        if self._nccl():
+            dist.all_gather_into_tensor(out, inp, group=self.group)
+            return
+        bufs = [self.torch.empty(inp.numel(), dtype=inp.dtype) for _ in range(self.world)]
+        dist.all_gather(bufs, inp.cpu(), group=self.group)
+        out.copy_(self.torch.cat(bufs))
+
+    def _reduce_scatter(self, out, inp):
+        import torch.distributed as dist
+
+        if self._nccl():
+            dist.reduce_scatter_tensor(out, inp, group=self.group)
+            return
+        t = inp.cpu()
+        dist.all_reduce(t, group=self.group)
+        out.copy_(t[self.rank * out.numel():(self.rank + 1) * out.numel()])
+
     def _gather_full(self, v):
         if self.world == 1:
             self.full.copy_(v)
             return self.full
-        import torch.distributed as dist
-
         self.pad[: v.numel()].copy_(v)
-        dist.all_gather_into_tensor(self.gath, self.pad, group=self.group)
+        self._all_gather(self.gath, self.pad)
         for r, (b, e) in enumerate(self.ranges):
             self.full[2 * b:2 * e].copy_(self.gath[r * self.maxlen: r * self.maxlen + 2 * (e - b)])
         return self.full
@@ -161,11 +186,9 @@ class GpuBackend:
         if self.world == 1:
             rows = self.part_full
         else:
-            import torch.distributed as dist
-
             for r, (b, e) in enumerate(self.ranges):
                 self.send[r * self.maxlen: r * self.maxlen + 2 * (e - b)].copy_(self.part_full[2 * b:2 * e])
-            dist.reduce_scatter_tensor(self.recv, self.send, group=self.group)
+            self._reduce_scatter(self.recv, self.send)
             rows = self.recv[: self.n]
         self.B.dlp_epilogue_rows(self.g, full, rows, out, self.rb, self.re, stream=self.stream)
 
@@ -198,7 +221,12 @@ class GpuBackend:
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(t, group=self.group)
+            if self._nccl():
+                dist.all_reduce(t, group=self.group)
+            else:
+                c = t.cpu()
+                dist.all_reduce(c, group=self.group)
+                t.copy_(c)
 
     def copy_(self, dst, src):
         dst.copy_(src)

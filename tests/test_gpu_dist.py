@@ -115,3 +115,69 @@ def test_dist_gmres_world1_sym_mode(bie):
     ref = oracle.gmres(og, f, oracle.OracleBD(og), tol=1e-8, max_iter=200)
     assert res["iters"] == ref["iters"] and res["converged"]
     assert (np.abs(res["hist"] - ref["hist"]) / ref["hist"]).max() < 1e-10
+
+
+def _gpu_worker(rank, world, port, mode, q):
+    """One rank of a world-size-2 solve on the single test GPU.  The ranks'
+    kernels never wait on one another: the collectives are gloo, host-side."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_04484_b200 as bie
+    from paper_1609_04484_b200.dist import GpuBackend, dist_gmres
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        p = make_problem(2)
+        g = bie.Geometry.from_problem(p)
+        be = GpuBackend(g, rank, world, mode=mode)
+        f = rhs_pipe(p)
+        x, res = dist_gmres(be, _t(f[2 * be.rb:2 * be.re]), tol=1e-8, max_iter=200)
+        out = [None] * world
+        dist.all_gather_object(out, (be.rb, be.re, x.cpu().numpy(), res))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["rows", "sym"])
+def test_dist_gmres_world2_gpu_backend(bie, mode):
+    """GpuBackend at world size 2 (every vector operation and matvec slice in
+    libbie.so kernels; gloo collectives) against the single-GPU solver."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p = make_problem(2)
+    g = bie.Geometry.from_problem(p)
+    f = rhs_pipe(p)
+    x1 = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    ref = bie.gmres_solve(g, bie.BlockDiag(g), _t(f), x1, tol=1e-8, max_iter=200)
+    res = out[0][3]
+    assert res["iters"] == ref["iters"] and res["converged"]
+    assert (np.abs(res["hist"] - ref["hist"]) / ref["hist"]).max() < 1e-10
+    x = np.zeros(2 * p.N)
+    for rb, re_, xr, _ in out:
+        x[2 * rb:2 * re_] = xr
+    xs = x1.cpu().numpy()
+    assert np.abs(x - xs).max() / np.abs(xs).max() < 1e-9

@@ -3,7 +3,7 @@
 tests/test_gpu_bd_gmres.py::test_gmres_golden compares the CUDA path against
 these files.  Inputs: bie_inputs (seeded); boundary data: pipe flow
 (P:l.217-227, reading C10); solver: reading C13 (tol 1e-8).
-usage: python tools/make_golden.py [config3_bd_pipe] [config4_none_pipe_prefix]
+usage: python tools/make_golden.py [config3_bd_pipe] [config4_none_pipe_prefix] [config4_bd_pipe_full]
 """
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -16,6 +16,8 @@ CASES = {
     "config3_bd_pipe": dict(config=3, pc="bd", tol=1e-8, max_iter=1000, env_runs=2),
     "config4_none_pipe_prefix": dict(config=4, pc="none", tol=1e-8, max_iter=6),
     "config4_bd_pipe_prefix": dict(config=4, pc="bdlu", tol=1e-8, max_iter=8, env_runs=2),
+    # the full config-4 BD solve (579 iterations on the GPU): ~1 h of oracle time per run
+    "config4_bd_pipe_full": dict(config=4, pc="bdlu", tol=1e-8, max_iter=2000, env_runs=1),
 }
 for name in (sys.argv[1:] or list(CASES)):
     c = CASES[name]
