@@ -70,8 +70,9 @@ typedef struct bie_blockdiag_s *bie_blockdiag_t;
  * domain (C2): (t_y,-t_x) on Gamma_0, -(cos,sin) on pores; kappa_n =
  * x''.n/|x'|^2.  The handle owns all device data; destroy frees it.
  * Errors: BIE_EINVAL (null pointer, n_outer or nodes_per_pore < 16 or odd
- * (S:l.55-57), n_pores < 0, outer_period <= 0), BIE_EGEOM (radius <= 0 or
- * non-finite input), BIE_ENOMEM, BIE_ECUDA.  Synchronous.
+ * (S:l.55-57), n_pores < 0, outer_period <= 0), BIE_EGEOM (radius <= 0,
+ * non-finite input, overlapping pores, a pore crossing or outside the outer
+ * wall -- S:l.36), BIE_ENOMEM, BIE_ECUDA.  Synchronous.
  */
 BIE_API int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const double *outer_ddxy,
                         int n_outer, double outer_period, const double *pore_c, const double *pore_r,

@@ -233,6 +233,41 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
             return BIE_EGEOM;
         }
     }
+    // Pores must be disjoint and inside Gamma_0 (S:l.36): no two discs overlap, every
+    // centre lies inside the outer polygon (winding number) and no outer node lies
+    // in a disc.  O(M^2 + M n_outer) on the host.
+    for (int a = 0; a < n_pores; ++a) {
+        for (int b = a + 1; b < n_pores; ++b) {
+            const double dx = pore_c[2 * a] - pore_c[2 * b], dy = pore_c[2 * a + 1] - pore_c[2 * b + 1];
+            const double rr = pore_r[a] + pore_r[b];
+            if (dx * dx + dy * dy <= rr * rr) {
+                set_error("bie_geometry_create: pores " + std::to_string(a) + " and " + std::to_string(b) +
+                          " overlap");
+                return BIE_EGEOM;
+            }
+        }
+        const double cx = pore_c[2 * a], cy = pore_c[2 * a + 1], r2 = pore_r[a] * pore_r[a];
+        int wind = 0;
+        for (int j = 0; j < n_outer; ++j) {
+            const double x0 = outer_xy[2 * j], y0 = outer_xy[2 * j + 1];
+            const int jn = (j + 1) % n_outer;
+            const double x1 = outer_xy[2 * jn], y1 = outer_xy[2 * jn + 1];
+            if ((x0 - cx) * (x0 - cx) + (y0 - cy) * (y0 - cy) <= r2) {
+                set_error("bie_geometry_create: pore " + std::to_string(a) + " crosses the outer wall");
+                return BIE_EGEOM;
+            }
+            const double cross = (x1 - x0) * (cy - y0) - (cx - x0) * (y1 - y0);
+            if (y0 <= cy) {
+                if (y1 > cy && cross > 0) ++wind;
+            } else if (y1 <= cy && cross < 0) {
+                --wind;
+            }
+        }
+        if (wind == 0) {
+            set_error("bie_geometry_create: pore " + std::to_string(a) + " lies outside the outer wall");
+            return BIE_EGEOM;
+        }
+    }
     Geometry *g = new Geometry();
     g->N = (int)Nll;
     g->M = n_pores;

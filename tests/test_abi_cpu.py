@@ -104,3 +104,50 @@ def test_slp_entry_points_validate_arguments(bie):
     assert L.bie_blockdiag_factor_slp(None, None, None) == -1
     assert L.bie_gmres_solve_slp(None, None, None, None, 1e-8, 10, None, None, None, None, None, None) == -1
     assert L.bie_kr_weights(None) == -1
+
+
+def test_geometry_validation_rejects_bad_pores(bie):
+    """Disjoint pores inside Gamma_0 (S:l.36) are checked on the host before any
+    device work: overlapping, wall-crossing and outside pores -> BIE_EGEOM."""
+    from bie_inputs.geometry import circle_outer
+
+    L = bie.lib()
+    h = ctypes.c_void_p()
+    xy, dxy, ddxy, T = circle_outer(64, 1.0)
+    dp = lambda a: np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    keep = []
+
+    def create(cs, rs):
+        c = np.ascontiguousarray(np.array(cs, dtype=np.float64).reshape(-1))
+        r = np.ascontiguousarray(np.array(rs, dtype=np.float64))
+        a = [np.ascontiguousarray(x.reshape(-1)) for x in (xy, dxy, ddxy)]
+        keep.append((a, c, r))
+        return L.bie_geometry_create(dp(a[0]), dp(a[1]), dp(a[2]), 64, T, dp(c), dp(r), len(rs), 32,
+                                     ctypes.byref(h))
+
+    assert create([[0.0, 0.0], [0.25, 0.0]], [0.2, 0.1]) == -2
+    assert b"overlap" in L.bie_last_error()
+    assert create([[0.9, 0.0]], [0.2]) == -2
+    assert b"crosses" in L.bie_last_error()
+    assert create([[3.0, 0.0]], [0.1]) == -2
+    assert b"outside" in L.bie_last_error()
+    # a valid geometry passes validation (then needs a device: BIE_ECUDA on a CPU-only host)
+    rc = create([[0.0, 0.0], [0.5, 0.0]], [0.2, 0.2])
+    assert rc != -2 and rc != -1
+
+
+@pytest.mark.parametrize("cid", [2, 3, 5])
+def test_config_geometries_pass_validation(bie, cid):
+    from bie_inputs import make_problem
+
+    p = make_problem(cid)
+    L = bie.lib()
+    h = ctypes.c_void_p()
+    arrs = [np.ascontiguousarray(a, dtype=np.float64).reshape(-1) for a in
+            (p.outer_xy, p.outer_dxy, p.outer_ddxy, p.pore_c, p.pore_r)]
+    dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    rc = L.bie_geometry_create(dp(arrs[0]), dp(arrs[1]), dp(arrs[2]), p.n_outer, float(p.period), dp(arrs[3]),
+                               dp(arrs[4]), p.M, p.n_pore, ctypes.byref(h))
+    if rc == 0:
+        L.bie_geometry_destroy(h)
+    assert rc not in (-1, -2), L.bie_last_error()
