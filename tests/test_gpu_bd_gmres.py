@@ -223,7 +223,8 @@ def test_gmres_deterministic(bie):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_none_pipe_prefix", "config4_bd_pipe_prefix"])
+@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_none_pipe_prefix", "config4_bd_pipe_prefix",
+                                  "config4_bd_pipe_full"])
 def test_gmres_golden(bie, name):
     """Large configs: histories produced by tools/make_golden.py (oracle only;
     config 4's BD uses the oracle's LU-solve form of the same operator)."""

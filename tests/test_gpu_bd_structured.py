@@ -83,7 +83,7 @@ def test_structured_bd_gmres_config2(bie, rhs):
     assert (np.abs(r["hist"] - ref["hist"])[big] / ref["hist"][big]).max() <= 1e-10
 
 
-@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_bd_pipe_prefix"])
+@pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_bd_pipe_prefix", "config4_bd_pipe_full"])
 def test_structured_bd_gmres_golden(bie, name):
     """Full-size configs in the bench's launch configuration (config 4 is the
     bench workload): oracle goldens with their C23 envelopes."""
