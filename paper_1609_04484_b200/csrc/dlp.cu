@@ -128,6 +128,14 @@ __host__ __device__ __forceinline__ int unit_owner(long long u, long long U, int
     return (int)(((u + 1) * (long long)P - 1) / U);
 }
 
+// Segment of unit u in a unit list (or slice) starting at ub.  Both all-pairs
+// kernels hand out fixed segments of Useg units through an atomic counter; a
+// target block's partial for segment s goes to slot s - seg_of(first unit of
+// the block), so the sums do not depend on which CTA ran which segment.
+__host__ __device__ __forceinline__ long long seg_of(long long u, long long ub, long long Useg) {
+    return (u - ub) / Useg;
+}
+
 struct PairArgs {
     const double2 *tpos;  // [Nt] target positions (pos + row_begin, or off-surface points)
     const double2 *pos;   // [N] source positions
@@ -139,6 +147,8 @@ struct PairArgs {
     int N, row_begin, Nt; // sources, first target, number of targets
     int nTS;
     long long U;
+    long long Useg, nseg;          // dynamic segments (see seg_of)
+    unsigned long long *counter;   // zeroed before the launch
 };
 
 // A3: all-pairs DLP sum.  Each persistent CTA walks a contiguous range of
@@ -158,11 +168,9 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
     constexpr int STAGE = (2 + NV) * TS;
     static_assert(STAGE % NT == 0, "stage must be a multiple of the CTA size");
     const int tid = threadIdx.x;
-    const int P = gridDim.x, p = blockIdx.x;
-    const long long U = a.U;
-    const long long u0 = ((long long)p * U) / P, u1 = ((long long)(p + 1) * U) / P;
-    if (u0 >= u1) return;
+    const long long U = a.U, Useg = a.Useg;
     const int N = a.N, nTS = a.nTS;
+    __shared__ long long s_seg;
 
     auto load_tile = [&](int buf, int ts) {
         double2 *s = smem + buf * STAGE;
@@ -200,6 +208,13 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
         }
     };
 
+    for (;;) {  // claim segments of Useg units (see seg_of)
+    if (tid == 0) s_seg = (long long)atomicAdd(a.counter, 1ULL);
+    __syncthreads();
+    const long long sg = s_seg;
+    __syncthreads();
+    if (sg >= a.nseg) break;
+    const long long u0 = sg * Useg, u1 = min(u0 + Useg, U);
     long long u = u0;
     int tb = (int)(u / nTS);
     load_targets(tb);
@@ -266,7 +281,7 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
         buf ^= 1;
         const bool seg_end = (u + 1 == u1) || ((u + 1) % nTS == 0);
         if (seg_end) {
-            const int slot = p - unit_owner((long long)tb * nTS, U, P);
+            const int slot = (int)(sg - seg_of((long long)tb * nTS, 0, Useg));
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 int it = tb * TB + r * NT + tid;
@@ -285,6 +300,7 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
             }
         }
     }
+    }  // segments
 }
 
 // A2: moments (reading C5).  Block b < M: pore b; block M: Gamma_0.
@@ -428,11 +444,7 @@ struct SymArgs {
     unsigned long long *counter;  // next free segment (zeroed before each launch)
 };
 
-// Segment of unit u in a slice starting at ub; target-partial slot of block A
-// in segment s is s - seg_of(max(off[A], ub)).
-__host__ __device__ __forceinline__ long long seg_of(long long u, long long ub, long long Useg) {
-    return (u - ub) / Useg;
-}
+
 
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
@@ -821,7 +833,7 @@ __device__ __forceinline__ void sum_strided(double2 &acc, const double *p, long 
 
 struct Chunk {
     int v0, nv, TB, nTS, P;
-    long long U;
+    long long U, Useg;
 };
 struct SymEpi {
     int on;                    // 1: partials come from the symmetric path (nvec = 1)
@@ -892,8 +904,8 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
     for (int c = 0; c < a.nchunks; ++c) {
         const Chunk ch = a.ch[c];
         const int tb = it / ch.TB;
-        const int first = unit_owner((long long)tb * ch.nTS, ch.U, ch.P);
-        const int last = unit_owner((long long)(tb + 1) * ch.nTS - 1, ch.U, ch.P);
+        const int first = (int)seg_of((long long)tb * ch.nTS, 0, ch.Useg);
+        const int last = (int)seg_of((long long)(tb + 1) * ch.nTS - 1, 0, ch.Useg);
         // NVC in {1, 4, 16}: nvec is one variant size -> a single chunk at v0 = 0
         const int nv = NVC > 0 ? NVC : ch.nv;
 #pragma unroll
@@ -1068,11 +1080,13 @@ static void make_sched(const Geometry *g, int vi, int Nt, PairSched &s, int op =
     long long Pmax = (long long)g->num_sms * std::max(1, op ? g->occ_slp[vi] : g->occ[vi]);
     s.P = (int)std::min<long long>(Pmax, s.U);
     // max slots per target block: ceil(P / nTB) + 1 bounds it; compute exactly
+    // ~16 segments per CTA: tail <= one segment, few slots per target block
+    s.Useg = std::max<long long>(4, (s.U + 16LL * s.P - 1) / (16LL * s.P));
     int S = 1;
     for (int tb = 0; tb < s.nTB; ++tb) {
-        int f = unit_owner((long long)tb * s.nTS, s.U, s.P);
-        int l = unit_owner((long long)(tb + 1) * s.nTS - 1, s.U, s.P);
-        S = std::max(S, l - f + 1);
+        const long long f = seg_of((long long)tb * s.nTS, 0, s.Useg);
+        const long long l = seg_of((long long)(tb + 1) * s.nTS - 1, 0, s.Useg);
+        S = std::max(S, (int)(l - f + 1));
     }
     s.S = S;
 }
@@ -1093,11 +1107,13 @@ int build_schedules(Geometry *g) {
             PairSched s;
             make_sched(g, vi, g->N, s, op);
             (op ? g->sched_slp : g->sched)[vi] = s;
-            need = std::max(need, (size_t)s.S * BIE_MAX_NVEC * 2 * (size_t)g->N);
+            need = std::max(need, (size_t)s.S * V.nv * 2 * (size_t)g->N);  // grows on demand in dlp_apply_impl
         }
     }
     cudaError_t e = cudaMalloc(&g->partial, need * sizeof(double));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(partial)");
+    e = cudaMalloc(&g->pair_counter, sizeof(unsigned long long) * 8);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(pair counters)");
     g->partial_elems = need;
     return BIE_OK;
 }
@@ -1363,7 +1379,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         need = std::max(need, (size_t)s.S * nvec * 2 * (size_t)Nt);
         sch[nch] = s;
         vis[nch] = vi;
-        ea.ch[nch] = Chunk{v, nv, s.TB, s.nTS, s.P, s.U};
+        ea.ch[nch] = Chunk{v, nv, s.TB, s.nTS, s.P, s.U, s.Useg};
         ++nch;
         v += nv;
     }
@@ -1376,6 +1392,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         g->partial_elems = need;
     }
     if (ev[1] && !sym) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
+    if (nch > 0) BIE_CUDA_TRY(cudaMemsetAsync(g->pair_counter, 0, sizeof(unsigned long long) * nch, st));
     for (int c = 0; c < nch; ++c) {
         PairArgs a;
         a.tpos = g->pos + row_begin;
@@ -1391,6 +1408,9 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         a.Nt = Nt;
         a.nTS = sch[c].nTS;
         a.U = sch[c].U;
+        a.Useg = sch[c].Useg;
+        a.nseg = (a.U + a.Useg - 1) / a.Useg;
+        a.counter = g->pair_counter + c;
         launch_pairs(vis[c], sch[c], a, st, op);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
@@ -1442,8 +1462,8 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
     const int it = active ? it_raw : Nt - 1;
     const double2 xi = tgt[it];
     const int tb = it / ch.TB;
-    const int first = unit_owner((long long)tb * ch.nTS, ch.U, ch.P);
-    const int last = unit_owner((long long)(tb + 1) * ch.nTS - 1, ch.U, ch.P);
+    const int first = (int)seg_of((long long)tb * ch.nTS, 0, ch.Useg);
+    const int last = (int)seg_of((long long)(tb + 1) * ch.nTS - 1, 0, ch.Useg);
     double2 u = make_double2(0.0, 0.0);
     for (int sl = 0; sl <= last - first; ++sl) {
         const double2 pv = reinterpret_cast<const double2 *>(partial + (long long)sl * 2LL * Nt)[it];
@@ -1647,9 +1667,13 @@ int field_eval_impl(Geometry *g, const double *sigma, const double2 *targets, in
     a.Nt = ntgt;
     a.nTS = s.nTS;
     a.U = s.U;
+    a.Useg = s.Useg;
+    a.nseg = (a.U + a.Useg - 1) / a.Useg;
+    a.counter = g->pair_counter;
+    BIE_CUDA_TRY(cudaMemsetAsync(g->pair_counter, 0, sizeof(unsigned long long), st));
     launch_pairs(0, s, a, st);
     count_launch();
-    k_field_epilogue<<<(ntgt + 127) / 128, 128, 0, st>>>(targets, g->partial, ntgt, Chunk{0, 1, s.TB, s.nTS, s.P, s.U},
+    k_field_epilogue<<<(ntgt + 127) / 128, 128, 0, st>>>(targets, g->partial, ntgt, Chunk{0, 1, s.TB, s.nTS, s.P, s.U, s.Useg},
                                                          g->pore, g->moments, g->M, out);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
@@ -1697,9 +1721,13 @@ int slp_field_eval_impl(Geometry *g, const double *sigma, const double2 *targets
     a.Nt = ntgt;
     a.nTS = s.nTS;
     a.U = s.U;
+    a.Useg = s.Useg;
+    a.nseg = (a.U + a.Useg - 1) / a.Useg;
+    a.counter = g->pair_counter;
+    BIE_CUDA_TRY(cudaMemsetAsync(g->pair_counter, 0, sizeof(unsigned long long), st));
     launch_pairs(0, s, a, st, 1);
     count_launch();
-    k_field_epilogue<<<(ntgt + 127) / 128, 128, 0, st>>>(targets, g->partial, ntgt, Chunk{0, 1, s.TB, s.nTS, s.P, s.U},
+    k_field_epilogue<<<(ntgt + 127) / 128, 128, 0, st>>>(targets, g->partial, ntgt, Chunk{0, 1, s.TB, s.nTS, s.P, s.U, s.Useg},
                                                          nullptr, nullptr, 0, out);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());

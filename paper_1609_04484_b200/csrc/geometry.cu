@@ -170,6 +170,7 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     }
     cudaFree(g->slp_s);
     cudaFree(g->sym_counter);
+    cudaFree(g->pair_counter);
     cudaFree(g->gm.V);
     cudaFree(g->gm.w);
     cudaFree(g->gm.t);

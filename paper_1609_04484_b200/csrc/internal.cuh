@@ -37,6 +37,7 @@ struct PairSched {
     int P = 0;          // persistent CTAs
     int S = 0;          // max partial slots per target block
     int smem = 0;
+    long long Useg = 1; // units per dynamically claimed segment
 };
 
 // GMRES workspace cached on the geometry (grow-only): per-call cudaMalloc /
@@ -87,6 +88,7 @@ struct Geometry {
     int slp_sym_variant = 1;  // (8,2) dual-source: fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
     unsigned long long *sym_counter = nullptr;  // dynamic segment counter of the symmetric kernel
+    unsigned long long *pair_counter = nullptr; // [8] counters of the one-sided launches of one apply
     long long sym_Useg = 1;                     // units per segment
     long long sym_U = 0;
     GmresWork gm;               // bie_gmres_solve* workspace
