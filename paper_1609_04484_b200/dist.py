@@ -31,13 +31,18 @@ def bodies_of_rows(row_begin: int, row_end: int, M: int, n_pore: int):
     return b0, b1
 
 
-def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000):
+def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000, lookahead: int = 3):
     """Left-preconditioned full GMRES (reading C13) on row-sharded vectors.
 
     be must provide: n, zeros(len), pc(x, out), apply_pc_op(v, out), apply_op(v, out),
     dots(V, ldv, nv, w, out), axpy(V, ldv, nv, c, alpha, beta, y), scale(x, s, y),
     sqrt(inp, out, m), givens(H, ldh, cs, sn, g, h, h2, k, scal), trisolve(H, ldh, g, y, iters),
-    allreduce_(t), copy_(dst, src), sub(a, b, out), host(t) -> numpy.
+    allreduce_(t), copy_(dst, src), sub(a, b, out), host(t) -> numpy, and
+    host_async(t, slot) -> handle / host_wait(handle) -> numpy (non-blocking read-back).
+    The convergence check of iteration k runs after iteration k + lookahead is
+    enqueued (as in bie_gmres_solve): later iterations are speculative and touch
+    only entries the finish does not read.  Every rank holds identical
+    replicated scalars, so all ranks stop at the same iteration.
     Returns (x_loc, dict(iters, hist, res_pc, res_true, converged))."""
     n = be.n
     ldh = max_iter + 1
@@ -65,6 +70,17 @@ def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000):
     be.scale(w, scal[0:1], vec(0))
     be.copy_(g[0:1], scal[0:1])
     it, conv = 0, False
+    pending = []
+
+    def check():
+        nonlocal it, conv
+        kk, hd = pending.pop(0)
+        est, brk = be.host_wait(hd)
+        hist.append(float(est))
+        it = kk + 1
+        if est < tol or brk != 0.0:
+            conv = True
+
     for k in range(max_iter):
         be.apply_pc_op(vec(k), w)
         norm_into(w, 1)
@@ -76,14 +92,15 @@ def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000):
         be.axpy(V, n, k + 1, h2, -1.0, 1.0, w)
         norm_into(w, 2)
         be.givens(H, ldh, cs, sn, g, h, h2, k, scal)
-        est, brk = be.host(scal[3:5])
-        hist.append(float(est))
-        it = k + 1
-        if est < tol or brk != 0.0:
-            conv = True
-            break
+        pending.append((k, be.host_async(scal[3:5], k)))
         if k + 1 < max_iter:
             be.scale(w, scal[2:3], vec(k + 1))
+        if len(pending) > lookahead:
+            check()
+            if conv:
+                break
+    while pending and not conv:
+        check()
     be.trisolve(H, ldh, g, tmp, it)
     be.axpy(V, n, it, tmp, 1.0, 0.0, x)
     # residual pair (P:l.678-686)
@@ -239,3 +256,16 @@ class GpuBackend:
 
     def host(self, t):
         return t.cpu().numpy()
+
+    def host_async(self, t, slot):
+        if not hasattr(self, "_ring"):
+            self._ring = self.torch.zeros((8, 2), dtype=self.torch.float64).pin_memory()
+            self._evs = [self.torch.cuda.Event() for _ in range(8)]
+        q = slot % 8
+        self._ring[q, : t.numel()].copy_(t, non_blocking=True)
+        self._evs[q].record()
+        return q
+
+    def host_wait(self, q):
+        self._evs[q].synchronize()
+        return self._ring[q].numpy().copy()

@@ -106,6 +106,12 @@ class CpuBackend:
     def host(self, t):
         return t.numpy().copy()
 
+    def host_async(self, t, slot):
+        return t.numpy().copy()
+
+    def host_wait(self, h):
+        return h
+
 
 def _free_port():
     s = socket.socket()
