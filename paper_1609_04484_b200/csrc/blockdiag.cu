@@ -380,19 +380,27 @@ struct CoopScratch {
     double *kbuf;    // [2][NB] row k before the swap
     double *A;       // [NB][NB] LU'd pivot rows
 };
+// RPT rows per thread: fewer CTAs make the per-column grid barrier cheaper.
+template <int RPT>
 __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopScratch cs, int k0, int nbe) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double red_v[4];
     __shared__ int red_i[4];
     __shared__ int s_p, s_src, s_bi;
+    __shared__ double s_pr[NB];  // the pivot row, staged once per CTA and column
     const int n2 = v.n2;
     const double *M = v.mat;  // one matrix per class launch
     const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
-    const int r = k0 + g * 128 + tid;  // this thread's panel row
-    const bool own = r < n2;
-    double w[NB];
+    int rr[RPT];
+    bool own[RPT];
+    double w[RPT][NB];
 #pragma unroll
-    for (int c = 0; c < NB; ++c) w[c] = (own && c < nbe) ? M[(long long)r * n2 + k0 + c] : 0.0;
+    for (int t = 0; t < RPT; ++t) {
+        rr[t] = k0 + g * 128 * RPT + t * 128 + tid;  // this thread's panel rows
+        own[t] = rr[t] < n2;
+#pragma unroll
+        for (int c = 0; c < NB; ++c) w[t][c] = (own[t] && c < nbe) ? M[(long long)rr[t] * n2 + k0 + c] : 0.0;
+    }
 #pragma unroll 1
     for (int c = 0; c < nbe; ++c) {
         const int k = k0 + c, par = c & 1;
@@ -400,12 +408,18 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
         int *ci_ = cs.cand_i + par * G;
         double *crow = cs.crow + (long long)par * G * NB;
         double *kb = cs.kbuf + par * NB;
-        double wc = 0.0;
+        double best = -1.0;
+        int bi = n2;
 #pragma unroll
-        for (int q = 0; q < NB; ++q)
-            if (q == c) wc = w[q];
-        double best = (own && r >= k) ? fabs(wc) : -1.0;
-        int bi = (own && r >= k) ? r : n2;
+        for (int t = 0; t < RPT; ++t) {
+            double wc = 0.0;
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+                if (q == c) wc = w[t][q];
+            const double b = (own[t] && rr[t] >= k) ? fabs(wc) : -1.0;
+            const int ix = (own[t] && rr[t] >= k) ? rr[t] : n2;
+            if (b > best || (b == best && ix < bi)) { best = b; bi = ix; }
+        }
         for (int o = 16; o > 0; o >>= 1) {
             const double ob = __shfl_down_sync(0xffffffffu, best, o);
             const int oi = __shfl_down_sync(0xffffffffu, bi, o);
@@ -423,13 +437,16 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
             s_bi = bi;
         }
         __syncthreads();
-        if (own && r == s_bi) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) crow[(long long)g * NB + q] = w[q];
-        }
-        if (own && r == k) {
+        for (int t = 0; t < RPT; ++t) {
+            if (own[t] && rr[t] == s_bi) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) kb[q] = w[q];
+                for (int q = 0; q < NB; ++q) crow[(long long)g * NB + q] = w[t][q];
+            }
+            if (own[t] && rr[t] == k) {
+#pragma unroll
+                for (int q = 0; q < NB; ++q) kb[q] = w[t][q];
+            }
         }
         grid.sync();
         int src = -1;
@@ -462,35 +479,37 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
         }
         __syncthreads();
         const int p = s_p;
-        const double *prow = s_src >= 0 ? crow + (long long)s_src * NB : kb;
-        if (own && r == k) {
+        if (tid < NB) s_pr[tid] = (s_src >= 0 ? crow + (long long)s_src * NB : kb)[tid];
+        __syncthreads();
+        const double *pr = s_pr;
+        double dd = pr[c];
+        if (dd == 0.0) dd = 1.0;
 #pragma unroll
-            for (int q = 0; q < NB; ++q) w[q] = prow[q];
-        } else if (own && r == p) {
+        for (int t = 0; t < RPT; ++t) {
+            if (own[t] && rr[t] == k) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) w[q] = kb[q];
-        }
-        if (own && r > k) {
-            double pr[NB];
+                for (int q = 0; q < NB; ++q) w[t][q] = pr[q];
+            } else if (own[t] && rr[t] == p) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) pr[q] = prow[q];
-            double dd = 1.0;
+                for (int q = 0; q < NB; ++q) w[t][q] = kb[q];
+            }
+            if (own[t] && rr[t] > k) {
+                double l = 0.0;
 #pragma unroll
-            for (int q = 0; q < NB; ++q)
-                if (q == c) dd = pr[q];
-            if (dd == 0.0) dd = 1.0;
-            double l = 0.0;
+                for (int q = 0; q < NB; ++q)
+                    if (q == c) { l = w[t][q] / dd; w[t][q] = l; }
 #pragma unroll
-            for (int q = 0; q < NB; ++q)
-                if (q == c) { l = w[q] / dd; w[q] = l; }
-#pragma unroll
-            for (int q = 0; q < NB; ++q)
-                if (q > c && q < nbe) w[q] -= l * pr[q];
+                for (int q = 0; q < NB; ++q)
+                    if (q > c && q < nbe) w[t][q] -= l * pr[q];
+            }
         }
     }
-    if (own && r < k0 + nbe) {
 #pragma unroll
-        for (int q = 0; q < NB; ++q) cs.A[(r - k0) * NB + q] = w[q];
+    for (int t = 0; t < RPT; ++t) {
+        if (own[t] && rr[t] < k0 + nbe) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) cs.A[(rr[t] - k0) * NB + q] = w[t][q];
+        }
     }
     grid.sync();
     if (g == 0) a11_inverse(cs.A, nbe, s.A11i);
@@ -893,12 +912,17 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     // cooperative multi-CTA panel for the single large block (Gamma_0 of configs 2-5)
     const bool coop = n2 > kSmemPanelRows && v.count == 1;
     CoopScratch cs{};
+    // rows per thread of the cooperative panel (tuning knob BIE_PANEL_RPT = 1 | 2;
+    // measured config 4: 1 row 0.72-0.74 s factor, 2 rows 0.78-0.80 s)
+    int rpt = 1;
+    if (const char *e = getenv("BIE_PANEL_RPT")) rpt = std::max(1, std::min(2, atoi(e)));
+    void *coop_kernel = rpt == 2 ? (void *)k_panel_coop<2> : (void *)k_panel_coop<1>;
     if (coop) {
         const int Gmax = (n2 + 127) / 128;
         int per_sm = 0, dev = 0, coop_ok = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
-        BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_panel_coop, 128, 0));
+        BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_kernel, 128, 0));
         if (!coop_ok || (long long)per_sm * g->num_sms < Gmax) {
             set_error("bie_blockdiag_factor: cooperative launch unavailable for the panel factorisation");
             return BIE_ECUDA;
@@ -919,9 +943,9 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     for (int k0 = 0; k0 < n2; k0 += NB) {
         int nbe = std::min(NB, n2 - k0);
         if (coop) {
-            int G = (n2 - k0 + 127) / 128;
+            int G = (n2 - k0 + 128 * rpt - 1) / (128 * rpt);
             void *args[] = {&v, &s, &cs, &k0, &nbe};
-            BIE_CUDA_TRY(cudaLaunchCooperativeKernel((void *)k_panel_coop, G, 128, args, 0, st));
+            BIE_CUDA_TRY(cudaLaunchCooperativeKernel(coop_kernel, G, 128, args, 0, st));
         } else if (n2 - k0 <= kSmemPanelRows) {
             k_panel_smem<<<v.count, 256, sizeof(double) * NB * (n2 - k0), st>>>(v, s, k0, nbe);
         } else {
