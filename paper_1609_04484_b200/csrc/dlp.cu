@@ -82,8 +82,8 @@ __device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, do
 // Table-driven variant for the symmetric SLP kernel (Tang-style reduction):
 // d = 2^e m, m in [1, 2); k = top 6 mantissa bits; tab[k] = (rc_k, -1/2 log rc_k)
 // with rc_k = RN(1 / (1 + (k + 1/2)/64)).  r = m rc_k - 1 (one FMA, |r| < 2^-7),
-// log m = log1p(r) - log rc_k, log1p(r) = r (1 - r/2 + ... - r^7/8) (truncation
-// < 2^-63).  Returns hl = -1/2 log d directly (scaled coefficients): 11 FP64
+// log m = log1p(r) - log rc_k, log1p(r) = r (1 - r/2 + ... + r^6/7) (truncation
+// r^8/8 < 2^-59).  Returns hl = -1/2 log d directly (scaled coefficients): 10 FP64
 // instructions instead of 18 + 1, plus one shared-memory lookup.
 struct LogTab {
     double2 e[64];
@@ -100,8 +100,7 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double2 tk = t.e[(hi >> 14) & 63];
     const double r = fma(m, tk.x, -1.0);
-    double q = 0.5 / 8.0;  // -1/2 (1 - r/2 + r^2/3 - ... - r^7/8)
-    q = fma(q, r, -0.5 / 7.0);
+    double q = -0.5 / 7.0;  // -1/2 (1 - r/2 + r^2/3 - ... + r^6/7); the r^7 term is < 2^-59
     q = fma(q, r, 0.5 / 6.0);
     q = fma(q, r, -0.5 / 5.0);
     q = fma(q, r, 0.5 / 4.0);
