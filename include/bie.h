@@ -330,6 +330,21 @@ BIE_API int bie_gmres_solve_batch_slp(bie_geometry_t g, bie_blockdiag_t bd, cons
                                       double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
                                       double *res_true, int *converged, void *stream);
 
+/*
+ * Row-sharded SLP (NEXT-1 x NEXT-4): the single-layer counterparts of
+ * bie_dlp_pairs_partial / bie_dlp_epilogue_rows / bie_blockdiag_factor_range
+ * (same slicing, layouts and errors).  bie_slp_pairs_partial
+ * writes the all-pairs sums sum_{j != i} w_j G(x_i, x_j) sigma_j of its slice
+ * into a full-size vector; bie_slp_epilogue_rows adds the Kapur-Rokhlin
+ * corrections of rows [row_begin, row_end) to the reduced pair sums.
+ */
+BIE_API int bie_slp_pairs_partial(bie_geometry_t g, const double *sigma, double *out_full, long long unit_begin,
+                                  long long unit_end, int block_begin, int block_end, void *stream);
+BIE_API int bie_slp_epilogue_rows(bie_geometry_t g, const double *sigma, const double *pairsum_rows,
+                                  double *out_rows, int row_begin, int row_end, void *stream);
+BIE_API int bie_blockdiag_factor_range_slp(bie_geometry_t g, int body_begin, int body_end, bie_blockdiag_t *out,
+                                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

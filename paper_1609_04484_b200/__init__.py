@@ -33,7 +33,9 @@ from ._bie import (  # noqa: F401
     profile_end,
     slp_apply,
     slp_apply_rows,
+    slp_epilogue_rows,
     slp_field_eval,
+    slp_pairs_partial,
     lib,
     lib_path,
     EXPORTED_SYMBOLS,

@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "bie_krylov_trisolve", "bie_dlp_sym_info", "bie_dlp_pairs_partial", "bie_dlp_epilogue_rows",
     "bie_kr_weights", "bie_slp_apply", "bie_slp_apply_rows", "bie_slp_field_eval", "bie_blockdiag_factor_slp",
     "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp", "bie_blockdiag_factor_structured",
+    "bie_slp_pairs_partial", "bie_slp_epilogue_rows", "bie_blockdiag_factor_range_slp",
 )
 
 
@@ -90,6 +91,9 @@ def lib():
         "bie_slp_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_blockdiag_factor_slp": [vp, ctypes.POINTER(vp), vp],
         "bie_blockdiag_factor_structured": [vp, ctypes.POINTER(vp), vp],
+        "bie_slp_pairs_partial": [vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong, c_int, c_int, vp],
+        "bie_slp_epilogue_rows": [vp, vp, vp, vp, c_int, c_int, vp],
+        "bie_blockdiag_factor_range_slp": [vp, c_int, c_int, ctypes.POINTER(vp), vp],
         "bie_gmres_solve_slp": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_gmres_solve_batch_slp": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_profile_begin": [vp],
@@ -276,9 +280,11 @@ class BlockDiag:
                 raise ValueError("the structured pore BD is built for the whole geometry and the DLP operator")
             _check(lib().bie_blockdiag_factor_structured(g.h, ctypes.byref(h), _stream_ptr(stream)))
         elif op == "slp":
-            if bodies is not None:
-                raise ValueError("the SLP block-diagonal preconditioner covers the whole geometry")
-            _check(lib().bie_blockdiag_factor_slp(g.h, ctypes.byref(h), _stream_ptr(stream)))
+            if bodies is None:
+                _check(lib().bie_blockdiag_factor_slp(g.h, ctypes.byref(h), _stream_ptr(stream)))
+            else:
+                _check(lib().bie_blockdiag_factor_range_slp(g.h, int(bodies[0]), int(bodies[1]), ctypes.byref(h),
+                                                            _stream_ptr(stream)))
         elif bodies is None:
             _check(lib().bie_blockdiag_factor(g.h, ctypes.byref(h), _stream_ptr(stream)))
         else:
@@ -441,4 +447,20 @@ def gmres_solve_batch_slp(g: Geometry, bd: BlockDiag | None, F, X, nrhs: int, to
     hist = hist.reshape(nrhs, max_iter + 1)
     return [dict(iters=int(it[r]), hist=hist[r, : it[r] + 1].copy(), res_pc=float(rp[r]), res_true=float(rt[r]),
                  converged=bool(conv[r])) for r in range(nrhs)]
+
+
+def slp_pairs_partial(g: Geometry, sigma, out_full, units, blocks, stream=None):
+    """SLP pair sums of a slice of the symmetric work into a full [2N] vector (bie_slp_pairs_partial)."""
+    _check(lib().bie_slp_pairs_partial(g.h, _dev_ptr(sigma, "sigma", 2 * g.N), _dev_ptr(out_full, "out", 2 * g.N),
+                                       int(units[0]), int(units[1]), int(blocks[0]), int(blocks[1]),
+                                       _stream_ptr(stream)))
+    return out_full
+
+
+def slp_epilogue_rows(g: Geometry, sigma, pairsum_rows, out_rows, row_begin: int, row_end: int, stream=None):
+    """out_rows = pairsum_rows + KR corrections on [row_begin, row_end) (bie_slp_epilogue_rows)."""
+    n = 2 * (row_end - row_begin)
+    _check(lib().bie_slp_epilogue_rows(g.h, _dev_ptr(sigma, "sigma", 2 * g.N), _dev_ptr(pairsum_rows, "pairsum", n),
+                                       _dev_ptr(out_rows, "out", n), row_begin, row_end, _stream_ptr(stream)))
+    return out_rows
 

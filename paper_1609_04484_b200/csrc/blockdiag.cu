@@ -1333,6 +1333,16 @@ int bie_blockdiag_factor_range(bie_geometry_t gh, int body_begin, int body_end, 
     return factor_range(g, body_begin, body_end, out, (cudaStream_t)stream);
 }
 
+int bie_blockdiag_factor_range_slp(bie_geometry_t gh, int body_begin, int body_end, bie_blockdiag_t *out,
+                                   void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out || body_begin < 0 || body_end > g->M + 1 || body_begin >= body_end) {
+        set_error("bie_blockdiag_factor_range_slp: invalid handle/output or body range not in [0, M+1]");
+        return BIE_EINVAL;
+    }
+    return factor_range(g, body_begin, body_end, out, (cudaStream_t)stream, 1);
+}
+
 int bie_blockdiag_rows(bie_blockdiag_t h, int *row_begin, int *row_end) {
     BlockDiag *bd = as_bd(h);
     if (!bd || !row_begin || !row_end) {

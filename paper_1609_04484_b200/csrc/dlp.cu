@@ -1535,7 +1535,7 @@ __global__ void __launch_bounds__(256) k_sym_gather(const double *__restrict__ t
 }
 
 int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long long ub, long long ue, int blk0,
-                       int blk1, cudaStream_t st) {
+                       int blk1, cudaStream_t st, int op = 0) {
     int rc = sym_prepare(g);
     if (rc) return rc;
     if (g->sym_state != 1) {
@@ -1555,7 +1555,13 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         g->prof_used += 4;
         BIE_CUDA_TRY(cudaEventRecord(ev[0], st));
     }
-    k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+    if (op) {  // single layer (NEXT-1): S = w sigma / 4pi and its (S, 0, 0) records
+        int rc2 = slp_prepare(g);
+        if (rc2) return rc2;
+        k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, 2LL * N, 1, N, g->slp_s, g->sym_Q);
+    } else {
+        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+    }
     count_launch();
     if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
     long long Useg = 1;
@@ -1583,11 +1589,17 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, U, ub, nullptr,
                    Useg,   (U + Useg - 1) / Useg, g->sym_counter};
         BIE_CUDA_TRY(cudaMemsetAsync(g->sym_counter, 0, sizeof(unsigned long long), st));
-        launch_sym(g->sym_variant, P, sa, st);
+        if (op)
+            launch_sym_slp(g->slp_sym_variant, P, sa, st);
+        else
+            launch_sym(g->sym_variant, P, sa, st);
         count_launch();
     }
     if (blk1 > blk0) {
-        k_dlp_diag<0><<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
+        if (op)
+            k_dlp_diag<1><<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, g->slp_s, g->sym_diag, N, blk0);
+        else
+            k_dlp_diag<0><<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
         count_launch();
     }
     if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -1604,7 +1616,13 @@ int epilogue_rows_impl(Geometry *g, const double *sigma, const double *presum, d
     const int N = g->N;
     const int Nt = re - rb;
     if (Nt <= 0) return BIE_OK;
-    if (!(flags & BIE_D_ONLY)) {
+    const int op = (flags & kOpSLP) ? 1 : 0;
+    if (op) {  // the KR correction needs S = w sigma / 4pi of the neighbours
+        int rc = slp_prepare(g);
+        if (rc) return rc;
+        k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, 2LL * N, 1, N, g->slp_s, nullptr);
+        count_launch();
+    } else if (!(flags & BIE_D_ONLY)) {
         k_moments<<<g->M + 1, 256, 0, st>>>(g->pos, g->nrm, g->w, g->pore, sigma, 2LL * N, 1, g->M, g->n_pore,
                                             g->wall_lo, N, g->wall_len, g->moments);
         count_launch();
@@ -1629,6 +1647,10 @@ int epilogue_rows_impl(Geometry *g, const double *sigma, const double *presum, d
     ea.flags = flags;
     ea.nchunks = 0;
     ea.presum = presum;
+    ea.op = op;
+    ea.n_pore = g->n_pore;
+    ea.slp_s = g->slp_s;
+    for (int k = 0; k < 6; ++k) ea.kr[k] = g->kr[k];
     k_epilogue<1><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
@@ -1809,6 +1831,34 @@ int bie_dlp_pairs_partial(bie_geometry_t gh, const double *sigma, double *out_fu
         return BIE_EINVAL;
     }
     return pairs_partial_impl(g, sigma, out_full, unit_begin, unit_end, block_begin, block_end, (cudaStream_t)stream);
+}
+
+int bie_slp_pairs_partial(bie_geometry_t gh, const double *sigma, double *out_full, long long unit_begin,
+                          long long unit_end, int block_begin, int block_end, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !sigma || !out_full || sigma == out_full) {
+        set_error("bie_slp_pairs_partial: invalid handle, null pointer or aliasing");
+        return BIE_EINVAL;
+    }
+    int rc = sym_prepare(g);
+    if (rc) return rc;
+    if (unit_begin < 0 || unit_end > g->sym_U || unit_begin > unit_end || block_begin < 0 ||
+        block_end > g->sym_nTB || block_begin > block_end) {
+        set_error("bie_slp_pairs_partial: unit or block range out of bounds (see bie_dlp_sym_info)");
+        return BIE_EINVAL;
+    }
+    return pairs_partial_impl(g, sigma, out_full, unit_begin, unit_end, block_begin, block_end, (cudaStream_t)stream,
+                              1);
+}
+
+int bie_slp_epilogue_rows(bie_geometry_t gh, const double *sigma, const double *pairsum_rows, double *out_rows,
+                          int row_begin, int row_end, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !sigma || !pairsum_rows || !out_rows || row_begin < 0 || row_end > g->N || row_begin > row_end) {
+        set_error("bie_slp_epilogue_rows: invalid handle, pointer or row range");
+        return BIE_EINVAL;
+    }
+    return epilogue_rows_impl(g, sigma, pairsum_rows, out_rows, row_begin, row_end, kOpSLP, (cudaStream_t)stream);
 }
 
 int bie_dlp_epilogue_rows(bie_geometry_t gh, const double *sigma, const double *pairsum_rows, double *out_rows,

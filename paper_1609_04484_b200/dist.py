@@ -122,9 +122,11 @@ class GpuBackend:
     row owners, and each rank adds the local terms of its rows
     (bie_dlp_pairs_partial -> reduce-scatter -> bie_dlp_epilogue_rows): the
     11-instruction pair kernel is kept at N > 1.
-    mode "rows": each rank evaluates its rows one-sidedly (bie_dlp_apply_rows)."""
+    mode "rows": each rank evaluates its rows one-sidedly (bie_dlp_apply_rows).
+    op "slp": the paper's single-layer operator (NEXT-1) through the bie_slp_*
+    counterparts (pairs_partial / epilogue_rows / apply_rows / range BD)."""
 
-    def __init__(self, g, rank: int, world: int, group=None, stream=None, mode: str = "sym"):
+    def __init__(self, g, rank: int, world: int, group=None, stream=None, mode: str = "sym", op: str = "dlp"):
         import torch
 
         from . import _bie as B
@@ -136,7 +138,10 @@ class GpuBackend:
         self.rb, self.re = self.ranges[rank]
         self.n = 2 * (self.re - self.rb)
         b0, b1 = bodies_of_rows(self.rb, self.re, g.M, g.n_pore)
-        self.bd = B.BlockDiag(g, bodies=(b0, b1))
+        if op not in ("dlp", "slp"):
+            raise ValueError("op must be 'dlp' or 'slp'")
+        self.op = op
+        self.bd = B.BlockDiag(g, bodies=(b0, b1), op=op)
         assert self.bd.rows == (self.rb, self.re)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
@@ -196,10 +201,15 @@ class GpuBackend:
 
     def apply_op(self, v, out):
         full = self._gather_full(v)
+        slp = self.op == "slp"
         if self.mode == "rows":
-            self.B.dlp_apply_rows(self.g, full, out, self.rb, self.re, stream=self.stream)
+            if slp:
+                self.B.slp_apply_rows(self.g, full, out, self.rb, self.re, stream=self.stream)
+            else:
+                self.B.dlp_apply_rows(self.g, full, out, self.rb, self.re, stream=self.stream)
             return
-        self.B.dlp_pairs_partial(self.g, full, self.part_full, self.units, self.blocks, stream=self.stream)
+        pairs = self.B.slp_pairs_partial if slp else self.B.dlp_pairs_partial
+        pairs(self.g, full, self.part_full, self.units, self.blocks, stream=self.stream)
         if self.world == 1:
             rows = self.part_full
         else:
@@ -207,7 +217,10 @@ class GpuBackend:
                 self.send[r * self.maxlen: r * self.maxlen + 2 * (e - b)].copy_(self.part_full[2 * b:2 * e])
             self._reduce_scatter(self.recv, self.send)
             rows = self.recv[: self.n]
-        self.B.dlp_epilogue_rows(self.g, full, rows, out, self.rb, self.re, stream=self.stream)
+        if slp:
+            self.B.slp_epilogue_rows(self.g, full, rows, out, self.rb, self.re, stream=self.stream)
+        else:
+            self.B.dlp_epilogue_rows(self.g, full, rows, out, self.rb, self.re, stream=self.stream)
 
     def pc(self, x, out):
         self.B.blockdiag_apply(self.bd, x, out, stream=self.stream)

@@ -117,7 +117,7 @@ def test_dist_gmres_world1_sym_mode(bie):
     assert (np.abs(res["hist"] - ref["hist"]) / ref["hist"]).max() < 1e-10
 
 
-def _gpu_worker(rank, world, port, mode, q):
+def _gpu_worker(rank, world, port, mode, q, op="dlp"):
     """One rank of a world-size-2 solve on the single test GPU.  The ranks'
     kernels never wait on one another: the collectives are gloo, host-side."""
     import os
@@ -135,7 +135,7 @@ def _gpu_worker(rank, world, port, mode, q):
         torch.cuda.set_device(0)
         p = make_problem(2)
         g = bie.Geometry.from_problem(p)
-        be = GpuBackend(g, rank, world, mode=mode)
+        be = GpuBackend(g, rank, world, mode=mode, op=op)
         f = rhs_pipe(p)
         x, res = dist_gmres(be, _t(f[2 * be.rb:2 * be.re]), tol=1e-8, max_iter=200)
         out = [None] * world
@@ -181,3 +181,95 @@ def test_dist_gmres_world2_gpu_backend(bie, mode):
         x[2 * rb:2 * re_] = xr
     xs = x1.cpu().numpy()
     assert np.abs(x - xs).max() / np.abs(xs).max() < 1e-9
+
+
+def test_slp_pairs_partial_slices_sum_to_full_matvec(bie):
+    """NEXT-1 x NEXT-4: slices of the SLP symmetric work plus the KR row epilogue
+    equal bie_slp_apply."""
+    import torch
+
+    for cid in (2, 3):
+        p = make_problem(cid)
+        g = bie.Geometry.from_problem(p)
+        U, nb = bie.dlp_sym_info(g)
+        s = _t(density(p)[0])
+        ref = torch.zeros_like(s)
+        bie.slp_apply(g, s, ref)
+        acc = torch.zeros_like(s)
+        part = torch.zeros_like(s)
+        for k in range(3):
+            bie.slp_pairs_partial(g, s, part, (U * k // 3, U * (k + 1) // 3), (nb * k // 3, nb * (k + 1) // 3))
+            acc += part
+        rb, re_ = 100, p.N - 37
+        out = torch.zeros(2 * (re_ - rb), dtype=torch.float64, device="cuda")
+        bie.slp_epilogue_rows(g, s, acc[2 * rb:2 * re_].contiguous(), out, rb, re_)
+        torch.cuda.synchronize()
+        r = ref.cpu().numpy()[2 * rb:2 * re_]
+        assert np.abs(out.cpu().numpy() - r).max() / np.abs(r).max() < 1e-13
+
+
+@pytest.mark.parametrize("mode", ["sym", "rows"])
+def test_dist_gmres_world1_slp(bie, mode):
+    """The row-sharded driver on the SLP system at world size 1 reproduces
+    bie_gmres_solve_slp (same kernels and reduction order in sym mode)."""
+    import torch
+
+    from paper_1609_04484_b200.dist import GpuBackend, dist_gmres
+
+    p = make_problem(2)
+    g = bie.Geometry.from_problem(p)
+    f = rhs_pipe(p)
+    be = GpuBackend(g, rank=0, world=1, mode=mode, op="slp")
+    x, res = dist_gmres(be, _t(f), tol=1e-8, max_iter=300)
+    torch.cuda.synchronize()
+    x1 = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    ref = bie.gmres_solve_slp(g, bie.BlockDiag(g, op="slp"), _t(f), x1, 1e-8, 300)
+    assert res["converged"] and ref["converged"]
+    if mode == "sym":
+        assert res["iters"] == ref["iters"]
+        assert (np.abs(res["hist"] - ref["hist"]) / ref["hist"]).max() < 1e-10
+    else:  # one-sided rows: different rounding of a nearly singular BD system (C26)
+        assert abs(res["iters"] - ref["iters"]) <= 2
+
+
+def test_dist_gmres_world2_gpu_backend_slp(bie):
+    """World size 2 on the SLP system (gloo collectives on the one test GPU)."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, "sym", q, "slp")) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p = make_problem(2)
+    g = bie.Geometry.from_problem(p)
+    f = rhs_pipe(p)
+    x1 = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    ref = bie.gmres_solve_slp(g, bie.BlockDiag(g, op="slp"), _t(f), x1, tol=1e-8, max_iter=200)
+    res = out[0][3]
+    assert res["converged"] and abs(res["iters"] - ref["iters"]) <= 2
+    # the nearly singular SLP BD system (C26): compare the well-determined output,
+    # the velocity field the density represents, inside the domain
+    x = np.zeros(2 * p.N)
+    for rb, re_, xr, _ in out:
+        x[2 * rb:2 * re_] = xr
+    rng = np.random.default_rng(2)
+    tg = np.stack([rng.uniform(0.5, 9.5, 300), rng.uniform(-0.5, 0.5, 300)], 1)
+    u2 = torch.zeros(600, dtype=torch.float64, device="cuda")
+    u1 = torch.zeros(600, dtype=torch.float64, device="cuda")
+    bie.slp_field_eval(g, _t(x), _t(tg), u2)
+    bie.slp_field_eval(g, x1, _t(tg), u1)
+    torch.cuda.synchronize()
+    a, b = u2.cpu().numpy(), u1.cpu().numpy()
+    assert np.abs(a - b).max() / np.abs(b).max() < 1e-6
