@@ -151,7 +151,14 @@ def cpu_baseline_sample(problem, seconds=12.0, max_rows=None):
         done_pairs += rows_per_batch * N
         batch += 1
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), None)
+    except OSError:
+        pass
     return {"value": done_pairs / t_used, "unit": "pair-interactions/s", "cores": cores, "kind": "oracle",
+            "cpu_model": model, "omp_num_threads": os.environ.get("OMP_NUM_THREADS"),
             "sample": f"{batch * rows_per_batch} strided target rows x all {N} sources of the config-{problem.config_id} "
                       f"completed DLP matvec (oracle/bie_oracle.c, OpenMP over rows), {t_used:.1f} s",
             "seconds": t_used}
