@@ -581,16 +581,23 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
                 const double ca = s_src[buf][w][2][la].x, cb = s_src[buf][w][2][lb].x;
 #pragma unroll
                 for (int r = 0; r < SR; ++r) {
-                    if constexpr (OP == 1) {
-                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xa.x, xa.y, qa.x, qa.y, ax[r], ay[r], bxA, byA,
-                                     s_log);
-                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xb.x, xb.y, qb.x, qb.y, ax[r], ay[r], bxB, byB,
-                                     s_log);
+                    double ta, tb, tc;
+                    if constexpr (QS) {
+                        const double2 ab = s_tqab[w][r][lane];
+                        ta = ab.x;
+                        tb = ab.y;
+                        tc = s_tqc[w][r][lane];
                     } else {
-                        dlp_pairpair(tx[r], ty[r], tqa[r], tqb[r], tqc[r], xa.x, xa.y, qa.x, qa.y, ca, ax[r], ay[r],
-                                     bxA, byA);
-                        dlp_pairpair(tx[r], ty[r], tqa[r], tqb[r], tqc[r], xb.x, xb.y, qb.x, qb.y, cb, ax[r], ay[r],
-                                     bxB, byB);
+                        ta = tqa[r];
+                        tb = tqb[r];
+                        tc = tqc[r];
+                    }
+                    if constexpr (OP == 1) {
+                        slp_pairpair(tx[r], ty[r], ta, tb, xa.x, xa.y, qa.x, qa.y, ax[r], ay[r], bxA, byA, s_log);
+                        slp_pairpair(tx[r], ty[r], ta, tb, xb.x, xb.y, qb.x, qb.y, ax[r], ay[r], bxB, byB, s_log);
+                    } else {
+                        dlp_pairpair(tx[r], ty[r], ta, tb, tc, xa.x, xa.y, qa.x, qa.y, ca, ax[r], ay[r], bxA, byA);
+                        dlp_pairpair(tx[r], ty[r], ta, tb, tc, xb.x, xb.y, qb.x, qb.y, cb, ax[r], ay[r], bxB, byB);
                     }
                 }
                 bxA = shfl_d(bxA, src_lane);
@@ -1122,10 +1129,10 @@ int build_schedules(Geometry *g) {
 // variants 6..8 keep the target quadratic forms in shared memory (QS)
 // variants 11..14 pipeline the source steps (TP = 1: loads one step ahead; 2: unroll 2)
 // variants 15..18 use dual-source steps (DS)
-static const int kNumSymVar = 21;
-static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2},
-                                           {8, 2}, {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4},
-                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {2, 8}, {8, 2}, {8, 2}};
+static const int kNumSymVar = 23;
+static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2}, {8, 2},
+                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4}, {4, 4}, {4, 4},
+                                           {4, 4}, {8, 2}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {8, 2}};
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
@@ -1148,6 +1155,8 @@ static void *sym_kernel(int v) {
         case 18: return reinterpret_cast<void *>(&k_dlp_sym<2, 8, 2, false, 0, 0, true>);
         case 19: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, false, 0, 0, true>);
         case 20: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 6, false, 0, 0, true>);
+        case 21: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, true, 0, 0, true>);
+        case 22: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, true, 0, 0, true>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
     }
 }
@@ -1174,6 +1183,8 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 18: k_dlp_sym<2, 8, 2, false, 0, 0, true><<<P, 256, 0, st>>>(sa); break;
         case 19: k_dlp_sym<8, 2, 5, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
         case 20: k_dlp_sym<8, 2, 6, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
+        case 21: k_dlp_sym<8, 2, 1, true, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
+        case 22: k_dlp_sym<8, 2, 5, true, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
         default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
     }
 }
