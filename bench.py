@@ -169,6 +169,10 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 for multi-process launches; the reference arm
+    # is the oracle on all of the box's host cores (set before liboracle loads OpenMP)
+    if ws > 1 or "OMP_NUM_THREADS" not in os.environ:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     from bie_inputs import make_problem
 
     p = make_problem(CONFIG_ID)
@@ -245,12 +249,18 @@ def run_gpu(args):
     from bie_inputs import density, make_problem, rhs_pipe
 
     ws, rank, local = _dist()
+    # --dist-backend gloo: a correctness run of the multi-rank flow when there are
+    # fewer GPUs than ranks (ranks share devices; never a timing run)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
@@ -318,6 +328,7 @@ def run_gpu(args):
     t_total = sum(step_ms) / 1e3
     if dist:
         tt = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        tt = tt.cpu() if args.dist_backend != "nccl" else tt
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total = tt.item()
     # N = 1: one solve; N > 1: ONE solve sharded over the ranks (strong scaling)
@@ -344,6 +355,7 @@ def run_gpu(args):
     e2e_s = sum(e2e_ms_each) / 1e3
     if dist:
         tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        tt = tt.cpu() if args.dist_backend != "nccl" else tt
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = tt.item()
 
@@ -506,6 +518,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--gmres-cap", type=int, default=2000)
     ap.add_argument("--no-config5", action="store_true", help="skip the config-5 (N = 1.06M) nvec sweep")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: check the multi-rank flow with ranks sharing a GPU (not a measurement)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
