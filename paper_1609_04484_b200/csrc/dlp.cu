@@ -753,7 +753,10 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
 }
 
 // Pairs inside one 512-node block (one-sided, all ordered pairs, self pair
-// zeroed by the rho^2 + 1e-300 rule).  One CTA per block, 128 threads x 4 targets.
+// zeroed by the rho^2 + 1e-300 rule).  Two CTAs per block (one per half of its
+// targets, 128 threads x 2 targets; all 512 sources staged): a config-4 launch
+// is 532 CTAs instead of 266 -- 3.6 instead of 1.8 CTAs per SM evens out the
+// partial last wave.  Per-target sums are unchanged (same sources, same order).
 // OP = 1: single-layer pairs (sigma = pre-scaled S, nw unused; the self pair
 // vanishes through slp_factors).
 template <int OP = 0>
@@ -761,8 +764,9 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
                                                   const double *__restrict__ sigma, double *diag, int N,
                                                   int blk0 = 0) {
     __shared__ double2 sp[3][kSymTB];
-    const int A = blk0 + blockIdx.x, tid = threadIdx.x;
+    const int A = blk0 + (blockIdx.x >> 1), half = blockIdx.x & 1, tid = threadIdx.x;
     const int base = A * kSymTB;
+    constexpr int RT = kSymTB / 256;  // targets per thread
     for (int q = tid; q < kSymTB; q += 128) {
         const int j = base + q;
         const bool ok = j < N;
@@ -771,10 +775,10 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
         sp[2][q] = ok ? reinterpret_cast<const double2 *>(sigma)[j] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    double tx[4], ty[4], ax[4], ay[4];
+    double tx[RT], ty[RT], ax[RT], ay[RT];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const double2 x = sp[0][r * 128 + tid];
+    for (int r = 0; r < RT; ++r) {
+        const double2 x = sp[0][half * 256 + r * 128 + tid];
         tx[r] = x.x;
         ty[r] = x.y;
         ax[r] = 0.0;
@@ -785,7 +789,7 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
     for (int jj = 0; jj < nsrc; ++jj) {
         const double2 xj = sp[0][jj], nj = sp[1][jj], sj = sp[2][jj];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < RT; ++r) {
             if constexpr (OP == 1) {
                 const double rx = tx[r] - xj.x;
                 const double ry = ty[r] - xj.y;
@@ -809,8 +813,8 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
         }
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int i = base + r * 128 + tid;
+    for (int r = 0; r < RT; ++r) {
+        const int i = base + half * 256 + r * 128 + tid;
         if (i < N) reinterpret_cast<double2 *>(diag)[i] = make_double2(ax[r], ay[r]);
     }
 }
@@ -1363,9 +1367,9 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
             count_launch();
         }
         if (op)
-            k_dlp_diag<1><<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+            k_dlp_diag<1><<<2 * g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
         else
-            k_dlp_diag<0><<<g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+            k_dlp_diag<0><<<2 * g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -1608,9 +1612,9 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
     }
     if (blk1 > blk0) {
         if (op)
-            k_dlp_diag<1><<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, g->slp_s, g->sym_diag, N, blk0);
+            k_dlp_diag<1><<<2 * (blk1 - blk0), 128, 0, st>>>(g->pos, g->nw, g->slp_s, g->sym_diag, N, blk0);
         else
-            k_dlp_diag<0><<<blk1 - blk0, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
+            k_dlp_diag<0><<<2 * (blk1 - blk0), 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
         count_launch();
     }
     if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
