@@ -759,12 +759,16 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
 // partial last wave.  Per-target sums are unchanged (same sources, same order).
 // OP = 1: single-layer pairs (sigma = pre-scaled S, nw unused; the self pair
 // vanishes through slp_factors).
+// split > 1 (few blocks, small N): the sources of a block are cut into `split`
+// ranges handled by separate CTAs, writing partial sums to diag + part * 2N (the
+// epilogue adds the parts in order), so small problems fill more SMs.
 template <int OP = 0>
 __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ pos, const double2 *__restrict__ nw,
                                                   const double *__restrict__ sigma, double *diag, int N,
-                                                  int blk0 = 0) {
+                                                  int blk0 = 0, int split = 1) {
     __shared__ double2 sp[3][kSymTB];
-    const int A = blk0 + (blockIdx.x >> 1), half = blockIdx.x & 1, tid = threadIdx.x;
+    const int part = blockIdx.x % split, bh = blockIdx.x / split;
+    const int A = blk0 + (bh >> 1), half = bh & 1, tid = threadIdx.x;
     const int base = A * kSymTB;
     constexpr int RT = kSymTB / 256;  // targets per thread
     for (int q = tid; q < kSymTB; q += 128) {
@@ -785,8 +789,10 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
         ay[r] = 0.0;
     }
     const int nsrc = min(kSymTB, N - base);
+    const int j0 = part * (kSymTB / split);
+    const int j1 = part == split - 1 ? nsrc : min(nsrc, (part + 1) * (kSymTB / split));
 #pragma unroll 2
-    for (int jj = 0; jj < nsrc; ++jj) {
+    for (int jj = j0; jj < j1; ++jj) {
         const double2 xj = sp[0][jj], nj = sp[1][jj], sj = sp[2][jj];
 #pragma unroll
         for (int r = 0; r < RT; ++r) {
@@ -815,7 +821,7 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
 #pragma unroll
     for (int r = 0; r < RT; ++r) {
         const int i = base + half * 256 + r * 128 + tid;
-        if (i < N) reinterpret_cast<double2 *>(diag)[i] = make_double2(ax[r], ay[r]);
+        if (i < N) reinterpret_cast<double2 *>(diag + (long long)part * 2LL * N)[i] = make_double2(ax[r], ay[r]);
     }
 }
 
@@ -852,6 +858,7 @@ struct SymEpi {
     const double *diag;        // [2N]
     const long long *off;      // [nTB + 1]
     long long Useg;            // units per segment (slot = segment - first segment of the block)
+    int dsplit;                // in-block sums come in dsplit parts [dsplit][2N]
 };
 struct EpiArgs {
     const double2 *pos, *nrm, *tan;
@@ -903,8 +910,8 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
             const int last = (int)seg_of(oB1 - 1, 0, a.sym.Useg);
             sum_strided(acc, a.sym.tgt_partial, 2LL * a.N, last - first + 1, i);
         }
-        {
-            const double2 pv = reinterpret_cast<const double2 *>(a.sym.diag)[i];
+        for (int q = 0; q < a.sym.dsplit; ++q) {
+            const double2 pv = reinterpret_cast<const double2 *>(a.sym.diag + (long long)q * 2LL * a.N)[i];
             acc.x += pv.x;
             acc.y += pv.y;
         }
@@ -1253,7 +1260,7 @@ static int sym_prepare(Geometry *g) {
         cudaMalloc(&g->sym_off, sizeof(long long) * (size_t)(nTB + 1)) != cudaSuccess ||
         cudaMalloc(&g->sym_tgt, sizeof(double) * 2 * (size_t)N * S) != cudaSuccess ||
         cudaMalloc(&g->sym_src, src_bytes) != cudaSuccess ||
-        cudaMalloc(&g->sym_diag, sizeof(double) * 2 * (size_t)N) != cudaSuccess) {
+        cudaMalloc(&g->sym_diag, sizeof(double) * 2 * (size_t)N * 4) != cudaSuccess) {
         (void)cudaGetLastError();  // clear the (non-sticky) allocation error
         return BIE_OK;
     }
@@ -1264,6 +1271,9 @@ static int sym_prepare(Geometry *g) {
     g->sym_P = P;
     g->sym_S = S;
     g->sym_Useg = Useg;
+    // in-block pairs: split each block's sources over up to 4 CTAs when there are
+    // too few blocks to fill the SMs (2 CTAs per block before splitting)
+    g->sym_dsplit = (int)std::max<long long>(1, std::min<long long>(4, (2LL * g->num_sms + 2LL * nTB - 1) / (2LL * nTB)));
     g->sym_state = 1;
     return BIE_OK;
 }
@@ -1367,13 +1377,15 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
             count_launch();
         }
         if (op)
-            k_dlp_diag<1><<<2 * g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+            k_dlp_diag<1><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, 0,
+                                                                         g->sym_dsplit);
         else
-            k_dlp_diag<0><<<2 * g->sym_nTB, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N);
+            k_dlp_diag<0><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, 0,
+                                                                         g->sym_dsplit);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
-        ea.sym = SymEpi{1, g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, g->sym_Useg};
+        ea.sym = SymEpi{1, g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, g->sym_Useg, g->sym_dsplit};
     }
     // decompose nvec into variant chunks (16, 8, 4, 2, 1)
     int v = sym ? nvec : 0;
@@ -1518,7 +1530,7 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
 __global__ void __launch_bounds__(256) k_sym_gather(const double *__restrict__ tgt, const double *__restrict__ src,
                                                     const double *__restrict__ diag, const long long *__restrict__ off,
                                                     int N, long long ub, long long U, long long Useg, int blk0,
-                                                    int blk1, double *out) {
+                                                    int blk1, double *out, int dsplit) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int B = i / kSymTB;
@@ -1533,9 +1545,11 @@ __global__ void __launch_bounds__(256) k_sym_gather(const double *__restrict__ t
         }
     }
     if (B >= blk0 && B < blk1) {
-        const double2 pv = reinterpret_cast<const double2 *>(diag)[i];
-        acc.x += pv.x;
-        acc.y += pv.y;
+        for (int q = 0; q < dsplit; ++q) {
+            const double2 pv = reinterpret_cast<const double2 *>(diag + (long long)q * 2LL * N)[i];
+            acc.x += pv.x;
+            acc.y += pv.y;
+        }
     }
     const int c = i / kSymChunk;
     for (int A = 0; A < B; ++A) {
@@ -1612,14 +1626,16 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
     }
     if (blk1 > blk0) {
         if (op)
-            k_dlp_diag<1><<<2 * (blk1 - blk0), 128, 0, st>>>(g->pos, g->nw, g->slp_s, g->sym_diag, N, blk0);
+            k_dlp_diag<1><<<2 * (blk1 - blk0) * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, g->slp_s, g->sym_diag, N,
+                                                                            blk0, g->sym_dsplit);
         else
-            k_dlp_diag<0><<<2 * (blk1 - blk0), 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0);
+            k_dlp_diag<0><<<2 * (blk1 - blk0) * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, blk0,
+                                                                            g->sym_dsplit);
         count_launch();
     }
     if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
     k_sym_gather<<<(N + 255) / 256, 256, 0, st>>>(g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, N, ub, U, Useg,
-                                                  blk0, blk1, out_full);
+                                                  blk0, blk1, out_full, g->sym_dsplit);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));

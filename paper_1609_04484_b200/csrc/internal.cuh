@@ -90,6 +90,7 @@ struct Geometry {
     unsigned long long *sym_counter = nullptr;  // dynamic segment counter of the symmetric kernel
     unsigned long long *pair_counter = nullptr; // [8] counters of the one-sided launches of one apply
     long long sym_Useg = 1;                     // units per segment
+    int sym_dsplit = 1;                         // source split of the in-block kernel (small N)
     long long sym_U = 0;
     GmresWork gm;               // bie_gmres_solve* workspace
     GmresWork gmb;              // bie_gmres_solve_batch* workspace (w holds Win | Wt | Wout)
