@@ -1,9 +1,16 @@
-// dlp.cu -- the completed double-layer matvec (A2-A5 of SURVEY.md s8(a)).
+// dlp.cu -- the completed double-layer matvec (A2-A5 of SURVEY.md s8(a)) and
+// the paper's single-layer operator with the Kapur-Rokhlin correction (NEXT-1).
 //
 //   k_moments   (A2)  per-pore lambda_k, mu_k and the wall scalar nu     O(N)
-//   k_dlp_pairs (A3)  all-pairs FP64 trapezoid DLP sum                   O(N^2)  <- hot
-//   k_epilogue  (A4+A5) split reduction, -1/2 sigma, self term, N0,
-//                       Stokeslet/rotlet completion                      O(N M)
+//   k_dlp_sym   (A3)  symmetric all-pairs sum, nvec = 1 (each unordered
+//                     pair once, dynamic segments)                       O(N^2)  <- hot
+//   k_dlp_diag  (A3)  pairs inside a 512-node block (one-sided)         O(512 N)
+//   k_dlp_pairs (A3)  one-sided all-pairs sum: nvec > 1, row ranges,
+//                     field targets                                      O(N^2)
+//   k_epilogue  (A4+A5) fixed-order partial sums, -1/2 sigma, self term, N0,
+//                       Stokeslet/rotlet completion (SLP: KR correction) O(N M)
+// Every pair kernel takes OP = 0 (completed DLP) or OP = 1 (SLP); all sums are
+// in a fixed order, so results are bitwise repeatable.
 //
 // Operator (P:l.243-248 with trapezoid weights P:l.310-319; readings C3-C5):
 //   y_i = -1/2 s_i + sum_{j != i} (r.nw_j)(r.s_j) r / rho^4 + selfc_i (t_i.s_i) t_i

@@ -11,6 +11,10 @@
 //   k_reduce    : h[j] = sum_chunk partial[chunk][j]
 //   k_multiaxpy : w -= V[0..k]^T h   (or x = V^T y)                     (reads V once)
 //   k_givens    : Hessenberg column update + new rotation on one thread
+// The host reads each iteration's estimate 3 iterations behind the enqueue
+// front (speculative iterations touch only entries the finish never reads), and
+// the workspace is cached on the geometry (no allocation per solve).  The same
+// driver serves the SLP system (kOpSLP) and batched multi-RHS solves.
 #include <cuda_runtime.h>
 
 #include <algorithm>
