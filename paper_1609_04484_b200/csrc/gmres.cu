@@ -189,6 +189,134 @@ __global__ void k_sqrt_n(const double *in, double *out, int n) {
     if (i < n) out[i] = sqrt(in[i]);
 }
 
+// ---------------------------------------------------------------------------
+// Batched (multi-RHS) forms of the vector kernels: blockIdx.z = active slot q,
+// system r = act[q].  System r's basis is V + r * sysV, its small state (cs, sn,
+// g, h, h2, scal) at small + r * smallper; slot q's work vector at W + q * n.
+// Per system the arithmetic and the reduction order are those of the single-
+// system kernels, so results are bitwise identical to looping over systems.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDotThreads) k_multidot_b(const double *__restrict__ V, long long sysV, long long ldv,
+                                                            int nv, const double *__restrict__ W, long long n,
+                                                            double *partial, int ldp, long long psys,
+                                                            const int *__restrict__ act, int self) {
+    __shared__ double ws[kChunk];
+    const int qs = blockIdx.z;
+    const double *w = W + (long long)qs * n;
+    const double *Vb = self ? w : V + (long long)act[qs] * sysV;  // self: the norm of w itself
+    const long long e0 = (long long)blockIdx.x * kChunk;
+    const int len = (int)std::min<long long>(kChunk, n - e0);
+    for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int j = blockIdx.y * (kDotThreads / 32) + wid;
+    if (j >= nv) return;
+    const double *vj = Vb + (long long)j * ldv + e0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    int q = lane;
+    for (; q + 96 < len; q += 128) {
+        const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64), a3 = __ldcs(vj + q + 96);
+        acc0 = fma(a0, ws[q], acc0);
+        acc1 = fma(a1, ws[q + 32], acc1);
+        acc2 = fma(a2, ws[q + 64], acc2);
+        acc3 = fma(a3, ws[q + 96], acc3);
+    }
+    for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
+    double acc = (acc0 + acc1) + (acc2 + acc3);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) partial[(long long)qs * psys + (long long)blockIdx.x * ldp + j] = acc;
+}
+
+// small[act[q]] + off [j] = sum_c partial_q[c][j] (fixed order); sqrt_out: then
+// the square root (norms)
+__global__ void k_reduce_b(const double *__restrict__ partial, int ldp, long long psys, int nchunks, int nv,
+                           double *small, long long smallper, long long off, const int *__restrict__ act,
+                           int sqrt_out) {
+    const int q = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nv) return;
+    const double *pq = partial + (long long)q * psys;
+    double t = 0.0;
+    for (int c = 0; c < nchunks; ++c) t += pq[(long long)c * ldp + j];
+    small[(long long)act[q] * smallper + off + j] = sqrt_out ? sqrt(t) : t;
+}
+
+// W_q[e] = beta * W_q[e] + alpha * sum_j V_r[j][e] * c_r[j]
+__global__ void __launch_bounds__(256) k_multiaxpy_b(const double *__restrict__ V, long long sysV, long long ldv,
+                                                     int nv, const double *small, long long smallper, long long coff,
+                                                     double alpha, double beta, double *W, long long n,
+                                                     const int *__restrict__ act) {
+    extern __shared__ double cs[];
+    const int qs = blockIdx.y, r = act[qs];
+    const double *c = small + (long long)r * smallper + coff;
+    for (int q = threadIdx.x; q < nv; q += blockDim.x) cs[q] = c[q];
+    __syncthreads();
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const double *Vb = V + (long long)r * sysV;
+    double acc = 0.0;
+    int j = 0;
+    for (; j + 4 <= nv; j += 4) {
+        const double a0 = Vb[(long long)j * ldv + e], a1 = Vb[(long long)(j + 1) * ldv + e];
+        const double a2 = Vb[(long long)(j + 2) * ldv + e], a3 = Vb[(long long)(j + 3) * ldv + e];
+        acc = fma(a0, cs[j], acc);
+        acc = fma(a1, cs[j + 1], acc);
+        acc = fma(a2, cs[j + 2], acc);
+        acc = fma(a3, cs[j + 3], acc);
+    }
+    for (; j < nv; ++j) acc = fma(Vb[(long long)j * ldv + e], cs[j], acc);
+    double *y = W + (long long)qs * n;
+    y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
+}
+
+// one thread per active slot: the Givens update of system act[q]; estimate and
+// breakdown flag also to est[2 q], est[2 q + 1] for one D2H copy
+__global__ void k_givens_b(double *Hbase, long long Hsys, double *small, long long smallper, int ldh, int k,
+                           const int *__restrict__ act, int na, double *est) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= na) return;
+    const int r = act[q];
+    double *b = small + (long long)r * smallper;
+    GmState s{Hbase + (long long)r * Hsys, b, b + ldh, b + 2 * ldh, b + 3 * ldh, b + 4 * ldh, b + 5 * ldh};
+    double *Hk = s.H + (long long)k * ldh;
+    for (int j = 0; j <= k; ++j) Hk[j] = s.h[j] + s.h2[j];
+    const double hk1 = s.scal[2];
+    Hk[k + 1] = hk1;
+    for (int j = 0; j < k; ++j) {
+        const double a = Hk[j], bb = Hk[j + 1];
+        Hk[j] = s.cs[j] * a + s.sn[j] * bb;
+        Hk[j + 1] = -s.sn[j] * a + s.cs[j] * bb;
+    }
+    const double a = Hk[k], bb = Hk[k + 1];
+    const double d = hypot(a, bb);
+    s.cs[k] = a / d;
+    s.sn[k] = bb / d;
+    Hk[k] = d;
+    Hk[k + 1] = 0.0;
+    s.g[k + 1] = -s.sn[k] * s.g[k];
+    s.g[k] = s.cs[k] * s.g[k];
+    s.scal[3] = fabs(s.g[k + 1]) / s.scal[0];
+    s.scal[4] = (hk1 <= 1e-14 * s.scal[1]) ? 1.0 : 0.0;
+    est[2 * q] = s.scal[3];
+    est[2 * q + 1] = s.scal[4];
+}
+
+// V_r[k + 1] = W_q / scal_r[2]  (blockIdx.y = slot; scal at small + r * smallper + scal_off)
+__global__ void k_scale_b(const double *W, long long n, double *V, long long sysV, long long koff,
+                          const double *small, long long smallper, long long scal_off, const int *__restrict__ act) {
+    const int qs = blockIdx.y, r = act[qs];
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) V[(long long)r * sysV + koff + e] = W[(long long)qs * n + e] / small[(long long)r * smallper + scal_off + 2];
+}
+
+// Win_q = V_r[k]  (blockIdx.y = slot)
+__global__ void k_gather_b(const double *V, long long sysV, long long koff, double *W, long long n,
+                           const int *__restrict__ act) {
+    const int qs = blockIdx.y;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) W[(long long)qs * n + e] = V[(long long)act[qs] * sysV + koff + e];
+}
+
 }  // namespace bie
 
 using namespace bie;
@@ -583,11 +711,18 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     GB_TRY(ensure(ws.w, ws.n_cap, 3 * (size_t)nrhs * n));
     GB_TRY(ensure(ws.H, ws.H_cap, (size_t)nrhs * ldh * max_iter));
     GB_TRY(ensure(ws.small, ws.small_cap, (size_t)nrhs * smallper));
-    GB_TRY(ensure(ws.partial, ws.partial_cap, (size_t)d.nchunks * ldh));
-    if (!ws.pinned) GB_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * 64 * 8));  // nrhs <= 64
+    // partials of all active systems + est[2][64] + act[64] (as ints)
+    const long long psys = (long long)d.nchunks * ldh;
+    GB_TRY(ensure(ws.partial, ws.partial_cap, (size_t)(nrhs * psys + 256)));
+    if (!ws.pinned) GB_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * 1024));  // 64 x 8 + est + act
     double *V = ws.V, *Win = ws.w, *Wt = ws.w + (size_t)nrhs * n, *Wout = ws.w + 2 * (size_t)nrhs * n;
     double *H = ws.H, *small = ws.small, *pinned = ws.pinned;
     d.partial = ws.partial;
+    double *d_est = ws.partial + nrhs * psys;
+    int *d_act = reinterpret_cast<int *>(d_est + 128);
+    double *h_est = pinned + 512;
+    int *h_act = reinterpret_cast<int *>(pinned + 640);
+    const long long sysV = (long long)ldh * n, Hsys = (long long)ldh * max_iter, scal_off = 5LL * ldh;
     GB_TRY(cudaMemsetAsync(H, 0, sizeof(double) * (size_t)nrhs * ldh * max_iter, st));
     GB_TRY(cudaMemsetAsync(small, 0, sizeof(double) * (size_t)nrhs * smallper, st));
     std::vector<GmState> S(nrhs);
@@ -633,36 +768,54 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
         count_launch();
         GB_TRY(cudaMemcpyAsync(S[r].g, S[r].scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
+    // Iteration: every vector operation of all active systems in one batched
+    // launch (blockIdx.z / y = slot), one D2H of the estimates, one sync.
+    const unsigned dot_y = (unsigned)((ldh + kDotThreads / 32 - 1) / (kDotThreads / 32));
     for (int k = 0; k < max_iter && !active.empty(); ++k) {
         const int na = (int)active.size();
-        for (int q = 0; q < na; ++q)
-            GB_TRY(cudaMemcpyAsync(Win + q * n, Vr(active[q], k), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        for (int q = 0; q < na; ++q) h_act[q] = active[q];
+        GB_TRY(cudaMemcpyAsync(d_act, h_act, sizeof(int) * na, cudaMemcpyHostToDevice, st));
+        k_gather_b<<<dim3(eb, na), 256, 0, st>>>(V, sysV, (long long)k * n, Win, n, d_act);
+        count_launch();
         GB_RC(batched_op(g, bd, Win, Wt, Wout, na, st, opf));
-        for (int q = 0; q < na; ++q) {
-            const int r = active[q];
-            GmState &s = S[r];
-            double *w = Wout + q * n;
-            double *Vb = Vr(r, 0);
-            GB_RC(norm_to(w, s.scal + 5, s.scal + 1));
-            GB_RC(multidot(Vb, n, k + 1, w, n, d, s.h, st));
-            GB_RC(multiaxpy(Vb, n, k + 1, s.h, -1.0, 1.0, w, n, st));
-            GB_RC(multidot(Vb, n, k + 1, w, n, d, s.h2, st));
-            GB_RC(multiaxpy(Vb, n, k + 1, s.h2, -1.0, 1.0, w, n, st));
-            GB_RC(norm_to(w, s.scal + 5, s.scal + 2));
-            k_givens<<<1, 1, 0, st>>>(s, k, ldh);
-            count_launch();
-            GB_TRY(cudaMemcpyAsync(pinned + 8 * r + 3, s.scal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-            if (k + 1 < max_iter) {
-                k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, Vr(r, k + 1), n);
-                count_launch();
-            }
+        const int nv = k + 1;
+        const unsigned gy = (unsigned)((nv + kDotThreads / 32 - 1) / (kDotThreads / 32));
+        (void)dot_y;
+        // w0 = ||w||
+        k_multidot_b<<<dim3(d.nchunks, 1, na), kDotThreads, 0, st>>>(nullptr, 0, 0, 1, Wout, n, d.partial, d.ldp,
+                                                                      psys, d_act, 1);
+        k_reduce_b<<<dim3(1, na), 128, 0, st>>>(d.partial, d.ldp, psys, d.nchunks, 1, small, smallper, scal_off + 1,
+                                                d_act, 1);
+        // CGS2: two passes h = V^T w, w -= V h
+        for (int pass = 0; pass < 2; ++pass) {
+            const long long hoff = (3LL + pass) * ldh;
+            k_multidot_b<<<dim3(d.nchunks, gy, na), kDotThreads, 0, st>>>(V, sysV, n, nv, Wout, n, d.partial, d.ldp,
+                                                                           psys, d_act, 0);
+            k_reduce_b<<<dim3((nv + 127) / 128, na), 128, 0, st>>>(d.partial, d.ldp, psys, d.nchunks, nv, small,
+                                                                   smallper, hoff, d_act, 0);
+            k_multiaxpy_b<<<dim3(eb, na), 256, sizeof(double) * nv, st>>>(V, sysV, n, nv, small, smallper, hoff, -1.0,
+                                                                          1.0, Wout, n, d_act);
         }
+        // hk1 = ||w||
+        k_multidot_b<<<dim3(d.nchunks, 1, na), kDotThreads, 0, st>>>(nullptr, 0, 0, 1, Wout, n, d.partial, d.ldp,
+                                                                      psys, d_act, 1);
+        k_reduce_b<<<dim3(1, na), 128, 0, st>>>(d.partial, d.ldp, psys, d.nchunks, 1, small, smallper, scal_off + 2,
+                                                d_act, 1);
+        k_givens_b<<<(na + 63) / 64, 64, 0, st>>>(H, Hsys, small, smallper, ldh, k, d_act, na, d_est);
+        count_launch(11);
+        GB_TRY(cudaMemcpyAsync(h_est, d_est, sizeof(double) * 2 * na, cudaMemcpyDeviceToHost, st));
+        if (k + 1 < max_iter) {
+            k_scale_b<<<dim3(eb, na), 256, 0, st>>>(Wout, n, V, sysV, (long long)(k + 1) * n, small, smallper,
+                                                     scal_off, d_act);
+            count_launch();
+        }
+        GB_TRY(cudaGetLastError());
         GB_TRY(cudaStreamSynchronize(st));
         std::vector<int> next;
         for (int q = 0; q < na; ++q) {
             const int r = active[q];
-            const double est = pinned[8 * r + 3];
-            const bool brk = pinned[8 * r + 4] != 0.0;
+            const double est = h_est[2 * q];
+            const bool brk = h_est[2 * q + 1] != 0.0;
             hist_host[(size_t)r * ldh + k + 1] = est;
             it[r] = k + 1;
             if (est < tol || brk)
