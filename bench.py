@@ -42,11 +42,10 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 
-def _ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+def _ncu_traffic(key="traffic_bytes_per_launch"):
+    """DRAM bytes per launch (or another field) of the dominant kernel from the committed ncu capture."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "round1", "k_dlp_sym_traffic.json")))[
-            "traffic_bytes_per_launch"]
+        return json.load(open(os.path.join(ROOT, "profiles", "round1", "k_dlp_sym_traffic.json")))[key]
     except Exception:
         return None
 
@@ -489,6 +488,7 @@ def run_gpu(args):
                      "traffic": _ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
                      "kernel_share_of_step": pairs_share,
                      "executed_flop_per_pair": 17,
+                     "ncu_fp64_pipe_active_pct": _ncu_traffic("fp64_pipe_active_pct"),
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
         "e2e": {"value": args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
                 "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8),
