@@ -167,6 +167,13 @@ struct Dot {
 // out[0..nv) = V[0..nv)^T w (deterministic)
 static int multidot(const double *V, long long ldv, int nv, const double *w, long long n, Dot &d, double *out,
                     cudaStream_t st) {
+    if (d.nchunks == 1) {  // one chunk (2N <= 4096): the partial IS the result, no reduction launch
+        k_multidot<<<dim3(1, (nv + kDotThreads / 32 - 1) / (kDotThreads / 32)), kDotThreads, 0, st>>>(
+            V, ldv, nv, w, n, out, 0);
+        count_launch();
+        BIE_CUDA_TRY(cudaGetLastError());
+        return BIE_OK;
+    }
     k_multidot<<<dim3(d.nchunks, (nv + kDotThreads / 32 - 1) / (kDotThreads / 32)), kDotThreads, 0, st>>>(
         V, ldv, nv, w, n, d.partial, d.ldp);
     k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, out, 0);
