@@ -1105,7 +1105,8 @@ static void make_sched(const Geometry *g, int vi, int Nt, PairSched &s, int op =
     s.P = (int)std::min<long long>(Pmax, s.U);
     // max slots per target block: ceil(P / nTB) + 1 bounds it; compute exactly
     // ~16 segments per CTA: tail <= one segment, few slots per target block
-    s.Useg = std::max<long long>(4, (s.U + 16LL * s.P - 1) / (16LL * s.P));
+    s.Useg = std::max<long long>(std::max<long long>(1, std::min<long long>(4, s.U / s.P)),
+                                 (s.U + 16LL * s.P - 1) / (16LL * s.P));
     int S = 1;
     for (int tb = 0; tb < s.nTB; ++tb) {
         const long long f = seg_of((long long)tb * s.nTS, 0, s.Useg);
@@ -1221,8 +1222,13 @@ static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
 
 // Segment size of the dynamic work distribution: about 24 segments per CTA
 // (tail <= one segment), at least 8 units so a segment amortises its start.
+// Below 8 units per CTA (small N), smaller segments so every CTA gets work
+// (config 2: 92 -> 44 us per matvec); measured at config 3, segments under 8
+// units cost more in per-segment start-up than they save in tail.
 static long long sym_useg(long long U, int P) {
-    return std::max<long long>(8, (U + 24LL * P - 1) / (24LL * P));
+    long long lo = std::max<long long>(1, std::min<long long>(8, U / P));
+    if (const char *e = getenv("BIE_SYM_USEG_MIN")) lo = std::max(1, atoi(e));  // tuning knob
+    return std::max<long long>(lo, (U + 24LL * P - 1) / (24LL * P));
 }
 
 // Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only).
