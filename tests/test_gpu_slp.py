@@ -317,3 +317,14 @@ def test_slp_one_sided_sampled_config3(bie):
     rows = _rows(p, 512)
     ref = og.slp_apply(s[0], rows=rows).reshape(-1, 2)
     assert np.abs(y[rows] - ref).max() / np.abs(ref).max() <= TOL
+
+
+def test_slp_matvec_config5_sampled_rows(bie):
+    """Config 5 (N = 1.06M), the symmetric SLP path, 128 strided rows vs the oracle."""
+    p = make_problem(5)
+    g, og = _setup(bie, p)
+    s = density(p, nvec=1)
+    y = _gpu_slp(bie, g, s, 1)[0].reshape(-1, 2)
+    rows = _rows(p, 128)
+    ref = og.slp_apply(s[0], rows=rows).reshape(-1, 2)
+    assert np.abs(y[rows] - ref).max() / np.abs(ref).max() <= TOL

@@ -199,3 +199,17 @@ def test_S7_slp_gmres_matches_dense_gmres():
     # large; compare at rounding level of |B^-1| |A|
     scale = n2 * np.abs(Pinv).max() * np.abs(A).max() * 1e-15
     assert np.abs(Pinv @ A[:, :4] - np.stack([bd.apply(c) for c in A[:, :4].T], 1)).max() <= scale
+
+
+def test_S8_kernel_symmetry_of_the_assembled_blocks():
+    """G(x, y) = G(y, x) and the KR weights depend only on |offset| (C25): on a
+    circle with equal arclength weights, B[i, j] = B[j, i]^T as 2x2 blocks (an
+    index, transpose or weight mix-up breaks it)."""
+    p = make_circle_problem(n_outer=48, R=0.9, pores=())
+    g = oracle.OracleGeometry(p)
+    B = g.slp_block(0)
+    n = g.N
+    Bb = B.reshape(n, 2, n, 2)
+    for i in range(0, n, 5):
+        for j in range(n):
+            assert np.abs(Bb[i, :, j, :] - Bb[j, :, i, :].T).max() <= 1e-15 * np.abs(B).max()
