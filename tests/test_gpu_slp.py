@@ -328,3 +328,21 @@ def test_slp_matvec_config5_sampled_rows(bie):
     rows = _rows(p, 128)
     ref = og.slp_apply(s[0], rows=rows).reshape(-1, 2)
     assert np.abs(y[rows] - ref).max() / np.abs(ref).max() <= TOL
+
+
+@pytest.mark.parametrize("n_pore", [16, 18])
+def test_minimum_nodes_per_pore(bie, n_pore):
+    """Edge case: the smallest allowed pores (16 nodes, and a non-power-of-two
+    count), where the +-6 KR neighbourhoods cover most of the curve."""
+    p = make_circle_problem(n_outer=32, R=1.0, pores=((0.3, 0.1, 0.2), (-0.4, -0.2, 0.15)), n_pore=n_pore)
+    g = bie.Geometry.from_problem(p)
+    og = oracle.OracleGeometry(p)
+    s = density(p, nvec=1, vec_id=6)
+    assert _relerr(_gpu_slp(bie, g, s, 1)[0], og.slp_apply(s[0])) <= TOL
+    import torch
+
+    sig = _t(s)
+    out = torch.full_like(sig, float("nan"))
+    bie.dlp_apply(g, sig, out, 1)
+    torch.cuda.synchronize()
+    assert _relerr(out.cpu().numpy(), og.apply(s[0])) <= TOL
