@@ -90,7 +90,7 @@ __device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, do
 // d = 2^e m, m in [1, 2); k = top 6 mantissa bits; tab[k] = (rc_k, -1/2 log rc_k)
 // with rc_k = RN(1 / (1 + (k + 1/2)/64)).  r = m rc_k - 1 (one FMA, |r| < 2^-7),
 // log m = log1p(r) - log rc_k, log1p(r) = r (1 - r/2 + ... + r^6/7) (truncation
-// r^8/8 < 2^-59).  Returns hl = -1/2 log d directly (scaled coefficients): 10 FP64
+// r^8/8 < 2^-59).  Returns hl = -1/2 log d directly (scaled coefficients): 9 FP64
 // instructions instead of 18 + 1, plus one shared-memory lookup.
 struct LogTab {
     double2 e[64];
@@ -114,8 +114,9 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     q = fma(q, r, -0.5 / 3.0);
     q = fma(q, r, 0.5 / 2.0);
     q = fma(q, r, -0.5);
-    const double ed = (double)e;
-    const double base = fma(ed, -0.5 * 0.69314718055994528623, fma(ed, -0.5 * 2.3190468138462996e-17, tk.y));
+    // e ln2 with ln2 rounded to double: the error |e| 2.3e-17 stays below half an
+    // ulp of e ln2 itself for every exponent a pair distance can have
+    const double base = fma((double)e, -0.5 * 0.69314718055994528623, tk.y);
     return fma(r, q, base);
 }
 
