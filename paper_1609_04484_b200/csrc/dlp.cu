@@ -77,14 +77,6 @@ __device__ __forceinline__ double log_pair(double d) {
     return fma((double)e, 0.69314718055994530942, lm);
 }
 
-__device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, double &inv) {
-    double d = fma(rx, rx, ry * ry);
-    d = d == 0.0 ? 1.0 : d;
-    double i = rcp_approx(d);
-    const double e = fma(-d, i, 1.0);
-    inv = fma(i, fma(e, e, e), i);
-    hl = -0.5 * log_pair(d);
-}
 
 // Table-driven variant for the symmetric SLP kernel (Tang-style reduction):
 // d = 2^e m, m in [1, 2); k = top 6 mantissa bits; tab[k] = (rc_k, -1/2 log rc_k)
@@ -118,6 +110,15 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     // ulp of e ln2 itself for every exponent a pair distance can have
     const double base = fma((double)e, -0.5 * 0.69314718055994528623, tk.y);
     return fma(r, q, base);
+}
+
+__device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, double &inv, const LogTab &lt) {
+    double d = fma(rx, rx, ry * ry);
+    d = d == 0.0 ? 1.0 : d;
+    double i = rcp_approx(d);
+    const double e = fma(-d, i, 1.0);
+    inv = fma(i, fma(e, e, e), i);
+    hl = neg_half_log_tab(d, lt);
 }
 
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src, int src_bytes) {
@@ -178,6 +179,8 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
     const long long U = a.U, Useg = a.Useg;
     const int N = a.N, nTS = a.nTS;
     __shared__ long long s_seg;
+    __shared__ LogTab s_log;  // OP = 1 only; visible after the first segment barrier
+    if constexpr (OP == 1) log_tab_init(s_log, tid, kPairThreads);
 
     auto load_tile = [&](int buf, int ts) {
         double2 *s = smem + buf * STAGE;
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
                     const double rx = tx[r] - xj.x;
                     const double ry = ty[r] - xj.y;
                     double hl, inv;
-                    slp_factors(rx, ry, hl, inv);
+                    slp_factors(rx, ry, hl, inv, s_log);
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
                         const double c = inv * fma(rx, sj[v].x, ry * sj[v].y);
@@ -775,6 +778,8 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
                                                   const double *__restrict__ sigma, double *diag, int N,
                                                   int blk0 = 0, int split = 1) {
     __shared__ double2 sp[3][kSymTB];
+    __shared__ LogTab s_log;  // OP = 1 only; visible after the staging barrier
+    if constexpr (OP == 1) log_tab_init(s_log, threadIdx.x, 128);
     const int part = blockIdx.x % split, bh = blockIdx.x / split;
     const int A = blk0 + (bh >> 1), half = bh & 1, tid = threadIdx.x;
     const int base = A * kSymTB;
@@ -808,7 +813,7 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
                 const double rx = tx[r] - xj.x;
                 const double ry = ty[r] - xj.y;
                 double hl, inv;
-                slp_factors(rx, ry, hl, inv);
+                slp_factors(rx, ry, hl, inv, s_log);
                 const double c = inv * fma(rx, sj.x, ry * sj.y);
                 ax[r] = fma(c, rx, fma(hl, sj.x, ax[r]));
                 ay[r] = fma(c, ry, fma(hl, sj.y, ay[r]));
