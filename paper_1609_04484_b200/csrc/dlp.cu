@@ -41,49 +41,14 @@ __device__ __forceinline__ double rcp_approx(double x) {
     return r;
 }
 
-// Single-layer pair factor (NEXT-1; P:l.270-276): for r = x_i - x_j returns
-// hl = -1/2 log rho^2 and inv = 1/rho^2, so that
-//   G(x_i, x_j) (w_j sigma_j) = hl S_j + (r . S_j) inv r,   S_j = w_j sigma_j / (4 pi).
-// r = 0 (the self pair, or zero-padded slots that coincide) maps rho^2 -> 1:
-// hl = 0 and the dyadic term vanishes with r, so no branch is needed.
-// Branch-free natural log for the pair loop (d > 0 and normal; pair distances
-// are never denormal).  d = 2^e m with m in [1/sqrt2, sqrt2) by integer ops,
-// s = (m - 1)/(m + 1) (|s| <= 0.1716) by seed + cubic Newton reciprocal, and
-// log m = 2 atanh s = s (2 + z (2/3 + 2/5 z + ... + 2/19 z^8)), z = s^2:
-// truncation <= 2 s^21 / 21 < 1e-17.  The library log() carries special-case
-// branches that keep ptxas from interleaving the independent pairs.
-__device__ __forceinline__ double log_pair(double d) {
-    const int hi = __double2hiint(d), lo = __double2loint(d);
-    const int mh = hi & 0x000fffff;
-    const int big = mh >= 0x6a09e;  // mantissa >= sqrt 2: use m / 2
-    const int e = (hi >> 20) - 1023 + big;
-    const double m = __hiloint2double(mh | (big ? 0x3fe00000 : 0x3ff00000), lo);
-    const double den = m + 1.0;
-    double i = rcp_approx(den);
-    const double ee = fma(-den, i, 1.0);
-    i = fma(i, fma(ee, ee, ee), i);
-    const double s = (m - 1.0) * i;
-    const double z = s * s;
-    double p = 2.0 / 19.0;
-    p = fma(p, z, 2.0 / 17.0);
-    p = fma(p, z, 2.0 / 15.0);
-    p = fma(p, z, 2.0 / 13.0);
-    p = fma(p, z, 2.0 / 11.0);
-    p = fma(p, z, 2.0 / 9.0);
-    p = fma(p, z, 2.0 / 7.0);
-    p = fma(p, z, 2.0 / 5.0);
-    p = fma(p, z, 2.0 / 3.0);
-    const double lm = s * fma(z, p, 2.0);
-    return fma((double)e, 0.69314718055994530942, lm);
-}
-
-
-// Table-driven variant for the symmetric SLP kernel (Tang-style reduction):
-// d = 2^e m, m in [1, 2); k = top 6 mantissa bits; tab[k] = (rc_k, -1/2 log rc_k)
-// with rc_k = RN(1 / (1 + (k + 1/2)/64)).  r = m rc_k - 1 (one FMA, |r| < 2^-7),
-// log m = log1p(r) - log rc_k, log1p(r) = r (1 - r/2 + ... + r^6/7) (truncation
-// r^8/8 < 2^-59).  Returns hl = -1/2 log d directly (scaled coefficients): 9 FP64
-// instructions instead of 18 + 1, plus one shared-memory lookup.
+// Branch-free log for the pair loops (the library log() carries special-case
+// branches that keep ptxas from interleaving independent pairs): a Tang-style
+// table reduction.  d = 2^e m, m in [1, 2); k = top 6 mantissa bits;
+// tab[k] = (rc_k, 1/2 log rc_k) with rc_k = RN(1 / (1 + (k + 1/2)/64)).
+// r = m rc_k - 1 (one FMA, |r| < 2^-7), log m = log1p(r) - log rc_k with
+// log1p(r) = r (1 - r/2 + ... + r^6/7) (truncation r^8/8 < 2^-59).  Returns
+// hl = -1/2 log d directly (scaled coefficients): 9 FP64 instructions plus one
+// shared-memory lookup.  d must be positive and normal (pair distances are).
 struct LogTab {
     double2 e[64];
 };
@@ -112,6 +77,11 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     return fma(r, q, base);
 }
 
+// Single-layer pair factor (NEXT-1; P:l.270-276): for r = x_i - x_j returns
+// hl = -1/2 log rho^2 and inv = 1/rho^2, so that
+//   G(x_i, x_j) (w_j sigma_j) = hl S_j + (r . S_j) inv r,   S_j = w_j sigma_j / (4 pi).
+// r = 0 (the self pair, or zero-padded slots that coincide) maps rho^2 -> 1:
+// hl = 0 and the dyadic term vanishes with r, so no branch is needed.
 __device__ __forceinline__ void slp_factors(double rx, double ry, double &hl, double &inv, const LogTab &lt) {
     double d = fma(rx, rx, ry * ry);
     d = d == 0.0 ? 1.0 : d;
@@ -1049,12 +1019,15 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         u[0].x += c0.x + c1.x;
         u[0].y += c0.y + c1.y;
     } else if (full) {
+        __shared__ LogTab s_log2;
+        log_tab_init(s_log2, threadIdx.x, blockDim.x);
+        __syncthreads();
         for (int k = 0; k < a.M; ++k) {
             const double4 pk = a.pore[k];
             const double rx = xi.x - pk.x, ry = xi.y - pk.y;
             const double rho2 = rx * rx + ry * ry;
             const double ir = 1.0 / rho2;
-            const double lg = 0.5 * log_pair(rho2);
+            const double lg = -neg_half_log_tab(rho2, s_log2);  // log rho
             const double rk = pk.z * ir;
             for (int v = 0; v < nvec; ++v) {
                 const double *m = a.moments + ((long long)v * a.M + k) * 3;
@@ -1516,6 +1489,8 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
         u.y += pv.y;
     }
     constexpr double k4pi = 1.0 / (4.0 * kPi);
+    __shared__ LogTab s_log;  // visible after the first tile barrier
+    log_tab_init(s_log, threadIdx.x, blockDim.x);
     for (int k0 = 0; k0 < M; k0 += 128) {
         const int nk = min(128, M - k0);
         __syncthreads();
@@ -1530,7 +1505,7 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
             const double rx = xi.x - pk.x, ry = xi.y - pk.y;
             const double rho2 = fma(rx, rx, ry * ry);
             const double ir = 1.0 / rho2;
-            const double lg = 0.5 * log_pair(rho2);
+            const double lg = -neg_half_log_tab(rho2, s_log);  // log rho
             const double rk = pk.z * ir;
             const double rl = (rx * pm.x + ry * pm.y) * ir;
             u.x += k4pi * (-lg * pm.x + rx * rl) + rk * ry * pm.z;
