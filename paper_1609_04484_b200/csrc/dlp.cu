@@ -47,20 +47,24 @@ __device__ __forceinline__ double rcp_approx(double x) {
 // tab[k] = (rc_k, 1/2 log rc_k) with rc_k = RN(1 / (1 + (k + 1/2)/64)).
 // r = m rc_k - 1 (one FMA, |r| < 2^-7), log m = log1p(r) - log rc_k with
 // log1p(r) = r (1 - r/2 + ... + r^6/7) (truncation r^8/8 < 2^-59).  Returns
-// hl = -1/2 log d directly (scaled coefficients): 9 FP64 instructions plus one
-// shared-memory lookup.  d must be positive and normal (pair distances are).
+// hl = -1/2 log d directly (scaled coefficients).  The unbiased exponent e comes
+// as a double from a second table indexed by the biased exponent bits (an LDS
+// instead of an I2F.F64 on the FP64 pipe): 9 FP64 instructions plus two
+// shared-memory lookups.  d must be positive and
+// normal (pair distances are).
 struct LogTab {
     double2 e[64];
+    double ex[2048];  // b - 1023 for biased exponent b (16 KiB)
 };
 __device__ __forceinline__ void log_tab_init(LogTab &t, int tid, int nthreads) {
     for (int k = tid; k < 64; k += nthreads) {
         const double rc = 1.0 / (1.0 + (k + 0.5) / 64.0);
         t.e[k] = make_double2(rc, 0.5 * log(rc));  // -1/2 log(1/rc) = 1/2 log rc
     }
+    for (int k = tid; k < 2048; k += nthreads) t.ex[k] = (double)(k - 1023);
 }
 __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     const int hi = __double2hiint(d), lo = __double2loint(d);
-    const int e = (hi >> 20) - 1023;
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double2 tk = t.e[(hi >> 14) & 63];
     const double r = fma(m, tk.x, -1.0);
@@ -73,7 +77,7 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     q = fma(q, r, -0.5);
     // e ln2 with ln2 rounded to double: the error |e| 2.3e-17 stays below half an
     // ulp of e ln2 itself for every exponent a pair distance can have
-    const double base = fma((double)e, -0.5 * 0.69314718055994528623, tk.y);
+    const double base = fma(t.ex[(hi >> 20) & 2047], -0.5 * 0.69314718055994528623, tk.y);
     return fma(r, q, base);
 }
 
@@ -396,8 +400,9 @@ __device__ __forceinline__ void slp_pairpair(double tx, double ty, double tsx, d
                                              double ssx, double ssy, double &ax, double &ay, double &bx,
                                              double &by, const LogTab &lt) {
     const double rx = tx - sx, ry = ty - sy;
-    double d = fma(rx, rx, ry * ry);
-    d = d == 0.0 ? 1.0 : d;  // zero padding only (no self pairs here): hl = 0, r = 0
+    // no self pairs here; coincident zero padding gets d = 1e-300 (finite hl and
+    // 1/rho^2, multiplied by a zero density and r = 0)
+    const double d = fma(rx, rx, fma(ry, ry, 1e-300));
     double i = rcp_approx(d);
     const double ee = fma(-d, i, 1.0);
     i = fma(i, fma(ee, ee, ee), i);
@@ -626,9 +631,9 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
                     const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
                     double hl0, hl1, i0, i1;
                     {
-                        double d0 = fma(rx0, rx0, ry0 * ry0), d1 = fma(rx1, rx1, ry1 * ry1);
-                        d0 = d0 == 0.0 ? 1.0 : d0;
-                        d1 = d1 == 0.0 ? 1.0 : d1;
+                        // zero padding only (no self pairs here): see slp_pairpair
+                        const double d0 = fma(rx0, rx0, fma(ry0, ry0, 1e-300));
+                        const double d1 = fma(rx1, rx1, fma(ry1, ry1, 1e-300));
                         i0 = rcp_approx(d0);
                         i1 = rcp_approx(d1);
                         const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
