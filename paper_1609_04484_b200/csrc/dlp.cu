@@ -47,23 +47,31 @@ __device__ __forceinline__ double rcp_approx(double x) {
 // tab[k] = (rc_k, 1/2 log rc_k) with rc_k = RN(1 / (1 + (k + 1/2)/64)).
 // r = m rc_k - 1 (one FMA, |r| < 2^-7), log m = log1p(r) - log rc_k with
 // log1p(r) = r (1 - r/2 + ... + r^6/7) (truncation r^8/8 < 2^-59).  Returns
-// hl = -1/2 log d directly (scaled coefficients).  The unbiased exponent e comes
-// as a double from a second table indexed by the biased exponent bits (an LDS
-// instead of an I2F.F64 on the FP64 pipe): 9 FP64 instructions plus two
-// shared-memory lookups.  d must be positive and
-// normal (pair distances are).
-struct LogTab {
+// hl = -1/2 log d directly (scaled coefficients): 9 FP64 instructions, one
+// shared-memory lookup and an I2F.F64 for the exponent.  With EX the exponent
+// comes as a double from a second table indexed by the biased exponent bits (an
+// LDS instead of the I2F, which occupies the FP64 pipe; 16 KiB more shared
+// memory, worth it in the symmetric SLP kernel: 20.4 -> 19.8 ms at config 4, but
+// not in the one-sided kernels, where it costs occupancy).  Both forms give
+// bit-identical results.  d must be positive and normal (pair distances are).
+template <bool EX>
+struct LogTabT {
     double2 e[64];
-    double ex[2048];  // b - 1023 for biased exponent b (16 KiB)
+    double ex[EX ? 2048 : 1];  // b - 1023 for biased exponent b
 };
-__device__ __forceinline__ void log_tab_init(LogTab &t, int tid, int nthreads) {
+using LogTab = LogTabT<false>;
+using LogTabX = LogTabT<true>;
+template <bool EX>
+__device__ __forceinline__ void log_tab_init(LogTabT<EX> &t, int tid, int nthreads) {
     for (int k = tid; k < 64; k += nthreads) {
         const double rc = 1.0 / (1.0 + (k + 0.5) / 64.0);
         t.e[k] = make_double2(rc, 0.5 * log(rc));  // -1/2 log(1/rc) = 1/2 log rc
     }
-    for (int k = tid; k < 2048; k += nthreads) t.ex[k] = (double)(k - 1023);
+    if constexpr (EX)
+        for (int k = tid; k < 2048; k += nthreads) t.ex[k] = (double)(k - 1023);
 }
-__device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
+template <bool EX>
+__device__ __forceinline__ double neg_half_log_tab(double d, const LogTabT<EX> &t) {
     const int hi = __double2hiint(d), lo = __double2loint(d);
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double2 tk = t.e[(hi >> 14) & 63];
@@ -77,7 +85,8 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTab &t) {
     q = fma(q, r, -0.5);
     // e ln2 with ln2 rounded to double: the error |e| 2.3e-17 stays below half an
     // ulp of e ln2 itself for every exponent a pair distance can have
-    const double base = fma(t.ex[(hi >> 20) & 2047], -0.5 * 0.69314718055994528623, tk.y);
+    const double e = EX ? t.ex[(hi >> 20) & 2047] : (double)((hi >> 20) - 1023);
+    const double base = fma(e, -0.5 * 0.69314718055994528623, tk.y);
     return fma(r, q, base);
 }
 
@@ -398,7 +407,7 @@ __device__ __forceinline__ void dlp_pairpair(double tx, double ty, double tqa, d
 
 __device__ __forceinline__ void slp_pairpair(double tx, double ty, double tsx, double tsy, double sx, double sy,
                                              double ssx, double ssy, double &ax, double &ay, double &bx,
-                                             double &by, const LogTab &lt) {
+                                             double &by, const LogTabX &lt) {
     const double rx = tx - sx, ry = ty - sy;
     // no self pairs here; coincident zero padding gets d = 1e-300 (finite hl and
     // 1/rho^2, multiplied by a zero density and r = 0)
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     static_assert(SR % 2 == 0, "two interleaved chains");
     __shared__ double2 red[SW][32];
     __shared__ __align__(16) double2 s_src[2][SW][3][32];  // [buf][warp][(x,y) | (qa,qb) | (qc,-)][lane]
-    __shared__ LogTab s_log;  // OP = 1 only
+    __shared__ LogTabT<OP == 1> s_log;  // OP = 1 only
     if constexpr (OP == 1) log_tab_init(s_log, threadIdx.x, 32 * SW);  // visible after the first segment barrier
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int p = blockIdx.x;
