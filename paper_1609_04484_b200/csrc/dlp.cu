@@ -826,13 +826,16 @@ __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ po
 // the loads issued 8 at a time (the adds stay sequential, so the order and the
 // result are unchanged; the loop was latency-bound on one load per add).
 __device__ __forceinline__ void sum_strided(double2 &acc, const double *p, long long stride, int n, int i) {
+    // SUM_ILP loads in flight per thread (16 measured no faster: the sum runs at
+    // ~4.2 TB/s over ~415 MB of partials at config 4)
+    constexpr int SUM_ILP = 8;
     int q = 0;
-    for (; q + 8 <= n; q += 8) {
-        double2 v[8];
+    for (; q + SUM_ILP <= n; q += SUM_ILP) {
+        double2 v[SUM_ILP];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = reinterpret_cast<const double2 *>(p + (long long)(q + t) * stride)[i];
+        for (int t = 0; t < SUM_ILP; ++t) v[t] = reinterpret_cast<const double2 *>(p + (long long)(q + t) * stride)[i];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < SUM_ILP; ++t) {
             acc.x += v[t].x;
             acc.y += v[t].y;
         }
@@ -993,11 +996,14 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         // in tiles of 128 (warp-broadcast reads); 1/rho^2 by seed + cubic Newton.
         __shared__ double4 s_pc[128];  // (cx, cy, r, -)
         __shared__ double4 s_pm[128];  // (lambda_x, lambda_y, mu, -)
-        __shared__ LogTab s_log;       // table log (visible after the first tile barrier)
+        __shared__ LogTabX s_log;      // table log (visible after the first tile barrier)
         log_tab_init(s_log, threadIdx.x, blockDim.x);
-        // staged per pore: (cx, cy) and (lambda/4pi, r_k mu); two accumulator
-        // pairs (even / odd pores) break the serial add chain
-        double2 c0 = make_double2(0.0, 0.0), c1 = make_double2(0.0, 0.0);
+        // staged per pore: (cx, cy) and (lambda/4pi, r_k mu); EPI_ILP accumulator
+        // pairs (pores q mod EPI_ILP) break the serial add chain
+        constexpr int EPI_ILP = 4;
+        double2 c[EPI_ILP];
+#pragma unroll
+        for (int u2 = 0; u2 < EPI_ILP; ++u2) c[u2] = make_double2(0.0, 0.0);
         for (int k0 = 0; k0 < a.M; k0 += 128) {
             const int nk = min(128, a.M - k0);
             __syncthreads();
@@ -1023,15 +1029,14 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
                 c.y += fma(nlg, pm.y, fma(rl, ry, -mr * rx));
             };
             int q = 0;
-#pragma unroll 2
-            for (; q + 2 <= nk; q += 2) {
-                pore_term(q, c0);
-                pore_term(q + 1, c1);
+            for (; q + EPI_ILP <= nk; q += EPI_ILP) {
+#pragma unroll
+                for (int u2 = 0; u2 < EPI_ILP; ++u2) pore_term(q + u2, c[u2]);
             }
-            if (q < nk) pore_term(q, c0);
+            for (; q < nk; ++q) pore_term(q, c[0]);
         }
-        u[0].x += c0.x + c1.x;
-        u[0].y += c0.y + c1.y;
+        u[0].x += (c[0].x + c[1].x) + (c[2].x + c[3].x);
+        u[0].y += (c[0].y + c[1].y) + (c[2].y + c[3].y);
     } else if (full) {
         __shared__ LogTab s_log2;
         log_tab_init(s_log2, threadIdx.x, blockDim.x);
