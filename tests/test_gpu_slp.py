@@ -346,3 +346,26 @@ def test_minimum_nodes_per_pore(bie, n_pore):
     bie.dlp_apply(g, sig, out, 1)
     torch.cuda.synchronize()
     assert _relerr(out.cpu().numpy(), og.apply(s[0])) <= TOL
+
+
+@pytest.mark.parametrize("scale", [1e-5, 1e5])
+@pytest.mark.parametrize("flags", [0, 2])  # symmetric path, one-sided path
+def test_length_scale_extremes(bie, scale, flags):
+    """Edge case: the same geometry at 1e-5 and 1e5 length units (rho^2 from
+    ~1e-17 to ~4e10: the table logs' mantissa and exponent tables over ~90
+    binades); SLP and DLP parity on N = 1,792 (several 512-blocks)."""
+    import torch
+
+    s_ = scale
+    p = make_circle_problem(n_outer=1024, R=1.0 * s_, n_pore=256, name=f"scaled{s_:g}",
+                            pores=((0.3 * s_, 0.1 * s_, 0.2 * s_), (-0.4 * s_, -0.2 * s_, 0.15 * s_),
+                                   (0.1 * s_, -0.5 * s_, 0.12 * s_)))
+    g = bie.Geometry.from_problem(p)
+    og = oracle.OracleGeometry(p)
+    s = density(p, nvec=1, vec_id=8)
+    assert _relerr(_gpu_slp(bie, g, s, 1, flags)[0], og.slp_apply(s[0])) <= TOL
+    sig = _t(s)
+    out = torch.full_like(sig, float("nan"))
+    bie.dlp_apply(g, sig, out, 1, flags)
+    torch.cuda.synchronize()
+    assert _relerr(out.cpu().numpy(), og.apply(s[0])) <= TOL
