@@ -96,6 +96,27 @@ def test_kr_weights_library_matches_oracle(bie):
     assert np.abs(bie.kr_weights() - oracle.kr_weights()).max() <= 4 * np.spacing(26.0)
 
 
+def test_krylov_entry_points_validate_arguments(bie):
+    """bie_krylov_*: bad arguments return BIE_EINVAL before any device access
+    (a host buffer stands in for the non-null pointers); n = 0 is a no-op."""
+    L = bie._bie.lib()
+    buf = np.zeros(64)
+    p = buf.ctypes.data
+    assert L.bie_krylov_dots(None, 8, 1, p, 8, p, None) == -1
+    assert L.bie_krylov_dots(p, 8, 0, p, 8, p, None) == -1  # nv < 1
+    assert L.bie_krylov_dots(p, 8, 1, p, -1, p, None) == -1  # n < 0
+    assert L.bie_krylov_axpy(p, 8, 1, None, 1.0, 0.0, p, 8, None) == -1
+    assert L.bie_krylov_axpy(p, 8, 1, p, 1.0, 0.0, p, 0, None) == 0  # empty: nothing launched
+    assert L.bie_krylov_scale(p, None, p, 8, None) == -1
+    assert L.bie_krylov_scale(p, p, p, 0, None) == 0
+    assert L.bie_krylov_sqrt(p, p, 0, None) == -1
+    assert L.bie_krylov_givens(p, 4, p, p, p, p, p, 3, p, None) == -1  # ldh < k + 2
+    assert L.bie_krylov_givens(p, 8, p, p, p, p, None, 3, p, None) == -1
+    assert L.bie_krylov_trisolve(p, 4, p, p, 5, None) == -1  # ldh < iters
+    assert L.bie_krylov_trisolve(p, 4, p, p, 0, None) == 0
+    assert b"krylov" in L.bie_last_error()
+
+
 def test_slp_entry_points_validate_arguments(bie):
     L = bie._bie.lib()
     assert L.bie_slp_apply(None, None, None, 1, 0, None) == -1
