@@ -1,4 +1,5 @@
 """Full config-4 single-layer (NEXT-1) BD-GMRES solve to 1e-8 (iterations, time, history samples)."""
+import json, sys, time
 import torch
 sys.path.insert(0, '.')
 import paper_1609_04484_b200 as bie
