@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -862,6 +863,59 @@ struct SymEpi {
     long long Useg;            // units per segment (slot = segment - first segment of the block)
     int dsplit;                // in-block sums come in dsplit parts [dsplit][2N]
 };
+// A5 completion field of every pore at one target (nvec = 1; readings C5/C6):
+// sum over pores k of the Stokeslet (lambda_k / 4 pi) and rotlet (r_k mu_k)
+// terms, pore records staged through shared memory in tiles of 128
+// (warp-broadcast reads); 1/rho^2 by seed + cubic Newton.  Every thread of the
+// CTA must call it (barriers); accumulators c[q mod 4] break the serial add chain.
+struct PoreStage {
+    double4 pc[128];  // (cx, cy, r, -)
+    double4 pm[128];  // (lambda_x / 4 pi, lambda_y / 4 pi, r mu, -)
+    LogTabX lt;       // table log (visible after the first tile barrier)
+};
+__device__ __forceinline__ double2 pore_completion(double2 xi, const double4 *__restrict__ pore,
+                                                   const double *__restrict__ moments, int M, PoreStage &ps,
+                                                   int tid, int nthreads) {
+    constexpr double k4pi = 1.0 / (4.0 * kPi);
+    constexpr int ILP = 4;
+    log_tab_init(ps.lt, tid, nthreads);
+    double2 c[ILP];
+#pragma unroll
+    for (int u2 = 0; u2 < ILP; ++u2) c[u2] = make_double2(0.0, 0.0);
+    for (int k0 = 0; k0 < M; k0 += 128) {
+        const int nk = min(128, M - k0);
+        __syncthreads();
+        for (int q = tid; q < nk; q += nthreads) {
+            const int k = k0 + q;
+            const double4 pk = pore[k];
+            ps.pc[q] = pk;
+            const double *m = moments + (long long)k * 3;
+            ps.pm[q] = make_double4(k4pi * m[0], k4pi * m[1], pk.z * m[2], 0.0);
+        }
+        __syncthreads();
+        auto pore_term = [&](int q, double2 &cc) {
+            const double4 pk = ps.pc[q], pm = ps.pm[q];
+            const double rx = xi.x - pk.x, ry = xi.y - pk.y;
+            const double rho2 = fma(rx, rx, ry * ry);
+            double ir = rcp_approx(rho2);
+            const double e = fma(-rho2, ir, 1.0);
+            ir = fma(ir, fma(e, e, e), ir);
+            const double nlg = neg_half_log_tab(rho2, ps.lt);  // -log rho
+            const double rl = fma(rx, pm.x, ry * pm.y) * ir;    // (r . lambda/4pi) / rho^2
+            const double mr = pm.z * ir;                         // r_k mu / rho^2
+            cc.x += fma(nlg, pm.x, fma(rl, rx, mr * ry));
+            cc.y += fma(nlg, pm.y, fma(rl, ry, -mr * rx));
+        };
+        int q = 0;
+        for (; q + ILP <= nk; q += ILP) {
+#pragma unroll
+            for (int u2 = 0; u2 < ILP; ++u2) pore_term(q + u2, c[u2]);
+        }
+        for (; q < nk; ++q) pore_term(q, c[0]);
+    }
+    return make_double2((c[0].x + c[1].x) + (c[2].x + c[3].x), (c[0].y + c[1].y) + (c[2].y + c[3].y));
+}
+
 struct EpiArgs {
     const double2 *pos, *nrm, *tan;
     const double *selfc;
@@ -900,6 +954,16 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
     const bool full = !(a.flags & BIE_D_ONLY);
     constexpr double k4pi = 1.0 / (4.0 * kPi);
     double2 u[NVC > 0 ? NVC : BIE_MAX_NVEC];
+    // nvec = 1: odd CTAs compute the (FP64-bound) completion field before the
+    // (memory-bound) partial sums, even CTAs after, so that the two phases
+    // overlap across the wave; the field is added at the same place either way
+    __shared__ std::conditional_t<NVC == 1, PoreStage, char> s_ps;
+    const bool pore_phase = NVC == 1 && full && a.op == 0;
+    const bool pore_first = pore_phase && (blockIdx.x & 1);
+    double2 pc = make_double2(0.0, 0.0);
+    if constexpr (NVC == 1) {
+        if (pore_first) pc = pore_completion(xi, a.pore, a.moments, a.M, s_ps, threadIdx.x, blockDim.x);
+    }
     if (a.presum) u[0] = reinterpret_cast<const double2 *>(a.presum)[it];
     if (a.sym.on) {
         // fixed order: target-side slots, the in-block pairs, then source-side
@@ -994,51 +1058,11 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
         }
     }
     if (full && NVC == 1) {
-        // nvec = 1: pore records (c, r, lambda, mu) staged through shared memory
-        // in tiles of 128 (warp-broadcast reads); 1/rho^2 by seed + cubic Newton.
-        __shared__ double4 s_pc[128];  // (cx, cy, r, -)
-        __shared__ double4 s_pm[128];  // (lambda_x, lambda_y, mu, -)
-        __shared__ LogTabX s_log;      // table log (visible after the first tile barrier)
-        log_tab_init(s_log, threadIdx.x, blockDim.x);
-        // staged per pore: (cx, cy) and (lambda/4pi, r_k mu); EPI_ILP accumulator
-        // pairs (pores q mod EPI_ILP) break the serial add chain
-        constexpr int EPI_ILP = 4;
-        double2 c[EPI_ILP];
-#pragma unroll
-        for (int u2 = 0; u2 < EPI_ILP; ++u2) c[u2] = make_double2(0.0, 0.0);
-        for (int k0 = 0; k0 < a.M; k0 += 128) {
-            const int nk = min(128, a.M - k0);
-            __syncthreads();
-            if ((int)threadIdx.x < nk) {
-                const int k = k0 + threadIdx.x;
-                const double4 pk = a.pore[k];
-                s_pc[threadIdx.x] = pk;
-                const double *m = a.moments + (long long)k * 3;
-                s_pm[threadIdx.x] = make_double4(k4pi * m[0], k4pi * m[1], pk.z * m[2], 0.0);
-            }
-            __syncthreads();
-            auto pore_term = [&](int q, double2 &c) {
-                const double4 pk = s_pc[q], pm = s_pm[q];
-                const double rx = xi.x - pk.x, ry = xi.y - pk.y;
-                const double rho2 = fma(rx, rx, ry * ry);
-                double ir = rcp_approx(rho2);
-                const double e = fma(-rho2, ir, 1.0);
-                ir = fma(ir, fma(e, e, e), ir);
-                const double nlg = neg_half_log_tab(rho2, s_log);  // -log rho
-                const double rl = fma(rx, pm.x, ry * pm.y) * ir;     // (r . lambda/4pi) / rho^2
-                const double mr = pm.z * ir;                          // r_k mu / rho^2
-                c.x += fma(nlg, pm.x, fma(rl, rx, mr * ry));
-                c.y += fma(nlg, pm.y, fma(rl, ry, -mr * rx));
-            };
-            int q = 0;
-            for (; q + EPI_ILP <= nk; q += EPI_ILP) {
-#pragma unroll
-                for (int u2 = 0; u2 < EPI_ILP; ++u2) pore_term(q + u2, c[u2]);
-            }
-            for (; q < nk; ++q) pore_term(q, c[0]);
+        if constexpr (NVC == 1) {
+            if (!pore_first) pc = pore_completion(xi, a.pore, a.moments, a.M, s_ps, threadIdx.x, blockDim.x);
         }
-        u[0].x += (c[0].x + c[1].x) + (c[2].x + c[3].x);
-        u[0].y += (c[0].y + c[1].y) + (c[2].y + c[3].y);
+        u[0].x += pc.x;
+        u[0].y += pc.y;
     } else if (full) {
         __shared__ LogTab s_log2;
         log_tab_init(s_log2, threadIdx.x, blockDim.x);
