@@ -1252,7 +1252,11 @@ static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
 static long long sym_useg(long long U, int P) {
     long long lo = std::max<long long>(1, std::min<long long>(8, U / P));
     if (const char *e = getenv("BIE_SYM_USEG_MIN")) lo = std::max(1, atoi(e));  // tuning knob
-    return std::max<long long>(lo, (U + 24LL * P - 1) / (24LL * P));
+    // segments per CTA (knob BIE_SYM_SEGS_PER_CTA); config 4, ms per matvec:
+    // 8: 13.170, 12: 13.172, 16: 13.173, 24: 13.185, 32: 13.193, 48: 13.237
+    long long per = 24;
+    if (const char *e = getenv("BIE_SYM_SEGS_PER_CTA")) per = std::max(1, atoi(e));
+    return std::max<long long>(lo, (U + per * P - 1) / (per * P));
 }
 
 // Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only).
