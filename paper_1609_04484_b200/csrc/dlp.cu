@@ -34,7 +34,7 @@ constexpr int kPairThreads = 128;
 struct Variant {
     int nv, R, TS;
 };
-static const Variant kVariants[5] = {{1, 4, 256}, {2, 2, 256}, {4, 2, 256}, {8, 1, 128}, {16, 1, 64}};
+static const Variant kVariants[5] = {{1, 4, 256}, {2, 2, 256}, {4, 4, 256}, {8, 1, 128}, {16, 1, 64}};
 
 __device__ __forceinline__ double rcp_approx(double x) {
     double r;
@@ -1098,7 +1098,7 @@ static void *variant_kernel(int idx, int op = 0) {
     switch (idx) {
         case 0: return pair_kernel_ptr<1, 4, 256>(op);
         case 1: return pair_kernel_ptr<2, 2, 256>(op);
-        case 2: return pair_kernel_ptr<4, 2, 256>(op);
+        case 2: return pair_kernel_ptr<4, 4, 256>(op);
         case 3: return pair_kernel_ptr<8, 1, 128>(op);
         default: return pair_kernel_ptr<16, 1, 64>(op);
     }
@@ -1324,7 +1324,7 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
         switch (vi) {
             case 0: k_dlp_pairs<1, 4, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
             case 1: k_dlp_pairs<2, 2, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
-            case 2: k_dlp_pairs<4, 2, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+            case 2: k_dlp_pairs<4, 4, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
             case 3: k_dlp_pairs<8, 1, 128, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
             default: k_dlp_pairs<16, 1, 64, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         }
@@ -1333,7 +1333,7 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
     switch (vi) {
         case 0: k_dlp_pairs<1, 4, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         case 1: k_dlp_pairs<2, 2, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
-        case 2: k_dlp_pairs<4, 2, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        case 2: k_dlp_pairs<4, 4, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         case 3: k_dlp_pairs<8, 1, 128><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         default: k_dlp_pairs<16, 1, 64><<<s.P, kPairThreads, s.smem, st>>>(a); break;
     }
