@@ -82,6 +82,24 @@ BIE_API int bie_geometry_destroy(bie_geometry_t g);
 BIE_API int bie_geometry_info(bie_geometry_t g, int *N, int *M);
 /* Copy node positions to host: pos_host [N][2]. Synchronous. */
 BIE_API int bie_geometry_nodes(bie_geometry_t g, double *pos_host);
+/*
+ * bie_geometry_node_table -- copy the whole A1 node table to host buffers:
+ * pos, nrm, tan [N][2], w [N], kappa [N] (kappa_n = x''.n/|x'|^2).  The table
+ * is uniquely defined by the inputs (reading C27: correctly rounded pore
+ * template, one fixed sequence of IEEE operations per quantity, no FMA
+ * contraction), so any implementation of the same formulas reproduces it bit
+ * for bit.  Errors: BIE_EINVAL (bad handle / null), BIE_ECUDA.  Synchronous.
+ */
+BIE_API int bie_geometry_node_table(bie_geometry_t g, double *pos, double *nrm, double *tan, double *w,
+                                    double *kappa);
+/*
+ * bie_pore_template -- host-only (no device needed): unit[j] = (cos, sin) of
+ * theta_j = 2 pi j / n, j < n, each CORRECTLY ROUNDED to double (reading C27 of
+ * DESIGN.md; exact octant reduction of j, double-double Taylor series, one
+ * rounding).  Pore node j of pore (c, r) is x = c + r unit[j] (P:l.191-204,
+ * C12).  unit: host [n][2].  Errors: BIE_EINVAL (null, n < 1).
+ */
+BIE_API int bie_pore_template(int n, double *unit);
 
 /*
  * bie_dlp_apply -- A2-A5: out = A sigma for nvec densities (async on stream).

@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (no FMA contraction, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lquadmath", "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -49,6 +49,8 @@ def lib():
         L.ora_nodes.restype = ctypes.c_int
         L.ora_nodes.argtypes = [dp, dp, dp, ctypes.c_int, ctypes.c_double, dp, dp, ctypes.c_int, ctypes.c_int,
                                 dp, dp, dp, dp, dp]
+        L.ora_pore_template.restype = None
+        L.ora_pore_template.argtypes = [ctypes.c_int, dp]
         L.ora_apply.restype = None
         L.ora_apply.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp,
                                 dp, dp, ctypes.c_int, ctypes.c_uint, ip, ctypes.c_int]
@@ -95,6 +97,12 @@ def lib():
         L.ora_slp_gmres.restype = ctypes.c_int
         L.ora_slp_gmres.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, ctypes.c_void_p, ctypes.c_int,
                                     dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
+        L.ora_gmres_set_perturbation.restype = None
+        L.ora_gmres_set_perturbation.argtypes = [dp, ctypes.c_ulonglong]
+        L.ora_cgs_dots.restype = None
+        L.ora_cgs_dots.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, dp]
+        L.ora_cgs_sub.restype = None
+        L.ora_cgs_sub.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, dp]
         L.ora_gmres.restype = ctypes.c_int
         L.ora_gmres.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, dp, dp, dp,
                                 ctypes.c_void_p, dp, dp, ctypes.c_double, ctypes.c_int, dp, dp, dp, ip]
@@ -406,6 +414,53 @@ def gmres_bdlu(geom: OracleGeometry, f, bdlu: OracleBDLU, tol=1e-8, max_iter=100
                               ctypes.byref(rt), ctypes.byref(conv))
     return dict(x=x, iters=it, hist=hist[: it + 1].copy(), res_pc=rp.value, res_true=rt.value,
                 converged=bool(conv.value))
+
+
+PERTURB_KEYS = ("A", "P", "dot", "norm", "sub")
+
+
+class perturbed:
+    """Sensitivity runs for the GMRES parity envelope (reading C23):
+    inside the block every primitive of the oracle's GMRES iteration gets
+    seeded Gaussian noise at the given level (keys of PERTURB_KEYS: A v,
+    P^-1 v, CGS inner products, norms, CGS subtractions -- see the C source).
+    Test infrastructure only; outside the block the oracle is unperturbed."""
+
+    def __init__(self, eps: dict, seed: int = 0):
+        self.eps = np.array([float(eps.get(k, 0.0)) for k in PERTURB_KEYS])
+        self.seed = int(seed)
+
+    def __enter__(self):
+        lib().ora_gmres_set_perturbation(_d(self.eps), self.seed)
+        return self
+
+    def __exit__(self, *exc):
+        lib().ora_gmres_set_perturbation(_d(np.zeros(5)), 0)
+
+
+def cgs_dots(V, w):
+    """out[j] = V_j . w with the oracle GMRES's own sequential sums (V: [nv, n])."""
+    V = _c(V)
+    nv, n = V.shape
+    out = np.zeros(nv)
+    lib().ora_cgs_dots(n, nv, _d(V), _d(_c(w)), _d(out))
+    return out
+
+
+def cgs_sub(V, h, w):
+    """w - V^T h with the oracle GMRES's own loop (returns a new array)."""
+    V = _c(V)
+    nv, n = V.shape
+    w = _c(w).copy()
+    lib().ora_cgs_sub(n, nv, _d(V), _d(_c(h)), _d(w))
+    return w
+
+
+def pore_template(n: int) -> np.ndarray:
+    """(cos, sin)(2 pi j / n), j < n, correctly rounded (reading C27) -> [n, 2]."""
+    out = np.zeros(2 * n)
+    lib().ora_pore_template(n, _d(out))
+    return out.reshape(n, 2)
 
 
 def lu(A):

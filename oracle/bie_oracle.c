@@ -30,6 +30,7 @@
  * (V10).  No function here is "parity unpinned".
  */
 #include <math.h>
+#include <quadmath.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -52,15 +53,45 @@
  *   w = 2 pi r / n_pore, t = (-sin, cos), kn = (x''.n)/|x'|^2 = 1/r
  * Dof order: pores 1..M (node k*n_pore + j), then Gamma_0 (P:l.734-736).
  * ------------------------------------------------------------------------- */
+/* Pore template (reading C27): (cos, sin)(2 pi j / n) correctly rounded to
+ * double -- exact octant reduction of the integer j, quad-precision
+ * (libquadmath, 113-bit) cos/sin of the reduced angle in [0, pi/4], one
+ * rounding.  Node positions are ill-conditioned for the operator (1 ulp moves
+ * the matvec by ~1e-12 at config 4), so the table must be uniquely defined. */
+void ora_pore_template(int n, double *unit)
+{
+    for (int j = 0; j < n; ++j) {
+        long long a = 8LL * j;
+        int o = (int)(a / n);
+        long long r = a - (long long)o * n;
+        long long k = (o & 1) ? n - r : r;
+        __float128 phi = (M_PIq / 4) * (__float128)k / (__float128)n;
+        double C = (double)cosq(phi), S = (double)sinq(phi), c, s;
+        switch (o) { /* theta = o pi/4 + phi (o even) or (o + 1) pi/4 - phi (o odd) */
+        case 0: c = C; s = S; break;
+        case 1: c = S; s = C; break;
+        case 2: c = -S; s = C; break;
+        case 3: c = -C; s = S; break;
+        case 4: c = -C; s = -S; break;
+        case 5: c = -S; s = -C; break;
+        case 6: c = S; s = -C; break;
+        default: c = C; s = -S; break;
+        }
+        unit[2 * j] = c;
+        unit[2 * j + 1] = s;
+    }
+}
+
 int ora_nodes(const double *oxy, const double *odxy, const double *oddxy, int n_outer, double T,
               const double *pc, const double *pr, int M, int n_pore,
               double *x, double *nrm, double *w, double *tan, double *kn)
 {
     int i = 0;
+    double *unit = (double *)malloc(2 * (size_t)(n_pore > 0 ? n_pore : 1) * sizeof(double));
+    ora_pore_template(n_pore, unit);
     for (int k = 0; k < M; ++k) {
         for (int j = 0; j < n_pore; ++j, ++i) {
-            double th = 2.0 * ORA_PI * (double)j / (double)n_pore;
-            double c = cos(th), s = sin(th);
+            double c = unit[2 * j], s = unit[2 * j + 1];
             double r = pr[k];
             double dx = -r * s, dy = r * c;       /* x'  */
             double ddx = -r * c, ddy = -r * s;    /* x'' */
@@ -75,6 +106,7 @@ int ora_nodes(const double *oxy, const double *odxy, const double *oddxy, int n_
             kn[i] = (ddx * nrm[2 * i] + ddy * nrm[2 * i + 1]) / (sp * sp);
         }
     }
+    free(unit);
     for (int j = 0; j < n_outer; ++j, ++i) {
         double dx = odxy[2 * j], dy = odxy[2 * j + 1];
         double sp = sqrt(dx * dx + dy * dy);
@@ -843,6 +875,68 @@ void ora_bd_free(void *h)
  * ------------------------------------------------------------------------- */
 typedef void (*ora_op)(void *ctx, const double *in, double *out);
 
+/* Sensitivity runs (reading C23; tools/make_golden.py).  Test
+ * infrastructure for the GMRES parity envelope, not part of the method: every
+ * primitive of the iteration gets seeded Gaussian noise at the measured
+ * GPU-vs-oracle disagreement of that primitive (profiles/round2/
+ * disagreement.json), so the envelope is the oracle's own sensitivity to
+ * exactly the rounding differences the GPU path introduces:
+ *   eps[0] A v        out_i += eps max|out| z_i
+ *   eps[1] P^-1 v     out_i += eps max|out| z_i
+ *   eps[2] V_j . w    h_j   += eps ||w|| z       (||V_j|| = 1)
+ *   eps[3] ||w||      nrm   *= 1 + eps z
+ *   eps[4] w -= V h   w_i   += eps max|w| z_i    (each CGS pass)
+ * z ~ N(0, 1) from a counter-based generator (splitmix64 of (seed, event, i),
+ * Box-Muller).  All eps = 0 (the default) leaves every result bit-identical
+ * to the unperturbed oracle. */
+static double ora_pert_eps[5] = {0, 0, 0, 0, 0};
+static unsigned long long ora_pert_seed = 0, ora_pert_calls = 0;
+
+void ora_gmres_set_perturbation(const double *eps5, unsigned long long seed)
+{
+    for (int q = 0; q < 5; ++q)
+        ora_pert_eps[q] = eps5 ? eps5[q] : 0.0;
+    ora_pert_seed = seed;
+    ora_pert_calls = 0;
+}
+
+static unsigned long long ora_splitmix(unsigned long long x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+static double ora_gauss(unsigned long long call, unsigned long long i)
+{
+    unsigned long long h = ora_splitmix(ora_splitmix(ora_pert_seed ^ (call << 32)) + i);
+    double u1 = ((h >> 11) + 1.0) * (1.0 / 9007199254740993.0); /* (0, 1] */
+    double u2 = (ora_splitmix(h) >> 11) * (1.0 / 9007199254740992.0);
+    return sqrt(-2.0 * log(u1)) * cos(2.0 * ORA_PI * u2);
+}
+
+/* vector primitive: v_i += eps max|v| z_i */
+static void ora_perturb(int n, double *v, double eps)
+{
+    if (eps == 0.0)
+        return;
+    const unsigned long long call = ora_pert_calls++;
+    double m = 0.0;
+    for (int i = 0; i < n; ++i)
+        m = fabs(v[i]) > m ? fabs(v[i]) : m;
+    for (int i = 0; i < n; ++i)
+        v[i] += eps * m * ora_gauss(call, (unsigned long long)i);
+}
+
+/* scalar primitive: x + eps scale z */
+static double ora_perturb_s(double x, double eps, double scale)
+{
+    if (eps == 0.0)
+        return x;
+    return x + eps * scale * ora_gauss(ora_pert_calls++, 0);
+}
+
 static double ora_dot(int n, const double *a, const double *b)
 {
     double s = 0.0;
@@ -868,11 +962,14 @@ static int ora_gmres_core(int n, ora_op A, void *actx, ora_op P, void *pctx, con
     int iters = 0;
     *converged = 0;
 
-    if (P)
+    if (P) {
         P(pctx, f, r);
-    else
+        ora_perturb(n, r, ora_pert_eps[1]);
+    } else {
         memcpy(r, f, (size_t)n * sizeof(double));
+    }
     double beta = sqrt(ora_dot(n, r, r));
+    beta = ora_perturb_s(beta, ora_pert_eps[3], beta);
     for (int i = 0; i < n; ++i)
         x[i] = 0.0;
     hist[0] = 1.0;
@@ -888,16 +985,25 @@ static int ora_gmres_core(int n, ora_op A, void *actx, ora_op P, void *pctx, con
     gv[0] = beta;
     for (int k = 0; k < max_iter; ++k) {
         A(actx, V[k], t);
-        if (P)
+        ora_perturb(n, t, ora_pert_eps[0]);
+        if (P) {
             P(pctx, t, wv);
-        else
+            ora_perturb(n, wv, ora_pert_eps[1]);
+        } else {
             memcpy(wv, t, (size_t)n * sizeof(double));
+        }
         double w0 = sqrt(ora_dot(n, wv, wv));
+        w0 = ora_perturb_s(w0, ora_pert_eps[3], w0);
         for (int pass = 0; pass < 2; ++pass) {
             double *hh = pass ? h2 : h;
 #pragma omp parallel for schedule(static) if (n > 4096)
             for (int j = 0; j <= k; ++j)
                 hh[j] = ora_dot(n, V[j], wv);
+            if (ora_pert_eps[2] != 0.0) {
+                double nw = sqrt(ora_dot(n, wv, wv));
+                for (int j = 0; j <= k; ++j)
+                    hh[j] = ora_perturb_s(hh[j], ora_pert_eps[2], nw);
+            }
 #pragma omp parallel for schedule(static) if (n > 4096)
             for (int i = 0; i < n; ++i) {
                 double s = wv[i];
@@ -905,10 +1011,12 @@ static int ora_gmres_core(int n, ora_op A, void *actx, ora_op P, void *pctx, con
                     s -= V[j][i] * hh[j];
                 wv[i] = s;
             }
+            ora_perturb(n, wv, ora_pert_eps[4]);
         }
         for (int j = 0; j <= k; ++j)
             H[(size_t)j * max_iter + k] = h[j] + h2[j];
         double hk1 = sqrt(ora_dot(n, wv, wv));
+        hk1 = ora_perturb_s(hk1, ora_pert_eps[3], hk1);
         H[(size_t)(k + 1) * max_iter + k] = hk1;
         for (int j = 0; j < k; ++j) {
             double a = H[(size_t)j * max_iter + k], b = H[(size_t)(j + 1) * max_iter + k];
@@ -979,6 +1087,27 @@ done:
     free(t);
     free(wv);
     return iters;
+}
+
+/* The iteration's own primitives, exported so the GPU-vs-oracle disagreement
+ * of each can be measured (tools/measure_disagreement.py): out[j] = V_j . w
+ * (sequential ascending sums, as in CGS) and w_i -= sum_j V_j,i h_j. */
+void ora_cgs_dots(int n, int nv, const double *V, const double *w, double *out)
+{
+#pragma omp parallel for schedule(static) if (n > 4096)
+    for (int j = 0; j < nv; ++j)
+        out[j] = ora_dot(n, V + (size_t)j * n, w);
+}
+
+void ora_cgs_sub(int n, int nv, const double *V, const double *h, double *w)
+{
+#pragma omp parallel for schedule(static) if (n > 4096)
+    for (int i = 0; i < n; ++i) {
+        double s = w[i];
+        for (int j = 0; j < nv; ++j)
+            s -= V[(size_t)j * n + i] * h[j];
+        w[i] = s;
+    }
 }
 
 /* --- dense special cases (V8) --- */

@@ -29,6 +29,7 @@ from ._bie import (  # noqa: F401
     gmres_solve_slp,
     kr_weights,
     launch_count,
+    pore_template,
     profile_begin,
     profile_end,
     slp_apply,

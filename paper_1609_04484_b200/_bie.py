@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "bie_kr_weights", "bie_slp_apply", "bie_slp_apply_rows", "bie_slp_field_eval", "bie_blockdiag_factor_slp",
     "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp", "bie_blockdiag_factor_structured",
     "bie_slp_pairs_partial", "bie_slp_epilogue_rows", "bie_blockdiag_factor_range_slp",
+    "bie_geometry_node_table", "bie_pore_template",
 )
 
 
@@ -64,6 +65,8 @@ def lib():
         "bie_geometry_destroy": [vp],
         "bie_geometry_info": [vp, ip, ip],
         "bie_geometry_nodes": [vp, dp],
+        "bie_geometry_node_table": [vp, dp, dp, dp, dp, dp],
+        "bie_pore_template": [c_int, dp],
         "bie_dlp_apply": [vp, vp, vp, c_int, c_uint, vp],
         "bie_dlp_apply_rows": [vp, vp, vp, c_int, c_uint, c_int, c_int, vp],
         "bie_dlp_apply_host": [vp, dp, dp, c_int, c_uint, vp],
@@ -171,6 +174,15 @@ class Geometry:
         _check(lib().bie_geometry_nodes(self.h, _dp(out)))
         return out.reshape(-1, 2)
 
+    def node_table(self) -> dict:
+        """The device node table (A1) copied to host: pos, nrm, tan [N, 2], w, kappa [N]."""
+        N = self.N
+        t = {k: np.zeros(2 * N) for k in ("pos", "nrm", "tan")}
+        t.update({k: np.zeros(N) for k in ("w", "kappa")})
+        _check(lib().bie_geometry_node_table(self.h, _dp(t["pos"]), _dp(t["nrm"]), _dp(t["tan"]), _dp(t["w"]),
+                                             _dp(t["kappa"])))
+        return t
+
     def close(self):
         if getattr(self, "h", None) and self.h.value:
             _check(lib().bie_geometry_destroy(self.h))
@@ -181,6 +193,13 @@ class Geometry:
             self.close()
         except Exception:
             pass
+
+
+def pore_template(n: int) -> np.ndarray:
+    """(cos, sin)(2 pi j / n), correctly rounded (bie_pore_template, host only) -> [n, 2]."""
+    out = np.zeros(2 * n)
+    _check(lib().bie_pore_template(int(n), _dp(out)))
+    return out.reshape(n, 2)
 
 
 def launch_count() -> int:

@@ -37,46 +37,142 @@ BlockDiag *as_bd(bie_blockdiag_t b) {
     return p;
 }
 
-// A1 node kernel.  P:l.296-309, P:l.318-319, P:l.354; readings C2, C7, C12.
-// Pores (node i = k*n_pore + j): x = c + r(cos, sin), n = -(cos, sin),
-// w = 2 pi r / n_pore, t = (-sin, cos), kappa_n = x_ss . n = 1/r.
+// Pore-node template (reading C27 of DESIGN.md): (C_j, S_j) = cos / sin of
+// theta_j = 2 pi j / n, CORRECTLY ROUNDED to double.  A 1-ulp difference in a
+// pore node position is amplified ~1e4 by the near-tangent cancellation in r.n
+// between neighbouring nodes of a small pore far from the origin (measured:
+// 2e-12 max-norm at config 4), so the node table must be uniquely defined, not
+// "within an ulp".  Exact octant reduction of the integer j, then Taylor
+// series in double-double arithmetic (|error| ~ 1e-32) and one final rounding.
+namespace {
+struct DD {
+    double hi, lo;
+};
+DD two_sum(double a, double b) {
+    const double s = a + b, bb = s - a;
+    return {s, (a - (s - bb)) + (b - bb)};
+}
+DD quick_two_sum(double a, double b) {
+    const double s = a + b;
+    return {s, b - (s - a)};
+}
+DD dd_add(DD a, DD b) {
+    DD s = two_sum(a.hi, b.hi);
+    const DD t = two_sum(a.lo, b.lo);
+    s.lo += t.hi;
+    s = quick_two_sum(s.hi, s.lo);
+    s.lo += t.lo;
+    return quick_two_sum(s.hi, s.lo);
+}
+DD dd_mul(DD a, DD b) {
+    const double p = a.hi * b.hi;
+    const double e = std::fma(a.hi, b.hi, -p) + (a.hi * b.lo + a.lo * b.hi);
+    return quick_two_sum(p, e);
+}
+DD dd_div_d(DD a, double b) {  // a / b, b a small integer
+    const double q1 = a.hi / b;
+    const double p = q1 * b, pe = std::fma(q1, b, -p);
+    const DD r = dd_add(a, DD{-p, -pe});
+    const double q2 = r.hi / b;
+    return quick_two_sum(q1, q2);
+}
+// sin and cos of phi in [0, pi/4] (double-double Taylor series)
+void dd_sincos(DD phi, DD &sn, DD &cs) {
+    const DD z2 = dd_mul(phi, phi);
+    DD term = phi, s = phi;
+    for (int k = 1; k < 40; ++k) {  // term_k = phi^(2k+1) / (2k+1)!
+        term = dd_div_d(dd_mul(term, z2), (double)(2 * k) * (double)(2 * k + 1));
+        s = dd_add(s, (k & 1) ? DD{-term.hi, -term.lo} : term);
+        if (std::fabs(term.hi) < 1e-36) break;
+    }
+    DD c = {1.0, 0.0};
+    term = {1.0, 0.0};
+    for (int k = 1; k < 40; ++k) {  // term_k = phi^(2k) / (2k)!
+        term = dd_div_d(dd_mul(term, z2), (double)(2 * k - 1) * (double)(2 * k));
+        c = dd_add(c, (k & 1) ? DD{-term.hi, -term.lo} : term);
+        if (std::fabs(term.hi) < 1e-36) break;
+    }
+    sn = s;
+    cs = c;
+}
+}  // namespace
+
+void pore_template(int n, std::vector<double2> &out) {
+    const DD pi4 = {0.78539816339744827900, 3.0616169978683830179e-17};  // pi / 4
+    out.resize(n);
+    for (int j = 0; j < n; ++j) {
+        const long long a = 8LL * j;
+        const int o = (int)(a / n);
+        const long long r = a - (long long)o * n;
+        const bool odd = o & 1;
+        const DD phi = dd_div_d(dd_mul(pi4, DD{(double)(odd ? n - r : r), 0.0}), (double)n);
+        DD sd, cd;
+        dd_sincos(phi, sd, cd);
+        const double S = sd.hi + sd.lo, C = cd.hi + cd.lo;
+        double c, s;  // theta_j = o pi/4 + phi (even o) or (o + 1) pi/4 - phi (odd o)
+        switch (o) {
+            case 0: c = C; s = S; break;
+            case 1: c = S; s = C; break;
+            case 2: c = -S; s = C; break;
+            case 3: c = -C; s = S; break;
+            case 4: c = -C; s = -S; break;
+            case 5: c = -S; s = -C; break;
+            case 6: c = S; s = -C; break;
+            default: c = C; s = -S; break;
+        }
+        out[j] = make_double2(c, s);
+    }
+}
+
+// A1 node kernel.  P:l.296-309, P:l.318-319, P:l.354; readings C2, C7, C12, C27.
+// Pores (node i = k*n_pore + j), e = template (C_j, S_j):
+//   x = c + r e, x' = r(-S, C), x'' = -r e, n = -e, t = x'/|x'|,
+//   w = 2 pi r / n_pore, kappa_n = x''.n / |x'|^2.
 // Gamma_0 (node i = wall_lo + j): w = |x'| T/n_outer, t = x'/|x'|,
 // n = (t_y, -t_x), kappa_n = x''.n / |x'|^2.
+// Every node quantity is one fixed sequence of correctly rounded operations
+// (explicit _rn intrinsics: no contraction into FMA), so the node table is
+// uniquely defined by the inputs (bit-identical to any implementation of the
+// same formulas, e.g. the oracle's).
 __global__ void k_nodes(int N, int M, int n_pore, int n_outer, double T, const double2 *__restrict__ oxy,
                         const double2 *__restrict__ odxy, const double2 *__restrict__ oddxy,
-                        const double4 *__restrict__ pore, double2 *pos, double2 *nw, double2 *nrm, double2 *tan,
-                        double *w, double *selfc) {
+                        const double4 *__restrict__ pore, const double2 *__restrict__ unit, double2 *pos, double2 *nw,
+                        double2 *nrm, double2 *tan, double *w, double *selfc, double *kappa) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     int wall_lo = M * n_pore;
-    double2 x, n, t;
-    double wi, kn;
+    double2 x, n, t, d1, d2;
+    double wi;
     if (i < wall_lo) {
         int k = i / n_pore, j = i - k * n_pore;
-        double4 p = pore[k];
-        double s, c;
-        sincospi(2.0 * (double)j / (double)n_pore, &s, &c);
-        x = make_double2(p.x + p.z * c, p.y + p.z * s);
-        n = make_double2(-c, -s);
-        t = make_double2(-s, c);
-        wi = 2.0 * kPi * p.z / (double)n_pore;
-        kn = 1.0 / p.z;
+        const double4 p = pore[k];
+        const double2 e = unit[j];
+        d1 = make_double2(-__dmul_rn(p.z, e.y), __dmul_rn(p.z, e.x));
+        d2 = make_double2(-__dmul_rn(p.z, e.x), -__dmul_rn(p.z, e.y));
+        x = make_double2(__dadd_rn(p.x, __dmul_rn(p.z, e.x)), __dadd_rn(p.y, __dmul_rn(p.z, e.y)));
+        n = make_double2(-e.x, -e.y);
+        wi = __ddiv_rn(__dmul_rn(2.0 * kPi, p.z), (double)n_pore);
     } else {
         int j = i - wall_lo;
-        double2 d1 = odxy[j], d2 = oddxy[j];
-        double sp = sqrt(d1.x * d1.x + d1.y * d1.y);
-        t = make_double2(d1.x / sp, d1.y / sp);
-        n = make_double2(t.y, -t.x);
+        d1 = odxy[j];
+        d2 = oddxy[j];
         x = oxy[j];
-        wi = sp * T / (double)n_outer;
-        kn = (d2.x * n.x + d2.y * n.y) / (sp * sp);
     }
+    const double sp2 = __dadd_rn(__dmul_rn(d1.x, d1.x), __dmul_rn(d1.y, d1.y));
+    const double sp = __dsqrt_rn(sp2);
+    t = make_double2(__ddiv_rn(d1.x, sp), __ddiv_rn(d1.y, sp));
+    if (i >= wall_lo) {
+        n = make_double2(t.y, -t.x);
+        wi = __ddiv_rn(__dmul_rn(sp, T), (double)n_outer);
+    }
+    const double kn = __ddiv_rn(__dadd_rn(__dmul_rn(d2.x, n.x), __dmul_rn(d2.y, n.y)), __dmul_rn(sp, sp));
     pos[i] = x;
     nrm[i] = n;
     tan[i] = t;
     w[i] = wi;
     nw[i] = make_double2(wi * n.x / kPi, wi * n.y / kPi);
     selfc[i] = wi * kn / (2.0 * kPi);
+    kappa[i] = kn;
 }
 
 // Kapur-Rokhlin sixth-order log-correction weights (P:l.321-330; reading C24
@@ -151,6 +247,7 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     cudaFree(g->tan);
     cudaFree(g->w);
     cudaFree(g->selfc);
+    cudaFree(g->kappa);
     cudaFree(g->pore);
     cudaFree(g->partial);
     cudaFree(g->moments);
@@ -280,13 +377,14 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dev);
     int N = g->N;
     int rc = BIE_OK;
-    double2 *d_oxy = nullptr, *d_odxy = nullptr, *d_oddxy = nullptr;
+    double2 *d_oxy = nullptr, *d_odxy = nullptr, *d_oddxy = nullptr, *d_unit = nullptr;
     std::vector<double4> hp(n_pores > 0 ? n_pores : 1);
     double wall_len = 0.0;
     auto fail = [&](int code) {
         cudaFree(d_oxy);
         cudaFree(d_odxy);
         cudaFree(d_oddxy);
+        cudaFree(d_unit);
         bie_geometry_destroy(reinterpret_cast<bie_geometry_t>(g));
         return code;
     };
@@ -301,6 +399,7 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     TRY(cudaMalloc(&g->tan, sizeof(double2) * N));
     TRY(cudaMalloc(&g->w, sizeof(double) * N));
     TRY(cudaMalloc(&g->selfc, sizeof(double) * N));
+    TRY(cudaMalloc(&g->kappa, sizeof(double) * N));
     TRY(cudaMalloc(&g->pore, sizeof(double4) * (n_pores > 0 ? n_pores : 1)));
     TRY(cudaMalloc(&d_oxy, sizeof(double2) * n_outer));
     TRY(cudaMalloc(&d_odxy, sizeof(double2) * n_outer));
@@ -308,6 +407,12 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     TRY(cudaMemcpy(d_oxy, outer_xy, sizeof(double2) * n_outer, cudaMemcpyHostToDevice));
     TRY(cudaMemcpy(d_odxy, outer_dxy, sizeof(double2) * n_outer, cudaMemcpyHostToDevice));
     TRY(cudaMemcpy(d_oddxy, outer_ddxy, sizeof(double2) * n_outer, cudaMemcpyHostToDevice));
+    {
+        std::vector<double2> unit;
+        pore_template(std::max(g->n_pore, 1), unit);
+        TRY(cudaMalloc(&d_unit, sizeof(double2) * unit.size()));
+        TRY(cudaMemcpy(d_unit, unit.data(), sizeof(double2) * unit.size(), cudaMemcpyHostToDevice));
+    }
     // |Gamma_k| = sum_j w_j over the pore's nodes (reading C5); on an equispaced
     // circle every w_j = 2 pi r / n, so the sum is n * w (computed the same way
     // as the kernel's w to keep the ratio w_j/|Gamma_k| exact).
@@ -320,7 +425,7 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     }
     TRY(cudaMemcpy(g->pore, hp.data(), sizeof(double4) * (n_pores > 0 ? n_pores : 1), cudaMemcpyHostToDevice));
     k_nodes<<<(N + 255) / 256, 256>>>(N, g->M, g->n_pore, n_outer, outer_period, d_oxy, d_odxy, d_oddxy, g->pore,
-                                      g->pos, g->nw, g->nrm, g->tan, g->w, g->selfc);
+                                      d_unit, g->pos, g->nw, g->nrm, g->tan, g->w, g->selfc, g->kappa);
     count_launch();
     TRY(cudaGetLastError());
     {
@@ -340,6 +445,7 @@ int bie_geometry_create(const double *outer_xy, const double *outer_dxy, const d
     cudaFree(d_oxy);
     cudaFree(d_odxy);
     cudaFree(d_oddxy);
+    cudaFree(d_unit);
     *out = reinterpret_cast<bie_geometry_t>(g);
     return BIE_OK;
 }
@@ -362,6 +468,32 @@ int bie_geometry_nodes(bie_geometry_t gh, double *pos_host) {
         return BIE_EINVAL;
     }
     BIE_CUDA_TRY(cudaMemcpy(pos_host, g->pos, sizeof(double2) * g->N, cudaMemcpyDeviceToHost));
+    return BIE_OK;
+}
+
+int bie_geometry_node_table(bie_geometry_t gh, double *pos, double *nrm, double *tan, double *w, double *kappa) {
+    Geometry *g = as_geom(gh);
+    if (!g || !pos || !nrm || !tan || !w || !kappa) {
+        set_error("bie_geometry_node_table: invalid handle or null output");
+        return BIE_EINVAL;
+    }
+    const size_t N = (size_t)g->N;
+    BIE_CUDA_TRY(cudaMemcpy(pos, g->pos, sizeof(double2) * N, cudaMemcpyDeviceToHost));
+    BIE_CUDA_TRY(cudaMemcpy(nrm, g->nrm, sizeof(double2) * N, cudaMemcpyDeviceToHost));
+    BIE_CUDA_TRY(cudaMemcpy(tan, g->tan, sizeof(double2) * N, cudaMemcpyDeviceToHost));
+    BIE_CUDA_TRY(cudaMemcpy(w, g->w, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    BIE_CUDA_TRY(cudaMemcpy(kappa, g->kappa, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    return BIE_OK;
+}
+
+int bie_pore_template(int n, double *unit) {
+    if (!unit || n < 1) {
+        set_error("bie_pore_template: null output or n < 1");
+        return BIE_EINVAL;
+    }
+    std::vector<double2> u;
+    pore_template(n, u);
+    std::memcpy(unit, u.data(), sizeof(double2) * (size_t)n);
     return BIE_OK;
 }
 

@@ -60,6 +60,7 @@ struct Geometry {
     double2 *tan = nullptr;   // t_j
     double *w = nullptr;      // w_j
     double *selfc = nullptr;  // w_j kappa_n,j / (2 pi)
+    double *kappa = nullptr;  // kappa_n,j = x''.n / |x'|^2
     double4 *pore = nullptr;  // (cx, cy, r, |Gamma_k|)
     double wall_len = 0.0;    // |Gamma_0|
     // host copies needed for scheduling / BD
@@ -130,6 +131,7 @@ BlockDiag *as_bd(bie_blockdiag_t b);
 
 // geometry.cu
 void kr_weights(double gamma[6]);
+void pore_template(int n, std::vector<double2> &out);  // correctly rounded (cos, sin)(2 pi j / n), reading C27
 // dlp.cu
 int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsigned flags, int row_begin,
                    int row_end, cudaStream_t s);

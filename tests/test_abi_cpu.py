@@ -172,3 +172,23 @@ def test_config_geometries_pass_validation(bie, cid):
     if rc == 0:
         L.bie_geometry_destroy(h)
     assert rc not in (-1, -2), L.bie_last_error()
+
+
+@pytest.mark.parametrize("n", [16, 18, 30, 64, 100, 128, 256, 1000, 4096])
+def test_pore_template_correctly_rounded(bie, n):
+    """Reading C27: the library's pore template (double-double Taylor series,
+    host code, no device) and the oracle's (libquadmath) are independent
+    implementations of one uniquely defined value -- cos/sin(2 pi j / n)
+    correctly rounded -- so they must agree bit for bit.  Also pinned to the
+    exact values at the octant points and to numpy within a few ulp."""
+    import oracle
+
+    u = bie.pore_template(n)
+    assert np.array_equal(u, oracle.pore_template(n))
+    th = 2 * np.pi * np.arange(n) / n
+    assert np.abs(u - np.stack([np.cos(th), np.sin(th)], 1)).max() < 2e-15
+    assert np.array_equal(u[0], [1.0, 0.0])
+    if n % 4 == 0:
+        assert np.array_equal(np.abs(u[n // 4]), [0.0, 1.0]) and np.array_equal(u[n // 2], [-1.0, 0.0])
+    if n % 8 == 0:
+        assert u[n // 8][0] == u[n // 8][1] == np.float64(np.sqrt(0.5))

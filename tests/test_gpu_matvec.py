@@ -247,3 +247,31 @@ def test_side_stream_and_profile_hooks(bie):
     assert pr["applies"] == 3 and pr["pairs_ms"] > 0 and pr["epilogue_ms"] > 0
     assert bie.launch_count() - n0 >= 3 * 4  # moments, quad, sym, diag, epilogue per apply
     assert _relerr(out.cpu().numpy(), og.apply(s)[0]) <= TOL
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_node_table_bit_exact(bie, cid):
+    """A1 parity (reading C27): the device node table equals the oracle's bit
+    for bit -- positions, normals, tangents, weights and curvature are one
+    fixed sequence of IEEE operations on the same inputs on both sides."""
+    p = make_problem(cid)
+    g = bie.Geometry.from_problem(p)
+    og = oracle.OracleGeometry(p)
+    t = g.node_table()
+    g.close()
+    assert np.array_equal(t["pos"], og.x)
+    assert np.array_equal(t["nrm"], og.nrm)
+    assert np.array_equal(t["tan"], og.tan)
+    assert np.array_equal(t["w"], og.w)
+    assert np.array_equal(t["kappa"], og.kn)
+
+
+@pytest.mark.parametrize("cid", [3, 4])
+def test_matvec_all_rows_parity(bie, cid):
+    """Every row (not a sample) of the config-3/4 completed matvec at 1e-12."""
+    p = make_problem(cid)
+    g, og = _setup(bie, p)
+    s = density(p, nvec=1, vec_id=70)
+    y = _gpu_apply(bie, g, s, 1)
+    ref = og.apply(s)
+    assert _relerr(y[0], ref[0]) <= TOL

@@ -128,6 +128,41 @@ def test_V3_rotation_in_bare_nullspace(g2):
     assert np.abs(bare).max() < 1e-13
 
 
+# ---------------------------------------------------------------- V11 N0 term (nu)
+def _wall_normal_density(p, R):
+    """sigma = n on Gamma_0 (outward of Omega_0, reading C2: n = x / R on a
+    circle centred at 0), zero on the pores -- built from the raw input curve."""
+    s = np.zeros(2 * p.N)
+    lo = p.M * p.n_pore
+    s[2 * lo:] = (p.outer_xy / R).reshape(-1)
+    return s, lo
+
+
+@pytest.mark.parametrize("R,n_outer,pores", [(1.0, 64, ((0.0, 0.0, 0.3),)),
+                                             (2.5, 96, ((0.4, -0.3, 0.5), (-1.1, 0.6, 0.35)))])
+def test_V11_nu_closed_form_circle(R, n_outer, pores):
+    """Closed form that fixes the null-space term N0 (reading C5, P:l.260-264).
+    On a circle of radius R, r.n_y = -rho^2 / (2R) for x, y on the curve, so the
+    DLP kernel applied to sigma = n is (1/pi) r / (4 R^2) and, the trapezoid
+    rule being exact for the degree-1 trigonometric integrand,
+    D[n] = n / 2 at every wall node: (-1/2 I + D)[n] = 0.  The self term
+    vanishes (t.n = 0) and lambda_k = mu_k = 0 (sigma = 0 on the pores), so the
+    completed operator gives A sigma = nu n on the wall rows with
+    nu = (1/|Gamma_0|) sum_j w_j n_j.n_j = 1, i.e. A sigma = n there.  Inside
+    Gamma_0 the same density is the zero Stokes flow (Dirichlet uniqueness):
+    A sigma = 0 on the pore rows up to the trapezoid error at the pores'
+    distance.  A sign or scale slip in nu fails the wall rows."""
+    p = make_circle_problem(n_outer, R, pores, 64)
+    g = oracle.OracleGeometry(p)
+    s, lo = _wall_normal_density(p, R)
+    y = g.apply(s)
+    assert np.abs(y[2 * lo:] - s[2 * lo:]).max() < 1e-14
+    assert np.abs(y[:2 * lo]).max() < 1e-13
+    # the D-only part alone vanishes on the wall rows (no N0 there)
+    d = -0.5 * s + g.apply(s, flags=oracle.D_ONLY)
+    assert np.abs(d[2 * lo:]).max() < 1e-14
+
+
 # ---------------------------------------------------------------- V4 completion
 def test_V4_completion_closed_forms(g2):
     p = g2.problem
