@@ -43,9 +43,10 @@ L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
 
 def _ncu_traffic(key="traffic_bytes_per_launch"):
-    """DRAM bytes per launch (or another field) of the dominant kernel from the committed ncu capture."""
+    """DRAM bytes per launch (or another field) of the dominant kernel from the committed
+    ncu --set full capture of the current kernel (profiles/round2/k_dlp_sym_traffic.json)."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "round1", "k_dlp_sym_traffic.json")))[key]
+        return json.load(open(os.path.join(ROOT, "profiles", "round2", "k_dlp_sym_traffic.json")))[key]
     except Exception:
         return None
 
@@ -163,6 +164,57 @@ def cpu_baseline_sample(problem, seconds=12.0, max_rows=None):
             "seconds": t_used}
 
 
+def cpu_gmres_baseline():
+    """The oracle's BD-GMRES on the host cores (TEST INFRA: oracle/), next to the
+    GPU solves (north_star; P:l.719-723 reports "Build PC" and "GMRES" per run):
+      config 3 -- a full solve to 1e-8 (BD in the oracle's LU-solve form);
+      config 4 -- bounded: LU of the 1000 pore blocks (timed), LU of the leading
+        4096^2 block of the 16384^2 wall block (timed, extrapolated x 64 = O(n^3)),
+        one oracle matvec (timed) as the cost of an iteration (BD apply and CGS2
+        are < 5% of it), times the GPU solve's iteration count -- extrapolated,
+        and labelled so."""
+    import numpy as np
+
+    import oracle
+    from bie_inputs import make_problem, rhs_pipe
+
+    out = {"cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "kind": "oracle"}
+    p = make_problem(3)
+    og = oracle.OracleGeometry(p)
+    f = rhs_pipe(p)
+    t0 = time.perf_counter()
+    bd = oracle.OracleBDLU(og)
+    t1 = time.perf_counter()
+    r = oracle.gmres_bdlu(og, f, bd, tol=1e-8, max_iter=1000)
+    t2 = time.perf_counter()
+    out["config3"] = {"build_pc_s": t1 - t0, "gmres_s": t2 - t1, "iters": r["iters"], "converged": r["converged"],
+                      "res_true": r["res_true"], "sample": "full oracle BD-GMRES solve (LU-form BD), measured"}
+    del bd
+    p = make_problem(4)
+    og = oracle.OracleGeometry(p)
+    nw = 2 * p.n_outer
+    t0 = time.perf_counter()
+    for b in range(p.M):  # the pore blocks, factored as the oracle's BD does
+        oracle.lu(og.bd_block(b))
+    t_pores = time.perf_counter() - t0
+    W = og.bd_block(p.M)[:4096, :4096].copy()
+    t0 = time.perf_counter()
+    oracle.lu(W)
+    t_w4096 = time.perf_counter() - t0
+    s = rhs_pipe(p)
+    t0 = time.perf_counter()
+    og.apply(s)
+    t_mv = time.perf_counter() - t0
+    build = t_pores + t_w4096 * (nw / 4096) ** 3
+    out["config4"] = {"build_pc_s_extrapolated": build, "pores_factor_s": t_pores,
+                      "wall_lu_4096_s": t_w4096, "matvec_s": t_mv,
+                      "gmres_s_per_iteration_extrapolated": t_mv,
+                      "sample": f"extrapolated: pore factors timed; wall LU ({nw}^2) from a timed 4096^2 LU x "
+                                f"{(nw / 4096) ** 3:.0f}; per iteration = one timed oracle matvec (BD apply and "
+                                f"CGS2 excluded, < 5% of it)"}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle as it stands, same metric/unit, rank 0 only."""
     ws, rank, _ = _dist()
@@ -218,13 +270,16 @@ def config5_sweep(bie, dev, stream):
         s = torch.from_numpy(density(p, nvec=nvec).reshape(-1)).to(dev)
         o = torch.zeros_like(s)
         bie.dlp_apply(g, s, o, nvec)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        bie.dlp_apply(g, s, o, nvec)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b)
-        res[f"nvec{nvec}"] = {"ms": ms, "pairs_per_s": nvec * p.N * p.N / (ms * 1e-3),
+        times = []
+        for _ in range(3):  # median of 3
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            bie.dlp_apply(g, s, o, nvec)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        ms = statistics.median(times)
+        res[f"nvec{nvec}"] = {"ms": ms, "ms_each": times, "pairs_per_s": nvec * p.N * p.N / (ms * 1e-3),
                               "alg_tflops": (11 + 8 * nvec) * p.N * p.N / (ms * 1e-3) / 1e12}
         del s, o
     og = oracle.OracleGeometry(p)
@@ -302,6 +357,8 @@ def run_gpu(args):
     for _ in range(max(3, args.warmup)):
         r = step()
     assert r["iters"] == GMRES_ITERS
+    # measured FP64 peak of this device (DFMA chains, libbie.so bie_fp64_peak), best of 3
+    fp64_meas = max(bie.fp64_peak(200000)["tflops"] for _ in range(3))
 
     # ---- timed region: device-resident inputs, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -340,14 +397,18 @@ def run_gpu(args):
     pairs_share = prof["pairs_ms"] / sum(step_ms)
 
     # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
+    # (N = 1: bie_gmres_solve_host, the C-ABI call with pinned HOST f and x)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk_e2e:
         for k in range(args.steps):
             flush.fill_(float(k))
             e2e_ev[k][0].record(stream)
-            f.copy_(f_host, non_blocking=True)
-            step()
-            x_host.copy_(x, non_blocking=True)
+            if ws == 1:
+                bie.gmres_solve_host(g, bd, f_host, x_host, tol=1e-30, max_iter=GMRES_ITERS)
+            else:
+                f.copy_(f_host, non_blocking=True)
+                step()
+                x_host.copy_(x, non_blocking=True)
             e2e_ev[k][1].record(stream)
         torch.cuda.synchronize()
     e2e_ms_each = [a.elapsed_time(b) for a, b in e2e_ev]
@@ -485,10 +546,15 @@ def run_gpu(args):
                                 else "all-pairs phase on this rank's slice of the symmetric work list"),
                      "bound": "alu", "achieved": achieved_tflops,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
-                     "traffic": _ncu_traffic(), "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
+                     "traffic": _ncu_traffic(), "traffic_source": "profiles/round2/k_dlp_sym_traffic.json "
+                     "(dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full, one launch)",
+                     "peak_measured": fp64_meas, "frac_of_measured": achieved_tflops / fp64_meas,
+                     "peak_measured_source": "bie_fp64_peak in this run: DFMA chains, 8 x 256-thread CTAs/SM",
+                     "flop_per_pair": FLOP_PER_PAIR, "kernel_ms": pair_ms,
                      "kernel_share_of_step": pairs_share,
                      "executed_flop_per_pair": 17,
                      "ncu_fp64_pipe_active_pct": _ncu_traffic("fp64_pipe_active_pct"),
+                     "ncu_fp64_pipe_source": "profiles/round2/k_dlp_sym_traffic.json (ncu capture of this kernel)",
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md s5)"},
         "e2e": {"value": args.steps * pairs_per_step / e2e_s, "unit": "pair-interactions/s",
                 "h2d_bytes_per_step": int(f_host.numel() * 8), "d2h_bytes_per_step": int(x_host.numel() * 8),
@@ -502,6 +568,13 @@ def run_gpu(args):
     if not args.no_cpu_baseline and ws == 1:
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline_sample(p, seconds=args.cpu_seconds).items()
                                 if k != "seconds"}
+        if not args.quick:
+            cg = cpu_gmres_baseline()
+            it4 = extra.get("gmres_solve", {}).get(f"config{CONFIG_ID}", {}).get("iters")
+            if it4:
+                cg["config4"]["iters_of_gpu_solve"] = it4
+                cg["config4"]["gmres_s_extrapolated"] = it4 * cg["config4"]["gmres_s_per_iteration_extrapolated"]
+            line["cpu_baseline"]["gmres"] = cg
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -28,6 +28,7 @@ from .geometry import (  # noqa: F401
     density,
     pore_node_positions,
     node_positions,
+    interior_grid,
 )
 from .rhs import (  # noqa: F401
     rhs_pipe,

@@ -212,3 +212,31 @@ def pore_node_positions(problem: Problem) -> np.ndarray:
 def node_positions(problem: Problem) -> np.ndarray:
     """All collocation points in dof order (pores first, then Gamma_0)."""
     return np.concatenate([pore_node_positions(problem), problem.outer_xy], axis=0)
+
+
+def interior_grid(problem: Problem, nx: int, ny: int):
+    """Evaluation points for the error field eps(x) (P:l.752-757): a regular
+    nx x ny grid over the pipe's bounding box, keeping only points inside the
+    fluid domain that are RELIABLE for the trapezoid rule -- farther than
+    sqrt(ds) from every boundary, ds the local node spacing of that boundary
+    (P:l.355-358 footnote).  Pure sampling; returns (P, 2)."""
+    L, H = problem.meta["L"], problem.meta["H"]
+    xs = (np.arange(nx) + 0.5) * L / nx
+    ys = -H + (np.arange(ny) + 0.5) * 2 * H / ny
+    P = np.stack(np.meshgrid(xs, ys, indexing="ij"), axis=-1).reshape(-1, 2)
+    keep = np.ones(P.shape[0], dtype=bool)
+    if problem.M:
+        ds_p = 2 * np.pi * problem.pore_r / problem.n_pore
+        for k in range(problem.M):
+            d = np.hypot(P[:, 0] - problem.pore_c[k, 0], P[:, 1] - problem.pore_c[k, 1]) - problem.pore_r[k]
+            keep &= d > np.sqrt(ds_p[k])
+    w = problem.outer_xy
+    seg = np.roll(w, -1, axis=0) - w
+    ds_w = np.hypot(seg[:, 0], seg[:, 1]).max()
+    # inside Gamma_0 (the mollified rectangle lies within [0, L] x [-H, H]) and far from it
+    from scipy.spatial import cKDTree
+
+    dw, _ = cKDTree(w).query(P)
+    keep &= dw > np.sqrt(ds_w) + ds_w
+    keep &= (np.abs(P[:, 1]) < H) & (P[:, 0] > 0) & (P[:, 0] < L)
+    return P[keep]

@@ -185,6 +185,18 @@ BIE_API int bie_blockdiag_block_inverse(bie_blockdiag_t bd, int body, double *ho
 BIE_API int bie_gmres_solve(bie_geometry_t g, bie_blockdiag_t bd, const double *f, double *x, double tol, int max_iter,
                     double *hist_host, int *iters, double *res_pc, double *res_true, int *converged,
                     void *stream);
+/*
+ * bie_gmres_solve_host -- bie_gmres_solve with HOST buffers (the end-to-end
+ * call): f_host [2N] is copied to a device staging buffer owned
+ * by the geometry, solved on the device, and x_host [2N] receives the solution.
+ * Pinned (cudaHostAlloc / torch pin_memory) buffers give async DMA copies on
+ * `stream`; pageable buffers also work.  Same outputs, bars and errors as
+ * bie_gmres_solve (+ BIE_EINVAL for f_host == x_host).  Synchronous: returns
+ * after x_host is written.  Not re-entrant per geometry (shared staging).
+ */
+BIE_API int bie_gmres_solve_host(bie_geometry_t g, bie_blockdiag_t bd, const double *f_host, double *x_host,
+                                 double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                                 double *res_true, int *converged, void *stream);
 
 /*
  * bie_gmres_solve_batch -- SURVEY s8(f) NEXT-3: nrhs independent left-
@@ -272,6 +284,14 @@ BIE_API const char *bie_last_error(void);
 BIE_API int bie_profile_begin(bie_geometry_t g);
 BIE_API int bie_profile_end(bie_geometry_t g, double *ms_moments, double *ms_pairs, double *ms_epilogue,
                             int *applies);
+/*
+ * bie_fp64_peak -- measurement hook: runs a DFMA-chain kernel (8 independent
+ * chains per thread, 8 x 256-thread CTAs per SM) for `iters` iterations on
+ * `stream` and returns the achieved FP64 rate (tflops, 2 flop per DFMA) and
+ * its duration (ms, CUDA events).  The measured denominator of the all-pairs
+ * roofline.  Errors: BIE_EINVAL, BIE_ECUDA.  Synchronous.
+ */
+BIE_API int bie_fp64_peak(int iters, double *tflops, double *ms, void *stream);
 BIE_API long long bie_launch_count(void);
 
 /*

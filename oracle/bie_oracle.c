@@ -1025,7 +1025,9 @@ static int ora_gmres_core(int n, ora_op A, void *actx, ora_op P, void *pctx, con
         }
         {
             double a = H[(size_t)k * max_iter + k], b = H[(size_t)(k + 1) * max_iter + k];
-            double d = hypot(a, b);
+            /* sqrt(a^2 + b^2) correctly rounded (reading C28: library hypot()s
+             * differ by an ulp; quad-precision evaluation, one rounding) */
+            double d = (double)sqrtq((__float128)a * a + (__float128)b * b);
             cs[k] = a / d;
             sn[k] = b / d;
             H[(size_t)k * max_iter + k] = d;

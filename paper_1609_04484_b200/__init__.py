@@ -24,12 +24,14 @@ from ._bie import (  # noqa: F401
     dlp_sym_info,
     field_eval,
     gmres_solve,
+    gmres_solve_host,
     gmres_solve_batch,
     gmres_solve_batch_slp,
     gmres_solve_slp,
     kr_weights,
     launch_count,
     pore_template,
+    fp64_peak,
     profile_begin,
     profile_end,
     slp_apply,

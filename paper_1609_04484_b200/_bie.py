@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "bie_kr_weights", "bie_slp_apply", "bie_slp_apply_rows", "bie_slp_field_eval", "bie_blockdiag_factor_slp",
     "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp", "bie_blockdiag_factor_structured",
     "bie_slp_pairs_partial", "bie_slp_epilogue_rows", "bie_blockdiag_factor_range_slp",
-    "bie_geometry_node_table", "bie_pore_template",
+    "bie_geometry_node_table", "bie_pore_template", "bie_gmres_solve_host", "bie_fp64_peak",
 )
 
 
@@ -75,6 +75,8 @@ def lib():
         "bie_blockdiag_destroy": [vp],
         "bie_blockdiag_block_inverse": [vp, c_int, dp, ctypes.c_longlong],
         "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
+        "bie_gmres_solve_host": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
+        "bie_fp64_peak": [c_int, dp, dp, vp],
         "bie_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_gmres_solve_batch": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_blockdiag_factor_range": [vp, c_int, c_int, ctypes.POINTER(vp), vp],
@@ -193,6 +195,13 @@ class Geometry:
             self.close()
         except Exception:
             pass
+
+
+def fp64_peak(iters: int = 20000, stream=None) -> dict:
+    """bie_fp64_peak: measured DFMA-chain FP64 rate of this device (TFLOP/s) and its duration."""
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().bie_fp64_peak(int(iters), ctypes.byref(tf), ctypes.byref(ms), _stream_ptr(stream)))
+    return dict(tflops=tf.value, ms=ms.value)
 
 
 def pore_template(n: int) -> np.ndarray:
@@ -404,6 +413,35 @@ def gmres_solve(g: Geometry, bd: BlockDiag | None, f, x, tol: float = 1e-8, max_
     _check(lib().bie_gmres_solve(g.h, None if bd is None else bd.h, _dev_ptr(f, "f", 2 * g.N),
                                  _dev_ptr(x, "x", 2 * g.N), float(tol), int(max_iter), _dp(hist), ctypes.byref(it),
                                  ctypes.byref(rp), ctypes.byref(rt), ctypes.byref(conv), _stream_ptr(stream)))
+    return dict(iters=it.value, hist=hist[: it.value + 1].copy(), res_pc=rp.value, res_true=rt.value,
+                converged=bool(conv.value))
+
+
+def _host_ptr(a, name, n):
+    """Address of a host float64 buffer (numpy array or CPU torch tensor, pinned or not)."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or a.size < n:
+            raise ValueError(f"{name} must be a contiguous float64 array with >= {n} elements")
+        return ctypes.c_void_p(a.ctypes.data)
+    import torch
+
+    if not isinstance(a, torch.Tensor) or a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous() \
+            or a.numel() < n:
+        raise ValueError(f"{name} must be a contiguous float64 host tensor with >= {n} elements")
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def gmres_solve_host(g: Geometry, bd: BlockDiag | None, f_host, x_host, tol: float = 1e-8, max_iter: int = 1000,
+                     stream=None):
+    """bie_gmres_solve_host: f_host / x_host are HOST buffers [2N] (pinned for async DMA);
+    H2D copy, solve and D2H copy inside the call, which returns after x_host is written."""
+    hist = np.zeros(max_iter + 1)
+    it, conv = ctypes.c_int(0), ctypes.c_int(0)
+    rp, rt = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().bie_gmres_solve_host(g.h, None if bd is None else bd.h, _host_ptr(f_host, "f_host", 2 * g.N),
+                                      _host_ptr(x_host, "x_host", 2 * g.N), float(tol), int(max_iter), _dp(hist),
+                                      ctypes.byref(it), ctypes.byref(rp), ctypes.byref(rt), ctypes.byref(conv),
+                                      _stream_ptr(stream)))
     return dict(iters=it.value, hist=hist[: it.value + 1].copy(), res_pc=rp.value, res_true=rt.value,
                 converged=bool(conv.value))
 

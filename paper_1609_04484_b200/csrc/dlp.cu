@@ -372,16 +372,67 @@ constexpr int kSymWarps = 4;
 constexpr int kSymTB = 32 * kSymR * kSymWarps;  // 512
 constexpr int kSymChunk = 32;
 
-__global__ void k_quad(const double2 *__restrict__ nw, const double *__restrict__ sigma, double4 *Q, int N) {
+// ---------------------------------------------------------------------------
+// Order-independent exact accumulation (symmetric path).  A pair-sum
+// contribution v (one unit's 512-target sum for a source, or one segment's
+// sum for a target) is scaled by 2^-E (E = exponent of max |Q|, so the window
+// follows the data) and split exactly into three integer limbs
+//   v 2^-E = x2 + x1 2^-32 + x0 2^-64 - t,  x2 = floor, x1, x0 in [0, 2^32),
+// (truncation t < 2^-64), each added with a 64-bit integer RED to its own
+// accumulator.  Integer addition is associative, so the totals -- and the
+// double the epilogue forms from them -- do not depend on which CTA added
+// what when: bitwise deterministic results with O(N) memory (3 x 2N words)
+// and no ordering waits.  The round-1 form kept one FP64 partial per
+// (512-node block, node): N x nTB doubles, 35 GB at config 5.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void fx_add(unsigned long long *acc, long long limb_stride, double v) {
+    const double f2 = floor(v);
+    const double t1 = (v - f2) * 4294967296.0;  // both steps exact
+    const double f1 = floor(t1);
+    const double f0 = floor((t1 - f1) * 4294967296.0);
+    atomicAdd(acc, (unsigned long long)(long long)f2);
+    atomicAdd(acc + limb_stride, (unsigned long long)f1);
+    atomicAdd(acc + 2 * limb_stride, (unsigned long long)f0);
+}
+// sum of the three limb totals (carry-normalised, exact) as a double, times 2^E
+__device__ __forceinline__ double fx_value(const unsigned long long *acc, long long limb_stride, double scale_back) {
+    unsigned long long x2 = acc[0], x1 = acc[limb_stride], x0 = acc[2 * limb_stride];
+    x1 += x0 >> 32;
+    x0 &= 0xffffffffull;
+    x2 += x1 >> 32;
+    x1 &= 0xffffffffull;
+    const double frac = __ull2double_rn((x1 << 32) | x0) * 0x1p-64;
+    return ((double)(long long)x2 + frac) * scale_back;
+}
+// 2^-E and 2^E for the accumulation window (E = exponent of max |Q|, 0 if Q = 0)
+__device__ __forceinline__ void fx_scales(const unsigned long long *qmax_bits, double &scale, double &scale_back) {
+    const double qm = __longlong_as_double((long long)*qmax_bits);
+    const int E = qm > 0.0 ? ilogb(qm) : 0;
+    scale = ldexp(1.0, -E);
+    scale_back = ldexp(1.0, E);
+}
+__device__ __forceinline__ void qmax_update(double m, unsigned long long *qmax_bits) {
+    // m >= 0: IEEE order of non-negative doubles is their integer order
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(qmax_bits, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_quad(const double2 *__restrict__ nw, const double *__restrict__ sigma, double4 *Q, int N,
+                       unsigned long long *qmax_bits) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= N) return;
-    const double2 a = nw[j];
-    const double2 b = reinterpret_cast<const double2 *>(sigma)[j];
-    // (Qxx, Qxy, Qyy - Qxx): with d = rx^2 + ry^2,
-    //   Qxx rx^2 + Qxy rx ry + Qyy ry^2 = Qxx d + Qxy rx ry + (Qyy - Qxx) ry^2,
-    // so the pair loop never forms rx^2 (21 instead of 22 FP64 instructions)
-    const double qxx = a.x * b.x;
-    Q[j] = make_double4(qxx, fma(a.x, b.y, a.y * b.x), fma(a.y, b.y, -qxx), 0.0);
+    double m = 0.0;
+    if (j < N) {
+        const double2 a = nw[j];
+        const double2 b = reinterpret_cast<const double2 *>(sigma)[j];
+        // (Qxx, Qxy, Qyy - Qxx): with d = rx^2 + ry^2,
+        //   Qxx rx^2 + Qxy rx ry + Qyy ry^2 = Qxx d + Qxy rx ry + (Qyy - Qxx) ry^2,
+        // so the pair loop never forms rx^2 (21 instead of 22 FP64 instructions)
+        const double qxx = a.x * b.x;
+        const double4 q = make_double4(qxx, fma(a.x, b.y, a.y * b.x), fma(a.y, b.y, -qxx), 0.0);
+        Q[j] = q;
+        m = fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z)));
+    }
+    qmax_update(m, qmax_bits);
 }
 
 // One unordered pair (target t, source s) of the symmetric kernels: the target
@@ -391,7 +442,10 @@ __device__ __forceinline__ void dlp_pairpair(double tx, double ty, double tqa, d
                                              double sy, double sqa, double sqb, double sqc, double &ax, double &ay,
                                              double &bx, double &by) {
     const double rx = tx - sx, ry = ty - sy;
-    const double yy = fma(ry, ry, 1e-300), xy = rx * ry;
+    // + 1e-150: below one ulp of any real pair distance^2, and keeps
+    // q = 1/d^2 <= 1e300 finite for coincident points (zero padding at a target
+    // that sits at the origin: cs q then stays finite and r = 0 zeroes it)
+    const double yy = fma(ry, ry, 1e-150), xy = rx * ry;
     const double d = fma(rx, rx, yy);
     double i = rcp_approx(d);
     const double cs = fma(sqa, d, fma(sqb, xy, sqc * yy));  // target <- source (Q' form, k_quad)
@@ -428,8 +482,8 @@ struct SymArgs {
     const double2 *pos;
     const double4 *Q;
     const long long *off;  // [nTB + 1] prefix of units per block
-    double *tgt_partial;   // [S][2N]
-    double *src_partial;   // [nTB][2N]
+    unsigned long long *acc;        // [3][2N] fixed-point limbs of the pair sums (fx_add; zeroed per launch)
+    const unsigned long long *qmax; // max |Q| (bits) from k_quad / k_slp_scale: accumulation window
     int N, nTB;
     long long U;           // units in this launch's slice [ub, ub + U) of the triangular list
     long long ub;          // 0 for the single-GPU matvec; a rank's slice start when sharded
@@ -439,8 +493,6 @@ struct SymArgs {
     unsigned long long *counter;  // next free segment (zeroed before each launch)
 };
 
-
-
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -449,25 +501,26 @@ __device__ __forceinline__ unsigned long long global_ns() {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-template <int SR, int SW, int MINB = 1, bool QS = false, int TP = 0, int OP = 0, bool DS = false>
+// A3, nvec = 1: symmetric all-pairs kernel.  SR targets per lane, SW warps
+// (SR SW 32 = 512-node blocks), NS sources per step: at step t lane l pairs
+// each of its targets with sources (l + t + k 32/NS) mod 32, k < NS, so every
+// step carries SR x NS independent pair chains and NS rotating source
+// accumulators (NS = 2 is the round-1 "dual-source" form).
+// Both sides flush into the fixed-point limb accumulators (fx_add): a unit's
+// 32 source sums (added over the warps in fixed order) at the unit's end, the
+// targets' register sums at a segment's end or block change.  The totals are
+// exact integers, so results are bitwise deterministic however the dynamic
+// segments were scheduled.
+// OP = 1: single-layer operator (NEXT-1); Q holds (S_x, S_y, 0, 0) with
+// S = w sigma / (4 pi) and both directions add hl S + (r.S) r / rho^2.
+// GR > 0 (DLP only): the pairs of GR targets x NS sources are written stage by
+// stage in lockstep (all differences, then all rho^2, all seeds, ...), which
+// changes the order ptxas's list scheduler starts from.
+template <int SR, int SW, int NS, int MINB = 1, int OP = 0, int UNR = (OP == 1 ? 2 : 1), int GR = 0>
 __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
-    // DS: dual-source steps -- each of 16 steps pairs every target with sources
-    // (l + t) and (l + t + 16); two rotating source accumulators give the
-    // independent chains with half the target registers of SR = 8.
-    // OP = 1: single-layer operator (NEXT-1).  Q holds (S_x, S_y, 0, 0) with
-    // S = w sigma / (4 pi); G is even in r, so both directions get
-    //   u += hl S + (r . S) r / rho^2   with the shared hl = -1/2 log rho^2, 1/rho^2.
-    // TP: source-step pipelining.  0: none; 1: the next step's source is read
-    // from shared memory one step ahead (hides the LDS latency at the loop
-    // head); 2: the step loop is unrolled by two.
-    // QS: keep the targets' quadratic forms in shared memory (lane-private
-    // slots) instead of registers, trading 3 shared loads per pair for 48
-    // registers (more resident warps)
-    __shared__ double2 s_tqab[QS ? SW : 1][QS ? SR : 1][32];
-    __shared__ double s_tqc[QS ? SW : 1][QS ? SR : 1][32];
     static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
-    static_assert(SR % 2 == 0, "two interleaved chains");
-    __shared__ double2 red[SW][32];
+    static_assert(NS == 2 || NS == 4, "2 or 4 sources per step");
+    constexpr int STEPS = 32 / NS;
     __shared__ __align__(16) double2 s_src[2][SW][3][32];  // [buf][warp][(x,y) | (qa,qb) | (qc,-)][lane]
     __shared__ LogTabT<OP == 1> s_log;  // OP = 1 only
     if constexpr (OP == 1) log_tab_init(s_log, threadIdx.x, 32 * SW);  // visible after the first segment barrier
@@ -476,14 +529,12 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     const long long U = a.U, Useg = a.Useg;
     if (a.trace && threadIdx.x == 0) a.trace[2 * p] = global_ns();
     const int N = a.N;
-    // Work distribution: the slice's unit list is cut into fixed segments that
-    // CTAs claim from an atomic counter.  A static equal split left the CTAs
-    // the warp schedulers favour idle for the last 40% of the launch (measured
-    // per-CTA durations 8.0 vs 13.8 ms); segment-indexed partial slots keep the
-    // summation order independent of which CTA ran which segment.
     __shared__ long long s_seg;
     int A = 0;
     long long offA = 0, offA1 = 0;
+    double fxs, fxb;
+    fx_scales(a.qmax, fxs, fxb);
+    const long long L = 2LL * N;  // limb stride
 
     double tx[SR], ty[SR], tqa[SR], tqb[SR], tqc[SR], ax[SR], ay[SR];
     auto load_targets = [&](int blk) {
@@ -498,14 +549,9 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
             }
             tx[r] = x.x;
             ty[r] = x.y;
-            if constexpr (QS) {
-                s_tqab[w][r][lane] = make_double2(q.x, q.y);
-                s_tqc[w][r][lane] = q.z;
-            } else {
-                tqa[r] = q.x;
-                tqb[r] = q.y;
-                tqc[r] = q.z;
-            }
+            tqa[r] = q.x;
+            tqb[r] = q.y;
+            tqc[r] = q.z;
             ax[r] = 0.0;
             ay[r] = 0.0;
         }
@@ -513,9 +559,7 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
     const int src_lane = (lane + 1) & 31;
     // The chunk's sources sit in this warp's shared-memory slice (double
     // buffered; the next unit's chunk is fetched by cp.async while this one is
-    // computed).  At step t lane l reads source (l + t) mod 32 (conflict-free),
-    // so the source data carry no loop dependency -- only the accumulators
-    // rotate by __shfl.
+    // computed); only the accumulators rotate by __shfl.
     auto fetch = [&](int buf, int blk, long long uoff) {  // chunk of unit uoff within block blk
         const int cc = (blk + 1) * (kSymTB / kSymChunk) + (int)uoff;
         const int jj = cc * kSymChunk + lane;
@@ -559,184 +603,108 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
         }
         cp_async_wait<1>();
         __syncwarp();
-        double sx, sy, sqa, sqb, sqc, bx = 0.0, by = 0.0;
-        // Two pair chains are written stage by stage in lockstep (targets r, r+1)
-        // and the source accumulator is split in two, so ptxas keeps two
-        // independent dependency chains per warp in flight (a single chain per
-        // warp left the FP64 pipe idle on DFMA latency: 72% active).
-        double bx1 = 0.0, by1 = 0.0;
-        double2 nxy, nab;
-        double nc;
-        if constexpr (DS) {
-            double bxA = 0.0, byA = 0.0, bxB = 0.0, byB = 0.0;
-            // unrolled by two for the single layer (19.84 -> 19.73 ms at config 4);
-            // the DLP is faster rolled (12.76 vs 12.80 ms)
-#pragma unroll(OP == 1 ? 2 : 1)
-            for (int t = 0; t < 16; ++t) {
-                const int la = (lane + t) & 31, lb = (lane + t + 16) & 31;
-                const double2 xa = s_src[buf][w][0][la], qa = s_src[buf][w][1][la];
-                const double2 xb = s_src[buf][w][0][lb], qb = s_src[buf][w][1][lb];
-                const double ca = s_src[buf][w][2][la].x, cb = s_src[buf][w][2][lb].x;
+        double bx[NS], by[NS];
 #pragma unroll
-                for (int r = 0; r < SR; ++r) {
-                    double ta, tb, tc;
-                    if constexpr (QS) {
-                        const double2 ab = s_tqab[w][r][lane];
-                        ta = ab.x;
-                        tb = ab.y;
-                        tc = s_tqc[w][r][lane];
-                    } else {
-                        ta = tqa[r];
-                        tb = tqb[r];
-                        tc = tqc[r];
+        for (int k = 0; k < NS; ++k) bx[k] = by[k] = 0.0;
+        // UNR: the step loop unrolled by two for the single layer (19.84 -> 19.73 ms
+        // at config 4, round 1); the DLP is faster rolled
+#pragma unroll(UNR)
+        for (int t = 0; t < STEPS; ++t) {
+            double2 xs[NS], qs[NS];
+            double cq[NS];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const int l = (lane + t + k * STEPS) & 31;
+                xs[k] = s_src[buf][w][0][l];
+                qs[k] = s_src[buf][w][1][l];
+                cq[k] = s_src[buf][w][2][l].x;
+            }
+            if constexpr (GR > 0 && OP == 0) {
+                constexpr int G = GR * NS;
+#pragma unroll
+                for (int r0 = 0; r0 < SR; r0 += GR) {
+                    double rx[G], ry[G], yy[G], xy[G], d[G], iv[G], cs[G], ct[G];
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const int r = r0 + q / NS, k = q % NS;
+                        rx[q] = tx[r] - xs[k].x;
+                        ry[q] = ty[r] - xs[k].y;
                     }
-                    if constexpr (OP == 1) {
-                        slp_pairpair(tx[r], ty[r], ta, tb, xa.x, xa.y, qa.x, qa.y, ax[r], ay[r], bxA, byA, s_log);
-                        slp_pairpair(tx[r], ty[r], ta, tb, xb.x, xb.y, qb.x, qb.y, ax[r], ay[r], bxB, byB, s_log);
-                    } else {
-                        dlp_pairpair(tx[r], ty[r], ta, tb, tc, xa.x, xa.y, qa.x, qa.y, ca, ax[r], ay[r], bxA, byA);
-                        dlp_pairpair(tx[r], ty[r], ta, tb, tc, xb.x, xb.y, qb.x, qb.y, cb, ax[r], ay[r], bxB, byB);
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        yy[q] = fma(ry[q], ry[q], 1e-150);
+                        xy[q] = rx[q] * ry[q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        d[q] = fma(rx[q], rx[q], yy[q]);
+                        iv[q] = rcp_approx(d[q]);
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const int r = r0 + q / NS, k = q % NS;
+                        cs[q] = fma(qs[k].x, d[q], fma(qs[k].y, xy[q], cq[k] * yy[q]));
+                        ct[q] = fma(tqa[r], d[q], fma(tqb[r], xy[q], tqc[r] * yy[q]));
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const double e = fma(-d[q], iv[q], 1.0);
+                        iv[q] = fma(iv[q], fma(e, e, e), iv[q]);
+                    }
+#pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const int r = r0 + q / NS, k = q % NS;
+                        const double qq = iv[q] * iv[q];
+                        const double av = cs[q] * qq, bv = ct[q] * qq;
+                        ax[r] = fma(av, rx[q], ax[r]);
+                        ay[r] = fma(av, ry[q], ay[r]);
+                        bx[k] = fma(-bv, rx[q], bx[k]);
+                        by[k] = fma(-bv, ry[q], by[k]);
                     }
                 }
-                bxA = shfl_d(bxA, src_lane);
-                byA = shfl_d(byA, src_lane);
-                bxB = shfl_d(bxB, src_lane);
-                byB = shfl_d(byB, src_lane);
-            }
-            // after 16 rotations source l's B-accumulator is back in lane l and
-            // its A-accumulator sits in lane l + 16
-            bx = bxB;
-            by = byB;
-            bx1 = __shfl_xor_sync(0xffffffffu, bxA, 16);
-            by1 = __shfl_xor_sync(0xffffffffu, byA, 16);
-        }
-        if constexpr (TP == 1 && !DS) {
-            nxy = s_src[buf][w][0][lane];
-            nab = s_src[buf][w][1][lane];
-            nc = s_src[buf][w][2][lane].x;
-        }
-#pragma unroll(TP == 2 ? 2 : 1)
-        for (int t = 0; t < (DS ? 0 : 32); ++t) {
-            if constexpr (TP == 1) {
-                sx = nxy.x;
-                sy = nxy.y;
-                sqa = nab.x;
-                sqb = nab.y;
-                sqc = nc;
-                const int sl = (lane + t + 1) & 31;
-                nxy = s_src[buf][w][0][sl];
-                nab = s_src[buf][w][1][sl];
-                nc = s_src[buf][w][2][sl].x;
             } else {
-                const int sl = (lane + t) & 31;
-                const double2 xy = s_src[buf][w][0][sl], ab = s_src[buf][w][1][sl];
-                sx = xy.x;
-                sy = xy.y;
-                sqa = ab.x;
-                sqb = ab.y;
-                sqc = s_src[buf][w][2][sl].x;
+#pragma unroll
+            for (int r = 0; r < SR; ++r) {
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    if constexpr (OP == 1)
+                        slp_pairpair(tx[r], ty[r], tqa[r], tqb[r], xs[k].x, xs[k].y, qs[k].x, qs[k].y, ax[r], ay[r],
+                                     bx[k], by[k], s_log);
+                    else
+                        dlp_pairpair(tx[r], ty[r], tqa[r], tqb[r], tqc[r], xs[k].x, xs[k].y, qs[k].x, qs[k].y, cq[k],
+                                     ax[r], ay[r], bx[k], by[k]);
+                }
+            }
             }
 #pragma unroll
-            for (int r = 0; r < SR; r += 2) {
-                if constexpr (OP == 1) {
-                    const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
-                    const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
-                    double hl0, hl1, i0, i1;
-                    {
-                        // zero padding only (no self pairs here): see slp_pairpair
-                        const double d0 = fma(rx0, rx0, fma(ry0, ry0, 1e-300));
-                        const double d1 = fma(rx1, rx1, fma(ry1, ry1, 1e-300));
-                        i0 = rcp_approx(d0);
-                        i1 = rcp_approx(d1);
-                        const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
-                        i0 = fma(i0, fma(e0, e0, e0), i0);
-                        i1 = fma(i1, fma(e1, e1, e1), i1);
-                        hl0 = neg_half_log_tab(d0, s_log);
-                        hl1 = neg_half_log_tab(d1, s_log);
-                    }
-                    const double ct0 = i0 * fma(rx0, sqa, ry0 * sqb), ct1 = i1 * fma(rx1, sqa, ry1 * sqb);
-                    const double cs0 = i0 * fma(rx0, tqa[r], ry0 * tqb[r]);
-                    const double cs1 = i1 * fma(rx1, tqa[r + 1], ry1 * tqb[r + 1]);
-                    ax[r] = fma(ct0, rx0, fma(hl0, sqa, ax[r]));
-                    ay[r] = fma(ct0, ry0, fma(hl0, sqb, ay[r]));
-                    ax[r + 1] = fma(ct1, rx1, fma(hl1, sqa, ax[r + 1]));
-                    ay[r + 1] = fma(ct1, ry1, fma(hl1, sqb, ay[r + 1]));
-                    bx = fma(cs0, rx0, fma(hl0, tqa[r], bx));
-                    by = fma(cs0, ry0, fma(hl0, tqb[r], by));
-                    bx1 = fma(cs1, rx1, fma(hl1, tqa[r + 1], bx1));
-                    by1 = fma(cs1, ry1, fma(hl1, tqb[r + 1], by1));
-                    continue;
-                }
-                const double rx0 = tx[r] - sx, rx1 = tx[r + 1] - sx;
-                const double ry0 = ty[r] - sy, ry1 = ty[r + 1] - sy;
-                const double yy0 = fma(ry0, ry0, 1e-300), yy1 = fma(ry1, ry1, 1e-300);
-                const double xy0 = rx0 * ry0, xy1 = rx1 * ry1;
-                const double d0 = fma(rx0, rx0, yy0), d1 = fma(rx1, rx1, yy1);
-                double i0 = rcp_approx(d0), i1 = rcp_approx(d1);
-                const double cs0 = fma(sqa, d0, fma(sqb, xy0, sqc * yy0));  // target <- source (Q' form)
-                const double cs1 = fma(sqa, d1, fma(sqb, xy1, sqc * yy1));
-                double qa0, qb0, qc0, qa1, qb1, qc1;
-                if constexpr (QS) {
-                    const double2 ab0 = s_tqab[w][r][lane], ab1 = s_tqab[w][r + 1][lane];
-                    qa0 = ab0.x;
-                    qb0 = ab0.y;
-                    qa1 = ab1.x;
-                    qb1 = ab1.y;
-                    qc0 = s_tqc[w][r][lane];
-                    qc1 = s_tqc[w][r + 1][lane];
-                } else {
-                    qa0 = tqa[r];
-                    qb0 = tqb[r];
-                    qc0 = tqc[r];
-                    qa1 = tqa[r + 1];
-                    qb1 = tqb[r + 1];
-                    qc1 = tqc[r + 1];
-                }
-                const double ct0 = fma(qa0, d0, fma(qb0, xy0, qc0 * yy0));  // source <- target
-                const double ct1 = fma(qa1, d1, fma(qb1, xy1, qc1 * yy1));
-                const double e0 = fma(-d0, i0, 1.0), e1 = fma(-d1, i1, 1.0);
-                i0 = fma(i0, fma(e0, e0, e0), i0);
-                i1 = fma(i1, fma(e1, e1, e1), i1);
-                const double q0 = i0 * i0, q1 = i1 * i1;
-                const double a0 = cs0 * q0, a1 = cs1 * q1;
-                const double b0 = ct0 * q0, b1 = ct1 * q1;
-                ax[r] = fma(a0, rx0, ax[r]);
-                ay[r] = fma(a0, ry0, ay[r]);
-                ax[r + 1] = fma(a1, rx1, ax[r + 1]);
-                ay[r + 1] = fma(a1, ry1, ay[r + 1]);
-                bx = fma(-b0, rx0, bx);
-                by = fma(-b0, ry0, by);
-                bx1 = fma(-b1, rx1, bx1);
-                by1 = fma(-b1, ry1, by1);
+            for (int k = 0; k < NS; ++k) {
+                bx[k] = shfl_d(bx[k], src_lane);
+                by[k] = shfl_d(by[k], src_lane);
             }
-            bx = shfl_d(bx, src_lane);
-            by = shfl_d(by, src_lane);
-            bx1 = shfl_d(bx1, src_lane);
-            by1 = shfl_d(by1, src_lane);
         }
-        bx += bx1;
-        by += by1;
-        // after 32 rotations every source is back in its lane
-        red[w][lane] = make_double2(bx, by);
-        __syncthreads();
-        if (w == 0 && j < N) {
-            double2 s = red[0][lane];
+        // after STEPS rotations, lane l's accumulator k belongs to source
+        // l + (k + 1) STEPS (mod 32): gather source l's NS parts in fixed order
+        double sx = 0.0, sy = 0.0;
 #pragma unroll
-            for (int q = 1; q < SW; ++q) {
-                s.x += red[q][lane].x;
-                s.y += red[q][lane].y;
-            }
-            reinterpret_cast<double2 *>(a.src_partial + (long long)A * 2LL * N)[j] = s;
+        for (int k = 0; k < NS; ++k) {
+            const int from = (lane - (k + 1) * STEPS) & 31;
+            sx += shfl_d(bx[k], from);
+            sy += shfl_d(by[k], from);
         }
-        __syncthreads();
+        // each warp adds its own 32 source sums: the limb totals do not depend on
+        // the order, so no cross-warp reduction (and no block barrier) per unit
+        if (j < N) {
+            fx_add(a.acc + 2LL * j, L, sx * fxs);
+            fx_add(a.acc + 2LL * j + 1, L, sy * fxs);
+        }
         if (u + 1 == u1 || u + 1 == offA1) {
-            const int slot = (int)(sg - seg_of(std::max(offA, a.ub), a.ub, Useg));
 #pragma unroll
             for (int r = 0; r < SR; ++r) {
                 const int i = A * kSymTB + w * (32 * SR) + r * 32 + lane;
-                if (i < N)
-                    reinterpret_cast<double2 *>(a.tgt_partial + (long long)slot * 2LL * N)[i] =
-                        make_double2(ax[r], ay[r]);
+                if (i < N) {
+                    fx_add(a.acc + 2LL * i, L, ax[r] * fxs);
+                    fx_add(a.acc + 2LL * i + 1, L, ay[r] * fxs);
+                }
             }
             if (u + 1 < u1) {
                 ++A;
@@ -856,11 +824,9 @@ struct Chunk {
 };
 struct SymEpi {
     int on;                    // 1: partials come from the symmetric path (nvec = 1)
-    const double *tgt_partial; // [S][2N]
-    const double *src_partial; // [nTB][2N]
-    const double *diag;        // [2N]
-    const long long *off;      // [nTB + 1]
-    long long Useg;            // units per segment (slot = segment - first segment of the block)
+    const unsigned long long *acc;   // [3][2N] fixed-point limbs of the pair sums (fx_add)
+    const unsigned long long *qmax;  // accumulation window (fx_scales)
+    const double *diag;        // [dsplit][2N] in-block pair sums (k_dlp_diag)
     int dsplit;                // in-block sums come in dsplit parts [dsplit][2N]
 };
 // A5 completion field of every pore at one target (nvec = 1; readings C5/C6):
@@ -966,22 +932,16 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
     }
     if (a.presum) u[0] = reinterpret_cast<const double2 *>(a.presum)[it];
     if (a.sym.on) {
-        // fixed order: target-side slots, the in-block pairs, then source-side
-        // partials of every earlier block
-        const int B = i / kSymTB;
-        double2 acc = make_double2(0.0, 0.0);
-        const long long oB = a.sym.off[B], oB1 = a.sym.off[B + 1];
-        if (oB1 > oB) {
-            const int first = (int)seg_of(oB, 0, a.sym.Useg);
-            const int last = (int)seg_of(oB1 - 1, 0, a.sym.Useg);
-            sum_strided(acc, a.sym.tgt_partial, 2LL * a.N, last - first + 1, i);
-        }
+        // exact limb totals of the symmetric kernel, then the in-block parts in order
+        double fxs, fxb;
+        fx_scales(a.sym.qmax, fxs, fxb);
+        double2 acc = make_double2(fx_value(a.sym.acc + 2LL * i, 2LL * a.N, fxb),
+                                   fx_value(a.sym.acc + 2LL * i + 1, 2LL * a.N, fxb));
         for (int q = 0; q < a.sym.dsplit; ++q) {
             const double2 pv = reinterpret_cast<const double2 *>(a.sym.diag + (long long)q * 2LL * a.N)[i];
             acc.x += pv.x;
             acc.y += pv.y;
         }
-        sum_strided(acc, a.sym.src_partial, 2LL * a.N, B, i);
         u[0] = acc;
     }
     for (int c = 0; c < a.nchunks; ++c) {
@@ -1167,84 +1127,48 @@ int build_schedules(Geometry *g) {
     return BIE_OK;
 }
 
-// (R, W) variants of the symmetric kernel (R targets per lane, W warps; R W = 16)
-// variants 3..5 add a minimum-blocks launch bound (register cap -> more warps)
-// variants 6..8 keep the target quadratic forms in shared memory (QS)
-// variants 11..14 pipeline the source steps (TP = 1: loads one step ahead; 2: unroll 2)
-// variants 15..18 use dual-source steps (DS)
-static const int kNumSymVar = 23;
-static const int kSymVar[kNumSymVar][2] = {{4, 4}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {4, 4}, {8, 2}, {8, 2},
-                                           {4, 4}, {4, 4}, {4, 4}, {8, 2}, {8, 2}, {4, 4}, {4, 4}, {4, 4},
-                                           {4, 4}, {8, 2}, {2, 8}, {8, 2}, {8, 2}, {8, 2}, {8, 2}};
+// Variants of the symmetric kernel (tuning knob BIE_SYM_VARIANT), (SR, SW, NS, MINB):
+// 0 = (8, 2, 2, 1) -- 2 warps/SMSP at 254 registers (default, fastest measured);
+// 1 = (4, 4, 4, 3) -- 3 warps/SMSP at <= 168 registers, 16 pairs per step;
+// 2 = (4, 4, 2, 3) -- 3 warps/SMSP, 8 pairs per step;
+// 3 = (8, 2, 2, 1) with the step loop unrolled by two;
+// 4, 5 = (8, 2, 2, 1) with lockstep pair groups of 2 / 4 targets (GR);
+// 6 = (4, 4, 2, 4) -- 4 warps/SMSP at <= 128 registers.
+static const int kNumSymVar = 7;
 static void *sym_kernel(int v) {
     switch (v) {
-        case 1: return reinterpret_cast<void *>(&k_dlp_sym<2, 8>);
-        case 2: return reinterpret_cast<void *>(&k_dlp_sym<8, 2>);
-        case 3: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5>);
-        case 4: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 6>);
-        case 5: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3>);
-        case 6: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, true>);
-        case 7: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, true>);
-        case 8: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, true>);
-        case 9: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4>);
-        case 10: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, true>);
-        case 11: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 1>);
-        case 12: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 2>);
-        case 13: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, false, 1>);
-        case 14: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, false, 1>);
-        case 15: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, false, 0, 0, true>);
-        case 16: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 3, false, 0, 0, true>);
-        case 17: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, false, 0, 0, true>);
-        case 18: return reinterpret_cast<void *>(&k_dlp_sym<2, 8, 2, false, 0, 0, true>);
-        case 19: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, false, 0, 0, true>);
-        case 20: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 6, false, 0, 0, true>);
-        case 21: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 1, true, 0, 0, true>);
-        case 22: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 5, true, 0, 0, true>);
-        default: return reinterpret_cast<void *>(&k_dlp_sym<4, 4>);
+        case 1: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, 3>);
+        case 2: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3>);
+        case 3: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2>);
+        case 4: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 2>);
+        case 5: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 4>);
+        case 6: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 4>);
+        default: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1>);
     }
 }
-static int sym_warps(int v) { return kSymVar[v][1]; }
+static int sym_warps(int v) { return (v == 0 || v == 3 || v == 4 || v == 5) ? 2 : 4; }
 static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
-        case 1: k_dlp_sym<2, 8><<<P, 256, 0, st>>>(sa); break;
-        case 2: k_dlp_sym<8, 2><<<P, 64, 0, st>>>(sa); break;
-        case 3: k_dlp_sym<8, 2, 5><<<P, 64, 0, st>>>(sa); break;
-        case 4: k_dlp_sym<8, 2, 6><<<P, 64, 0, st>>>(sa); break;
-        case 5: k_dlp_sym<4, 4, 3><<<P, 128, 0, st>>>(sa); break;
-        case 6: k_dlp_sym<8, 2, 1, true><<<P, 64, 0, st>>>(sa); break;
-        case 7: k_dlp_sym<8, 2, 5, true><<<P, 64, 0, st>>>(sa); break;
-        case 8: k_dlp_sym<4, 4, 3, true><<<P, 128, 0, st>>>(sa); break;
-        case 9: k_dlp_sym<4, 4, 4><<<P, 128, 0, st>>>(sa); break;
-        case 10: k_dlp_sym<4, 4, 4, true><<<P, 128, 0, st>>>(sa); break;
-        case 11: k_dlp_sym<8, 2, 1, false, 1><<<P, 64, 0, st>>>(sa); break;
-        case 12: k_dlp_sym<8, 2, 1, false, 2><<<P, 64, 0, st>>>(sa); break;
-        case 13: k_dlp_sym<4, 4, 4, false, 1><<<P, 128, 0, st>>>(sa); break;
-        case 14: k_dlp_sym<4, 4, 3, false, 1><<<P, 128, 0, st>>>(sa); break;
-        case 15: k_dlp_sym<4, 4, 4, false, 0, 0, true><<<P, 128, 0, st>>>(sa); break;
-        case 16: k_dlp_sym<4, 4, 3, false, 0, 0, true><<<P, 128, 0, st>>>(sa); break;
-        case 17: k_dlp_sym<8, 2, 1, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
-        case 18: k_dlp_sym<2, 8, 2, false, 0, 0, true><<<P, 256, 0, st>>>(sa); break;
-        case 19: k_dlp_sym<8, 2, 5, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
-        case 20: k_dlp_sym<8, 2, 6, false, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
-        case 21: k_dlp_sym<8, 2, 1, true, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
-        case 22: k_dlp_sym<8, 2, 5, true, 0, 0, true><<<P, 64, 0, st>>>(sa); break;
-        default: k_dlp_sym<4, 4><<<P, 128, 0, st>>>(sa); break;
+        case 1: k_dlp_sym<4, 4, 4, 3><<<P, 128, 0, st>>>(sa); break;
+        case 2: k_dlp_sym<4, 4, 2, 3><<<P, 128, 0, st>>>(sa); break;
+        case 3: k_dlp_sym<8, 2, 2, 1, 0, 2><<<P, 64, 0, st>>>(sa); break;
+        case 4: k_dlp_sym<8, 2, 2, 1, 0, 1, 2><<<P, 64, 0, st>>>(sa); break;
+        case 5: k_dlp_sym<8, 2, 2, 1, 0, 1, 4><<<P, 64, 0, st>>>(sa); break;
+        case 6: k_dlp_sym<4, 4, 2, 4><<<P, 128, 0, st>>>(sa); break;
+        default: k_dlp_sym<8, 2, 2, 1><<<P, 64, 0, st>>>(sa); break;
     }
 }
 
 // Single-layer symmetric kernel variants (tuning knob BIE_SLP_SYM_VARIANT):
-// 0 = (8,2) with one-step-ahead source loads, 1 = (8,2) dual-source (default),
-// 2 = (4,4) dual-source at 3 CTAs/SM, 3 = (4,4) dual-source at 4 CTAs/SM.
+// 0 = (8, 2, 2) (default), 1 = (4, 4, 2) at 3 CTAs/SM.
 static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
-        case 1: k_dlp_sym<8, 2, 1, false, 0, 1, true><<<P, 64, 0, st>>>(sa); break;
-        case 2: k_dlp_sym<4, 4, 3, false, 0, 1, true><<<P, 128, 0, st>>>(sa); break;
-        case 3: k_dlp_sym<4, 4, 4, false, 0, 1, true><<<P, 128, 0, st>>>(sa); break;
-        default: k_dlp_sym<8, 2, 1, false, 1, 1><<<P, 64, 0, st>>>(sa); break;
+        case 1: k_dlp_sym<4, 4, 2, 3, 1><<<P, 128, 0, st>>>(sa); break;
+        default: k_dlp_sym<8, 2, 2, 1, 1><<<P, 64, 0, st>>>(sa); break;
     }
 }
 
-// Segment size of the dynamic work distribution: about 24 segments per CTA
+// Segment size of the dynamic work distribution: about 8 segments per CTA
 // (tail <= one segment), at least 8 units so a segment amortises its start.
 // Below 8 units per CTA (small N), smaller segments so every CTA gets work
 // (config 2: 92 -> 44 us per matvec); measured at config 3, segments under 8
@@ -1252,70 +1176,98 @@ static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
 static long long sym_useg(long long U, int P) {
     long long lo = std::max<long long>(1, std::min<long long>(8, U / P));
     if (const char *e = getenv("BIE_SYM_USEG_MIN")) lo = std::max(1, atoi(e));  // tuning knob
-    // segments per CTA (knob BIE_SYM_SEGS_PER_CTA); config 4, ms per matvec:
-    // 8: 13.170, 12: 13.172, 16: 13.173, 24: 13.185, 32: 13.193, 48: 13.237
-    long long per = 24;
+    // segments per CTA (knob BIE_SYM_SEGS_PER_CTA); config 4, ms per matvec (round 1):
+    // 8: 13.170, 12: 13.172, 16: 13.173, 24: 13.185, 32: 13.193, 48: 13.237.
+    // Each segment writes one 512-node slot of target partials, so fewer
+    // segments also mean fewer slots (DRAM traffic ~ segments x 8 KB).
+    long long per = 8;
     if (const char *e = getenv("BIE_SYM_SEGS_PER_CTA")) per = std::max(1, atoi(e));
     return std::max<long long>(lo, (U + per * P - 1) / (per * P));
 }
 
-// Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only).
-// src_partial is [nTB][2N] doubles; above a 48 GiB cap (or without 8 GiB of
-// free headroom) the path is disabled and
-// the one-sided kernel is used instead.
+// Schedule of one launch over the slice [ub, ub + U) of the unit list for
+// operator op: persistent CTAs P and units per segment Useg.
+struct SymPlan {
+    int P = 1;
+    long long Useg = 1;
+};
+static SymPlan sym_plan(const Geometry *g, long long U, int op) {
+    SymPlan pl;
+    pl.P = (int)std::max<long long>(1, std::min<long long>((long long)g->num_sms * g->sym_occ[op], U));
+    pl.Useg = sym_useg(U, pl.P);
+    return pl;
+}
+
+// Lazily allocate the symmetric path's schedule and buffers (nvec = 1 only):
+// O(N) memory -- the fixed-point limb accumulators [3][2N] (fx_add), the
+// in-block parts [4][2N], the per-node quadratic forms and the block table.
 static int sym_prepare(Geometry *g) {
     if (g->sym_state != 0) return BIE_OK;
     const int N = g->N;
     const int nTB = (N + kSymTB - 1) / kSymTB;
     const long long nC = (N + kSymChunk - 1) / kSymChunk;
-    const size_t src_bytes = sizeof(double) * 2 * (size_t)N * nTB;
     if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(kNumSymVar - 1, atoi(e)));  // tuning knob
-    if (const char *e = getenv("BIE_SLP_SYM_VARIANT")) g->slp_sym_variant = std::max(0, std::min(3, atoi(e)));
-    {
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        // cap: 48 GiB and leave 8 GiB of headroom (config 5 needs 35 GB)
-        if (src_bytes > (48ull << 30) || src_bytes + (8ull << 30) > free_b) {
-            g->sym_state = -1;
-            return BIE_OK;
-        }
-    }
+    if (const char *e = getenv("BIE_SLP_SYM_VARIANT")) g->slp_sym_variant = std::max(0, std::min(1, atoi(e)));
     std::vector<long long> off(nTB + 1, 0);
     for (int A = 0; A < nTB; ++A) {
         long long n = nC - (long long)(A + 1) * (kSymTB / kSymChunk);
         off[A + 1] = off[A] + std::max(0LL, n);
     }
     const long long U = off[nTB];
-    int occ = 0;
-    BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel(g->sym_variant), 32 * sym_warps(g->sym_variant), 0));
-    const int P = (int)std::max<long long>(1, std::min<long long>((long long)g->num_sms * std::max(1, occ), U));
-    const long long Useg = sym_useg(U, P);
-    int S = 1;
-    for (int A = 0; A < nTB; ++A) {
-        if (off[A + 1] == off[A]) continue;
-        S = std::max(S, (int)(seg_of(off[A + 1] - 1, 0, Useg) - seg_of(off[A], 0, Useg) + 1));
+    for (int op = 0; op < 2; ++op) {
+        int occ = 0;
+        void *k = op ? (g->slp_sym_variant == 1 ? reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3, 1>)
+                                                : reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 1>))
+                     : sym_kernel(g->sym_variant);
+        const int threads = op ? (g->slp_sym_variant == 1 ? 128 : 64) : 32 * sym_warps(g->sym_variant);
+        BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, 0));
+        g->sym_occ[op] = std::max(1, occ);
     }
-    g->sym_state = -1;  // stays -1 (one-sided fallback) if an allocation fails
-    if (cudaMalloc(&g->sym_counter, sizeof(unsigned long long)) != cudaSuccess ||
+    g->sym_nTB = nTB;
+    g->sym_U = U;
+    g->sym_state = -1;  // stays -1 (one-sided path) if an allocation fails
+    if (cudaMalloc(&g->sym_counter, sizeof(unsigned long long) * 2) != cudaSuccess ||
         cudaMalloc(&g->sym_Q, sizeof(double4) * (size_t)N) != cudaSuccess ||
         cudaMalloc(&g->sym_off, sizeof(long long) * (size_t)(nTB + 1)) != cudaSuccess ||
-        cudaMalloc(&g->sym_tgt, sizeof(double) * 2 * (size_t)N * S) != cudaSuccess ||
-        cudaMalloc(&g->sym_src, src_bytes) != cudaSuccess ||
+        cudaMalloc(&g->sym_acc, sizeof(unsigned long long) * 6 * (size_t)N) != cudaSuccess ||
         cudaMalloc(&g->sym_diag, sizeof(double) * 2 * (size_t)N * 4) != cudaSuccess) {
         (void)cudaGetLastError();  // clear the (non-sticky) allocation error
         return BIE_OK;
     }
     BIE_CUDA_TRY(cudaMemcpy(g->sym_off, off.data(), sizeof(long long) * (size_t)(nTB + 1), cudaMemcpyHostToDevice));
-    if (getenv("BIE_SYM_TRACE")) cudaMalloc(&g->sym_trace, sizeof(unsigned long long) * 2 * (size_t)P);
-    g->sym_nTB = nTB;
-    g->sym_U = U;
-    g->sym_P = P;
-    g->sym_S = S;
-    g->sym_Useg = Useg;
+    const SymPlan p0 = sym_plan(g, U, 0), p1 = sym_plan(g, U, 1);
+    if (getenv("BIE_SYM_TRACE"))
+        cudaMalloc(&g->sym_trace, sizeof(unsigned long long) * 2 * (size_t)std::max(p0.P, p1.P));
+    g->sym_P = p0.P;
+    g->sym_Useg = p0.Useg;
     // in-block pairs: split each block's sources over up to 4 CTAs when there are
     // too few blocks to fill the SMs (2 CTAs per block before splitting)
     g->sym_dsplit = (int)std::max<long long>(1, std::min<long long>(4, (2LL * g->num_sms + 2LL * nTB - 1) / (2LL * nTB)));
     g->sym_state = 1;
+    return BIE_OK;
+}
+
+// The max |Q| word (sym_counter[1]) must be zero before k_quad / k_slp_scale.
+static int sym_pre(Geometry *g, cudaStream_t st) {
+    BIE_CUDA_TRY(cudaMemsetAsync(g->sym_counter, 0, sizeof(unsigned long long) * 2, st));
+    return BIE_OK;
+}
+
+// Launch the symmetric kernel on the slice [ub, ub + U) (zeroes the limb
+// accumulators first; the segment counter and max |Q| were zeroed by sym_pre).
+static int sym_launch(Geometry *g, long long ub, long long U, int op, cudaStream_t st) {
+    BIE_CUDA_TRY(cudaMemsetAsync(g->sym_acc, 0, sizeof(unsigned long long) * 6 * (size_t)g->N, st));
+    if (U <= 0) return BIE_OK;
+    const SymPlan pl = sym_plan(g, U, op);
+    SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_acc, g->sym_counter + 1, g->N, g->sym_nTB, U, ub,
+               (ub == 0 && U == g->sym_U) ? g->sym_trace : nullptr, pl.Useg, (U + pl.Useg - 1) / pl.Useg,
+               g->sym_counter};
+    if (op)
+        launch_sym_slp(g->slp_sym_variant, pl.P, sa, st);
+    else
+        launch_sym(g->sym_variant, pl.P, sa, st);
+    count_launch();
+    BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
 }
 
@@ -1342,16 +1294,22 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
 // NEXT-1: S = w sigma / (4 pi) for every vector (the single-layer source
 // strength), and for the symmetric path also the (S_x, S_y, 0, 0) records.
 __global__ void k_slp_scale(const double *__restrict__ w, const double *__restrict__ sigma, long long stride,
-                            int nvec, int N, double *S, double4 *Q) {
+                            int nvec, int N, double *S, double4 *Q, unsigned long long *qmax_bits = nullptr) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= N) return;
-    const double f = w[j] * (1.0 / (4.0 * kPi));
-    for (int v = 0; v < nvec; ++v) {
-        const double2 sj = reinterpret_cast<const double2 *>(sigma + (long long)v * stride)[j];
-        const double2 o = make_double2(f * sj.x, f * sj.y);
-        reinterpret_cast<double2 *>(S + (long long)v * 2LL * N)[j] = o;
-        if (Q && v == 0) Q[j] = make_double4(o.x, o.y, 0.0, 0.0);
+    double m = 0.0;
+    if (j < N) {
+        const double f = w[j] * (1.0 / (4.0 * kPi));
+        for (int v = 0; v < nvec; ++v) {
+            const double2 sj = reinterpret_cast<const double2 *>(sigma + (long long)v * stride)[j];
+            const double2 o = make_double2(f * sj.x, f * sj.y);
+            reinterpret_cast<double2 *>(S + (long long)v * 2LL * N)[j] = o;
+            if (Q && v == 0) {
+                Q[j] = make_double4(o.x, o.y, 0.0, 0.0);
+                m = fmax(fabs(o.x), fabs(o.y));
+            }
+        }
     }
+    if (qmax_bits) qmax_update(m, qmax_bits);
 }
 
 static int slp_prepare(Geometry *g) {
@@ -1393,30 +1351,24 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     EpiArgs ea{};
     const bool sym = nvec == 1 && row_begin == 0 && row_end == N && !(flags & BIE_ONE_SIDED) &&
                      sym_prepare(g) == BIE_OK && g->sym_state == 1;
+    if (sym) {
+        int rc = sym_pre(g, st);
+        if (rc) return rc;
+    }
     if (op) {
         k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, stride, nvec, N, g->slp_s,
-                                                     sym ? g->sym_Q : nullptr);
+                                                     sym ? g->sym_Q : nullptr, sym ? g->sym_counter + 1 : nullptr);
         count_launch();
         sigma = g->slp_s;  // the pair kernels read S
     }
     if (sym) {
         if (!op) {
-            k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+            k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N, g->sym_counter + 1);
             count_launch();
         }
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
-        if (g->sym_U > 0) {
-            SymArgs sa{g->pos,         g->sym_Q,   g->sym_off, g->sym_tgt,
-                       g->sym_src,     N,          g->sym_nTB, g->sym_U,
-                       0,              g->sym_trace, g->sym_Useg, (g->sym_U + g->sym_Useg - 1) / g->sym_Useg,
-                       g->sym_counter};
-            BIE_CUDA_TRY(cudaMemsetAsync(g->sym_counter, 0, sizeof(unsigned long long), st));
-            if (op)
-                launch_sym_slp(g->slp_sym_variant, g->sym_P, sa, st);
-            else
-                launch_sym(g->sym_variant, g->sym_P, sa, st);
-            count_launch();
-        }
+        int rc = sym_launch(g, 0, g->sym_U, op, st);
+        if (rc) return rc;
         if (op)
             k_dlp_diag<1><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, 0,
                                                                          g->sym_dsplit);
@@ -1426,7 +1378,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
-        ea.sym = SymEpi{1, g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, g->sym_Useg, g->sym_dsplit};
+        ea.sym = SymEpi{1, g->sym_acc, g->sym_counter + 1, g->sym_diag, g->sym_dsplit};
     }
     // decompose nvec into variant chunks (16, 8, 4, 2, 1)
     int v = sym ? nvec : 0;
@@ -1570,40 +1522,24 @@ __global__ void __launch_bounds__(128) k_field_epilogue(const double2 *__restric
 // [blk0, blk1) into a full-size vector; the ranks' vectors are reduce-scattered
 // and each rank finishes its rows with bie_dlp_epilogue_rows.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_sym_gather(const double *__restrict__ tgt, const double *__restrict__ src,
-                                                    const double *__restrict__ diag, const long long *__restrict__ off,
-                                                    int N, long long ub, long long U, long long Useg, int blk0,
-                                                    int blk1, double *out, int dsplit) {
+__global__ void __launch_bounds__(256) k_sym_gather(const unsigned long long *__restrict__ acc,
+                                                    const unsigned long long *__restrict__ qmax,
+                                                    const double *__restrict__ diag, int N, int blk0, int blk1,
+                                                    double *out, int dsplit) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int B = i / kSymTB;
-    double2 acc = make_double2(0.0, 0.0);
-    const long long lo = max(off[B], ub), hi = min(off[B + 1], ub + U);
-    if (hi > lo) {
-        const int first = (int)seg_of(lo, ub, Useg), last = (int)seg_of(hi - 1, ub, Useg);
-        for (int sl = 0; sl <= last - first; ++sl) {
-            const double2 pv = reinterpret_cast<const double2 *>(tgt + (long long)sl * 2LL * N)[i];
-            acc.x += pv.x;
-            acc.y += pv.y;
-        }
-    }
+    double fxs, fxb;
+    fx_scales(qmax, fxs, fxb);
+    double2 v = make_double2(fx_value(acc + 2LL * i, 2LL * N, fxb), fx_value(acc + 2LL * i + 1, 2LL * N, fxb));
     if (B >= blk0 && B < blk1) {
         for (int q = 0; q < dsplit; ++q) {
             const double2 pv = reinterpret_cast<const double2 *>(diag + (long long)q * 2LL * N)[i];
-            acc.x += pv.x;
-            acc.y += pv.y;
+            v.x += pv.x;
+            v.y += pv.y;
         }
     }
-    const int c = i / kSymChunk;
-    for (int A = 0; A < B; ++A) {
-        const long long u = off[A] + (c - (A + 1) * (kSymTB / kSymChunk));
-        if (u >= ub && u < ub + U) {
-            const double2 pv = reinterpret_cast<const double2 *>(src + (long long)A * 2LL * N)[i];
-            acc.x += pv.x;
-            acc.y += pv.y;
-        }
-    }
-    reinterpret_cast<double2 *>(out)[i] = acc;
+    reinterpret_cast<double2 *>(out)[i] = v;
 }
 
 int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long long ub, long long ue, int blk0,
@@ -1627,46 +1563,20 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         g->prof_used += 4;
         BIE_CUDA_TRY(cudaEventRecord(ev[0], st));
     }
+    rc = sym_pre(g, st);
+    if (rc) return rc;
     if (op) {  // single layer (NEXT-1): S = w sigma / 4pi and its (S, 0, 0) records
         int rc2 = slp_prepare(g);
         if (rc2) return rc2;
-        k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, 2LL * N, 1, N, g->slp_s, g->sym_Q);
+        k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, 2LL * N, 1, N, g->slp_s, g->sym_Q,
+                                                     g->sym_counter + 1);
     } else {
-        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N);
+        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N, g->sym_counter + 1);
     }
     count_launch();
     if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
-    long long Useg = 1;
-    if (U > 0) {
-        // slots needed for this slice
-        std::vector<long long> off(g->sym_nTB + 1);
-        BIE_CUDA_TRY(cudaMemcpy(off.data(), g->sym_off, sizeof(long long) * off.size(), cudaMemcpyDeviceToHost));
-        int occ = 0;
-        BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym_kernel(g->sym_variant),
-                                                                   32 * sym_warps(g->sym_variant), 0));
-        const int P = (int)std::max<long long>(1, std::min<long long>((long long)g->num_sms * std::max(1, occ), U));
-        Useg = sym_useg(U, P);
-        int S = 1;
-        for (int A = 0; A < g->sym_nTB; ++A) {
-            const long long lo = std::max(off[A], ub), hi = std::min(off[A + 1], ue);
-            if (hi > lo) S = std::max(S, (int)(seg_of(hi - 1, ub, Useg) - seg_of(lo, ub, Useg) + 1));
-        }
-        if (S > g->sym_S) {
-            BIE_CUDA_TRY(cudaStreamSynchronize(st));
-            cudaFree(g->sym_tgt);
-            g->sym_tgt = nullptr;
-            BIE_CUDA_TRY(cudaMalloc(&g->sym_tgt, sizeof(double) * 2 * (size_t)N * S));
-            g->sym_S = S;
-        }
-        SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_tgt, g->sym_src, N, g->sym_nTB, U, ub, nullptr,
-                   Useg,   (U + Useg - 1) / Useg, g->sym_counter};
-        BIE_CUDA_TRY(cudaMemsetAsync(g->sym_counter, 0, sizeof(unsigned long long), st));
-        if (op)
-            launch_sym_slp(g->slp_sym_variant, P, sa, st);
-        else
-            launch_sym(g->sym_variant, P, sa, st);
-        count_launch();
-    }
+    rc = sym_launch(g, ub, U, op, st);  // (zeroes the accumulators even for an empty slice)
+    if (rc) return rc;
     if (blk1 > blk0) {
         if (op)
             k_dlp_diag<1><<<2 * (blk1 - blk0) * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, g->slp_s, g->sym_diag, N,
@@ -1677,8 +1587,8 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         count_launch();
     }
     if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
-    k_sym_gather<<<(N + 255) / 256, 256, 0, st>>>(g->sym_tgt, g->sym_src, g->sym_diag, g->sym_off, N, ub, U, Useg,
-                                                  blk0, blk1, out_full, g->sym_dsplit);
+    k_sym_gather<<<(N + 255) / 256, 256, 0, st>>>(g->sym_acc, g->sym_counter + 1, g->sym_diag, N, blk0, blk1,
+                                                  out_full, g->sym_dsplit);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));

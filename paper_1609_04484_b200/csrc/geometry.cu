@@ -285,8 +285,7 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     if (g->gmb.pinned) cudaFreeHost(g->gmb.pinned);
     cudaFree(g->sym_Q);
     cudaFree(g->sym_off);
-    cudaFree(g->sym_tgt);
-    cudaFree(g->sym_src);
+    cudaFree(g->sym_acc);
     cudaFree(g->sym_diag);
     g->magic = 0;
     delete g;

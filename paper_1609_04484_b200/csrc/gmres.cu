@@ -87,27 +87,41 @@ __global__ void k_reduce(const double *__restrict__ partial, int ldp, int nchunk
     out[j] = accumulate ? out[j] + t : t;
 }
 
-// y[e] = beta * y[e] + alpha * sum_j V[j][e] * c[j]   (c in device memory, nv <= max_iter+1)
+// y[e] = beta * y[e] + alpha * sum_j V[j][e] * c[j]   (c in device memory, any nv).
+// The coefficients are staged through shared memory in tiles of kAxpyTile
+// (static 16 KB, so no dynamic-smem limit on nv = k + 1); the sum over j stays
+// one sequential FMA chain per element, so results do not depend on the tiling.
+constexpr int kAxpyTile = 2048;
+__device__ __forceinline__ double axpy_chain(const double *__restrict__ V, long long ldv, int j0, int j1,
+                                             const double *cs, long long e, double acc) {
+    int j = j0;
+    for (; j + 4 <= j1; j += 4) {
+        const double a0 = V[(long long)j * ldv + e], a1 = V[(long long)(j + 1) * ldv + e];
+        const double a2 = V[(long long)(j + 2) * ldv + e], a3 = V[(long long)(j + 3) * ldv + e];
+        acc = fma(a0, cs[j - j0], acc);
+        acc = fma(a1, cs[j + 1 - j0], acc);
+        acc = fma(a2, cs[j + 2 - j0], acc);
+        acc = fma(a3, cs[j + 3 - j0], acc);
+    }
+    for (; j < j1; ++j) acc = fma(V[(long long)j * ldv + e], cs[j - j0], acc);
+    return acc;
+}
+
 __global__ void __launch_bounds__(256) k_multiaxpy(const double *__restrict__ V, long long ldv, int nv,
                                                    const double *__restrict__ c, double alpha, double beta,
                                                    double *y, long long n) {
-    extern __shared__ double cs[];
-    for (int q = threadIdx.x; q < nv; q += blockDim.x) cs[q] = c[q];
-    __syncthreads();
+    __shared__ double cs[kAxpyTile];
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n) return;
+    const bool act = e < n;
     double acc = 0.0;
-    int j = 0;
-    for (; j + 4 <= nv; j += 4) {
-        const double a0 = V[(long long)j * ldv + e], a1 = V[(long long)(j + 1) * ldv + e];
-        const double a2 = V[(long long)(j + 2) * ldv + e], a3 = V[(long long)(j + 3) * ldv + e];
-        acc = fma(a0, cs[j], acc);
-        acc = fma(a1, cs[j + 1], acc);
-        acc = fma(a2, cs[j + 2], acc);
-        acc = fma(a3, cs[j + 3], acc);
+    for (int j0 = 0; j0 < nv; j0 += kAxpyTile) {
+        const int j1 = min(nv, j0 + kAxpyTile);
+        __syncthreads();
+        for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) cs[q] = c[j0 + q];
+        __syncthreads();
+        if (act) acc = axpy_chain(V, ldv, j0, j1, cs, e, acc);
     }
-    for (; j < nv; ++j) acc = fma(V[(long long)j * ldv + e], cs[j], acc);
-    y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
+    if (act) y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
 }
 
 __global__ void k_sqrt(const double *in, double *out) { *out = sqrt(*in); }
@@ -130,28 +144,54 @@ struct GmState {
     double *scal;   // [0] beta, [1] w0^2 -> w0, [2] hk1^2 -> hk1, [3] est, [4] breakdown flag, [5] tmp
 };
 
-// Hessenberg column k: H[:,k] = h + h2, H[k+1,k] = hk1; apply old rotations, new rotation.
-__global__ void k_givens(GmState s, int k, int ldh) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double *Hk = s.H + (long long)k * ldh;
-    for (int j = 0; j <= k; ++j) Hk[j] = s.h[j] + s.h2[j];
-    const double hk1 = s.scal[2];
+// sqrt(a^2 + b^2) correctly rounded (reading C28): a^2 + b^2 exactly as a
+// double-double, a correctly rounded sqrt of its head, one Newton correction
+// in double-double, one final rounding.  Library hypot() implementations
+// differ by an ulp (glibc vs CUDA), which left the Givens recurrence of the
+// two GMRES implementations not uniquely defined.
+__device__ __forceinline__ double hypot_cr(double a, double b) {
+    const double p = a * a, pe = fma(a, a, -p);
+    const double q = b * b, qe = fma(b, b, -q);
+    const double sh = p + q, t = sh - p;
+    double se = (p - (sh - t)) + (q - t);
+    se += pe + qe;
+    const double s1 = sh + se, s1e = se - (s1 - sh);
+    if (s1 == 0.0) return 0.0;
+    const double r = __dsqrt_rn(s1);
+    const double rr = r * r, rre = fma(r, r, -rr);
+    return r + (((s1 - rr) - rre) + s1e) / (2.0 * r);
+}
+
+// One Givens step of GMRES (reading C13): H[:,k] = h + h2, H[k+1,k] = hk1,
+// old rotations, new rotation, g, estimate, breakdown flag.  Every operation is
+// the oracle's, in its order, without contraction (_rn intrinsics) and with a
+// correctly rounded hypot, so equal inputs give bit-identical outputs.
+__device__ __forceinline__ void givens_step(double *Hk, double *cs, double *sn, double *g, const double *h,
+                                            const double *h2, double *scal, int k) {
+    for (int j = 0; j <= k; ++j) Hk[j] = __dadd_rn(h[j], h2[j]);
+    const double hk1 = scal[2];
     Hk[k + 1] = hk1;
     for (int j = 0; j < k; ++j) {
         const double a = Hk[j], b = Hk[j + 1];
-        Hk[j] = s.cs[j] * a + s.sn[j] * b;
-        Hk[j + 1] = -s.sn[j] * a + s.cs[j] * b;
+        Hk[j] = __dadd_rn(__dmul_rn(cs[j], a), __dmul_rn(sn[j], b));
+        Hk[j + 1] = __dadd_rn(__dmul_rn(-sn[j], a), __dmul_rn(cs[j], b));
     }
     const double a = Hk[k], b = Hk[k + 1];
-    const double d = hypot(a, b);
-    s.cs[k] = a / d;
-    s.sn[k] = b / d;
+    const double d = hypot_cr(a, b);
+    cs[k] = __ddiv_rn(a, d);
+    sn[k] = __ddiv_rn(b, d);
     Hk[k] = d;
     Hk[k + 1] = 0.0;
-    s.g[k + 1] = -s.sn[k] * s.g[k];
-    s.g[k] = s.cs[k] * s.g[k];
-    s.scal[3] = fabs(s.g[k + 1]) / s.scal[0];
-    s.scal[4] = (hk1 <= 1e-14 * s.scal[1]) ? 1.0 : 0.0;
+    g[k + 1] = __dmul_rn(-sn[k], g[k]);
+    g[k] = __dmul_rn(cs[k], g[k]);
+    scal[3] = __ddiv_rn(fabs(g[k + 1]), scal[0]);
+    scal[4] = (hk1 <= __dmul_rn(1e-14, scal[1])) ? 1.0 : 0.0;
+}
+
+// Hessenberg column k: H[:,k] = h + h2, H[k+1,k] = hk1; apply old rotations, new rotation.
+__global__ void k_givens(GmState s, int k, int ldh) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    givens_step(s.H + (long long)k * ldh, s.cs, s.sn, s.g, s.h, s.h2, s.scal, k);
 }
 
 // y = H^{-1} g (upper triangular, iters x iters), one CTA
@@ -200,8 +240,7 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
 
 static int multiaxpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,
                      long long n, cudaStream_t st) {
-    size_t smem = sizeof(double) * (size_t)std::max(nv, 1);
-    k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, smem, st>>>(V, ldv, nv, c, alpha, beta, y, n);
+    k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, ldv, nv, c, alpha, beta, y, n);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
@@ -263,30 +302,26 @@ __global__ void k_reduce_b(const double *__restrict__ partial, int ldp, long lon
     small[(long long)act[q] * smallper + off + j] = sqrt_out ? sqrt(t) : t;
 }
 
-// W_q[e] = beta * W_q[e] + alpha * sum_j V_r[j][e] * c_r[j]
+// W_q[e] = beta * W_q[e] + alpha * sum_j V_r[j][e] * c_r[j]  (coefficients tiled as in k_multiaxpy)
 __global__ void __launch_bounds__(256) k_multiaxpy_b(const double *__restrict__ V, long long sysV, long long ldv,
                                                      int nv, const double *small, long long smallper, long long coff,
                                                      double alpha, double beta, double *W, long long n,
                                                      const int *__restrict__ act) {
-    extern __shared__ double cs[];
+    __shared__ double cs[kAxpyTile];
     const int qs = blockIdx.y, r = act[qs];
     const double *c = small + (long long)r * smallper + coff;
-    for (int q = threadIdx.x; q < nv; q += blockDim.x) cs[q] = c[q];
-    __syncthreads();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n) return;
+    const bool on = e < n;
     const double *Vb = V + (long long)r * sysV;
     double acc = 0.0;
-    int j = 0;
-    for (; j + 4 <= nv; j += 4) {
-        const double a0 = Vb[(long long)j * ldv + e], a1 = Vb[(long long)(j + 1) * ldv + e];
-        const double a2 = Vb[(long long)(j + 2) * ldv + e], a3 = Vb[(long long)(j + 3) * ldv + e];
-        acc = fma(a0, cs[j], acc);
-        acc = fma(a1, cs[j + 1], acc);
-        acc = fma(a2, cs[j + 2], acc);
-        acc = fma(a3, cs[j + 3], acc);
+    for (int j0 = 0; j0 < nv; j0 += kAxpyTile) {
+        const int j1 = min(nv, j0 + kAxpyTile);
+        __syncthreads();
+        for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) cs[q] = c[j0 + q];
+        __syncthreads();
+        if (on) acc = axpy_chain(Vb, ldv, j0, j1, cs, e, acc);
     }
-    for (; j < nv; ++j) acc = fma(Vb[(long long)j * ldv + e], cs[j], acc);
+    if (!on) return;
     double *y = W + (long long)qs * n;
     y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
 }
@@ -300,25 +335,7 @@ __global__ void k_givens_b(double *Hbase, long long Hsys, double *small, long lo
     const int r = act[q];
     double *b = small + (long long)r * smallper;
     GmState s{Hbase + (long long)r * Hsys, b, b + ldh, b + 2 * ldh, b + 3 * ldh, b + 4 * ldh, b + 5 * ldh};
-    double *Hk = s.H + (long long)k * ldh;
-    for (int j = 0; j <= k; ++j) Hk[j] = s.h[j] + s.h2[j];
-    const double hk1 = s.scal[2];
-    Hk[k + 1] = hk1;
-    for (int j = 0; j < k; ++j) {
-        const double a = Hk[j], bb = Hk[j + 1];
-        Hk[j] = s.cs[j] * a + s.sn[j] * bb;
-        Hk[j + 1] = -s.sn[j] * a + s.cs[j] * bb;
-    }
-    const double a = Hk[k], bb = Hk[k + 1];
-    const double d = hypot(a, bb);
-    s.cs[k] = a / d;
-    s.sn[k] = bb / d;
-    Hk[k] = d;
-    Hk[k + 1] = 0.0;
-    s.g[k + 1] = -s.sn[k] * s.g[k];
-    s.g[k] = s.cs[k] * s.g[k];
-    s.scal[3] = fabs(s.g[k + 1]) / s.scal[0];
-    s.scal[4] = (hk1 <= 1e-14 * s.scal[1]) ? 1.0 : 0.0;
+    givens_step(s.H + (long long)k * ldh, s.cs, s.sn, s.g, s.h, s.h2, s.scal, k);
     est[2 * q] = s.scal[3];
     est[2 * q + 1] = s.scal[4];
 }
@@ -636,6 +653,29 @@ extern "C" int bie_gmres_solve(bie_geometry_t gh, bie_blockdiag_t bdh, const dou
                             res_true, converged, stream);
 }
 
+// End-to-end form with HOST buffers: f is copied to the
+// geometry's device staging buffer, solved there, and x copied back; the call
+// returns after the D2H copy has completed.  Pinned host memory makes both
+// copies DMA transfers on `stream`; pageable memory works (driver-staged).
+extern "C" int bie_gmres_solve_host(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f_host, double *x_host,
+                                    double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
+                                    double *res_true, int *converged, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !f_host || !x_host || f_host == x_host) {
+        set_error("bie_gmres_solve_host: invalid handle, null host buffer or f == x");
+        return BIE_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = sizeof(double) * 2 * (size_t)g->N;
+    BIE_CUDA_TRY(cudaMemcpyAsync(g->stage_in, f_host, bytes, cudaMemcpyHostToDevice, st));
+    int rc = gmres_solve_impl("bie_gmres_solve_host", BIE_FULL, gh, bdh, g->stage_in, g->stage_out, tol, max_iter,
+                              hist_host, iters, res_pc, res_true, converged, stream);
+    if (rc) return rc;
+    BIE_CUDA_TRY(cudaMemcpyAsync(x_host, g->stage_out, bytes, cudaMemcpyDeviceToHost, st));
+    BIE_CUDA_TRY(cudaStreamSynchronize(st));
+    return BIE_OK;
+}
+
 extern "C" int bie_gmres_solve_slp(bie_geometry_t gh, bie_blockdiag_t bdh, const double *f, double *x, double tol,
                                    int max_iter, double *hist_host, int *iters, double *res_pc, double *res_true,
                                    int *converged, void *stream) {
@@ -815,7 +855,7 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
                                                                            psys, d_act, 0);
             k_reduce_b<<<dim3((nv + 127) / 128, na), 128, 0, st>>>(d.partial, d.ldp, psys, d.nchunks, nv, small,
                                                                    smallper, hoff, d_act, 0);
-            k_multiaxpy_b<<<dim3(eb, na), 256, sizeof(double) * nv, st>>>(V, sysV, n, nv, small, smallper, hoff, -1.0,
+            k_multiaxpy_b<<<dim3(eb, na), 256, 0, st>>>(V, sysV, n, nv, small, smallper, hoff, -1.0,
                                                                           1.0, Wout, n, d_act);
         }
         // hk1 = ||w||

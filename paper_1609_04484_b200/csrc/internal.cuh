@@ -82,13 +82,13 @@ struct Geometry {
     int sym_state = 0;            // 0 = not prepared, 1 = ready, -1 = unavailable (memory cap)
     double4 *sym_Q = nullptr;     // [N] per-node quadratic forms
     long long *sym_off = nullptr; // [nTB + 1] unit prefix per 512-node block
-    double *sym_tgt = nullptr;    // [S][2N]
-    double *sym_src = nullptr;    // [nTB][2N]
+    unsigned long long *sym_acc = nullptr;  // [3][2N] fixed-point limbs of the pair sums (dlp.cu fx_add)
+    int sym_occ[2] = {1, 1};      // resident CTAs per SM of the DLP / SLP symmetric kernel
     double *sym_diag = nullptr;   // [2N]
-    int sym_nTB = 0, sym_P = 0, sym_S = 0, sym_variant = 17;  // (R, W) = (8, 2) dual-source: fastest measured
-    int slp_sym_variant = 1;  // (8,2) dual-source: fastest measured
+    int sym_nTB = 0, sym_P = 0, sym_variant = 0;  // (SR, SW, NS) = (8, 2, 2): fastest measured
+    int slp_sym_variant = 0;  // (8, 2, 2): fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
-    unsigned long long *sym_counter = nullptr;  // dynamic segment counter of the symmetric kernel
+    unsigned long long *sym_counter = nullptr;  // [0] dynamic segment counter, [1] max |Q| bits (accumulation window)
     unsigned long long *pair_counter = nullptr; // [8] counters of the one-sided launches of one apply
     long long sym_Useg = 1;                     // units per segment
     int sym_dsplit = 1;                         // source split of the in-block kernel (small N)

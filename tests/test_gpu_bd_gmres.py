@@ -146,42 +146,83 @@ def test_gmres_parity_bd(bie, case):
     assert abs(res["res_pc"] - ref["res_pc"]) <= 1e-6 * ref["res_pc"] + 1e-13
 
 
-def _oracle_envelope(og, f, n_runs=4, eps=1e-13):
-    """Oracle no-PC histories under 1e-13 relative perturbations of f (reading C23;
-    1e-13 is the GPU-vs-oracle matvec agreement level)."""
+EPS_FILE = os.path.join(os.path.dirname(GOLDEN), "..", "profiles", "round2", "disagreement.json")
+ENV_RUNS = 3
+ENV_FACTOR = 2.0  # GPU history within 2x the oracle's own sensitivity envelope (reading C23)
+
+
+def _perturbation(cid, pc):
+    """Measured GPU-vs-oracle disagreement per primitive (tools/measure_disagreement.py,
+    profiles/round2/disagreement.json): the noise levels of the envelope runs."""
+    d = json.load(open(EPS_FILE))[f"config{cid}"]
+    eps = {"A": max(x["rms"] for x in d["matvec"]), "dot": d["dot"]["rms"], "norm": d["norm"]["rms"],
+           "sub": d["sub"]["rms"]}
+    if pc:
+        eps["P"] = max(x["rms"] for x in d["bd_explicit"] + d["bd_structured"])
+    return eps
+
+
+def _oracle_envelope(og, f, cid, bd=None):
+    """ENV_RUNS oracle solves with every iteration primitive perturbed at its
+    measured GPU-vs-oracle disagreement (reading C23)."""
     runs = []
-    for s in range(n_runs):
-        rng = np.random.default_rng(100 + s)
-        runs.append(oracle.gmres(og, f * (1 + eps * rng.standard_normal(f.size)), None, tol=1e-8, max_iter=1000))
+    for s in range(ENV_RUNS):
+        with oracle.perturbed(_perturbation(cid, bd is not None), seed=2000 + s):
+            runs.append(oracle.gmres(og, f, bd, tol=1e-8, max_iter=1000))
     return runs
+
+
+def _env_check(h, hr, runs_hist, label, horizon=None):
+    """|h - hr| / hr <= max(1e-10, ENV_FACTOR * running max over runs); returns
+    the per-iteration ratio of the GPU deviation to the bar (logged).
+    horizon: compare only while the oracle's own envelope is below it (the
+    predictability horizon of a chaotic history, reading C23)."""
+    n = len(hr)
+    env = np.zeros(n)
+    for rh in runs_hist:
+        m = min(n, len(rh))
+        env[:m] = np.maximum(env[:m], np.abs(np.asarray(rh[:m]) - hr[:m]) / hr[:m])
+    env = np.maximum.accumulate(env)
+    bar = np.maximum(1e-10, ENV_FACTOR * env)
+    big = hr > FLOOR
+    if horizon is not None:
+        big &= env <= horizon
+    rel = np.abs(h - hr) / hr
+    ratio = rel / bar
+    print(f"{label}: compared {int(big.sum())}/{n} entries, max GPU dev {rel[big].max():.3e}, "
+          f"max env {env[big].max():.3e}, max dev/bar {ratio[big].max():.3f}")
+    assert np.all(rel[big] <= bar[big]), (rel[big].max(), env[big].max())
+    return ratio
+
+
+NOPC_HORIZON = 1e-3
 
 
 @pytest.mark.parametrize("case", list(CASES))
 def test_gmres_parity_nopc(bie, case):
-    """No-PC histories are ill conditioned (reading C23: the oracle's own history
-    moves by up to 13% on config 2, and the off-centre tiny case changes its
-    iteration count, under 1e-15 perturbations of f).  The GPU history must
-    lie within 10x the oracle's own perturbation envelope (floor 1e-10), and
-    its iteration count within the perturbed oracle runs' range."""
+    """No-PC histories are chaotic (reading C23): perturbations at the rounding
+    level grow geometrically, so past some iteration the oracle's own history
+    is not determined by its inputs.  The GPU history must lie within 2x the
+    oracle's sensitivity envelope (three runs, every primitive perturbed at its
+    measured GPU-vs-oracle disagreement; floor 1e-10) for every iteration
+    before that envelope reaches 1e-3 (the predictability horizon), and the
+    iteration count within the perturbed runs' range (+-1)."""
     import torch
 
     mk, rhs = CASES[case]
     p = mk()
+    cid = 1 if case.startswith("c1") else 2
     c = _setup(bie, p, with_bd=False)
     f = rhs(p)
     ref = oracle.gmres(c["og"], f, None, tol=1e-8, max_iter=1000)
-    runs = _oracle_envelope(c["og"], f)
+    runs = _oracle_envelope(c["og"], f, cid)
     x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
     res = bie.gmres_solve(c["g"], None, _t(f), x, tol=1e-8, max_iter=1000)
     its = [r["iters"] for r in runs] + [ref["iters"]]
     assert min(its) - 1 <= res["iters"] <= max(its) + 1, (res["iters"], its)
     n = min([res["iters"]] + its) + 1
-    hr = ref["hist"][:n]
-    env = np.max([np.abs(r["hist"][:n] - hr) / hr for r in runs], axis=0)
-    env = np.maximum.accumulate(env)  # a chaotic divergence only grows
-    big = hr > FLOOR
-    rel = np.abs(res["hist"][:n] - hr) / hr
-    assert np.all(rel[big] <= np.maximum(1e-10, 10 * env[big])), (rel.max(), env.max())
+    _env_check(np.asarray(res["hist"][:n]), np.asarray(ref["hist"][:n]), [r["hist"] for r in runs], case,
+               horizon=NOPC_HORIZON)
     assert res["converged"] and res["res_true"] < 1e-7
 
 
@@ -223,6 +264,25 @@ def test_gmres_deterministic(bie):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+def _golden(name):
+    path = os.path.join(GOLDEN, f"gmres_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"golden {path} not generated")
+    gd = json.load(open(path))
+    assert len(gd["envelope_runs"]) >= 1, "golden without envelope runs"
+    return gd
+
+
+def golden_check(res, gd, label):
+    """Iteration count equal to the oracle's (and inside the envelope runs'
+    range); history within max(1e-10, 2 x the oracle's envelope)."""
+    its = gd["envelope_iters"] + [gd["iters"]]
+    assert res["iters"] == gd["iters"] and min(its) <= res["iters"] <= max(its), (res["iters"], its)
+    assert res["converged"] == gd["converged"]
+    hr = np.asarray(gd["hist"])
+    return _env_check(np.asarray(res["hist"]), hr, gd["envelope_runs"], label)
+
+
 @pytest.mark.parametrize("name", ["config3_bd_pipe", "config4_none_pipe_prefix", "config4_bd_pipe_prefix",
                                   "config4_bd_pipe_full"])
 def test_gmres_golden(bie, name):
@@ -230,10 +290,7 @@ def test_gmres_golden(bie, name):
     config 4's BD uses the oracle's LU-solve form of the same operator)."""
     import torch
 
-    path = os.path.join(GOLDEN, f"gmres_{name}.json")
-    if not os.path.exists(path):
-        pytest.skip(f"golden {path} not generated")
-    gd = json.load(open(path))
+    gd = _golden(name)
     p = make_problem(gd["config"])
     use_bd = gd["pc"] in ("bd", "bdlu")
     c = _setup(bie, p, with_bd=use_bd)
@@ -241,13 +298,7 @@ def test_gmres_golden(bie, name):
     assert abs(np.linalg.norm(f) - gd["f_norm"]) < 1e-12 * gd["f_norm"]
     x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
     res = bie.gmres_solve(c["g"], c["bd"] if use_bd else None, _t(f), x, tol=gd["tol"], max_iter=gd["max_iter"])
-    assert res["iters"] == gd["iters"] and res["converged"] == gd["converged"]
-    hr = np.asarray(gd["hist"])
-    env = np.maximum.accumulate(np.asarray(gd.get("envelope", np.zeros(hr.size))))
-    rel = np.abs(np.asarray(res["hist"]) - hr) / hr
-    # 1e-10 bar, relaxed only where the oracle's own history moves more under
-    # 1e-13 perturbations of f (reading C23)
-    assert np.all(rel <= np.maximum(1e-10, 10 * env)), (rel.max(), env.max())
+    golden_check(res, gd, name)
 
 
 def test_abi_handle_and_argument_errors(bie):
@@ -292,3 +343,56 @@ def test_pinned_host_end_to_end(bie):
     y = ho.numpy().reshape(4, -1)
     for v in range(4):
         assert np.abs(y[v] - ref[v]).max() / np.abs(ref[v]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("structured", [False, True])
+def test_gmres_solve_host_bitwise_equals_device(bie, structured):
+    """bie_gmres_solve_host (host f / x, pinned, copies inside the call -- the
+    bench's e2e path) gives bit-identical histories and solutions to the
+    device-pointer call, and matches the oracle like it (config 2, BD)."""
+    import torch
+
+    p = make_problem(2)
+    c = _setup(bie, p)
+    bd = bie.BlockDiag(c["g"], structured=True) if structured else c["bd"]
+    f = rhs_pipe(p)
+    x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
+    rd = bie.gmres_solve(c["g"], bd, _t(f), x, tol=1e-8, max_iter=300)
+    fh = torch.from_numpy(f.copy()).pin_memory()
+    xh = torch.full_like(fh, float("nan")).pin_memory()
+    rh = bie.gmres_solve_host(c["g"], bd, fh, xh, tol=1e-8, max_iter=300)
+    assert rh["iters"] == rd["iters"] and np.array_equal(rh["hist"], rd["hist"])
+    assert np.array_equal(xh.numpy(), x.cpu().numpy())
+    assert rh["res_true"] == rd["res_true"] and rh["res_pc"] == rd["res_pc"]
+    xp = np.zeros(f.size)  # pageable numpy buffers are accepted too
+    rp = bie.gmres_solve_host(c["g"], bd, f, xp, tol=1e-8, max_iter=300)
+    assert np.array_equal(rp["hist"], rd["hist"]) and np.array_equal(xp, xh.numpy())
+    ref = oracle.gmres(c["og"], f, _obd(c), tol=1e-8, max_iter=300)
+    _cmp_gmres(rh, ref)
+
+
+def test_krylov_axpy_beyond_one_coefficient_tile(bie):
+    """k_multiaxpy stages its coefficients in tiles of 2048 (one
+    dynamic-smem block failed to launch for nv > 6144 -- a GMRES past ~6100
+    iterations).  nv = 7000 basis vectors against a rigorous rounding bound, and
+    the same sum split into two calls at the tile boundary."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    nv, n = 7000, 1000
+    V = rng.standard_normal((nv, n))
+    c = rng.standard_normal(nv)
+    Vd, cd = _t(V), _t(c)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    bie.Krylov.axpy(Vd, n, nv, cd, 1.0, 0.0, y, n)
+    torch.cuda.synchronize()
+    ref = V.T @ c
+    bound = nv * 1.2e-16 * (np.abs(V).T @ np.abs(c))
+    assert np.all(np.abs(y.cpu().numpy() - ref) <= bound)
+    # the same chain continued across two calls (beta = 1): 2048 + rest
+    y2 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    bie.Krylov.axpy(Vd, n, 2048, cd, 1.0, 0.0, y2, n)
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    bie.Krylov.axpy(Vd[2048 * n:], n, nv - 2048, cd[2048:], 1.0, 0.0, z, n)
+    torch.cuda.synchronize()
+    assert np.abs((y2 + z).cpu().numpy() - ref).max() <= 2 * bound.max()

@@ -92,17 +92,15 @@ def test_structured_bd_gmres_golden(bie, name):
     path = os.path.join(GOLDEN, f"gmres_{name}.json")
     if not os.path.exists(path):
         pytest.skip("golden not generated")
-    gd = json.load(open(path))
+    from test_gpu_bd_gmres import _golden, golden_check
+
+    gd = _golden(name)
     p = make_problem(gd["config"])
     g = bie.Geometry.from_problem(p)
     f = rhs_pipe(p)
     x = torch.zeros(f.size, dtype=torch.float64, device="cuda")
     r = bie.gmres_solve(g, bie.BlockDiag(g, structured=True), _t(f), x, tol=gd["tol"], max_iter=gd["max_iter"])
-    assert r["iters"] == gd["iters"]
-    hr = np.asarray(gd["hist"])
-    env = np.maximum.accumulate(np.asarray(gd["envelope"]))
-    rel = np.abs(np.asarray(r["hist"]) - hr) / hr
-    assert np.all(rel <= np.maximum(1e-10, 10 * env)), rel.max()
+    golden_check(r, gd, name + " (structured BD)")
 
 
 def test_structured_bd_errors(bie):

@@ -4,6 +4,9 @@
 Bars: matvec and field evaluation max-norm relative 1e-12 per vector (as C15);
 BD inverses and GMRES histories of the nearly singular SLP blocks follow the
 conditioning readings C23/C26 (envelopes measured with the oracle here)."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -167,17 +170,29 @@ def test_slp_blockdiag_inverse_and_apply(bie):
         assert np.abs(zc[2 * lo:2 * hi] - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def _envelope(og, f, max_iter):
-    """Oracle self-sensitivity of the SLP BD-GMRES history (C23/C26): explicit
-    inverses vs LU solves, and a 1e-13 relative perturbation of f."""
+EPS_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "round2", "disagreement.json")
+
+
+def _slp_perturbation(cid):
+    """Measured GPU-vs-oracle disagreement of the SLP primitives (matvec, BD
+    apply) and the Krylov primitives (tools/measure_disagreement.py)."""
+    d = json.load(open(EPS_FILE))[f"config{cid}"]
+    return {"A": max(x["rms"] for x in d["slp_matvec"]), "P": max(x["rms"] for x in d["slp_bd"]),
+            "dot": d["dot"]["rms"], "norm": d["norm"]["rms"], "sub": d["sub"]["rms"]}
+
+
+def _envelope(og, f, max_iter, cid):
+    """Oracle self-sensitivity of the SLP BD-GMRES history (C23/C26): three runs
+    with every iteration primitive perturbed at its measured GPU-vs-oracle
+    disagreement (the near-singular SLP blocks make P^-1 the dominant term)."""
     a = oracle.slp_gmres(og, f, oracle.OracleSLPBD(og), tol=1e-8, max_iter=max_iter)
-    b = oracle.slp_gmres(og, f, oracle.OracleSLPBDLU(og), tol=1e-8, max_iter=max_iter)
-    rng = np.random.default_rng(1)
-    c = oracle.slp_gmres(og, f * (1 + 1e-13 * rng.standard_normal(f.size)), oracle.OracleSLPBD(og), tol=1e-8,
-                         max_iter=max_iter)
-    k = min(len(a["hist"]), len(b["hist"]), len(c["hist"]))
-    env = np.maximum(np.abs(a["hist"][:k] - b["hist"][:k]), np.abs(a["hist"][:k] - c["hist"][:k])) / a["hist"][:k]
-    return a, np.maximum.accumulate(env), {a["iters"], b["iters"], c["iters"]}
+    runs = []
+    for s_ in range(3):
+        with oracle.perturbed(_slp_perturbation(cid), seed=3000 + s_):
+            runs.append(oracle.slp_gmres(og, f, oracle.OracleSLPBD(og), tol=1e-8, max_iter=max_iter))
+    k = min([len(a["hist"])] + [len(r["hist"]) for r in runs])
+    env = np.max([np.abs(r["hist"][:k] - a["hist"][:k]) / a["hist"][:k] for r in runs], axis=0)
+    return a, np.maximum.accumulate(env), {a["iters"]} | {r["iters"] for r in runs}
 
 
 @pytest.mark.parametrize("cid", [1, 2])
@@ -188,15 +203,16 @@ def test_slp_bd_gmres_parity(bie, cid):
     g, og = _setup(bie, p)
     f = rhs_pipe(p) if cid > 1 else np.ascontiguousarray(
         np.stack([-og.x.reshape(-1, 2)[:, 1], og.x.reshape(-1, 2)[:, 0]], 1).reshape(-1))
-    ref, env, its = _envelope(og, f, 300)
+    ref, env, its = _envelope(og, f, 300, cid)
     bd = bie.BlockDiag(g, op="slp")
     x = torch.zeros(2 * p.N, dtype=torch.float64, device="cuda")
     r = bie.gmres_solve_slp(g, bd, _t(f), x, 1e-8, 300)
     assert r["converged"] and ref["converged"]
-    assert min(its) - 1 <= r["iters"] <= max(its) + 1, (r["iters"], its)
+    assert min(its) <= r["iters"] <= max(its), (r["iters"], its)
     k = min(len(r["hist"]), len(env))
-    bar = np.maximum(1e-10, 10 * env[:k])
+    bar = np.maximum(1e-10, 2 * env[:k])
     rel = np.abs(r["hist"][:k] - ref["hist"][:k]) / ref["hist"][:k]
+    print(f"SLP config {cid}: max GPU dev {rel.max():.3e}, max env {env.max():.3e}, dev/bar {(rel / bar).max():.3f}")
     assert np.all(rel <= bar), (rel.max(), np.argmax(rel / bar))
 
 

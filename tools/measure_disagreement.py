@@ -105,6 +105,21 @@ def main():
         torch.cuda.synchronize()
         ys = oracle.cgs_sub(Vh, rd, wh)
         rec["sub"] = stats(y.cpu().numpy(), ys)
+        if cid <= 2:  # NEXT-1 single-layer operator and its BD (configs 1-2, C26)
+            rs = og.slp_apply(s)
+            rec["slp_matvec"], rec["slp_bd"] = [], []
+            bds = bie.BlockDiag(g, op="slp")
+            obs = oracle.OracleSLPBD(og)
+            for v in range(nv):
+                x = sig[v * 2 * p.N:(v + 1) * 2 * p.N]
+                o = torch.zeros_like(x)
+                bie.slp_apply(g, x, o)
+                ob = torch.zeros_like(x)
+                bie.blockdiag_apply(bds, x, ob)
+                torch.cuda.synchronize()
+                rec["slp_matvec"].append(stats(o.cpu().numpy(), rs[v]))
+                rec["slp_bd"].append(stats(ob.cpu().numpy(), obs.apply(s[v])))
+            bds.close()
         res[f"config{cid}"] = rec
         print(json.dumps({f"config{cid}": rec}), flush=True)
         g.close()
