@@ -463,26 +463,50 @@ def run_gpu(args):
                                    "iters": rr["iters"], "converged": rr["converged"], "max_iter": mi,
                                    "res_pc": rr["res_pc"], "res_true": rr["res_true"], "tol": 1e-8}
         extra["gmres_solve"] = sol
-        # NEXT-3: 16 right-hand sides on config 3 -- batched solver vs 16 single solves
+        # NEXT-3: the paper's three scenarios on config 3 -- pipe flow (P:l.217-227),
+        # shear on all curves (P:l.634-638) and the Stokeslet/rotlet exact solution
+        # (P:l.933-958) -- batched solver vs single solves; NEXT-2: the represented
+        # field on a reliable interior grid and the paper's eps(x) (P:l.752-757)
+        from bie_inputs import (interior_grid, node_positions, rhs_shear_all, stokeslet_rotlet_field,
+                                stokeslet_rotlet_params)
+
         pp = make_problem(3)
         gg = bie.Geometry.from_problem(pp)
         bdd = bie.BlockDiag(gg, structured=True)
-        F = torch.from_numpy(density(pp, nvec=16, vec_id=100).reshape(-1)).to(dev)
+        cs_, lam_, mu_ = stokeslet_rotlet_params(pp)
+        Fs = np.stack([rhs_pipe(pp), rhs_shear_all(pp),
+                       stokeslet_rotlet_field(node_positions(pp), cs_, lam_, mu_).reshape(-1)])
+        F = torch.from_numpy(Fs.reshape(-1).copy()).to(dev)
         X = torch.zeros_like(F)
-        bie.gmres_solve_batch(gg, bdd, F, X, nrhs=16, tol=1e-8, max_iter=1000)  # warm-up
+        bie.gmres_solve_batch(gg, bdd, F, X, nrhs=3, tol=1e-8, max_iter=1000)  # warm-up
         torch.cuda.synchronize()
         tb = time.perf_counter()
-        rb_ = bie.gmres_solve_batch(gg, bdd, F, X, nrhs=16, tol=1e-8, max_iter=1000)
+        rb_ = bie.gmres_solve_batch(gg, bdd, F, X, nrhs=3, tol=1e-8, max_iter=1000)
         torch.cuda.synchronize()
         tb = time.perf_counter() - tb
-        ts = time.perf_counter()
         n2 = 2 * pp.N
-        for r in range(16):
-            bie.gmres_solve(gg, bdd, F[r * n2:(r + 1) * n2], X[r * n2:(r + 1) * n2], tol=1e-8, max_iter=1000)
+        Xs = torch.zeros_like(F)
+        ts = time.perf_counter()
+        for r in range(3):
+            bie.gmres_solve(gg, bdd, F[r * n2:(r + 1) * n2], Xs[r * n2:(r + 1) * n2], tol=1e-8, max_iter=1000)
         torch.cuda.synchronize()
         ts = time.perf_counter() - ts
-        extra["multi_rhs"] = {"config": 3, "nrhs": 16, "batched_s": tb, "sequential_s": ts,
-                              "iters": [r["iters"] for r in rb_], "all_converged": all(r["converged"] for r in rb_)}
+        xs = X.cpu().numpy().reshape(3, -1, 2)
+        wl = pp.M * pp.n_pore
+        pts = interior_grid(pp, 400, 24)
+        u = torch.zeros(pts.size, dtype=torch.float64, device=dev)
+        bie.field_eval(gg, X[2 * n2:3 * n2], torch.from_numpy(pts.reshape(-1).copy()).to(dev), u)
+        uu = u.cpu().numpy().reshape(-1, 2)
+        uref = stokeslet_rotlet_field(pts, cs_, lam_, mu_)
+        nu_, nr_ = np.linalg.norm(uu, axis=1), np.linalg.norm(uref, axis=1)
+        eps_x = np.abs(nu_ - nr_) / nr_
+        extra["multi_rhs"] = {
+            "config": 3, "scenarios": ["pipe", "shear_all", "stokeslet_rotlet"], "nrhs": 3, "batched_s": tb,
+            "sequential_s": ts, "iters": [r["iters"] for r in rb_], "all_converged": all(r["converged"] for r in rb_),
+            "shear_pore_over_wall_density": float(np.abs(xs[1, :wl]).max() / np.abs(xs[1, wl:]).max()),
+            "stokeslet_eps_x": {"max": float(eps_x.max()), "median": float(np.median(eps_x)), "points": int(pts.shape[0]),
+                                "definition": "| |u| - |u_ref| | / |u_ref| on grid points with d(x, Gamma) > sqrt(ds) "
+                                              "(P:l.752-757, P:l.355-358), tol 1e-8 solve"}}
         # NEXT-1: the paper's own single-layer operator (KR-6 corrected) on the same
         # geometry, and an SLP BD-GMRES solve on config 3
         slp = {}

@@ -1133,8 +1133,11 @@ int build_schedules(Geometry *g) {
 // 2 = (4, 4, 2, 3) -- 3 warps/SMSP, 8 pairs per step;
 // 3 = (8, 2, 2, 1) with the step loop unrolled by two;
 // 4, 5 = (8, 2, 2, 1) with lockstep pair groups of 2 / 4 targets (GR);
-// 6 = (4, 4, 2, 4) -- 4 warps/SMSP at <= 128 registers.
-static const int kNumSymVar = 7;
+// 6 = (4, 4, 2, 4) -- 4 warps/SMSP at <= 128 registers;
+// 7 = (4, 4, 4, 1) -- 2 warps/SMSP, 16 pairs per step, registers for the pairs;
+// 8 = (8, 2, 2, 1) lockstep groups of 4 targets with the step loop unrolled by two;
+// 9 = (8, 2, 2, 1) lockstep groups of all 8 targets.
+static const int kNumSymVar = 10;
 static void *sym_kernel(int v) {
     switch (v) {
         case 1: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, 3>);
@@ -1143,10 +1146,13 @@ static void *sym_kernel(int v) {
         case 4: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 2>);
         case 5: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 4>);
         case 6: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 4>);
+        case 7: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, 1>);
+        case 8: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2, 4>);
+        case 9: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 8>);
         default: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1>);
     }
 }
-static int sym_warps(int v) { return (v == 0 || v == 3 || v == 4 || v == 5) ? 2 : 4; }
+static int sym_warps(int v) { return (v == 0 || v == 3 || v == 4 || v == 5 || v == 8 || v == 9) ? 2 : 4; }
 static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
         case 1: k_dlp_sym<4, 4, 4, 3><<<P, 128, 0, st>>>(sa); break;
@@ -1155,6 +1161,9 @@ static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
         case 4: k_dlp_sym<8, 2, 2, 1, 0, 1, 2><<<P, 64, 0, st>>>(sa); break;
         case 5: k_dlp_sym<8, 2, 2, 1, 0, 1, 4><<<P, 64, 0, st>>>(sa); break;
         case 6: k_dlp_sym<4, 4, 2, 4><<<P, 128, 0, st>>>(sa); break;
+        case 7: k_dlp_sym<4, 4, 4, 1><<<P, 128, 0, st>>>(sa); break;
+        case 8: k_dlp_sym<8, 2, 2, 1, 0, 2, 4><<<P, 64, 0, st>>>(sa); break;
+        case 9: k_dlp_sym<8, 2, 2, 1, 0, 1, 8><<<P, 64, 0, st>>>(sa); break;
         default: k_dlp_sym<8, 2, 2, 1><<<P, 64, 0, st>>>(sa); break;
     }
 }

@@ -21,6 +21,9 @@
 #include <cstdlib>
 #include <string>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "internal.cuh"
@@ -381,10 +384,23 @@ int bie_krylov_dots(const double *V, long long ldv, int nv, const double *w, lon
     Dot d;
     d.nchunks = (int)((n + kChunk - 1) / kChunk);
     d.ldp = nv;
-    BIE_CUDA_TRY(cudaMallocAsync(&d.partial, sizeof(double) * (size_t)d.nchunks * nv, st));
-    int rc = multidot(V, ldv, nv, w, n, d, out, st);
-    cudaFreeAsync(d.partial, st);
-    return rc;
+    if (d.nchunks > 1) {
+        // grow-only scratch per stream (work on one stream is ordered, so reuse is
+        // safe); a cudaMallocAsync per call cost ~10 us in the sharded driver
+        static std::mutex mu;
+        static std::unordered_map<cudaStream_t, std::pair<double *, size_t>> scratch;
+        const size_t need = (size_t)d.nchunks * nv;
+        std::lock_guard<std::mutex> lock(mu);
+        auto &e = scratch[st];
+        if (e.second < need) {
+            if (e.first) BIE_CUDA_TRY(cudaFreeAsync(e.first, st));
+            const size_t cap = std::max(need, 2 * e.second);
+            BIE_CUDA_TRY(cudaMallocAsync(&e.first, sizeof(double) * cap, st));
+            e.second = cap;
+        }
+        d.partial = e.first;
+    }
+    return multidot(V, ldv, nv, w, n, d, out, st);
 }
 
 int bie_krylov_axpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,

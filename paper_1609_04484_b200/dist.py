@@ -31,24 +31,34 @@ def bodies_of_rows(row_begin: int, row_end: int, M: int, n_pore: int):
     return b0, b1
 
 
-def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000, lookahead: int = 3):
+def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000, lookahead: int = 3, fold_norms: bool = True):
     """Left-preconditioned full GMRES (reading C13) on row-sharded vectors.
 
     be must provide: n, zeros(len), pc(x, out), apply_pc_op(v, out), apply_op(v, out),
     dots(V, ldv, nv, w, out), axpy(V, ldv, nv, c, alpha, beta, y), scale(x, s, y),
-    sqrt(inp, out, m), givens(H, ldh, cs, sn, g, h, h2, k, scal), trisolve(H, ldh, g, y, iters),
+    sqrt(inp, out, m), pythag(ss, h, m, out) (out = sqrt(ss - h[:m].h[:m]), replicated scalars),
+    givens(H, ldh, cs, sn, g, h, h2, k, scal), trisolve(H, ldh, g, y, iters),
     allreduce_(t), copy_(dst, src), sub(a, b, out), host(t) -> numpy, and
     host_async(t, slot) -> handle / host_wait(handle) -> numpy (non-blocking read-back).
-    The convergence check of iteration k runs after iteration k + lookahead is
+    Collectives per iteration: TWO all-reduces, each of k + 2 doubles -- the
+    first carries V^T w and ||w||^2 (w0, the breakdown reference), the second
+    V^T w' and ||w'||^2 after the first CGS pass; hk1 = ||w' - V h2|| is then
+    sqrt(||w'||^2 - ||h2||^2) (V orthonormal; h2 is at the rounding level of w',
+    so the difference from the direct norm is at the rounding level).  The
+    convergence check of iteration k runs after iteration k + lookahead is
     enqueued (as in bie_gmres_solve): later iterations are speculative and touch
     only entries the finish does not read.  Every rank holds identical
     replicated scalars, so all ranks stop at the same iteration.
+    fold_norms=False: four all-reduces per iteration with the direct norms
+    ||w|| (the operation sequence of bie_gmres_solve; used to check the two
+    drivers bit for bit at world size 1).
     Returns (x_loc, dict(iters, hist, res_pc, res_true, converged))."""
     n = be.n
     ldh = max_iter + 1
     V = be.zeros(ldh * n)
     H = be.zeros(ldh * max_iter)
     cs, sn, g, h, h2, tmp = (be.zeros(ldh) for _ in range(6))
+    red = be.zeros(ldh + 1)  # [V^T w | w.w] of one all-reduce
     scal = be.zeros(8)
     w, t = be.zeros(n), be.zeros(n)
     x = be.zeros(n)
@@ -60,6 +70,12 @@ def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000, lookahead: in
         be.dots(v, 0, 1, v, tmp[0:1])
         be.allreduce_(tmp[0:1])
         be.sqrt(tmp[0:1], scal[i:i + 1], 1)
+
+    def project(k, hh):  # hh[:k+1] = V^T w and red[k+1] = w.w, one all-reduce
+        be.dots(V, n, k + 1, w, red[:k + 1])
+        be.dots(w, 0, 1, w, red[k + 1:k + 2])
+        be.allreduce_(red[:k + 2])
+        be.copy_(hh[:k + 1], red[:k + 1])
 
     be.pc(f_loc, w)
     norm_into(w, 0)
@@ -83,14 +99,22 @@ def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000, lookahead: in
 
     for k in range(max_iter):
         be.apply_pc_op(vec(k), w)
-        norm_into(w, 1)
-        be.dots(V, n, k + 1, w, h[:k + 1])
-        be.allreduce_(h[:k + 1])
-        be.axpy(V, n, k + 1, h, -1.0, 1.0, w)
-        be.dots(V, n, k + 1, w, h2[:k + 1])
-        be.allreduce_(h2[:k + 1])
-        be.axpy(V, n, k + 1, h2, -1.0, 1.0, w)
-        norm_into(w, 2)
+        if fold_norms:
+            project(k, h)                                  # all-reduce 1: h, ||w||^2
+            be.sqrt(red[k + 1:k + 2], scal[1:2], 1)        # w0
+            be.axpy(V, n, k + 1, h, -1.0, 1.0, w)
+            project(k, h2)                                 # all-reduce 2: h2, ||w'||^2
+            be.axpy(V, n, k + 1, h2, -1.0, 1.0, w)
+            be.pythag(red[k + 1:k + 2], h2, k + 1, scal[2:3])  # hk1 = sqrt(||w'||^2 - ||h2||^2)
+        else:
+            norm_into(w, 1)
+            be.dots(V, n, k + 1, w, h[:k + 1])
+            be.allreduce_(h[:k + 1])
+            be.axpy(V, n, k + 1, h, -1.0, 1.0, w)
+            be.dots(V, n, k + 1, w, h2[:k + 1])
+            be.allreduce_(h2[:k + 1])
+            be.axpy(V, n, k + 1, h2, -1.0, 1.0, w)
+            norm_into(w, 2)
         be.givens(H, ldh, cs, sn, g, h, h2, k, scal)
         pending.append((k, be.host_async(scal[3:5], k)))
         if k + 1 < max_iter:
@@ -114,6 +138,46 @@ def dist_gmres(be, f_loc, tol: float = 1e-8, max_iter: int = 1000, lookahead: in
     return x, dict(iters=it, hist=np.array(hist), res_pc=float(r5 / beta), res_true=float(r6 / r7), converged=conv)
 
 
+# Per-iteration cost model of one rank, measured on one B200 at
+# config 4: the symmetric pair kernel costs C_UNIT seconds per (512-node block,
+# 32-node chunk) unit; BD applies stream their inverses from HBM at HBM_BPS;
+# row-local work (epilogue, CGS2 at the bench's 50-iteration depth) costs C_ROW
+# per node.
+C_UNIT = 22.6e-9
+HBM_BPS = 6.5e12
+C_ROW = 3.0e-9
+
+
+def unit_split(U: int, world: int, fixed_s):
+    """Slices [u_r, u_{r+1}) of the U symmetric-kernel units so that every
+    rank's modelled iteration time (its units + its fixed work fixed_s[r], i.e.
+    BD apply and row-local work) is equal; ranks whose fixed work alone exceeds
+    the balanced time get no units."""
+    fixed = np.asarray(fixed_s, dtype=np.float64)
+    act = np.ones(world, dtype=bool)
+    for _ in range(world):
+        T = (C_UNIT * U + fixed[act].sum()) / act.sum()
+        share = np.where(act, (T - fixed) / C_UNIT, 0.0)
+        if np.all(share[act] >= 0):
+            break
+        act &= share > 0
+    share = np.maximum(share, 0.0)
+    cuts = np.concatenate([[0.0], np.cumsum(share)])
+    cuts = np.round(cuts / cuts[-1] * U).astype(np.int64)
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def rank_fixed_work(M: int, n_pore: int, N: int, rb: int, re: int) -> float:
+    """Modelled seconds per iteration of a rank's non-pair work: streaming its
+    explicit BD inverses ((2 n_b)^2 doubles per body) and its row-local work."""
+    wall_lo = M * n_pore
+    pores = max(0, min(re, wall_lo) - rb) // n_pore if n_pore else 0
+    bd_bytes = pores * (2 * n_pore) ** 2 * 8
+    if re > wall_lo:
+        bd_bytes += (2 * (N - wall_lo)) ** 2 * 8
+    return bd_bytes / HBM_BPS + C_ROW * (re - rb)
+
+
 class GpuBackend:
     """libbie.so kernels + torch.distributed (NCCL) collectives for one rank.
 
@@ -126,14 +190,17 @@ class GpuBackend:
     op "slp": the paper's single-layer operator (NEXT-1) through the bie_slp_*
     counterparts (pairs_partial / epilogue_rows / apply_rows / range BD)."""
 
-    def __init__(self, g, rank: int, world: int, group=None, stream=None, mode: str = "sym", op: str = "dlp"):
+    def __init__(self, g, rank: int, world: int, group=None, mode: str = "sym", op: str = "dlp",
+                 balance: bool = True):
         import torch
 
         from . import _bie as B
 
         self.torch, self.B = torch, B
         self.g, self.rank, self.world, self.group = g, rank, world, group
-        self.stream = stream
+        # every kernel, copy and collective of this backend runs on torch's current
+        # stream (one stream: no cross-stream ordering to get wrong)
+        self.stream = None
         self.ranges = partition_rows(g.N, g.M, g.n_pore, world)
         self.rb, self.re = self.ranges[rank]
         self.n = 2 * (self.re - self.rb)
@@ -153,8 +220,13 @@ class GpuBackend:
         self.mode = mode
         if mode == "sym":
             U, nblk = B.dlp_sym_info(g)
-            self.units = (U * rank // world, U * (rank + 1) // world)
             self.blocks = (nblk * rank // world, nblk * (rank + 1) // world)
+            # units weighted against each rank's fixed per-iteration work (its BD
+            # apply -- the 2.15 GB Gamma_0 inverse at config 4 -- and its rows)
+            fixed = [rank_fixed_work(g.M, g.n_pore, g.N, b, e) for b, e in self.ranges]
+            self.unit_slices = unit_split(U, world, fixed) if balance else \
+                [(U * r // world, U * (r + 1) // world) for r in range(world)]
+            self.units = self.unit_slices[rank]
             self.part_full = torch.zeros(2 * g.N, dtype=torch.float64, device=dev)
             self.send = torch.zeros(world * self.maxlen, dtype=torch.float64, device=dev)
             self.recv = torch.zeros(self.maxlen, dtype=torch.float64, device=dev)
@@ -240,6 +312,15 @@ class GpuBackend:
 
     def sqrt(self, inp, out, m):
         self.B.Krylov.sqrt(inp, out, m, self.stream)
+
+    def pythag(self, ss, h, m, out):
+        if not hasattr(self, "_one"):
+            self._one = self.torch.ones(1, dtype=self.torch.float64, device=self.dev)
+        if not hasattr(self, "_hh"):
+            self._hh = self.torch.zeros(1, dtype=self.torch.float64, device=self.dev)
+        self.B.Krylov.dots(h, m, 1, h, m, self._hh, self.stream)
+        self.B.Krylov.axpy(self._hh, 0, 1, self._one, -1.0, 1.0, ss, 1, self.stream)
+        self.B.Krylov.sqrt(ss, out, 1, self.stream)
 
     def givens(self, H, ldh, cs, sn, g, h, h2, k, scal):
         self.B.Krylov.givens(H, ldh, cs, sn, g, h, h2, k, scal, self.stream)

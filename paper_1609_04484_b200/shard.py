@@ -19,16 +19,23 @@ def body_boundaries(N: int, M: int, n_pore: int) -> List[int]:
 
 def partition_rows(N: int, M: int, n_pore: int, world: int) -> List[Tuple[int, int]]:
     """Contiguous [begin, end) node ranges, one per rank, cut at body boundaries
-    nearest to the equal-work cuts r*N/world.  Every rank gets >= 1 body when
-    world <= number of bodies; surplus ranks get empty ranges."""
+    nearest to the equal-work cuts r*N/world.  Every rank gets at least one body:
+    world must not exceed the number of bodies (M + 1), and cuts that would
+    collapse onto the same boundary are moved to the next free one."""
     if world < 1:
         raise ValueError("world must be >= 1")
-    bounds = sorted(set(body_boundaries(N, M, n_pore)))
+    bounds = sorted(set(body_boundaries(N, M, n_pore)))  # body starts + N
+    nbodies = len(bounds) - 1
+    if world > nbodies:
+        raise ValueError(f"world ({world}) exceeds the number of bodies ({nbodies}): a rank would own no rows")
     cuts = [0]
     for r in range(1, world):
         ideal = r * N / world
-        best = min(bounds, key=lambda b: (abs(b - ideal), b))
-        cuts.append(max(best, cuts[-1]))
+        # keep at least one body for each of the remaining ranks
+        lo_i = bounds.index(cuts[-1]) + 1
+        hi_i = nbodies - (world - r)
+        cand = bounds[lo_i:hi_i + 1]
+        cuts.append(min(cand, key=lambda b: (abs(b - ideal), b)))
     cuts.append(N)
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 

@@ -5,6 +5,7 @@ compute here is a CPU backend on the oracle (rows of the completed operator,
 body-local BD blocks, plain vector loops), so the test checks the sharding,
 the all-gather of the density, the all-reduced inner products and the
 replicated Givens updates against the single-process oracle solve."""
+import decimal
 import math
 import os
 import socket
@@ -68,6 +69,10 @@ class CpuBackend:
     def sqrt(self, inp, out, m):
         out[:m] = torch.sqrt(inp[:m])
 
+    def pythag(self, ss, h, m, out):
+        hh = float(np.dot(h[:m].numpy(), h[:m].numpy()))
+        out[0] = math.sqrt(float(ss[0]) - hh)
+
     def givens(self, H, ldh, cs, sn, g, h, h2, k, scal):  # same arithmetic as k_givens
         col = H[k * ldh:(k + 1) * ldh]
         for j in range(k + 1):
@@ -79,7 +84,8 @@ class CpuBackend:
             col[j] = float(cs[j]) * a + float(sn[j]) * b
             col[j + 1] = -float(sn[j]) * a + float(cs[j]) * b
         a, b = float(col[k]), float(col[k + 1])
-        d = math.hypot(a, b)
+        # correctly rounded sqrt(a^2 + b^2), as both GMRES implementations (reading C28)
+        d = float((decimal.Decimal(a) ** 2 + decimal.Decimal(b) ** 2).sqrt(decimal.Context(prec=60)))
         cs[k], sn[k] = a / d, b / d
         col[k], col[k + 1] = d, 0.0
         g[k + 1] = -float(sn[k]) * float(g[k])

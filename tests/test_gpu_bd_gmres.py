@@ -153,12 +153,14 @@ ENV_FACTOR = 2.0  # GPU history within 2x the oracle's own sensitivity envelope 
 
 def _perturbation(cid, pc):
     """Measured GPU-vs-oracle disagreement per primitive (tools/measure_disagreement.py,
-    profiles/round2/disagreement.json): the noise levels of the envelope runs."""
+    profiles/round2/disagreement.json): the noise levels of the envelope runs --
+    the worst of random densities and the Krylov-like vectors of the iteration."""
     d = json.load(open(EPS_FILE))[f"config{cid}"]
-    eps = {"A": max(x["rms"] for x in d["matvec"]), "dot": d["dot"]["rms"], "norm": d["norm"]["rms"],
+    kry = d["matvec_krylov_bd" if pc else "matvec_krylov_nopc"]
+    eps = {"A": max(x["rms"] for x in d["matvec"] + kry), "dot": d["dot"]["rms"], "norm": d["norm"]["rms"],
            "sub": d["sub"]["rms"]}
     if pc:
-        eps["P"] = max(x["rms"] for x in d["bd_explicit"] + d["bd_structured"])
+        eps["P"] = max(x["rms"] for x in d["bd_explicit"] + d["bd_structured"] + d["bd_krylov"])
     return eps
 
 

@@ -82,3 +82,34 @@ def test_sharded_matvec_world2_gloo():
     p = make_problem(2)
     ref = oracle.OracleGeometry(p).apply(density(p)[0])
     assert np.array_equal(y, ref)
+
+
+def test_partition_rows_rejects_empty_ranks():
+    """ADVICE r1: surplus ranks used to get empty ranges (and a wrong body range);
+    now every rank owns >= 1 body or the call fails loudly."""
+    import pytest
+
+    from paper_1609_04484_b200.shard import partition_rows
+
+    r = partition_rows(1792, 10, 128, 11)
+    assert all(e > b for b, e in r) and r[0][0] == 0 and r[-1][1] == 1792
+    with pytest.raises(ValueError):
+        partition_rows(1792, 10, 128, 12)
+
+
+def test_unit_split_balances_fixed_work():
+    """dist.unit_split: units + fixed work equal across ranks (config-4 model);
+    a rank whose fixed work exceeds the balanced time gets no units."""
+    from paper_1609_04484_b200.dist import C_UNIT, rank_fixed_work, unit_split
+    from paper_1609_04484_b200.shard import partition_rows
+
+    N, M, n = 136192, 1000, 128
+    for W in (2, 4, 8):
+        ranges = partition_rows(N, M, n, W)
+        fixed = [rank_fixed_work(M, n, N, b, e) for b, e in ranges]
+        sl = unit_split(566000, W, fixed)
+        assert sl[0][0] == 0 and sl[-1][1] == 566000
+        t = [(u1 - u0) * C_UNIT + f for (u0, u1), f in zip(sl, fixed)]
+        assert max(t) / min(t) < 1.001
+    sl = unit_split(100, 2, [1.0, 0.0])
+    assert sl == [(0, 0), (0, 100)]

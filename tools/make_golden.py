@@ -43,12 +43,16 @@ CASES = {
 
 def perturbation(cid: int, pc: str) -> dict:
     """Noise levels per primitive for config cid: the worst measured rms
-    disagreement (max-norm-relative for vectors, ||w||-relative for dots)."""
+    disagreement (max-norm-relative for vectors, ||w||-relative for dots) over
+    random densities AND the Krylov-like vectors of the same iteration (P^-1 A
+    powers for BD, A powers without PC), which carry up to ~3x the random
+    level."""
     d = json.load(open(EPS_FILE))[f"config{cid}"]
-    eps = {"A": max(x["rms"] for x in d["matvec"]), "dot": d["dot"]["rms"], "norm": d["norm"]["rms"],
+    kry = d["matvec_krylov_bd" if pc != "none" else "matvec_krylov_nopc"]
+    eps = {"A": max(x["rms"] for x in d["matvec"] + kry), "dot": d["dot"]["rms"], "norm": d["norm"]["rms"],
            "sub": d["sub"]["rms"]}
     if pc != "none":
-        eps["P"] = max(x["rms"] for x in d["bd_explicit"] + d["bd_structured"])
+        eps["P"] = max(x["rms"] for x in d["bd_explicit"] + d["bd_structured"] + d["bd_krylov"])
     return eps
 
 
