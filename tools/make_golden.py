@@ -17,6 +17,13 @@ usage: python tools/make_golden.py [case ...]      (default: all cases)
 The full config-4 solve takes ~2 h of oracle time per run on 6-8 host
 threads; each finished run is written out immediately (partial files are
 valid goldens with fewer envelope runs, and say so).
+
+Long cases can run as independent processes, one per solve, and be merged:
+  python tools/make_golden.py CASE --run -1      (unperturbed)
+  python tools/make_golden.py CASE --run K       (perturbed run K, seed 1000 + K)
+  python tools/make_golden.py CASE --merge       (-> tests/golden/gmres_CASE.json)
+Each --run writes tests/golden/parts/CASE.runK.json; the merged file is the
+same record main() writes (same seeds, same noise levels).
 """
 import json
 import os
@@ -62,8 +69,77 @@ def solve(g, f, bd, c):
     return oracle.gmres(g, f, bd, tol=c["tol"], max_iter=c["max_iter"])
 
 
+def _setup(name):
+    c = CASES[name]
+    p = make_problem(c["config"])
+    g = oracle.OracleGeometry(p)
+    f = rhs_pipe(p)
+    eps = perturbation(c["config"], c["pc"])
+    t0 = time.time()
+    bd = None if c["pc"] == "none" else (oracle.OracleBDLU(g) if c["pc"] == "bdlu" else oracle.OracleBD(g))
+    return c, g, f, eps, bd, time.time() - t0
+
+
+def run_one(name, k):
+    """One solve of CASE as its own process: k = -1 unperturbed, else perturbed run k."""
+    c, g, f, eps, bd, tb = _setup(name)
+    t0 = time.time()
+    if k < 0:
+        r = solve(g, f, bd, c)
+    else:
+        with oracle.perturbed(eps, seed=1000 + k):
+            r = solve(g, f, bd, c)
+    part = dict(name=name, run=k, iters=r["iters"], converged=r["converged"], hist=[float(h) for h in r["hist"]],
+                res_pc=r["res_pc"], res_true=r["res_true"], f_norm=float(np.linalg.norm(f)), perturbation=eps,
+                oracle_build_s=tb, oracle_gmres_s=time.time() - t0,
+                omp_threads=os.environ.get("OMP_NUM_THREADS", str(os.cpu_count())))
+    d = os.path.join(OUT, "parts")
+    os.makedirs(d, exist_ok=True)
+    path = os.path.join(d, f"{name}.run{k}.json")
+    json.dump(part, open(path + ".tmp", "w"), indent=1)
+    os.replace(path + ".tmp", path)
+    print(name, "run", k, r["iters"], f"{time.time() - t0:.0f}s", flush=True)
+
+
+def merge(name):
+    c = CASES[name]
+    d = os.path.join(OUT, "parts")
+    base = json.load(open(os.path.join(d, f"{name}.run-1.json")))
+    h = np.asarray(base["hist"])
+    rec = dict(name=name, **c, f_norm=base["f_norm"], iters=base["iters"], converged=base["converged"],
+               hist=base["hist"], res_pc=base["res_pc"], res_true=base["res_true"],
+               perturbation=base["perturbation"], envelope_runs=[], envelope_iters=[], envelope=[],
+               oracle_build_s=base["oracle_build_s"], oracle_gmres_s=base["oracle_gmres_s"],
+               source="oracle/bie_oracle.c via tools/make_golden.py (one process per solve, merged); inputs "
+                      "bie_inputs seeded config; noise levels profiles/round2/disagreement.json",
+               omp_threads=base["omp_threads"])
+    env = np.zeros(len(h))
+    for k in range(RUNS):
+        pth = os.path.join(d, f"{name}.run{k}.json")
+        if not os.path.exists(pth):
+            continue
+        rp = json.load(open(pth))
+        assert rp["perturbation"] == base["perturbation"]
+        n = min(len(h), len(rp["hist"]))
+        env[:n] = np.maximum(env[:n], np.abs(np.asarray(rp["hist"][:n]) - h[:n]) / h[:n])
+        rec["envelope_runs"].append(rp["hist"])
+        rec["envelope_iters"].append(rp["iters"])
+    rec["envelope"] = [float(e) for e in env]
+    rec["envelope_complete"] = len(rec["envelope_runs"]) == RUNS
+    path = os.path.join(OUT, f"gmres_{name}.json")
+    json.dump(rec, open(path + ".tmp", "w"), indent=1)
+    os.replace(path + ".tmp", path)
+    print(name, "merged", len(rec["envelope_runs"]), "envelope runs, max env", float(env.max()))
+
+
 def main():
-    for name in (sys.argv[1:] or list(CASES)):
+    args = sys.argv[1:]
+    if "--run" in args:
+        i = args.index("--run")
+        return run_one(args[0], int(args[i + 1]))
+    if "--merge" in args:
+        return merge(args[0])
+    for name in (args or list(CASES)):
         c = CASES[name]
         p = make_problem(c["config"])
         g = oracle.OracleGeometry(p)

@@ -19,4 +19,13 @@ for r in rows[2:]:
         if k in hdr:
             i = hdr.index(k)
             print(f"{k:80s} {r[i]:>22s} {units[i]}")
+    # every warp-stall reason above 0.05 per issue
+    for i, k in enumerate(hdr):
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio") and k not in keys:
+            try:
+                v = float(r[i])
+            except ValueError:
+                continue
+            if v >= 0.05:
+                print(f"{k:80s} {r[i]:>22s} {units[i]}")
     print()

@@ -1,0 +1,112 @@
+"""Register-operand reads of the FP64 instructions in a kernel's hot loop (SASS).
+
+Round-2 finding (tools/fp64_mix2.cu, profiles/round2/fp64_mix2*.txt): on the
+B200 a DFMA whose three 64-bit operands all come from the register file runs
+at ~60% of the FP64 pipe, DMUL/DADD with two at ~90%, DFMA with two operands
+served by the operand-reuse cache at ~94%.  The FP64 pipe of the pair kernels
+is therefore bound by register-file reads, not by the instruction count.
+
+This script counts, for each FP64 instruction (DFMA/DMUL/DADD) of the largest
+basic-block region of a function, the 64-bit register operands that must be
+read from the register file: an operand is free if the previous instruction
+(of any kind) had the same register in the same slot marked `.reuse`.
+
+usage: cuobjdump -sass lib.so > x.sass; python tools/sass_reads.py x.sass NAME_SUBSTRING [...]
+"""
+import re
+import sys
+
+OPS = ("DFMA", "DMUL", "DADD")
+
+
+def functions(path):
+    cur, name = [], None
+    for line in open(path):
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            if name:
+                yield name, cur
+            name, cur = m.group(1), []
+            continue
+        m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
+        if m and name:
+            cur.append((int(m.group(1), 16), m.group(2).strip()))
+    if name:
+        yield name, cur
+
+
+def parse(ins):
+    # strip predicate
+    ins = re.sub(r"^@!?U?P\w+\s+", "", ins)
+    parts = ins.split(None, 1)
+    op = parts[0]
+    args = [a.strip() for a in parts[1].split(",")] if len(parts) > 1 else []
+    return op, args
+
+
+def reg_of(arg):
+    m = re.match(r"^[-|]*(R\d+)(\.reuse)?", arg)
+    return (m.group(1), bool(m.group(2))) if m else (None, False)
+
+
+def loop_region(code):
+    """The largest backward-branch loop body: [target, branch]."""
+    best = None
+    for addr, ins in code:
+        m = re.search(r"BRA\s+(?:`\(\.L_x_\d+\)|0x([0-9a-f]+))", ins)
+        if not m:
+            continue
+        # target address from the label table is not printed by cuobjdump; use explicit hex if present
+        if m.group(1):
+            tgt = int(m.group(1), 16)
+            if tgt < addr and (best is None or addr - tgt > best[1] - best[0]):
+                best = (tgt, addr)
+    return best
+
+
+def analyse(code, lo=None, hi=None):
+    prev_reuse = {}  # slot -> reg marked .reuse by the previous instruction
+    n_fp64 = reads = 0
+    per_op = {}
+    for addr, ins in code:
+        if lo is not None and not (lo <= addr <= hi):
+            continue
+        op, args = parse(ins)
+        base = op.split(".")[0]
+        srcs = args[1:] if args else []
+        cur_reuse = {}
+        if base in OPS:
+            n_fp64 += 1
+            r = 0
+            for slot, a in enumerate(srcs[:3]):
+                reg, reuse = reg_of(a)
+                if reg is None or reg == "RZ":
+                    continue
+                if prev_reuse.get(slot) != reg:
+                    r += 1
+                if reuse:
+                    cur_reuse[slot] = reg
+            reads += r
+            per_op[base] = per_op.get(base, 0) + 1
+        else:
+            for slot, a in enumerate(srcs[:3]):
+                reg, reuse = reg_of(a)
+                if reg and reuse:
+                    cur_reuse[slot] = reg
+        prev_reuse = cur_reuse
+    return n_fp64, reads, per_op
+
+
+def main():
+    path = sys.argv[1]
+    pats = sys.argv[2:]
+    for name, code in functions(path):
+        if pats and not any(p in name for p in pats):
+            continue
+        reg = loop_region(code)
+        n, r, po = analyse(code, *(reg or (None, None)))
+        print(f"{name[:70]:70s} loop={reg} fp64={n} reads={r} reads/fp64={r / max(n, 1):.3f} {po}")
+
+
+if __name__ == "__main__":
+    main()
