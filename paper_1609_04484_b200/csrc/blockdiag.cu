@@ -1016,36 +1016,48 @@ __global__ void k_struct_WG(const double *__restrict__ X, int n2, double *W, dou
 }
 
 // Y[:, col] = X V[:, col] for col < ncols; column col is vector col / M,
-// pore col % M, at base + (col / M) * stride + n2 * (col % M).  32 x 32 tiles.
+// pore col % M, at base + (col / M) * stride + n2 * (col % M).  Tiles of 32
+// columns x 8 RT rows (RT rows per thread); every output is one sequential FMA
+// chain over k = 0 .. n2-1, so the tile shape does not change the result.
+// RT = 4 for large M; RT = 1 when the 32-row grid would leave most SMs idle
+// (config 2: 8 -> 32 CTAs).
+template <int RT>
 __global__ void __launch_bounds__(256) k_struct_gemm(const double *__restrict__ X, int n2, int M, int ncols,
                                                      const double *__restrict__ in, double *out, long long stride) {
-    __shared__ double Xs[32][33];
+    constexpr int TR = 8 * RT;  // tile rows
+    __shared__ double Xs[TR][33];
     __shared__ double Vs[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 8 row groups of 4 rows
-    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 8 row groups of RT rows
+    const int r0 = blockIdx.y * TR, c0 = blockIdx.x * 32;
     const int col = c0 + tx;
     const long long cbase = col < ncols ? (long long)(col / M) * stride + (long long)n2 * (col % M) : 0;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[RT];
+#pragma unroll
+    for (int q = 0; q < RT; ++q) acc[q] = 0.0;
     for (int k0 = 0; k0 < n2; k0 += 32) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int rr = ty * 4 + q;  // X tile row, V tile k
+        for (int q = 0; q < RT; ++q) {
+            const int rr = ty * RT + q;  // X tile row
             Xs[rr][tx] = (r0 + rr < n2 && k0 + tx < n2) ? X[(long long)(r0 + rr) * n2 + k0 + tx] : 0.0;
-            Vs[rr][tx] = (col < ncols && k0 + rr < n2) ? in[cbase + k0 + rr] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int kk = ty * 4 + q;  // V tile k
+            Vs[kk][tx] = (col < ncols && k0 + kk < n2) ? in[cbase + k0 + kk] : 0.0;
         }
         __syncthreads();
 #pragma unroll 8
         for (int kk = 0; kk < 32; ++kk) {
             const double v = Vs[kk][tx];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = fma(Xs[ty * 4 + q][kk], v, acc[q]);
+            for (int q = 0; q < RT; ++q) acc[q] = fma(Xs[ty * RT + q][kk], v, acc[q]);
         }
         __syncthreads();
     }
     if (col < ncols) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int r = r0 + ty * 4 + q;
+        for (int q = 0; q < RT; ++q) {
+            const int r = r0 + ty * RT + q;
             if (r < n2) out[cbase + r] = acc[q];
         }
     }
@@ -1084,8 +1096,13 @@ int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec,
     if (bd->structured) {
         const int M = g->M, n2 = 2 * g->n_pore, ncols = nvec * M;
         if (M > 0) {
-            dim3 grid((unsigned)((ncols + 31) / 32), (unsigned)((n2 + 31) / 32));
-            k_struct_gemm<<<grid, 256, 0, st>>>(bd->sX, n2, M, ncols, in, out, stride);
+            const unsigned gx = (unsigned)((ncols + 31) / 32);
+            if ((long long)gx * ((n2 + 31) / 32) >= 2LL * g->num_sms)
+                k_struct_gemm<4><<<dim3(gx, (unsigned)((n2 + 31) / 32)), 256, 0, st>>>(bd->sX, n2, M, ncols, in, out,
+                                                                                    stride);
+            else
+                k_struct_gemm<1><<<dim3(gx, (unsigned)((n2 + 7) / 8)), 256, 0, st>>>(bd->sX, n2, M, ncols, in, out,
+                                                                                  stride);
             k_struct_corr<<<(ncols * 32 + 255) / 256, 256, 0, st>>>(bd->sW, bd->sM, n2, M, ncols, out, stride);
             count_launch(2);
             BIE_CUDA_TRY(cudaGetLastError());

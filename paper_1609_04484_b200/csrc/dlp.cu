@@ -1232,6 +1232,10 @@ static int sym_prepare(Geometry *g) {
         BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, 0));
         g->sym_occ[op] = std::max(1, occ);
     }
+    // in-block pairs: split each block's sources over up to 16 CTAs when there are
+    // too few blocks to fill the SMs (2 CTAs per block before splitting; config 2:
+    // 4 blocks x 2 x 16 = 128 CTAs of 32 sources each)
+    g->sym_dsplit = (int)std::max<long long>(1, std::min<long long>(16, (2LL * g->num_sms + 2LL * nTB - 1) / (2LL * nTB)));
     g->sym_nTB = nTB;
     g->sym_U = U;
     g->sym_state = -1;  // stays -1 (one-sided path) if an allocation fails
@@ -1239,7 +1243,7 @@ static int sym_prepare(Geometry *g) {
         cudaMalloc(&g->sym_Q, sizeof(double4) * (size_t)N) != cudaSuccess ||
         cudaMalloc(&g->sym_off, sizeof(long long) * (size_t)(nTB + 1)) != cudaSuccess ||
         cudaMalloc(&g->sym_acc, sizeof(unsigned long long) * 6 * (size_t)N) != cudaSuccess ||
-        cudaMalloc(&g->sym_diag, sizeof(double) * 2 * (size_t)N * 4) != cudaSuccess) {
+        cudaMalloc(&g->sym_diag, sizeof(double) * 2 * (size_t)N * g->sym_dsplit) != cudaSuccess) {
         (void)cudaGetLastError();  // clear the (non-sticky) allocation error
         return BIE_OK;
     }
@@ -1249,9 +1253,6 @@ static int sym_prepare(Geometry *g) {
         cudaMalloc(&g->sym_trace, sizeof(unsigned long long) * 2 * (size_t)std::max(p0.P, p1.P));
     g->sym_P = p0.P;
     g->sym_Useg = p0.Useg;
-    // in-block pairs: split each block's sources over up to 4 CTAs when there are
-    // too few blocks to fill the SMs (2 CTAs per block before splitting)
-    g->sym_dsplit = (int)std::max<long long>(1, std::min<long long>(4, (2LL * g->num_sms + 2LL * nTB - 1) / (2LL * nTB)));
     g->sym_state = 1;
     return BIE_OK;
 }

@@ -16,6 +16,8 @@ static thread_local std::string g_last_error;
 static std::atomic<long long> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static std::atomic<unsigned long long> g_bd_serial{0};
+unsigned long long next_bd_serial() { return ++g_bd_serial; }
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -277,6 +279,9 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     if (g->gm.pinned) cudaFreeHost(g->gm.pinned);
     for (auto &ev : g->gm.evs)
         if (ev) cudaEventDestroy(ev);
+    if (g->gm.gexec) cudaGraphExecDestroy(g->gm.gexec);
+    if (g->gm.graph) cudaGraphDestroy(g->gm.graph);
+    if (g->gm.cap) cudaStreamDestroy(g->gm.cap);
     cudaFree(g->gmb.V);
     cudaFree(g->gmb.w);
     cudaFree(g->gmb.H);

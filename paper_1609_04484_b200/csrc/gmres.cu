@@ -34,34 +34,40 @@ constexpr int kChunk = 4096;      // elements of the 2N dimension per multidot C
 constexpr int kDotThreads = 128;  // 4 basis vectors share one staged w chunk
 
 // partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv).
-// Grid (chunks, ceil(nv / 8)); each of the 8 warps owns one basis vector j and
-// reduces the whole 4096-element chunk (fixed lane order -> deterministic).
+// Grid (chunks, Gy); warp wid of CTA y owns basis vectors j = 4y + wid + 4 Gy q
+// and reduces the whole 4096-element chunk for each (fixed lane order ->
+// deterministic; the j loop does not change any per-j sum).  kdev != nullptr
+// (GMRES graph body): nv = min(*kdev + 1, nv), the iteration count read on the
+// device.  sq: store sqrt of the dot (a norm; single-chunk case only).
 __global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restrict__ V, long long ldv, int nv,
-                                                          const double *__restrict__ w, long long n,
-                                                          double *partial, int ldp) {
+                                                          const int *kdev, const double *__restrict__ w, long long n,
+                                                          double *partial, int ldp, int sq) {
+    if (kdev) nv = min(*kdev + 1, nv);
+    if ((int)blockIdx.y * (kDotThreads / 32) >= nv) return;
     __shared__ double ws[kChunk];
     const long long e0 = (long long)blockIdx.x * kChunk;
     const int len = (int)std::min<long long>(kChunk, n - e0);
     for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int j = blockIdx.y * (kDotThreads / 32) + wid;
-    if (j >= nv) return;
-    const double *vj = V + (long long)j * ldv + e0;
-    // four independent streams per lane keep enough loads in flight for HBM
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    int q = lane;
-    for (; q + 96 < len; q += 128) {
-        const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64), a3 = __ldcs(vj + q + 96);
-        acc0 = fma(a0, ws[q], acc0);
-        acc1 = fma(a1, ws[q + 32], acc1);
-        acc2 = fma(a2, ws[q + 64], acc2);
-        acc3 = fma(a3, ws[q + 96], acc3);
+    for (int j = blockIdx.y * (kDotThreads / 32) + wid; j < nv; j += gridDim.y * (kDotThreads / 32)) {
+        const double *vj = V + (long long)j * ldv + e0;
+        // four independent streams per lane keep enough loads in flight for HBM
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        int q = lane;
+        for (; q + 96 < len; q += 128) {
+            const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64),
+                         a3 = __ldcs(vj + q + 96);
+            acc0 = fma(a0, ws[q], acc0);
+            acc1 = fma(a1, ws[q + 32], acc1);
+            acc2 = fma(a2, ws[q + 64], acc2);
+            acc3 = fma(a3, ws[q + 96], acc3);
+        }
+        for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
+        double acc = (acc0 + acc1) + (acc2 + acc3);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) partial[(long long)blockIdx.x * ldp + j] = sq ? sqrt(acc) : acc;
     }
-    for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
-    double acc = (acc0 + acc1) + (acc2 + acc3);
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) partial[(long long)blockIdx.x * ldp + j] = acc;
 }
 
 // out[j] = (accumulate ? out[j] : 0) + sum_c partial[c * ldp + j]  (fixed order)
@@ -82,12 +88,14 @@ __device__ __forceinline__ double sum_chunks(const double *__restrict__ p, long 
     return t;
 }
 
-__global__ void k_reduce(const double *__restrict__ partial, int ldp, int nchunks, int nv, double *out,
-                         int accumulate) {
+__global__ void k_reduce(const double *__restrict__ partial, int ldp, int nchunks, int nv, const int *kdev,
+                         double *out, int accumulate, int sq) {
+    if (kdev) nv = min(*kdev + 1, nv);
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= nv) return;
     const double t = sum_chunks(partial + j, ldp, nchunks);
-    out[j] = accumulate ? out[j] + t : t;
+    const double r = accumulate ? out[j] + t : t;
+    out[j] = sq ? sqrt(r) : r;
 }
 
 // y[e] = beta * y[e] + alpha * sum_j V[j][e] * c[j]   (c in device memory, any nv).
@@ -111,8 +119,9 @@ __device__ __forceinline__ double axpy_chain(const double *__restrict__ V, long 
 }
 
 __global__ void __launch_bounds__(256) k_multiaxpy(const double *__restrict__ V, long long ldv, int nv,
-                                                   const double *__restrict__ c, double alpha, double beta,
-                                                   double *y, long long n) {
+                                                   const int *kdev, const double *__restrict__ c, double alpha,
+                                                   double beta, double *y, long long n) {
+    if (kdev) nv = min(*kdev + 1, nv);
     __shared__ double cs[kAxpyTile];
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool act = e < n;
@@ -197,6 +206,40 @@ __global__ void k_givens(GmState s, int k, int ldh) {
     givens_step(s.H + (long long)k * ldh, s.cs, s.sn, s.g, s.h, s.h2, s.scal, k);
 }
 
+// Graph-body form of the Givens step: the iteration index k = ctl[0] lives on
+// the device.  Writes hist[k + 1] = estimate, ctl[1] = converged (estimate < tol
+// or happy breakdown, the host check of reading C13), advances ctl[0] and, in
+// the CUDA-graph solve, sets the while-loop condition (continue while not
+// converged and k + 1 < max_iter).
+__global__ void k_givens_dev(GmState s, int *ctl, int ldh, int max_iter, double tol, double *hist,
+                             cudaGraphConditionalHandle cond, int use_cond) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int k = ctl[0];
+    unsigned cont = 0;
+    if (k < max_iter) {
+        givens_step(s.H + (long long)k * ldh, s.cs, s.sn, s.g, s.h, s.h2, s.scal, k);
+        const double est = s.scal[3];
+        const int conv = (est < tol || s.scal[4] != 0.0) ? 1 : 0;
+        hist[k + 1] = est;
+        ctl[1] = conv;
+        ctl[0] = k + 1;
+        cont = (!conv && k + 1 < max_iter) ? 1u : 0u;
+    }
+    if (use_cond) cudaGraphSetConditional(cond, cont);
+}
+
+// v = x / (*s) into the current-vector buffer and into V[ctl[0]] (when
+// ctl[0] < max_iter): the next Krylov vector, at the device-side index.
+__global__ void k_scale_store(const double *x, const double *s, double *V, long long n, const int *ctl,
+                              int max_iter, double *vcur) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const double y = x[e] / *s;
+    vcur[e] = y;
+    const int k = *ctl;
+    if (k < max_iter) V[(long long)k * n + e] = y;
+}
+
 // y = H^{-1} g (upper triangular, iters x iters), one CTA
 __global__ void k_trisolve(const double *H, int ldh, const double *g, double *y, int iters) {
     __shared__ double red[32];
@@ -223,27 +266,30 @@ struct Dot {
     int ldp = 0;
 };
 
-// out[0..nv) = V[0..nv)^T w (deterministic)
+// out[0..nv) = V[0..nv)^T w (deterministic).  kdev: nv = min(*kdev + 1, nv) on
+// the device (graph body; the grid is sized for the cap nv).  sq: out = sqrt.
 static int multidot(const double *V, long long ldv, int nv, const double *w, long long n, Dot &d, double *out,
-                    cudaStream_t st) {
+                    cudaStream_t st, const int *kdev = nullptr, int sq = 0) {
+    const int gy_full = (nv + kDotThreads / 32 - 1) / (kDotThreads / 32);
+    // device-side nv: cap the y extent (each warp loops over its vectors) so
+    // that the mostly idle tail of a max_iter-sized grid stays small
+    const int gy = kdev ? std::max(1, std::min(gy_full, (4 * 148 + d.nchunks - 1) / d.nchunks)) : gy_full;
     if (d.nchunks == 1) {  // one chunk (2N <= 4096): the partial IS the result, no reduction launch
-        k_multidot<<<dim3(1, (nv + kDotThreads / 32 - 1) / (kDotThreads / 32)), kDotThreads, 0, st>>>(
-            V, ldv, nv, w, n, out, 0);
+        k_multidot<<<dim3(1, gy), kDotThreads, 0, st>>>(V, ldv, nv, kdev, w, n, out, 0, sq);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
     }
-    k_multidot<<<dim3(d.nchunks, (nv + kDotThreads / 32 - 1) / (kDotThreads / 32)), kDotThreads, 0, st>>>(
-        V, ldv, nv, w, n, d.partial, d.ldp);
-    k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, out, 0);
+    k_multidot<<<dim3(d.nchunks, gy), kDotThreads, 0, st>>>(V, ldv, nv, kdev, w, n, d.partial, d.ldp, 0);
+    k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, kdev, out, 0, sq);
     count_launch(2);
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
 }
 
 static int multiaxpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,
-                     long long n, cudaStream_t st) {
-    k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, ldv, nv, c, alpha, beta, y, n);
+                     long long n, cudaStream_t st, const int *kdev = nullptr) {
+    k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, ldv, nv, kdev, c, alpha, beta, y, n);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
@@ -464,6 +510,19 @@ int bie_krylov_trisolve(const double *H, int ldh, const double *g, double *y, in
 }  // extern "C"
 
 // opf: BIE_FULL (the completed DLP) or kOpSLP (the single-layer operator, NEXT-1)
+//
+// One GMRES iteration is a fixed sequence of launches whose only varying
+// argument, the iteration index k, lives on the device (ctl[0]): operator apply
+// on v_k (kept in vcur), ||w||, CGS2 over V[0..k], hk1, Givens (k_givens_dev)
+// and v_{k+1} (k_scale_store).  The solve captures that sequence ONCE into the
+// body of a CUDA-graph conditional WHILE node; k_givens_dev sets the loop
+// condition, so a whole solve is one graph launch with no host round trip per
+// iteration.  The instantiated graph is cached on the geometry and reused while
+// the operator, BD handle, tol, max_iter and the workspace are unchanged.  With
+// profiling on (bie_profile_begin: per-apply events, which a graph body cannot
+// hold) or BIE_GMRES_GRAPH=0 the same sequence is enqueued from the host with a
+// kLook-iteration lookahead instead.  Both forms launch the same kernels with the
+// same arguments, so results are bitwise identical.
 static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie_blockdiag_t bdh, const double *f,
                             double *x, double tol, int max_iter, double *hist_host, int *iters, double *res_pc,
                             double *res_true, int *converged, void *stream) {
@@ -492,30 +551,13 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     GmState s{};
     Dot d;
     constexpr int kMaxLook = 7;
-    int kLook = 3;                     // iterations enqueued ahead of the host's convergence check
+    int kLook = 3;                     // host-driven form: iterations enqueued ahead of the check
     if (const char *e = getenv("BIE_GMRES_LOOKAHEAD")) kLook = std::max(1, std::min(kMaxLook, atoi(e)));
-    const int kRing = kLook + 1;       // estimate slots / events in flight
-    int rc = BIE_OK;
+    const int kRing = kLook + 1;
+    bool use_graph = !g->prof;
+    if (const char *e = getenv("BIE_GMRES_GRAPH")) use_graph = use_graph && atoi(e) != 0;
     d.nchunks = (int)((n + kChunk - 1) / kChunk);
     d.ldp = ldh;
-    auto cleanup = [&]() {};           // the workspace stays cached on the geometry
-#define GM_TRY(expr)                                       \
-    do {                                                   \
-        cudaError_t _e = (expr);                           \
-        if (_e != cudaSuccess) {                           \
-            rc = cuda_fail(_e, #expr);                     \
-            cleanup();                                     \
-            return rc;                                     \
-        }                                                  \
-    } while (0)
-#define GM_RC(expr)                                        \
-    do {                                                   \
-        rc = (expr);                                       \
-        if (rc != BIE_OK) {                                \
-            cleanup();                                     \
-            return rc;                                     \
-        }                                                  \
-    } while (0)
     GmresWork &ws = g->gm;
     auto ensure = [&](double *&ptr, size_t &cap, size_t need) -> cudaError_t {
         if (need <= cap) return cudaSuccess;
@@ -526,15 +568,15 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
         if (e == cudaSuccess) cap = need;
         return e;
     };
-    GM_TRY(ensure(ws.V, ws.V_cap, (size_t)ldh * n));
-    GM_TRY(ensure(ws.w, ws.n_cap, 2 * (size_t)n));  // w and t = w + n
-    GM_TRY(ensure(ws.H, ws.H_cap, (size_t)ldh * max_iter));
-    GM_TRY(ensure(ws.small, ws.small_cap, 5 * (size_t)ldh + 8));
-    GM_TRY(ensure(ws.partial, ws.partial_cap, (size_t)d.nchunks * ldh));
-    if (!ws.pinned) GM_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * (8 + 2 * (kMaxLook + 1))));
+    BIE_CUDA_TRY(ensure(ws.V, ws.V_cap, (size_t)ldh * n));
+    BIE_CUDA_TRY(ensure(ws.w, ws.n_cap, 3 * (size_t)n));  // w | t | vcur
+    BIE_CUDA_TRY(ensure(ws.H, ws.H_cap, (size_t)ldh * max_iter));
+    BIE_CUDA_TRY(ensure(ws.small, ws.small_cap, 6 * (size_t)ldh + 16));
+    BIE_CUDA_TRY(ensure(ws.partial, ws.partial_cap, (size_t)d.nchunks * ldh));
+    if (!ws.pinned) BIE_CUDA_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * (8 + 2 * (kMaxLook + 1))));
     for (int q = 0; q < kRing; ++q)
-        if (!ws.evs[q]) GM_TRY(cudaEventCreateWithFlags(&ws.evs[q], cudaEventDisableTiming));
-    double *V = ws.V, *w = ws.w, *t = ws.w + n;
+        if (!ws.evs[q]) BIE_CUDA_TRY(cudaEventCreateWithFlags(&ws.evs[q], cudaEventDisableTiming));
+    double *V = ws.V, *w = ws.w, *t = ws.w + n, *vcur = ws.w + 2 * n;
     double *pinned = ws.pinned;
     cudaEvent_t *evs = ws.evs;
     s.H = ws.H;
@@ -543,122 +585,161 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     s.g = ws.small + 2 * ldh;
     s.h = ws.small + 3 * ldh;
     s.h2 = ws.small + 4 * ldh;
-    s.scal = ws.small + 5 * ldh;
+    s.scal = ws.small + 5 * ldh;                         // 8 scalars
+    double *hist_d = ws.small + 5 * ldh + 8;             // [ldh] estimates
+    int *ctl = reinterpret_cast<int *>(ws.small + 6 * ldh + 8);  // [0] k, [1] converged
     d.partial = ws.partial;
-    GM_TRY(cudaMemsetAsync(s.g, 0, sizeof(double) * ldh, st));
-    GM_TRY(cudaMemsetAsync(s.H, 0, sizeof(double) * (size_t)ldh * max_iter, st));
+    BIE_CUDA_TRY(cudaMemsetAsync(s.g, 0, sizeof(double) * ldh, st));
+    BIE_CUDA_TRY(cudaMemsetAsync(s.H, 0, sizeof(double) * (size_t)ldh * max_iter, st));
+    BIE_CUDA_TRY(cudaMemsetAsync(ctl, 0, 2 * sizeof(int), st));
 
-    auto apply_op = [&](const double *in, double *out) -> int {  // out = P^{-1} A in
+    auto apply_op = [&](const double *in, double *out, cudaStream_t q) -> int {  // out = P^{-1} A in
         if (bd) {
-            int r = dlp_apply_impl(g, in, t, 1, opf, 0, g->N, st);
+            int r = dlp_apply_impl(g, in, t, 1, opf, 0, g->N, q);
             if (r) return r;
-            return blockdiag_apply_impl(bd, t, out, 1, st);
+            return blockdiag_apply_impl(bd, t, out, 1, q);
         }
-        return dlp_apply_impl(g, in, out, 1, opf, 0, g->N, st);
+        return dlp_apply_impl(g, in, out, 1, opf, 0, g->N, q);
     };
-    auto norm_to = [&](const double *v, double *dst) -> int {  // dst = ||v|| (device)
-        int r = multidot(v, 0, 1, v, n, d, s.scal + 5, st);
-        if (r) return r;
-        k_sqrt<<<1, 1, 0, st>>>(s.scal + 5, dst);
-        count_launch();
+    auto norm_to = [&](const double *v, double *dst, cudaStream_t q) -> int {  // dst = ||v|| (device)
+        return multidot(v, 0, 1, v, n, d, dst, q, nullptr, 1);
+    };
+    const unsigned eb = (unsigned)((n + 255) / 256);
+    // one iteration at the device-side index k = ctl[0]
+    auto body = [&](cudaStream_t q, cudaGraphConditionalHandle cond, int use_cond) -> int {
+        int r;
+        if ((r = apply_op(vcur, w, q))) return r;
+        if ((r = norm_to(w, s.scal + 1, q))) return r;  // w0 = ||P^{-1} A v_k||
+        // CGS2 over V[0..k]
+        if ((r = multidot(V, n, ldh, w, n, d, s.h, q, ctl))) return r;
+        if ((r = multiaxpy(V, n, ldh, s.h, -1.0, 1.0, w, n, q, ctl))) return r;
+        if ((r = multidot(V, n, ldh, w, n, d, s.h2, q, ctl))) return r;
+        if ((r = multiaxpy(V, n, ldh, s.h2, -1.0, 1.0, w, n, q, ctl))) return r;
+        if ((r = norm_to(w, s.scal + 2, q))) return r;  // hk1
+        k_givens_dev<<<1, 1, 0, q>>>(s, ctl, ldh, max_iter, tol, hist_d, cond, use_cond);
+        k_scale_store<<<eb, 256, 0, q>>>(w, s.scal + 2, V, n, ctl, max_iter, vcur);
+        count_launch(2);
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
     };
-    const unsigned eb = (unsigned)((n + 255) / 256);
 
     // r0 = P^{-1} f, beta = ||r0||, v0 = r0 / beta
     if (bd) {
-        GM_RC(blockdiag_apply_impl(bd, f, w, 1, st));
+        BIE_RC_TRY(blockdiag_apply_impl(bd, f, w, 1, st));
     } else {
-        GM_TRY(cudaMemcpyAsync(w, f, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        BIE_CUDA_TRY(cudaMemcpyAsync(w, f, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     }
-    GM_RC(norm_to(w, s.scal + 0));
-    GM_TRY(cudaMemcpyAsync(pinned, s.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
-    GM_TRY(cudaStreamSynchronize(st));
+    BIE_RC_TRY(norm_to(w, s.scal + 0, st));
+    BIE_CUDA_TRY(cudaMemcpyAsync(pinned, s.scal, sizeof(double), cudaMemcpyDeviceToHost, st));
+    BIE_CUDA_TRY(cudaStreamSynchronize(st));
     const double beta = pinned[0];
     hist_host[0] = 1.0;
     *iters = 0;
     *converged = 0;
-    GM_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
+    BIE_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * n, st));
     if (beta == 0.0) {
         *converged = 1;
         *res_pc = 0.0;
         *res_true = 0.0;
-        cleanup();
         return BIE_OK;
     }
-    k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 0, V, n);
+    k_scale_store<<<eb, 256, 0, st>>>(w, s.scal + 0, V, n, ctl, max_iter, vcur);  // ctl[0] = 0: V[0]
     count_launch();
-    GM_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
-    // kLook-iteration lookahead: iteration k is enqueued before the host reads
-    // the estimate of iteration k - kLook, so the device queue holds ~kLook
-    // matvecs of work and a late host thread (descheduled, or waiting on a
-    // driver lock) does not idle the GPU.  Iterations after the converged one
-    // are speculative: iteration k only touches H[:,k], g[k], g[k+1], cs/sn[k]
-    // and V[k+1], none of which the finish (columns 0..it-1) reads; after a
-    // happy breakdown they may compute NaNs in those unused entries only.
+    BIE_CUDA_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
     int it = 0;
-    bool done = false;
-    auto check = [&](int kk) -> int {  // read the estimate of iteration kk (its slot)
-        BIE_CUDA_TRY(cudaEventSynchronize(evs[kk % kRing]));
-        const double est = pinned[8 + 2 * (kk % kRing)];
-        const bool brk = pinned[9 + 2 * (kk % kRing)] != 0.0;
-        hist_host[kk + 1] = est;
-        it = kk + 1;
-        if (est < tol || brk) {
-            *converged = 1;
-            done = true;
+    bool conv = false;
+    if (use_graph) {
+        const GmGraphKey key{bd, bd ? bd->serial : 0, opf, max_iter, tol, V, w, ws.small, ws.partial, g->partial,
+                             g->slp_s};
+        if (!ws.gexec || !(ws.gkey == key)) {
+            if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
+            if (ws.graph) cudaGraphDestroy(ws.graph);
+            ws.gexec = nullptr;
+            ws.graph = nullptr;
+            // buffers the apply allocates lazily must exist before the capture
+            BIE_RC_TRY(apply_op(vcur, w, st));
+            if (!ws.cap) BIE_CUDA_TRY(cudaStreamCreateWithFlags(&ws.cap, cudaStreamNonBlocking));
+            BIE_CUDA_TRY(cudaGraphCreate(&ws.graph, 0));
+            cudaGraphConditionalHandle cond;
+            BIE_CUDA_TRY(cudaGraphConditionalHandleCreate(&cond, ws.graph, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = cond;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            BIE_CUDA_TRY(cudaGraphAddNode(&node, ws.graph, nullptr, 0, &cp));
+            cudaGraph_t bg = cp.conditional.phGraph_out[0];
+            BIE_CUDA_TRY(cudaStreamBeginCaptureToGraph(ws.cap, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+            const long long c0 = bie_launch_count();
+            const int rb = body(ws.cap, cond, 1);
+            cudaGraph_t cap_out = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(ws.cap, &cap_out);
+            ws.body_launches = bie_launch_count() - c0;
+            count_launch(-(int)ws.body_launches);  // counted per executed iteration below
+            if (rb != BIE_OK) return rb;
+            BIE_CUDA_TRY(ce);
+            BIE_CUDA_TRY(cudaGraphInstantiate(&ws.gexec, ws.graph, 0));
+            ws.gkey = key;
         }
-        return BIE_OK;
-    };
-    for (int k = 0; k < max_iter && !done; ++k) {
-        double *vk = V + (long long)k * n;
-        GM_RC(apply_op(vk, w));
-        GM_RC(norm_to(w, s.scal + 1));  // w0 = ||P^{-1} A v_k||
-        // CGS2
-        GM_RC(multidot(V, n, k + 1, w, n, d, s.h, st));
-        GM_RC(multiaxpy(V, n, k + 1, s.h, -1.0, 1.0, w, n, st));
-        GM_RC(multidot(V, n, k + 1, w, n, d, s.h2, st));
-        GM_RC(multiaxpy(V, n, k + 1, s.h2, -1.0, 1.0, w, n, st));
-        GM_RC(norm_to(w, s.scal + 2));  // hk1
-        k_givens<<<1, 1, 0, st>>>(s, k, ldh);
-        count_launch();
-        GM_TRY(cudaGetLastError());
-        GM_TRY(cudaMemcpyAsync(pinned + 8 + 2 * (k % kRing), s.scal + 3, 2 * sizeof(double),
-                               cudaMemcpyDeviceToHost, st));
-        GM_TRY(cudaEventRecord(evs[k % kRing], st));
-        if (k + 1 < max_iter) {
-            k_scale_div<<<eb, 256, 0, st>>>(w, s.scal + 2, V + (long long)(k + 1) * n, n);
-            count_launch();
+        BIE_CUDA_TRY(cudaGraphLaunch(ws.gexec, st));
+        BIE_CUDA_TRY(cudaMemcpyAsync(pinned + 1, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        BIE_CUDA_TRY(cudaStreamSynchronize(st));
+        const int *hc = reinterpret_cast<const int *>(pinned + 1);
+        it = hc[0];
+        conv = hc[1] != 0;
+        count_launch((int)(ws.body_launches * it));
+    } else {
+        // host-driven: iteration k is enqueued before the host reads the state of
+        // iteration k - kLook (so the device queue holds ~kLook iterations of
+        // work).  Iterations after the converged one are speculative: they touch
+        // only H[:,k], g[k..k+1], cs/sn[k], hist[k+1] and V[k+1], none of which
+        // the finish reads (after a happy breakdown possibly NaNs, unused).
+        bool done = false;
+        auto check = [&](int kk) -> int {
+            BIE_CUDA_TRY(cudaEventSynchronize(evs[kk % kRing]));
+            const int *hc = reinterpret_cast<const int *>(pinned + 8 + 2 * (kk % kRing));
+            it = kk + 1;
+            if (hc[1]) {
+                conv = true;
+                done = true;
+            }
+            return BIE_OK;
+        };
+        for (int k = 0; k < max_iter && !done; ++k) {
+            BIE_RC_TRY(body(st, cudaGraphConditionalHandle{}, 0));
+            BIE_CUDA_TRY(cudaMemcpyAsync(pinned + 8 + 2 * (k % kRing), ctl, 2 * sizeof(int),
+                                         cudaMemcpyDeviceToHost, st));
+            BIE_CUDA_TRY(cudaEventRecord(evs[k % kRing], st));
+            if (k >= kLook) BIE_RC_TRY(check(k - kLook));
         }
-        if (k >= kLook) GM_RC(check(k - kLook));
+        while (!done && it < max_iter) BIE_RC_TRY(check(it));  // the iterations still in flight
     }
-    while (!done && it < max_iter) GM_RC(check(it));  // the iterations still in flight
     *iters = it;
+    *converged = conv ? 1 : 0;
     // y = H^{-1} g, x = V y
     k_trisolve<<<1, 256, 0, st>>>(s.H, ldh, s.g, s.h, it);
     count_launch();
-    GM_TRY(cudaGetLastError());
-    GM_RC(multiaxpy(V, n, it, s.h, 1.0, 0.0, x, n, st));
+    BIE_CUDA_TRY(cudaGetLastError());
+    BIE_RC_TRY(multiaxpy(V, n, it, s.h, 1.0, 0.0, x, n, st));
     // residual pair (P:l.678-686): r = f - A x
-    GM_RC(dlp_apply_impl(g, x, t, 1, opf, 0, g->N, st));
+    BIE_RC_TRY(dlp_apply_impl(g, x, t, 1, opf, 0, g->N, st));
     k_sub<<<eb, 256, 0, st>>>(f, t, w, n);
     count_launch();
-    GM_RC(norm_to(w, s.scal + 6));
-    GM_RC(norm_to(f, s.scal + 7));
+    BIE_RC_TRY(norm_to(w, s.scal + 6, st));
+    BIE_RC_TRY(norm_to(f, s.scal + 7, st));
     if (bd) {
-        GM_RC(blockdiag_apply_impl(bd, w, t, 1, st));
-        GM_RC(norm_to(t, s.scal + 5));
-        GM_TRY(cudaMemcpyAsync(pinned + 5, s.scal + 5, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BIE_RC_TRY(blockdiag_apply_impl(bd, w, t, 1, st));
+        BIE_RC_TRY(norm_to(t, s.scal + 5, st));
+        BIE_CUDA_TRY(cudaMemcpyAsync(pinned + 5, s.scal + 5, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     } else {
-        GM_TRY(cudaMemcpyAsync(pinned + 6, s.scal + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BIE_CUDA_TRY(cudaMemcpyAsync(pinned + 6, s.scal + 6, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     }
-    GM_TRY(cudaStreamSynchronize(st));
+    if (it > 0)
+        BIE_CUDA_TRY(cudaMemcpyAsync(hist_host + 1, hist_d + 1, sizeof(double) * it, cudaMemcpyDeviceToHost, st));
+    BIE_CUDA_TRY(cudaStreamSynchronize(st));
     *res_true = pinned[6] / pinned[7];
     *res_pc = bd ? pinned[5] / beta : *res_true;
-#undef GM_TRY
-#undef GM_RC
-    cleanup();
     return BIE_OK;
 }
 
@@ -810,12 +891,8 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     }
     auto Vr = [&](int r, int k) { return V + ((size_t)r * ldh + k) * n; };
     auto norm_to = [&](const double *v, double *tmp, double *dst) -> int {
-        int q = multidot(v, 0, 1, v, n, d, tmp, st);
-        if (q) return q;
-        k_sqrt<<<1, 1, 0, st>>>(tmp, dst);
-        count_launch();
-        BIE_CUDA_TRY(cudaGetLastError());
-        return BIE_OK;
+        (void)tmp;
+        return multidot(v, 0, 1, v, n, d, dst, st, nullptr, 1);
     };
     // r0 = P^{-1} f for all systems at once
     if (bd) {

@@ -24,6 +24,11 @@ int cuda_fail(cudaError_t e, const char *what);
         cudaError_t _e = (expr);                                    \
         if (_e != cudaSuccess) return ::bie::cuda_fail(_e, #expr);  \
     } while (0)
+#define BIE_RC_TRY(expr)                \
+    do {                                \
+        const int _rc = (expr);         \
+        if (_rc != BIE_OK) return _rc;  \
+    } while (0)
 
 // Static, perfectly balanced partition of the (target-block x source-tile)
 // work units of the all-pairs kernel over a persistent grid.
@@ -40,6 +45,25 @@ struct PairSched {
     long long Useg = 1; // units per dynamically claimed segment
 };
 
+struct BlockDiag;
+// What a captured GMRES iteration graph depends on (gmres.cu): the operator, the
+// BD handle (pointer + serial, so a new factorisation at a reused address
+// does not match), tol, max_iter and every buffer the body's kernels address.
+struct GmGraphKey {
+    const BlockDiag *bd = nullptr;
+    unsigned long long bd_serial = 0;
+    unsigned opf = 0;
+    int max_iter = 0;
+    double tol = 0.0;
+    const void *V = nullptr, *w = nullptr, *small = nullptr, *partial = nullptr, *gpartial = nullptr,
+               *slp_s = nullptr;
+    bool operator==(const GmGraphKey &o) const {
+        return bd == o.bd && bd_serial == o.bd_serial && opf == o.opf && max_iter == o.max_iter && tol == o.tol &&
+               V == o.V && w == o.w && small == o.small && partial == o.partial && gpartial == o.gpartial &&
+               slp_s == o.slp_s;
+    }
+};
+
 // GMRES workspace cached on the geometry (grow-only): per-call cudaMalloc /
 // cudaMallocHost left the device idle for up to ~1 s in some steps.
 struct GmresWork {
@@ -47,6 +71,12 @@ struct GmresWork {
     size_t V_cap = 0, n_cap = 0, H_cap = 0, small_cap = 0, partial_cap = 0;
     double *pinned = nullptr;  // 8 + 2 * 8 doubles
     cudaEvent_t evs[8] = {};
+    // bie_gmres_solve*: the captured iteration loop (conditional WHILE graph)
+    cudaStream_t cap = nullptr;  // private capture stream
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    GmGraphKey gkey;
+    long long body_launches = 0;  // kernels per iteration of the graph body
 };
 
 struct Geometry {
@@ -104,8 +134,10 @@ struct Geometry {
 // process-wide count of kernels launched by the library (bie_launch_count)
 void count_launch(int n = 1);
 
+unsigned long long next_bd_serial();
 struct BlockDiag {
     uint32_t magic = kBlockMagic;
+    unsigned long long serial = next_bd_serial();  // distinguishes factorisations (GMRES graph cache)
     Geometry *g = nullptr;
     int b0 = 0, b1 = 0;             // body range [b0, b1) (pores 0..M-1, wall M)
     int op = 0;                     // 0: blocks of the completed DLP; 1: of the SLP (NEXT-1)
