@@ -356,6 +356,20 @@ BIE_API int bie_slp_field_eval(bie_geometry_t g, const double *sigma, const doub
 BIE_API int bie_blockdiag_factor_slp(bie_geometry_t g, bie_blockdiag_t *out, void *stream);
 
 /*
+ * bie_blockdiag_factor_structured_slp -- the same SLP BD preconditioner with
+ * the pore blocks inverted through their structure (P:l.655-657 footnote:
+ * "accelerated using the FFT").  On a pore of equispaced nodes x_j = c + r
+ * (cos, sin)(2 pi j / n) the SLP block satisfies T_i^T B[i][j] T_j = b(j - i),
+ * T_j the rotation by 2 pi j / n, so B = D C D^T with C block-circulant; its
+ * exact inverse is block-circulant with first block row d(m) (one 2x2 complex
+ * inverse per Fourier mode).  Stored per pore: d(m), 4 n doubles.  The wall is
+ * inverted exactly as in bie_blockdiag_factor_slp.  Apply, block_inverse and
+ * the GMRES calls behave as for bie_blockdiag_factor_slp.  Errors: BIE_EINVAL,
+ * BIE_ECUDA, BIE_ESINGULAR (a singular Fourier block or a zero wall pivot).
+ */
+BIE_API int bie_blockdiag_factor_structured_slp(bie_geometry_t g, bie_blockdiag_t *out, void *stream);
+
+/*
  * bie_gmres_solve_slp / bie_gmres_solve_batch_slp -- bie_gmres_solve and
  * bie_gmres_solve_batch on the SLP system A_SLP sigma = f (P:l.596-601,
  * 661-663).  bd must be NULL or come from bie_blockdiag_factor_slp on g

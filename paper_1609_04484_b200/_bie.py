@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "bie_krylov_trisolve", "bie_dlp_sym_info", "bie_dlp_pairs_partial", "bie_dlp_epilogue_rows",
     "bie_kr_weights", "bie_slp_apply", "bie_slp_apply_rows", "bie_slp_field_eval", "bie_blockdiag_factor_slp",
     "bie_gmres_solve_slp", "bie_gmres_solve_batch_slp", "bie_blockdiag_factor_structured",
+    "bie_blockdiag_factor_structured_slp",
     "bie_slp_pairs_partial", "bie_slp_epilogue_rows", "bie_blockdiag_factor_range_slp",
     "bie_geometry_node_table", "bie_pore_template", "bie_gmres_solve_host", "bie_fp64_peak",
 )
@@ -96,6 +97,7 @@ def lib():
         "bie_slp_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_blockdiag_factor_slp": [vp, ctypes.POINTER(vp), vp],
         "bie_blockdiag_factor_structured": [vp, ctypes.POINTER(vp), vp],
+        "bie_blockdiag_factor_structured_slp": [vp, ctypes.POINTER(vp), vp],
         "bie_slp_pairs_partial": [vp, vp, vp, ctypes.c_longlong, ctypes.c_longlong, c_int, c_int, vp],
         "bie_slp_epilogue_rows": [vp, vp, vp, vp, c_int, c_int, vp],
         "bie_blockdiag_factor_range_slp": [vp, c_int, c_int, ctypes.POINTER(vp), vp],
@@ -297,16 +299,19 @@ class BlockDiag:
     """bie_blockdiag_t: explicit per-body inverses (A6).  bodies=(b0, b1) factors
     only that body range (row sharding); its apply takes local vectors.
     op="slp": blocks of the single-layer operator (bie_blockdiag_factor_slp).
-    structured=True: pore blocks from one reference inverse + rank-2 Woodbury
-    terms (bie_blockdiag_factor_structured; DLP only)."""
+    structured=True: DLP pore blocks from one reference inverse + rank-2
+    Woodbury terms (bie_blockdiag_factor_structured); with op="slp", pore
+    blocks as rotating-frame block-circulant inverses
+    (bie_blockdiag_factor_structured_slp)."""
 
     def __init__(self, g: Geometry, stream=None, bodies=None, op: str = "dlp", structured: bool = False):
         h = ctypes.c_void_p()
         self.op = op
         if structured:
-            if op != "dlp" or bodies is not None:
-                raise ValueError("the structured pore BD is built for the whole geometry and the DLP operator")
-            _check(lib().bie_blockdiag_factor_structured(g.h, ctypes.byref(h), _stream_ptr(stream)))
+            if bodies is not None:
+                raise ValueError("the structured pore BD is built for the whole geometry")
+            fn = lib().bie_blockdiag_factor_structured_slp if op == "slp" else lib().bie_blockdiag_factor_structured
+            _check(fn(g.h, ctypes.byref(h), _stream_ptr(stream)))
         elif op == "slp":
             if bodies is None:
                 _check(lib().bie_blockdiag_factor_slp(g.h, ctypes.byref(h), _stream_ptr(stream)))

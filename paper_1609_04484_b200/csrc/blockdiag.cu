@@ -837,6 +837,20 @@ __global__ void k_unpermute(BDView v, BDScratch s) {
     for (int j = threadIdx.x; j < n2; j += blockDim.x) M[perm[j]] = row[j];
 }
 
+// Rows too long for shared memory (n2 > 27k: the config-5 wall, 32768 columns):
+// rows [r0, r0 + NB) staged in the panel workspace W (NB x n2 per matrix).
+__global__ void k_unpermute_g(BDView v, BDScratch s, int r0) {
+    const int m = blockIdx.y, r = r0 + blockIdx.x;
+    const int n2 = v.n2;
+    if (r >= n2) return;
+    double *M = v.mat + (long long)m * v.mstride + (long long)r * n2;
+    double *row = s.W + (long long)m * n2 * NB + (long long)blockIdx.x * n2;
+    const int *perm = reinterpret_cast<const int *>(s.T + (long long)m * n2 * NB);
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) row[j] = M[j];
+    __syncthreads();
+    for (int j = threadIdx.x; j < n2; j += blockDim.x) M[perm[j]] = row[j];
+}
+
 // ------------------------------------------------------------------ apply (A7)
 // One warp per row of the explicit inverse; NVA vectors per pass.
 // Vectors are local to the handle's body range: local row 0 is node row_lo.
@@ -974,9 +988,16 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     }
     k_perm<<<v.count, 32, 0, st>>>(v, s);
     size_t rowbytes = sizeof(double) * (size_t)n2;
-    if (rowbytes > 48 * 1024)
-        BIE_CUDA_TRY(cudaFuncSetAttribute(k_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowbytes));
-    k_unpermute<<<dim3(n2, v.count), 256, rowbytes, st>>>(v, s);
+    if (rowbytes <= 200 * 1024) {
+        if (rowbytes > 48 * 1024)
+            BIE_CUDA_TRY(cudaFuncSetAttribute(k_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rowbytes));
+        k_unpermute<<<dim3(n2, v.count), 256, rowbytes, st>>>(v, s);
+    } else {
+        for (int r0 = 0; r0 < n2; r0 += NB) {
+            k_unpermute_g<<<dim3(NB, v.count), 256, 0, st>>>(v, s, r0);
+            count_launch();
+        }
+    }
     count_launch(2);
     BIE_CUDA_TRY(cudaGetLastError());
     cudaFreeAsync(s.W, st);
@@ -1063,6 +1084,129 @@ __global__ void __launch_bounds__(256) k_struct_gemm(const double *__restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// SLP pore blocks through their rotating-frame circulant structure (NEXT-1 x
+// NEXT-4; P:l.655-657 footnote: the pore blocks can be "accelerated using the
+// FFT").  Pore k's nodes are x_j = c_k + r_k (cos, sin)(theta_j), theta_j =
+// 2 pi j / n (reading C12), and its SLP block B[i][j] = W_ij G(x_i - x_j)
+// (2x2 blocks; W periodic in j - i, C25) satisfies, with T_j = R(theta_j),
+//   T_i^T B[i][j] T_j = b((j - i) mod n)       (G(R v) = R G(v) R^T),
+// so B = D C D^T, D = diag(T_j), C block-circulant with first block row b(m).
+// C^-1 is block-circulant with first block row
+//   d(m) = (1/n) sum_f chat(f)^-1 w^{-fm},  chat(f) = sum_m b(m) w^{fm},  w = e^{2 pi i/n}
+// (one 2x2 complex inverse per frequency).  Factor: one CTA per pore, direct
+// O(n^2) DFTs in FP64 from the node table (the entries are those of
+// k_bd_assemble_slp).  Apply: y_i = T_i sum_m d(m) T_{i+m}^T v_{(i+m) mod n}.
+// Storage 4 n doubles per pore (config 5: 33 MB instead of 17 GB of dense
+// inverses).
+__global__ void __launch_bounds__(256) k_circ_factor(const double2 *__restrict__ pos, const double *__restrict__ w,
+                                                     KRWeights kr, const double2 *__restrict__ tmpl, int n,
+                                                     double *D, int *flag) {
+    extern __shared__ double sh[];
+    double *b = sh;                                          // [n][4]  b(m), row-major 2x2
+    double *ci = sh + 4 * n;                                 // [n][8]  chat(f)^-1 (re, im per entry)
+    double2 *tw = reinterpret_cast<double2 *>(sh + 12 * n);  // [n]     (cos, sin)(2 pi m / n)
+    const int k = blockIdx.x, lo = k * n;
+    for (int m = threadIdx.x; m < n; m += blockDim.x) {
+        const double2 t = tmpl[m];
+        tw[m] = t;
+        double e00 = 0.0, e01 = 0.0, e11 = 0.0;
+        if (m != 0) {
+            const int kk = min(m, n - m);
+            double W = w[lo + m];
+            if (kk <= 6) W *= 1.0 + kr.g[kk - 1];
+            const double2 xi = pos[lo], xj = pos[lo + m];
+            const double rx = xi.x - xj.x, ry = xi.y - xj.y;
+            const double rho2 = rx * rx + ry * ry;
+            const double lg = 0.5 * log(rho2);
+            const double f = W * (1.0 / (4.0 * kPi));
+            e00 = f * (-lg + rx * rx / rho2);
+            e01 = f * (rx * ry / rho2);
+            e11 = f * (-lg + ry * ry / rho2);
+        }
+        // b(m) = B[0][m] T_m  (T_0 = I)
+        b[4 * m + 0] = e00 * t.x + e01 * t.y;
+        b[4 * m + 1] = -e00 * t.y + e01 * t.x;
+        b[4 * m + 2] = e01 * t.x + e11 * t.y;
+        b[4 * m + 3] = -e01 * t.y + e11 * t.x;
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+        double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+        int idx = 0;  // f m mod n
+        for (int m = 0; m < n; ++m) {
+            const double2 c = tw[idx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                re[q] = fma(b[4 * m + q], c.x, re[q]);
+                im[q] = fma(b[4 * m + q], c.y, im[q]);
+            }
+            idx += f;
+            if (idx >= n) idx -= n;
+        }
+        // inverse of [[a, bb], [c, d]] (complex): [[d, -bb], [-c, a]] / (a d - bb c)
+        const double dr = (re[0] * re[3] - im[0] * im[3]) - (re[1] * re[2] - im[1] * im[2]);
+        const double di = (re[0] * im[3] + im[0] * re[3]) - (re[1] * im[2] + im[1] * re[2]);
+        const double den = dr * dr + di * di;
+        if (!(den > 0.0) || !isfinite(den)) atomicExch(flag, 1);
+        const double ir = dr / den, ii = -di / den;  // 1 / det
+        const double er[4] = {re[3], -re[1], -re[2], re[0]}, ei[4] = {im[3], -im[1], -im[2], im[0]};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            ci[8 * f + 2 * q] = er[q] * ir - ei[q] * ii;
+            ci[8 * f + 2 * q + 1] = er[q] * ii + ei[q] * ir;
+        }
+    }
+    __syncthreads();
+    const double inv_n = 1.0 / n;
+    for (int m = threadIdx.x; m < n; m += blockDim.x) {
+        double re[4] = {0.0, 0.0, 0.0, 0.0};
+        int idx = 0;  // f m mod n;  Re(z conj(w^{fm})) = zr c + zi s
+        for (int f = 0; f < n; ++f) {
+            const double2 c = tw[idx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) re[q] = fma(ci[8 * f + 2 * q], c.x, fma(ci[8 * f + 2 * q + 1], c.y, re[q]));
+            idx += m;
+            if (idx >= n) idx -= n;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) D[((long long)k * n + m) * 4 + q] = re[q] * inv_n;
+    }
+}
+
+// y_i = T_i sum_m d_k(m) T_{i+m}^T v_{(i+m) mod n}, one CTA per (vector, pore)
+// column; v and d_k staged in shared memory.
+__global__ void __launch_bounds__(128) k_circ_apply(const double *__restrict__ D, const double2 *__restrict__ tmpl,
+                                                    int n, int M, const double *__restrict__ in, double *out,
+                                                    long long stride) {
+    extern __shared__ double sh[];
+    double2 *vt = reinterpret_cast<double2 *>(sh);  // [n] T_j^T v_j
+    double *d = sh + 2 * n;                         // [n][4]
+    const int col = blockIdx.x, k = col % M;
+    const long long base = (long long)(col / M) * stride + 2LL * n * k;
+    const double *Dk = D + (long long)k * n * 4;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double2 t = tmpl[j];
+        const double vx = in[base + 2 * j], vy = in[base + 2 * j + 1];
+        vt[j] = make_double2(t.x * vx + t.y * vy, -t.y * vx + t.x * vy);
+    }
+    for (int q = threadIdx.x; q < 4 * n; q += blockDim.x) d[q] = Dk[q];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double ax = 0.0, ay = 0.0;
+        int j = i;
+        for (int m = 0; m < n; ++m) {
+            const double2 v = vt[j];
+            ax = fma(d[4 * m], v.x, fma(d[4 * m + 1], v.y, ax));
+            ay = fma(d[4 * m + 2], v.x, fma(d[4 * m + 3], v.y, ay));
+            if (++j == n) j = 0;
+        }
+        const double2 t = tmpl[i];
+        out[base + 2 * i] = t.x * ax - t.y * ay;
+        out[base + 2 * i + 1] = t.y * ax + t.x * ay;
+    }
+}
+
 // Rank-2 Woodbury correction, one warp per column (fixed-order sums).
 __global__ void k_struct_corr(const double *__restrict__ W, const double *__restrict__ Mk, int n2, int M, int ncols,
                               double *out, long long stride) {
@@ -1095,7 +1239,12 @@ int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec,
     int row_lo = bd->row_lo, rows_k = rows_loc, kb0 = bd->b0;
     if (bd->structured) {
         const int M = g->M, n2 = 2 * g->n_pore, ncols = nvec * M;
-        if (M > 0) {
+        if (M > 0 && bd->structured == 2) {  // SLP pores: rotating-frame circulant inverses
+            k_circ_apply<<<ncols, 128, sizeof(double) * 6 * g->n_pore, st>>>(bd->sD, bd->sTmpl, g->n_pore, M, in, out,
+                                                                             stride);
+            count_launch();
+            BIE_CUDA_TRY(cudaGetLastError());
+        } else if (M > 0) {
             const unsigned gx = (unsigned)((ncols + 31) / 32);
             if ((long long)gx * ((n2 + 31) / 32) >= 2LL * g->num_sms)
                 k_struct_gemm<4><<<dim3(gx, (unsigned)((n2 + 31) / 32)), 256, 0, st>>>(bd->sX, n2, M, ncols, in, out,
@@ -1158,6 +1307,8 @@ int bie_blockdiag_destroy(bie_blockdiag_t h) {
     cudaFree(bd->sW);
     cudaFree(bd->sG);
     cudaFree(bd->sM);
+    cudaFree(bd->sD);
+    cudaFree(bd->sTmpl);
     bd->magic = 0;
     delete bd;
     return BIE_OK;
@@ -1340,6 +1491,81 @@ int bie_blockdiag_factor_structured(bie_geometry_t gh, bie_blockdiag_t *out, voi
     return BIE_OK;
 }
 
+int bie_blockdiag_factor_structured_slp(bie_geometry_t gh, bie_blockdiag_t *out, void *stream) {
+    Geometry *g = as_geom(gh);
+    if (!g || !out) {
+        set_error("bie_blockdiag_factor_structured_slp: invalid geometry handle or null output");
+        return BIE_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    *out = nullptr;
+    BlockDiag *bd = new BlockDiag();
+    bd->g = g;
+    bd->b0 = 0;
+    bd->b1 = g->M + 1;
+    bd->nb = g->M + 1;
+    bd->op = 1;
+    bd->structured = 2;
+    for (int b = 0; b <= g->M; ++b) {
+        bd->lo.push_back(b < g->M ? b * g->n_pore : g->wall_lo);
+        bd->n.push_back(b < g->M ? g->n_pore : g->n_outer);
+    }
+    const long long wsz = 4LL * g->n_outer * g->n_outer;
+    bd->off = {0, wsz};  // explicit storage: the wall only
+    bd->row_lo = 0;
+    bd->row_hi = g->N;
+    int *d_flag = nullptr;
+    auto fail = [&](int rc) {
+        cudaFree(d_flag);
+        bie_blockdiag_destroy(reinterpret_cast<bie_blockdiag_t>(bd));
+        return rc;
+    };
+    cudaError_t e = cudaMalloc(&bd->inv, sizeof(double) * (size_t)wsz);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(wall inverse)"));
+    e = cudaMalloc(&bd->d_off, sizeof(long long) * 2);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(offsets)"));
+    e = cudaMemcpy(bd->d_off, bd->off.data(), sizeof(long long) * 2, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemcpy(offsets)"));
+    e = cudaMalloc(&d_flag, sizeof(int) * 2);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(flags)"));
+    e = cudaMemsetAsync(d_flag, 0, sizeof(int) * 2, st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMemsetAsync(flags)"));
+    const int n = g->n_pore;
+    if (g->M > 0) {
+        std::vector<double2> t;
+        pore_template(n, t);
+        e = cudaMalloc(&bd->sD, sizeof(double) * 4 * (size_t)n * g->M);
+        if (e == cudaSuccess) e = cudaMalloc(&bd->sTmpl, sizeof(double2) * (size_t)n);
+        if (e == cudaSuccess) e = cudaMemcpy(bd->sTmpl, t.data(), sizeof(double2) * (size_t)n, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc/cudaMemcpy(circulant pore blocks)"));
+        KRWeights kr;
+        for (int q = 0; q < 6; ++q) kr.g[q] = g->kr[q];
+        k_circ_factor<<<g->M, 256, sizeof(double) * 14 * (size_t)n, st>>>(g->pos, g->w, kr, bd->sTmpl, n, bd->sD,
+                                                                         d_flag);
+        count_launch();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(cuda_fail(e, "k_circ_factor"));
+    }
+    {
+        BDView wv{bd->inv, 0, 2 * g->n_outer, 1, g->M};
+        int rc = factor_class(g, wv, g->wall_lo, g->n_outer, true, st, d_flag + 1, 1);
+        if (rc) return fail(rc);
+    }
+    int flags[2] = {0, 0};
+    e = cudaMemcpyAsync(flags, d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "bie_blockdiag_factor_structured_slp (kernels)"));
+    if (flags[0] || flags[1]) {
+        set_error(std::string("bie_blockdiag_factor_structured_slp: ") +
+                  (flags[0] ? "a pore block has a singular Fourier block" : "the outer-wall block is singular") +
+                  (flags[0] ? "" : " (zero pivot, body " + std::to_string(g->M) + ")"));
+        return fail(BIE_ESINGULAR);
+    }
+    cudaFree(d_flag);
+    *out = reinterpret_cast<bie_blockdiag_t>(bd);
+    return BIE_OK;
+}
+
 int bie_blockdiag_factor_range(bie_geometry_t gh, int body_begin, int body_end, bie_blockdiag_t *out,
                                void *stream) {
     Geometry *g = as_geom(gh);
@@ -1397,8 +1623,33 @@ int bie_blockdiag_block_inverse(bie_blockdiag_t h, int body, double *host, long 
             BIE_CUDA_TRY(cudaMemcpy(host, bd->inv, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost));
             return BIE_OK;
         }
-        // B_k^-1 = X - W M_k Z, Z = U^T X (materialised on the host for inspection)
         const int n2 = 2 * g->n_pore;
+        if (bd->structured == 2) {  // B_k^-1 [i][j] = T_i d_k((j - i) mod n) T_j^T
+            const int n = g->n_pore;
+            if (host_len < (long long)n2 * n2) {
+                set_error("bie_blockdiag_block_inverse: host buffer too small");
+                return BIE_EINVAL;
+            }
+            std::vector<double> d(4 * (size_t)n);
+            std::vector<double2> t;
+            pore_template(n, t);
+            BIE_CUDA_TRY(cudaMemcpy(d.data(), bd->sD + 4LL * n * body, sizeof(double) * d.size(),
+                                    cudaMemcpyDeviceToHost));
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) {
+                    const double *e = d.data() + 4 * (size_t)((j - i + n) % n);
+                    const double ci = t[i].x, si = t[i].y, cj = t[j].x, sj = t[j].y;
+                    // P = e T_j^T, then T_i P
+                    const double p00 = e[0] * cj - e[1] * sj, p01 = e[0] * sj + e[1] * cj;
+                    const double p10 = e[2] * cj - e[3] * sj, p11 = e[2] * sj + e[3] * cj;
+                    host[(size_t)(2 * i) * n2 + 2 * j] = ci * p00 - si * p10;
+                    host[(size_t)(2 * i) * n2 + 2 * j + 1] = ci * p01 - si * p11;
+                    host[(size_t)(2 * i + 1) * n2 + 2 * j] = si * p00 + ci * p10;
+                    host[(size_t)(2 * i + 1) * n2 + 2 * j + 1] = si * p01 + ci * p11;
+                }
+            return BIE_OK;
+        }
+        // B_k^-1 = X - W M_k Z, Z = U^T X (materialised on the host for inspection)
         if (host_len < (long long)n2 * n2) {
             set_error("bie_blockdiag_block_inverse: host buffer too small");
             return BIE_EINVAL;

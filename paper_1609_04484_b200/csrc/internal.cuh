@@ -156,6 +156,10 @@ struct BlockDiag {
     double *sG = nullptr;           // [4]         G = U^T X U
     double *sM = nullptr;           // [M][4]      M_k = c_k (I + c_k G)^-1
     std::vector<double> h_M;        // host copy of M_k
+    // structured == 2: SLP pore blocks as block-circulant matrices in the
+    // rotating frame (bie_blockdiag_factor_structured_slp, blockdiag.cu)
+    double *sD = nullptr;           // [M][n_p][4]  first block row d_k(m) of the rotating-frame inverse
+    double2 *sTmpl = nullptr;       // [n_p]        (cos, sin)(2 pi j / n_p), the pore node angles
 };
 
 Geometry *as_geom(bie_geometry_t g);
