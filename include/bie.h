@@ -37,6 +37,7 @@ extern "C" {
 #define BIE_ESINGULAR (-3)  /* a BD block has a zero pivot (S:l.386: fail loudly) */
 #define BIE_ECUDA (-4)      /* CUDA launch/runtime error */
 #define BIE_ENOMEM (-5)     /* device or host allocation failed */
+#define BIE_ECHECK (-6)     /* checked build: corrupted allocation canary or failed device bounds check */
 
 /* bie_dlp_apply flags */
 #define BIE_FULL 0u    /* -1/2 I + D + self term + N0 + pore completion (reading C5/C6) */
@@ -293,6 +294,20 @@ BIE_API int bie_profile_end(bie_geometry_t g, double *ms_moments, double *ms_pai
  */
 BIE_API int bie_fp64_peak(int iters, double *tflops, double *ms, void *stream);
 BIE_API long long bie_launch_count(void);
+
+/*
+ * bie_debug_check -- verification hook of the checked build
+ * (lib/libbie_checked.so, compiled with -DBIE_CHECKED), the
+ * stand-in for compute-sanitizer memcheck on a pool that does not allow it:
+ * synchronises the device, verifies the 256-byte canaries on both sides of
+ * every live library allocation (and of every allocation freed since the last
+ * call) and reads the device-side bounds-check flags.  *checked_allocs = the
+ * number of live allocations verified (-1 in the normal build, which checks
+ * nothing and returns BIE_OK); *dcheck_line = source line of the first failed
+ * device check (0 if none).  Errors: BIE_ECHECK (message names the
+ * violation), BIE_EINVAL (null output), BIE_ECUDA.
+ */
+BIE_API int bie_debug_check(int *checked_allocs, int *dcheck_line);
 
 /*
  * bie_blockdiag_factor_structured -- NEXT-4: the same BD

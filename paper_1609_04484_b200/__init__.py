@@ -30,6 +30,7 @@ from ._bie import (  # noqa: F401
     gmres_solve_slp,
     kr_weights,
     launch_count,
+    debug_check,
     pore_template,
     fp64_peak,
     profile_begin,

@@ -7,7 +7,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libbie.so")
+# BIE_CHECKED=1 selects the checked build (allocation canaries, NaN-filled fresh
+# memory, device bounds checks) -- a test configuration
+_LIB_PATH = os.path.join(_HERE, "lib", "libbie_checked.so" if os.environ.get("BIE_CHECKED") == "1" else "libbie.so")
 
 BIE_OK = 0
 BIE_EINVAL = -1
@@ -15,12 +17,13 @@ BIE_EGEOM = -2
 BIE_ESINGULAR = -3
 BIE_ECUDA = -4
 BIE_ENOMEM = -5
+BIE_ECHECK = -6
 BIE_FULL = 0
 BIE_D_ONLY = 1
 BIE_MAX_NVEC = 16
 
 _CODES = {BIE_EINVAL: "BIE_EINVAL", BIE_EGEOM: "BIE_EGEOM", BIE_ESINGULAR: "BIE_ESINGULAR",
-          BIE_ECUDA: "BIE_ECUDA", BIE_ENOMEM: "BIE_ENOMEM"}
+          BIE_ECUDA: "BIE_ECUDA", BIE_ENOMEM: "BIE_ENOMEM", BIE_ECHECK: "BIE_ECHECK"}
 
 EXPORTED_SYMBOLS = (
     "bie_geometry_create", "bie_geometry_destroy", "bie_geometry_info", "bie_geometry_nodes",
@@ -35,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "bie_blockdiag_factor_structured_slp",
     "bie_slp_pairs_partial", "bie_slp_epilogue_rows", "bie_blockdiag_factor_range_slp",
     "bie_geometry_node_table", "bie_pore_template", "bie_gmres_solve_host", "bie_fp64_peak",
+    "bie_debug_check",
 )
 
 
@@ -78,6 +82,7 @@ def lib():
         "bie_gmres_solve": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_gmres_solve_host": [vp, vp, vp, vp, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_fp64_peak": [c_int, dp, dp, vp],
+        "bie_debug_check": [ip, ip],
         "bie_field_eval": [vp, vp, vp, c_int, vp, vp],
         "bie_gmres_solve_batch": [vp, vp, vp, vp, c_int, c_double, c_int, dp, ip, dp, dp, ip, vp],
         "bie_blockdiag_factor_range": [vp, c_int, c_int, ctypes.POINTER(vp), vp],
@@ -211,6 +216,15 @@ def pore_template(n: int) -> np.ndarray:
     out = np.zeros(2 * n)
     _check(lib().bie_pore_template(int(n), _dp(out)))
     return out.reshape(n, 2)
+
+
+def debug_check() -> int:
+    """bie_debug_check: verify allocation canaries and device bounds checks
+    (checked build); returns the number of allocations verified, -1 in the
+    normal build.  Raises BieError(BIE_ECHECK) on a violation."""
+    n, line = ctypes.c_int(), ctypes.c_int()
+    _check(lib().bie_debug_check(ctypes.byref(n), ctypes.byref(line)))
+    return n.value
 
 
 def launch_count() -> int:

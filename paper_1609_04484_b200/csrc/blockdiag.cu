@@ -11,8 +11,8 @@
 //                   matrix) -> pivots; A11^{-1} from L11 U11.
 //   2. k_swap     : apply the panel's row swaps to the whole matrix.
 //   3. k_copy_T   : T = M[:, K];   k_make_G : G = A11^{-1} M[K, :], G[:, K] = A11^{-1}
-//   4. k_update   : M[i, :] = (i in K) ? G[i-k0, :] : base(i, :) - T[i, :] G
-//                   (base = M off K, 0 on K)  -- the rank-NB sweep, DFMA tiles.
+//   4. k_update3  : M[i, :] = (i in K) ? G[i-k0, :] : base(i, :) - T[i, :] G
+//                   (base = M off K, 0 on K)  -- the rank-NB sweep on the FP64 tensor cores (DMMA).
 // After the last panel, columns are unpermuted (A^{-1} = M P).  Batched over
 // all blocks of one size class (pores share one size; Gamma_0 is its own class).
 // Apply: one warp per row of the explicit inverses (HBM-bound batched GEMV).
@@ -570,68 +570,6 @@ __global__ void k_make_G(BDView v, BDScratch s, int k0, int nbe) {
     }
 }
 
-// The sweep: 64x64 output tile per CTA, 256 threads, 4x4 outputs per thread.
-constexpr int UT = 64;
-__global__ void __launch_bounds__(256) k_update(BDView v, BDScratch s, int k0, int nbe) {
-    const int m = blockIdx.z;
-    const int n2 = v.n2;
-    const int i0 = blockIdx.y * UT, j0 = blockIdx.x * UT;
-    __shared__ double Ts[UT][NB + 1];
-    __shared__ double Gs[NB][UT + 1];
-    const double *T = s.T + (long long)m * n2 * NB;
-    const double *G = s.G + (long long)m * NB * n2;
-    double *M = v.mat + (long long)m * v.mstride;
-    const int tid = threadIdx.x;
-    for (int q = tid; q < UT * NB; q += 256) {
-        int r = q / NB, c = q % NB;
-        int gi = i0 + r;
-        Ts[r][c] = gi < n2 ? T[(long long)gi * NB + c] : 0.0;
-    }
-    for (int q = tid; q < NB * UT; q += 256) {
-        int c = q / UT, jj = q % UT;
-        int gj = j0 + jj;
-        Gs[c][jj] = gj < n2 ? G[(long long)c * n2 + gj] : 0.0;
-    }
-    __syncthreads();
-    const int tr = tid / 16, tc = tid % 16;  // rows tr + 16*a, cols tc + 16*b
-    double acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-#pragma unroll 8
-    for (int c = 0; c < NB; ++c) {
-        double ta[4], gb[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) ta[a] = Ts[tr + 16 * a][c];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) gb[b] = Gs[c][tc + 16 * b];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fma(ta[a], gb[b], acc[a][b]);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int gi = i0 + tr + 16 * a;
-        if (gi >= n2) continue;
-        const bool rowK = gi >= k0 && gi < k0 + nbe;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int gj = j0 + tc + 16 * b;
-            if (gj >= n2) continue;
-            double *dst = M + (long long)gi * n2 + gj;
-            if (rowK) {
-                *dst = Gs[gi - k0][tc + 16 * b];
-            } else {
-                const bool colK = gj >= k0 && gj < k0 + nbe;
-                const double base = colK ? 0.0 : *dst;
-                *dst = base - acc[a][b];
-            }
-        }
-    }
-}
-
 // The sweep, v2: 128x128 output tile per CTA, 256 threads, 8x8 outputs per
 // thread (rows tr + 16a, columns 2tc + 32b + {0,1}); T staged transposed and G
 // row-wise in shared memory (12 shared loads per 64 DFMA per panel column).
@@ -875,6 +813,8 @@ __global__ void __launch_bounds__(256) k_bd_apply(const double *__restrict__ inv
     }
     const int n2 = 2 * n;
     const int lr = 2 * (node - lo) + (warp & 1);
+    // the row lies inside body b's inverse: [off[b - b0], off[b - b0 + 1])
+    BIE_DCHECK(b >= b0 && off[b - b0] + (long long)(lr + 1) * n2 <= off[b - b0 + 1]);
     const double2 *row = reinterpret_cast<const double2 *>(inv + off[b - b0] + (long long)lr * n2);
     const int lo_loc = lo - row_lo;
     double acc[NVA];
@@ -948,9 +888,9 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         BIE_CUDA_TRY(cudaMallocAsync(&cs.A, sizeof(double) * NB * NB, st));
     }
     const size_t upd_smem = sizeof(double) * 2 * NB * UT2P;
-    // sweep kernel: 0 = DMMA tensor-core tiles (default), 1 = 64x64 DFMA, 2 = 128x128 DFMA (tuning knob)
+    // sweep kernel: 0 = DMMA tensor-core tiles (default), 1 = 128x128 DFMA tiles (A/B knob)
     int upd_variant = 0;
-    if (const char *e = getenv("BIE_BD_UPDATE")) upd_variant = std::max(0, std::min(2, atoi(e)));
+    if (const char *e = getenv("BIE_BD_UPDATE")) upd_variant = std::max(0, std::min(1, atoi(e)));
     BIE_CUDA_TRY(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
     BIE_CUDA_TRY(cudaFuncSetAttribute(k_panel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(double) * NB * kSmemPanelRows)));
@@ -969,11 +909,9 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         k_swap<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
         k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), v.count), 256, 0, st>>>(v, s, k0, nbe);
         k_make_G<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
-        if (upd_variant == 2)
+        if (upd_variant == 1)
             k_update2<<<dim3((n2 + UT2 - 1) / UT2, (n2 + UT2 - 1) / UT2, v.count), 256, upd_smem, st>>>(v, s, k0,
                                                                                                        nbe);
-        else if (upd_variant == 1)
-            k_update<<<dim3((n2 + UT - 1) / UT, (n2 + UT - 1) / UT, v.count), 256, 0, st>>>(v, s, k0, nbe);
         else
             k_update3<<<dim3((n2 + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3, v.count), 128, 0, st>>>(v, s, k0, nbe);
         count_launch(5);
@@ -1678,3 +1616,5 @@ int bie_blockdiag_block_inverse(bie_blockdiag_t h, int body, double *host, long 
 }
 
 }  // extern "C"
+
+BIE_DCHECK_TU(blockdiag)

@@ -141,6 +141,7 @@ struct PairArgs {
     long long U;
     long long Useg, nseg;          // dynamic segments (see seg_of)
     unsigned long long *counter;   // zeroed before the launch
+    long long partial_len = 0;     // doubles in partial (checked build: BIE_DCHECK on stores)
 };
 
 // A3: all-pairs DLP sum.  Each persistent CTA walks a contiguous range of
@@ -282,8 +283,9 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
                 if (it < a.Nt) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
-                        double2 *dst = reinterpret_cast<double2 *>(
-                            a.partial + ((long long)slot * a.nvec_total + a.v0 + v) * 2LL * a.Nt);
+                        const long long o = ((long long)slot * a.nvec_total + a.v0 + v) * 2LL * a.Nt;
+                        BIE_DCHECK(slot >= 0 && o + 2LL * it + 1 < a.partial_len);
+                        double2 *dst = reinterpret_cast<double2 *>(a.partial + o);
                         dst[it] = acc[r][v];
                     }
                 }
@@ -585,6 +587,7 @@ __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
         }
         A = lo;
     }
+    BIE_DCHECK(A >= 0 && A < a.nTB);
     offA = a.off[A];
     offA1 = a.off[A + 1];
     load_targets(A);
@@ -1127,49 +1130,23 @@ int build_schedules(Geometry *g) {
     return BIE_OK;
 }
 
-// Variants of the symmetric kernel (tuning knob BIE_SYM_VARIANT), (SR, SW, NS, MINB):
-// 0 = (8, 2, 2, 1) -- 2 warps/SMSP at 254 registers (default, fastest measured);
-// 1 = (4, 4, 4, 3) -- 3 warps/SMSP at <= 168 registers, 16 pairs per step;
-// 2 = (4, 4, 2, 3) -- 3 warps/SMSP, 8 pairs per step;
-// 3 = (8, 2, 2, 1) with the step loop unrolled by two;
-// 4, 5 = (8, 2, 2, 1) with lockstep pair groups of 2 / 4 targets (GR);
-// 6 = (4, 4, 2, 4) -- 4 warps/SMSP at <= 128 registers;
-// 7 = (4, 4, 4, 1) -- 2 warps/SMSP, 16 pairs per step, registers for the pairs;
-// 8 = (8, 2, 2, 1) lockstep groups of 4 targets with the step loop unrolled by two;
-// 9 = (8, 2, 2, 1) lockstep groups of all 8 targets.
-static const int kNumSymVar = 10;
+// Symmetric DLP kernel variants (BIE_SYM_VARIANT, A/B only): 0 = (8 targets
+// per lane, 2 warps, 2 sources per step, lockstep groups of 4, step loop
+// unrolled by 2) -- the default, fastest measured (12.73 ms at config 4);
+// 1 = (4, 4, 2) capped at 3 CTAs of 4 warps per SM (3 warps per SMSP).
+// Round 1-2 sweeps of the other shapes: DESIGN.md s5.
+static const int kNumSymVar = 2;
 static void *sym_kernel(int v) {
-    switch (v) {
-        case 1: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, 3>);
-        case 2: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3>);
-        case 3: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2>);
-        case 4: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 2>);
-        case 5: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 4>);
-        case 6: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 4>);
-        case 7: return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 4, 1>);
-        case 8: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2, 4>);
-        case 9: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 1, 8>);
-        default: return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1>);
-    }
+    if (v == 1) return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3>);
+    return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2, 4>);
 }
-static int sym_warps(int v) { return (v == 0 || v == 3 || v == 4 || v == 5 || v == 8 || v == 9) ? 2 : 4; }
+static int sym_warps(int v) { return v == 1 ? 4 : 2; }
 static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
-    switch (v) {
-        case 1: k_dlp_sym<4, 4, 4, 3><<<P, 128, 0, st>>>(sa); break;
-        case 2: k_dlp_sym<4, 4, 2, 3><<<P, 128, 0, st>>>(sa); break;
-        case 3: k_dlp_sym<8, 2, 2, 1, 0, 2><<<P, 64, 0, st>>>(sa); break;
-        case 4: k_dlp_sym<8, 2, 2, 1, 0, 1, 2><<<P, 64, 0, st>>>(sa); break;
-        case 5: k_dlp_sym<8, 2, 2, 1, 0, 1, 4><<<P, 64, 0, st>>>(sa); break;
-        case 6: k_dlp_sym<4, 4, 2, 4><<<P, 128, 0, st>>>(sa); break;
-        case 7: k_dlp_sym<4, 4, 4, 1><<<P, 128, 0, st>>>(sa); break;
-        case 8: k_dlp_sym<8, 2, 2, 1, 0, 2, 4><<<P, 64, 0, st>>>(sa); break;
-        case 9: k_dlp_sym<8, 2, 2, 1, 0, 1, 8><<<P, 64, 0, st>>>(sa); break;
-        default: k_dlp_sym<8, 2, 2, 1><<<P, 64, 0, st>>>(sa); break;
-    }
+    if (v == 1)
+        k_dlp_sym<4, 4, 2, 3><<<P, 128, 0, st>>>(sa);
+    else
+        k_dlp_sym<8, 2, 2, 1, 0, 2, 4><<<P, 64, 0, st>>>(sa);
 }
-
-// Single-layer symmetric kernel variants (tuning knob BIE_SLP_SYM_VARIANT):
-// 0 = (8, 2, 2) (default), 1 = (4, 4, 2) at 3 CTAs/SM.
 static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
         case 1: k_dlp_sym<4, 4, 2, 3, 1><<<P, 128, 0, st>>>(sa); break;
@@ -1424,6 +1401,8 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     if (nch > 0) BIE_CUDA_TRY(cudaMemsetAsync(g->pair_counter, 0, sizeof(unsigned long long) * nch, st));
     for (int c = 0; c < nch; ++c) {
         PairArgs a;
+
+        a.partial_len = (long long)g->partial_elems;
         a.tpos = g->pos + row_begin;
         a.pos = g->pos;
         a.nw = g->nw;
@@ -1669,6 +1648,8 @@ int field_eval_impl(Geometry *g, const double *sigma, const double2 *targets, in
         g->partial_elems = need;
     }
     PairArgs a;
+
+    a.partial_len = (long long)g->partial_elems;
     a.tpos = targets;
     a.pos = g->pos;
     a.nw = g->nw;
@@ -1723,6 +1704,8 @@ int slp_field_eval_impl(Geometry *g, const double *sigma, const double2 *targets
         g->partial_elems = need;
     }
     PairArgs a;
+
+    a.partial_len = (long long)g->partial_elems;
     a.tpos = targets;
     a.pos = g->pos;
     a.nw = g->nw;
@@ -1926,3 +1909,5 @@ int bie_dlp_apply_host(bie_geometry_t gh, const double *sigma_host, double *out_
 }
 
 }  // extern "C"
+
+BIE_DCHECK_TU(dlp)

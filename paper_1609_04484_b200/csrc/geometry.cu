@@ -550,3 +550,5 @@ int bie_kr_weights(double *gamma) {
 }
 
 }  // extern "C"
+
+BIE_DCHECK_TU(geometry)

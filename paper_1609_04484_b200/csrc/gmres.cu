@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restri
         for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
         double acc = (acc0 + acc1) + (acc2 + acc3);
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        BIE_DCHECK(j < ldp || gridDim.x == 1);
         if (lane == 0) partial[(long long)blockIdx.x * ldp + j] = sq ? sqrt(acc) : acc;
     }
 }
@@ -1028,3 +1029,5 @@ extern "C" int bie_gmres_solve_batch_slp(bie_geometry_t gh, bie_blockdiag_t bdh,
     return gmres_batch_impl("bie_gmres_solve_batch_slp", kOpSLP, gh, bdh, F, X, nrhs, tol, max_iter, hist_host,
                             iters, res_pc, res_true, converged, stream);
 }
+
+BIE_DCHECK_TU(gmres)

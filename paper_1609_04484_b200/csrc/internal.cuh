@@ -8,6 +8,57 @@
 
 #include "../../include/bie.h"
 
+// ---------------------------------------------------------------------------
+// Checked build (-DBIE_CHECKED, lib/libbie_checked.so): the
+// stand-in for compute-sanitizer, which this GPU pool does not allow.  Every
+// device allocation of the library gets 256-byte canary regions on both sides
+// and is filled with 0xFF bytes (a NaN in every double, so a read of memory
+// no kernel wrote propagates into the parity checks); bie_debug_check()
+// verifies all live canaries, and freeing checks the block's own.  Kernels
+// carry BIE_DCHECK(index bounds) on their global stores; a failed check
+// records its source line in a device flag that bie_debug_check() reports.
+// ---------------------------------------------------------------------------
+namespace bie {
+cudaError_t chk_malloc(void **p, size_t bytes, cudaStream_t st, bool async);
+cudaError_t chk_free(void *p, cudaStream_t st, bool async);
+}  // namespace bie
+#ifdef BIE_CHECKED
+template <class T>
+static inline cudaError_t bie_chk_cudaMalloc(T **p, size_t b) {
+    return ::bie::chk_malloc(reinterpret_cast<void **>(p), b, nullptr, false);
+}
+template <class T>
+static inline cudaError_t bie_chk_cudaMallocAsync(T **p, size_t b, cudaStream_t st) {
+    return ::bie::chk_malloc(reinterpret_cast<void **>(p), b, st, true);
+}
+#define cudaMalloc(p, b) bie_chk_cudaMalloc((p), (b))
+#define cudaMallocAsync(p, b, st) bie_chk_cudaMallocAsync((p), (b), (st))
+#define cudaFree(p) ::bie::chk_free((void *)(p), nullptr, false)
+#define cudaFreeAsync(p, st) ::bie::chk_free((void *)(p), (st), true)
+// per translation unit: first failing line of a device-side check
+static __device__ int bie_dcheck_line = 0;
+#define BIE_DCHECK(cond)                                          \
+    do {                                                          \
+        if (!(cond)) atomicCAS(&bie_dcheck_line, 0, __LINE__);   \
+    } while (0)
+#define BIE_DCHECK_TU(name)                                                            \
+    namespace bie {                                                                    \
+    int dcheck_##name() {                                                              \
+        int h = 0;                                                                     \
+        cudaMemcpyFromSymbol(&h, bie_dcheck_line, sizeof(int));                        \
+        return h;                                                                      \
+    }                                                                                  \
+    }
+#else
+#define BIE_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#define BIE_DCHECK_TU(name)                  \
+    namespace bie {                          \
+    int dcheck_##name() { return 0; }        \
+    }
+#endif
+
 namespace bie {
 
 constexpr double kPi = 3.14159265358979323846;
@@ -115,7 +166,7 @@ struct Geometry {
     unsigned long long *sym_acc = nullptr;  // [3][2N] fixed-point limbs of the pair sums (dlp.cu fx_add)
     int sym_occ[2] = {1, 1};      // resident CTAs per SM of the DLP / SLP symmetric kernel
     double *sym_diag = nullptr;   // [2N]
-    int sym_nTB = 0, sym_P = 0, sym_variant = 8;  // (8, 2, 2), lockstep groups of 4, unrolled by 2: fastest measured
+    int sym_nTB = 0, sym_P = 0, sym_variant = 0;  // (8, 2, 2), lockstep groups of 4, unrolled by 2: fastest measured
     int slp_sym_variant = 0;  // (8, 2, 2): fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
     unsigned long long *sym_counter = nullptr;  // [0] dynamic segment counter, [1] max |Q| bits (accumulation window)

@@ -20,3 +20,16 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_verify(request):
+    """Under BIE_CHECKED=1 (the checked library) every GPU test
+    ends with bie_debug_check: allocation canaries intact, no failed device
+    bounds check.  A no-op otherwise."""
+    yield
+    if os.environ.get("BIE_CHECKED") == "1" and request.node.get_closest_marker("gpu"):
+        import paper_1609_04484_b200 as bie
+
+        n = bie.debug_check()
+        assert n >= 0, "BIE_CHECKED=1 but the normal library was loaded"

@@ -106,12 +106,15 @@ def test_structured_bd_gmres_golden(bie, name):
 def test_structured_bd_errors(bie):
     p = make_problem(1)
     g = bie.Geometry.from_problem(p)
-    with pytest.raises(ValueError):
-        bie.BlockDiag(g, structured=True, op="slp")
+    with pytest.raises(ValueError):  # structured BDs cover the whole geometry
+        bie.BlockDiag(g, structured=True, bodies=(0, 1))
     bd = bie.BlockDiag(g, structured=True)
+    sbd = bie.BlockDiag(g, structured=True, op="slp")
     import torch
 
     f = _t(density(p, nvec=1)[0])
     x = torch.zeros_like(f)
     with pytest.raises(bie.BieError):  # a DLP-operator handle refused by the SLP solver
         bie.gmres_solve_slp(g, bd, f, x, 1e-8, 10)
+    with pytest.raises(bie.BieError):  # and an SLP-operator handle by the DLP solver
+        bie.gmres_solve(g, sbd, f, x, 1e-8, 10)
