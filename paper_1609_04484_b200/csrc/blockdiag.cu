@@ -978,8 +978,8 @@ __global__ void k_struct_WG(const double *__restrict__ X, int n2, double *W, dou
 // pore col % M, at base + (col / M) * stride + n2 * (col % M).  Tiles of 32
 // columns x 8 RT rows (RT rows per thread); every output is one sequential FMA
 // chain over k = 0 .. n2-1, so the tile shape does not change the result.
-// RT = 4 for large M; RT = 1 when the 32-row grid would leave most SMs idle
-// (config 2: 8 -> 32 CTAs).
+// RT = 4 when the 32-row grid fills the SMs (config 4: 30 us per apply; RT = 1
+// there measured 63 us); RT = 1 otherwise (config 2: 8 -> 32 CTAs).
 template <int RT>
 __global__ void __launch_bounds__(256) k_struct_gemm(const double *__restrict__ X, int n2, int M, int ncols,
                                                      const double *__restrict__ in, double *out, long long stride) {
@@ -1184,7 +1184,7 @@ int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec,
             BIE_CUDA_TRY(cudaGetLastError());
         } else if (M > 0) {
             const unsigned gx = (unsigned)((ncols + 31) / 32);
-            if ((long long)gx * ((n2 + 31) / 32) >= 2LL * g->num_sms)
+            if ((long long)gx * ((n2 + 31) / 32) >= g->num_sms)  // config 4: 256 CTAs of 32 rows
                 k_struct_gemm<4><<<dim3(gx, (unsigned)((n2 + 31) / 32)), 256, 0, st>>>(bd->sX, n2, M, ncols, in, out,
                                                                                     stride);
             else
