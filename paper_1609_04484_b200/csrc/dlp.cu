@@ -237,11 +237,22 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
                     const double ry = ty[r] - xj.y;
                     double hl, inv;
                     slp_factors(rx, ry, hl, inv, s_log);
+                    if constexpr (NV >= 2) {
+                        // r / rho^2 once per pair: 6 FP64 instructions per vector instead of 7
+                        const double ix = inv * rx, iy = inv * ry;
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        const double c = inv * fma(rx, sj[v].x, ry * sj[v].y);
-                        acc[r][v].x = fma(c, rx, fma(hl, sj[v].x, acc[r][v].x));
-                        acc[r][v].y = fma(c, ry, fma(hl, sj[v].y, acc[r][v].y));
+                        for (int v = 0; v < NV; ++v) {
+                            const double rs = fma(rx, sj[v].x, ry * sj[v].y);
+                            acc[r][v].x = fma(rs, ix, fma(hl, sj[v].x, acc[r][v].x));
+                            acc[r][v].y = fma(rs, iy, fma(hl, sj[v].y, acc[r][v].y));
+                        }
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            const double c = inv * fma(rx, sj[v].x, ry * sj[v].y);
+                            acc[r][v].x = fma(c, rx, fma(hl, sj[v].x, acc[r][v].x));
+                            acc[r][v].y = fma(c, ry, fma(hl, sj[v].y, acc[r][v].y));
+                        }
                     }
                     continue;
                 }
@@ -253,14 +264,16 @@ __global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
                 const double e = fma(-rho2, inv, 1.0);
                 inv = fma(inv, fma(e, e, e), inv);
                 const double q = (rn * inv) * inv;  // (r.nw)/rho^4
-                if constexpr (NV >= 8) {
-                    // tensor form: P = q r r^T once per pair (5 ops), 4 DFMA per vector
-                    const double qx = q * rx;
-                    const double pxx = qx * rx, pxy = qx * ry, pyy = (q * ry) * ry;
+                if constexpr (NV >= 2) {
+                    // g = q r once per pair (2 DMUL), then (r.sigma) g: 4 FP64
+                    // instructions per vector (11 + 2 + 4 nvec per pair; the round-1
+                    // forms took 11 + 5 nvec, or 16 + 4 nvec with P = q r r^T)
+                    const double gx = q * rx, gy = q * ry;
 #pragma unroll
                     for (int v = 0; v < NV; ++v) {
-                        acc[r][v].x = fma(pxx, sj[v].x, fma(pxy, sj[v].y, acc[r][v].x));
-                        acc[r][v].y = fma(pxy, sj[v].x, fma(pyy, sj[v].y, acc[r][v].y));
+                        const double rs = fma(rx, sj[v].x, ry * sj[v].y);
+                        acc[r][v].x = fma(rs, gx, acc[r][v].x);
+                        acc[r][v].y = fma(rs, gy, acc[r][v].y);
                     }
                 } else {
 #pragma unroll
