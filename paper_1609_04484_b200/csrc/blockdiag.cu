@@ -796,6 +796,7 @@ template <int NVA>
 __global__ void __launch_bounds__(256) k_bd_apply(const double *__restrict__ inv, const long long *__restrict__ off,
                                                   int wall_lo, int n_pore, int N, int b0, int row_lo, int rows_loc,
                                                   const double *in, double *out, long long stride, int v0) {
+    pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= 2 * rows_loc) return;
@@ -983,6 +984,7 @@ __global__ void k_struct_WG(const double *__restrict__ X, int n2, double *W, dou
 template <int RT>
 __global__ void __launch_bounds__(256) k_struct_gemm(const double *__restrict__ X, int n2, int M, int ncols,
                                                      const double *__restrict__ in, double *out, long long stride) {
+    pdl_wait();
     constexpr int TR = 8 * RT;  // tile rows
     __shared__ double Xs[TR][33];
     __shared__ double Vs[32][33];
@@ -1117,6 +1119,7 @@ __global__ void __launch_bounds__(256) k_circ_factor(const double2 *__restrict__
 __global__ void __launch_bounds__(128) k_circ_apply(const double *__restrict__ D, const double2 *__restrict__ tmpl,
                                                     int n, int M, const double *__restrict__ in, double *out,
                                                     long long stride) {
+    pdl_wait();
     extern __shared__ double sh[];
     double2 *vt = reinterpret_cast<double2 *>(sh);  // [n] T_j^T v_j
     double *d = sh + 2 * n;                         // [n][4]
@@ -1148,6 +1151,7 @@ __global__ void __launch_bounds__(128) k_circ_apply(const double *__restrict__ D
 // Rank-2 Woodbury correction, one warp per column (fixed-order sums).
 __global__ void k_struct_corr(const double *__restrict__ W, const double *__restrict__ Mk, int n2, int M, int ncols,
                               double *out, long long stride) {
+    pdl_wait();
     const int col = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (col >= ncols) return;
@@ -1178,19 +1182,20 @@ int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec,
     if (bd->structured) {
         const int M = g->M, n2 = 2 * g->n_pore, ncols = nvec * M;
         if (M > 0 && bd->structured == 2) {  // SLP pores: rotating-frame circulant inverses
-            k_circ_apply<<<ncols, 128, sizeof(double) * 6 * g->n_pore, st>>>(bd->sD, bd->sTmpl, g->n_pore, M, in, out,
-                                                                             stride);
+            BIE_LAUNCH(k_circ_apply, ncols, 128, sizeof(double) * 6 * g->n_pore, st, bd->sD, bd->sTmpl, g->n_pore, M,
+                       in, out, stride);
             count_launch();
             BIE_CUDA_TRY(cudaGetLastError());
         } else if (M > 0) {
             const unsigned gx = (unsigned)((ncols + 31) / 32);
             if ((long long)gx * ((n2 + 31) / 32) >= g->num_sms)  // config 4: 256 CTAs of 32 rows
-                k_struct_gemm<4><<<dim3(gx, (unsigned)((n2 + 31) / 32)), 256, 0, st>>>(bd->sX, n2, M, ncols, in, out,
-                                                                                    stride);
+                BIE_LAUNCH(k_struct_gemm<4>, dim3(gx, (unsigned)((n2 + 31) / 32)), 256, 0, st, bd->sX, n2, M, ncols,
+                           in, out, stride);
             else
-                k_struct_gemm<1><<<dim3(gx, (unsigned)((n2 + 7) / 8)), 256, 0, st>>>(bd->sX, n2, M, ncols, in, out,
-                                                                                  stride);
-            k_struct_corr<<<(ncols * 32 + 255) / 256, 256, 0, st>>>(bd->sW, bd->sM, n2, M, ncols, out, stride);
+                BIE_LAUNCH(k_struct_gemm<1>, dim3(gx, (unsigned)((n2 + 7) / 8)), 256, 0, st, bd->sX, n2, M, ncols,
+                           in, out, stride);
+            BIE_LAUNCH(k_struct_corr, (ncols * 32 + 255) / 256, 256, 0, st, bd->sW, bd->sM, n2, M, ncols, out,
+                       stride);
             count_launch(2);
             BIE_CUDA_TRY(cudaGetLastError());
         }
@@ -1207,18 +1212,18 @@ int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec,
     while (v < nvec) {
         int rem = nvec - v;
         if (rem >= 4) {
-            k_bd_apply<4><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, kb0,
-                                                      row_lo, rows_k, in, out, stride, v);
+            BIE_LAUNCH(k_bd_apply<4>, blocks, threads, 0, st, bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N,
+                       kb0, row_lo, rows_k, in, out, stride, v);
             v += 4;
             count_launch();
         } else if (rem >= 2) {
-            k_bd_apply<2><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, kb0,
-                                                      row_lo, rows_k, in, out, stride, v);
+            BIE_LAUNCH(k_bd_apply<2>, blocks, threads, 0, st, bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N,
+                       kb0, row_lo, rows_k, in, out, stride, v);
             v += 2;
             count_launch();
         } else {
-            k_bd_apply<1><<<blocks, threads, 0, st>>>(bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N, kb0,
-                                                      row_lo, rows_k, in, out, stride, v);
+            BIE_LAUNCH(k_bd_apply<1>, blocks, threads, 0, st, bd->inv, bd->d_off, g->wall_lo, g->n_pore, g->N,
+                       kb0, row_lo, rows_k, in, out, stride, v);
             v += 1;
             count_launch();
         }

@@ -318,6 +318,7 @@ __global__ void k_moments(const double2 *__restrict__ pos, const double2 *__rest
                           const double *__restrict__ w, const double4 *__restrict__ pore, const double *sigma,
                           long long sig_stride, int nvec, int M, int n_pore, int wall_lo, int N, double wall_len,
                           double *moments /* [nvec][M][3], then [nvec] nu */) {
+    pdl_wait();
     __shared__ double red[3][256];
     const int b = blockIdx.x, tid = threadIdx.x;
     for (int v = 0; v < nvec; ++v) {
@@ -432,10 +433,21 @@ __device__ __forceinline__ void qmax_update(double m, unsigned long long *qmax_b
     if ((threadIdx.x & 31) == 0) atomicMax(qmax_bits, (unsigned long long)__double_as_longlong(m));
 }
 
+// node j's three limb pairs of the symmetric kernel's accumulators (zeroed
+// here, in the O(N) kernel that precedes every symmetric launch, instead of a
+// separate memset per apply)
+__device__ __forceinline__ void zero_limbs(unsigned long long *acc, int j, int N) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+        reinterpret_cast<ulonglong2 *>(acc + 2LL * N * q)[j] = make_ulonglong2(0ull, 0ull);
+}
+
 __global__ void k_quad(const double2 *__restrict__ nw, const double *__restrict__ sigma, double4 *Q, int N,
-                       unsigned long long *qmax_bits) {
+                       unsigned long long *qmax_bits, unsigned long long *acc) {
+    pdl_wait();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     double m = 0.0;
+    if (j < N) zero_limbs(acc, j, N);
     if (j < N) {
         const double2 a = nw[j];
         const double2 b = reinterpret_cast<const double2 *>(sigma)[j];
@@ -533,6 +545,7 @@ __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync
 // changes the order ptxas's list scheduler starts from.
 template <int SR, int SW, int NS, int MINB = 1, int OP = 0, int UNR = (OP == 1 ? 2 : 1), int GR = 0>
 __global__ void __launch_bounds__(32 * SW, MINB) k_dlp_sym(SymArgs a) {
+    pdl_wait();
     static_assert(SR * SW * 32 == kSymTB, "block size fixed at 512");
     static_assert(NS == 2 || NS == 4, "2 or 4 sources per step");
     constexpr int STEPS = 32 / NS;
@@ -748,6 +761,7 @@ template <int OP = 0>
 __global__ void __launch_bounds__(128) k_dlp_diag(const double2 *__restrict__ pos, const double2 *__restrict__ nw,
                                                   const double *__restrict__ sigma, double *diag, int N,
                                                   int blk0 = 0, int split = 1) {
+    pdl_wait();
     __shared__ double2 sp[3][kSymTB];
     __shared__ LogTab s_log;  // OP = 1 only; visible after the staging barrier
     if constexpr (OP == 1) log_tab_init(s_log, threadIdx.x, 128);
@@ -925,6 +939,7 @@ struct EpiArgs {
 // registers); NVC == 0: generic nvec.
 template <int NVC>
 __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
+    pdl_wait();
     const int it_raw = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = it_raw < a.Nt;  // inactive threads still join the block barriers
     const int it = active ? it_raw : a.Nt - 1;
@@ -1156,14 +1171,14 @@ static void *sym_kernel(int v) {
 static int sym_warps(int v) { return v == 1 ? 4 : 2; }
 static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
     if (v == 1)
-        k_dlp_sym<4, 4, 2, 3><<<P, 128, 0, st>>>(sa);
+        BIE_LAUNCH((k_dlp_sym<4, 4, 2, 3>), P, 128, 0, st, sa);
     else
-        k_dlp_sym<8, 2, 2, 1, 0, 2, 4><<<P, 64, 0, st>>>(sa);
+        BIE_LAUNCH((k_dlp_sym<8, 2, 2, 1, 0, 2, 4>), P, 64, 0, st, sa);
 }
 static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
     switch (v) {
-        case 1: k_dlp_sym<4, 4, 2, 3, 1><<<P, 128, 0, st>>>(sa); break;
-        default: k_dlp_sym<8, 2, 2, 1, 1><<<P, 64, 0, st>>>(sa); break;
+        case 1: BIE_LAUNCH((k_dlp_sym<4, 4, 2, 3, 1>), P, 128, 0, st, sa); break;
+        default: BIE_LAUNCH((k_dlp_sym<8, 2, 2, 1, 1>), P, 64, 0, st, sa); break;
     }
 }
 
@@ -1253,10 +1268,9 @@ static int sym_pre(Geometry *g, cudaStream_t st) {
     return BIE_OK;
 }
 
-// Launch the symmetric kernel on the slice [ub, ub + U) (zeroes the limb
-// accumulators first; the segment counter and max |Q| were zeroed by sym_pre).
+// Launch the symmetric kernel on the slice [ub, ub + U).  The limb accumulators
+// were zeroed by k_quad / k_slp_scale, the segment counter and max |Q| by sym_pre.
 static int sym_launch(Geometry *g, long long ub, long long U, int op, cudaStream_t st) {
-    BIE_CUDA_TRY(cudaMemsetAsync(g->sym_acc, 0, sizeof(unsigned long long) * 6 * (size_t)g->N, st));
     if (U <= 0) return BIE_OK;
     const SymPlan pl = sym_plan(g, U, op);
     SymArgs sa{g->pos, g->sym_Q, g->sym_off, g->sym_acc, g->sym_counter + 1, g->N, g->sym_nTB, U, ub,
@@ -1294,9 +1308,12 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
 // NEXT-1: S = w sigma / (4 pi) for every vector (the single-layer source
 // strength), and for the symmetric path also the (S_x, S_y, 0, 0) records.
 __global__ void k_slp_scale(const double *__restrict__ w, const double *__restrict__ sigma, long long stride,
-                            int nvec, int N, double *S, double4 *Q, unsigned long long *qmax_bits = nullptr) {
+                            int nvec, int N, double *S, double4 *Q, unsigned long long *qmax_bits = nullptr,
+                            unsigned long long *acc = nullptr) {
+    pdl_wait();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     double m = 0.0;
+    if (acc && j < N) zero_limbs(acc, j, N);
     if (j < N) {
         const double f = w[j] * (1.0 / (4.0 * kPi));
         for (int v = 0; v < nvec; ++v) {
@@ -1344,8 +1361,8 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     }
     if (full) {
         count_launch();
-        k_moments<<<g->M + 1, 256, 0, st>>>(g->pos, g->nrm, g->w, g->pore, sigma, stride, nvec, g->M, g->n_pore,
-                                            g->wall_lo, N, g->wall_len, g->moments);
+        BIE_LAUNCH(k_moments, g->M + 1, 256, 0, st, g->pos, g->nrm, g->w, g->pore, sigma, stride, nvec, g->M,
+                   g->n_pore, g->wall_lo, N, g->wall_len, g->moments);
         BIE_CUDA_TRY(cudaGetLastError());
     }
     EpiArgs ea{};
@@ -1356,25 +1373,26 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         if (rc) return rc;
     }
     if (op) {
-        k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, stride, nvec, N, g->slp_s,
-                                                     sym ? g->sym_Q : nullptr, sym ? g->sym_counter + 1 : nullptr);
+        BIE_LAUNCH(k_slp_scale, (N + 255) / 256, 256, 0, st, g->w, sigma, stride, nvec, N, g->slp_s,
+                   sym ? g->sym_Q : nullptr, sym ? g->sym_counter + 1 : nullptr, sym ? g->sym_acc : nullptr);
         count_launch();
         sigma = g->slp_s;  // the pair kernels read S
     }
     if (sym) {
         if (!op) {
-            k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N, g->sym_counter + 1);
+            BIE_LAUNCH(k_quad, (N + 255) / 256, 256, 0, st, g->nw, sigma, g->sym_Q, N, g->sym_counter + 1,
+                       g->sym_acc);
             count_launch();
         }
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
         int rc = sym_launch(g, 0, g->sym_U, op, st);
         if (rc) return rc;
         if (op)
-            k_dlp_diag<1><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, 0,
-                                                                         g->sym_dsplit);
+            BIE_LAUNCH(k_dlp_diag<1>, 2 * g->sym_nTB * g->sym_dsplit, 128, 0, st, g->pos, g->nw, sigma, g->sym_diag,
+                       N, 0, g->sym_dsplit);
         else
-            k_dlp_diag<0><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, st>>>(g->pos, g->nw, sigma, g->sym_diag, N, 0,
-                                                                         g->sym_dsplit);
+            BIE_LAUNCH(k_dlp_diag<0>, 2 * g->sym_nTB * g->sym_dsplit, 128, 0, st, g->pos, g->nw, sigma, g->sym_diag,
+                       N, 0, g->sym_dsplit);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -1460,13 +1478,13 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
     ea.flags = flags;
     ea.nchunks = nch;
     if (nvec == 1)
-        k_epilogue<1><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+        BIE_LAUNCH(k_epilogue<1>, (Nt + 127) / 128, 128, 0, st, ea);
     else if (nvec == 4)
-        k_epilogue<4><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+        BIE_LAUNCH(k_epilogue<4>, (Nt + 127) / 128, 128, 0, st, ea);
     else if (nvec == 16)
-        k_epilogue<16><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+        BIE_LAUNCH(k_epilogue<16>, (Nt + 127) / 128, 128, 0, st, ea);
     else
-        k_epilogue<0><<<(Nt + 127) / 128, 128, 0, st>>>(ea);
+        BIE_LAUNCH(k_epilogue<0>, (Nt + 127) / 128, 128, 0, st, ea);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     if (ev[3]) BIE_CUDA_TRY(cudaEventRecord(ev[3], st));
@@ -1571,13 +1589,13 @@ int pairs_partial_impl(Geometry *g, const double *sigma, double *out_full, long 
         int rc2 = slp_prepare(g);
         if (rc2) return rc2;
         k_slp_scale<<<(N + 255) / 256, 256, 0, st>>>(g->w, sigma, 2LL * N, 1, N, g->slp_s, g->sym_Q,
-                                                     g->sym_counter + 1);
+                                                     g->sym_counter + 1, g->sym_acc);
     } else {
-        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N, g->sym_counter + 1);
+        k_quad<<<(N + 255) / 256, 256, 0, st>>>(g->nw, sigma, g->sym_Q, N, g->sym_counter + 1, g->sym_acc);
     }
     count_launch();
     if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
-    rc = sym_launch(g, ub, U, op, st);  // (zeroes the accumulators even for an empty slice)
+    rc = sym_launch(g, ub, U, op, st);  // (k_quad / k_slp_scale zeroed the accumulators, even for an empty slice)
     if (rc) return rc;
     if (blk1 > blk0) {
         if (op)

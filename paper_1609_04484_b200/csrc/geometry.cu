@@ -18,6 +18,13 @@ static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 static std::atomic<unsigned long long> g_bd_serial{0};
 unsigned long long next_bd_serial() { return ++g_bd_serial; }
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("BIE_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
 
 void set_error(const std::string &msg) { g_last_error = msg; }
 

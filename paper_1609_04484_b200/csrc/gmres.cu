@@ -33,123 +33,6 @@ namespace bie {
 constexpr int kChunk = 4096;      // elements of the 2N dimension per multidot CTA
 constexpr int kDotThreads = 128;  // 4 basis vectors share one staged w chunk
 
-// partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv).
-// Grid (chunks, Gy); warp wid of CTA y owns basis vectors j = 4y + wid + 4 Gy q
-// and reduces the whole 4096-element chunk for each (fixed lane order ->
-// deterministic; the j loop does not change any per-j sum).  kdev != nullptr
-// (GMRES graph body): nv = min(*kdev + 1, nv), the iteration count read on the
-// device.  sq: store sqrt of the dot (a norm; single-chunk case only).
-__global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restrict__ V, long long ldv, int nv,
-                                                          const int *kdev, const double *__restrict__ w, long long n,
-                                                          double *partial, int ldp, int sq) {
-    if (kdev) nv = min(*kdev + 1, nv);
-    if ((int)blockIdx.y * (kDotThreads / 32) >= nv) return;
-    __shared__ double ws[kChunk];
-    const long long e0 = (long long)blockIdx.x * kChunk;
-    const int len = (int)std::min<long long>(kChunk, n - e0);
-    for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j = blockIdx.y * (kDotThreads / 32) + wid; j < nv; j += gridDim.y * (kDotThreads / 32)) {
-        const double *vj = V + (long long)j * ldv + e0;
-        // four independent streams per lane keep enough loads in flight for HBM
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        int q = lane;
-        for (; q + 96 < len; q += 128) {
-            const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64),
-                         a3 = __ldcs(vj + q + 96);
-            acc0 = fma(a0, ws[q], acc0);
-            acc1 = fma(a1, ws[q + 32], acc1);
-            acc2 = fma(a2, ws[q + 64], acc2);
-            acc3 = fma(a3, ws[q + 96], acc3);
-        }
-        for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
-        double acc = (acc0 + acc1) + (acc2 + acc3);
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        BIE_DCHECK(j < ldp || gridDim.x == 1);
-        if (lane == 0) partial[(long long)blockIdx.x * ldp + j] = sq ? sqrt(acc) : acc;
-    }
-}
-
-// out[j] = (accumulate ? out[j] : 0) + sum_c partial[c * ldp + j]  (fixed order)
-// Sum of column j over the chunks in chunk order.  The loads are issued in
-// batches of 16 ahead of the (still sequential, so bitwise unchanged) adds: the
-// serial load-add loop was latency-bound (8.9 us per launch at 67 chunks).
-__device__ __forceinline__ double sum_chunks(const double *__restrict__ p, long long ldp, int nchunks) {
-    double t = 0.0;
-    int c = 0;
-    for (; c + 16 <= nchunks; c += 16) {
-        double v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = p[(long long)(c + u) * ldp];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) t += v[u];
-    }
-    for (; c < nchunks; ++c) t += p[(long long)c * ldp];
-    return t;
-}
-
-__global__ void k_reduce(const double *__restrict__ partial, int ldp, int nchunks, int nv, const int *kdev,
-                         double *out, int accumulate, int sq) {
-    if (kdev) nv = min(*kdev + 1, nv);
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= nv) return;
-    const double t = sum_chunks(partial + j, ldp, nchunks);
-    const double r = accumulate ? out[j] + t : t;
-    out[j] = sq ? sqrt(r) : r;
-}
-
-// y[e] = beta * y[e] + alpha * sum_j V[j][e] * c[j]   (c in device memory, any nv).
-// The coefficients are staged through shared memory in tiles of kAxpyTile
-// (static 16 KB, so no dynamic-smem limit on nv = k + 1); the sum over j stays
-// one sequential FMA chain per element, so results do not depend on the tiling.
-constexpr int kAxpyTile = 2048;
-__device__ __forceinline__ double axpy_chain(const double *__restrict__ V, long long ldv, int j0, int j1,
-                                             const double *cs, long long e, double acc) {
-    int j = j0;
-    for (; j + 4 <= j1; j += 4) {
-        const double a0 = V[(long long)j * ldv + e], a1 = V[(long long)(j + 1) * ldv + e];
-        const double a2 = V[(long long)(j + 2) * ldv + e], a3 = V[(long long)(j + 3) * ldv + e];
-        acc = fma(a0, cs[j - j0], acc);
-        acc = fma(a1, cs[j + 1 - j0], acc);
-        acc = fma(a2, cs[j + 2 - j0], acc);
-        acc = fma(a3, cs[j + 3 - j0], acc);
-    }
-    for (; j < j1; ++j) acc = fma(V[(long long)j * ldv + e], cs[j - j0], acc);
-    return acc;
-}
-
-__global__ void __launch_bounds__(256) k_multiaxpy(const double *__restrict__ V, long long ldv, int nv,
-                                                   const int *kdev, const double *__restrict__ c, double alpha,
-                                                   double beta, double *y, long long n) {
-    if (kdev) nv = min(*kdev + 1, nv);
-    __shared__ double cs[kAxpyTile];
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool act = e < n;
-    double acc = 0.0;
-    for (int j0 = 0; j0 < nv; j0 += kAxpyTile) {
-        const int j1 = min(nv, j0 + kAxpyTile);
-        __syncthreads();
-        for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) cs[q] = c[j0 + q];
-        __syncthreads();
-        if (act) acc = axpy_chain(V, ldv, j0, j1, cs, e, acc);
-    }
-    if (act) y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
-}
-
-__global__ void k_sqrt(const double *in, double *out) { *out = sqrt(*in); }
-
-// y = x / (*s)
-__global__ void k_scale_div(const double *x, const double *s, double *y, long long n) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) y[e] = x[e] / *s;
-}
-
-__global__ void k_sub(const double *a, const double *b, double *y, long long n) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) y[e] = a[e] - b[e];
-}
-
 struct GmState {
     double *H;      // column-major: H[k * ldh + j], ldh = max_iter + 1
     double *cs, *sn, *g;
@@ -201,38 +84,189 @@ __device__ __forceinline__ void givens_step(double *Hk, double *cs, double *sn, 
     scal[4] = (hk1 <= __dmul_rn(1e-14, scal[1])) ? 1.0 : 0.0;
 }
 
+// Tail of a fused kernel (GMRES iteration): after the thread that
+// finishes h_{k+1,k} = ||w|| has stored it, it runs the Givens step of
+// iteration k = ctl[0] (k_givens_dev's work: hist[k + 1], ctl[1] = converged,
+// ctl[0] = k + 1 and, in the CUDA-graph solve, the while-loop condition).
+struct GivensTail {
+    GmState s;
+    int *ctl = nullptr;
+    int ldh = 0, max_iter = 0;
+    double tol = 0.0;
+    double *hist = nullptr;
+    cudaGraphConditionalHandle cond = 0;
+    int use_cond = 0;
+    int on = 0;
+};
+__device__ __forceinline__ void givens_tail(const GivensTail &t) {
+    const int k = t.ctl[0];
+    unsigned cont = 0;
+    if (k < t.max_iter) {
+        givens_step(t.s.H + (long long)k * t.ldh, t.s.cs, t.s.sn, t.s.g, t.s.h, t.s.h2, t.s.scal, k);
+        const double est = t.s.scal[3];
+        const int conv = (est < t.tol || t.s.scal[4] != 0.0) ? 1 : 0;
+        t.hist[k + 1] = est;
+        t.ctl[1] = conv;
+        t.ctl[0] = k + 1;
+        cont = (!conv && k + 1 < t.max_iter) ? 1u : 0u;
+    }
+    if (t.use_cond) cudaGraphSetConditional(t.cond, cont);
+}
+
+// partial[c * ldp + j] = sum_{e in chunk c} V[j][e] * w[e] for j in [0, nv).
+// Grid (chunks, Gy); warp wid of CTA y owns basis vectors j = 4y + wid + 4 Gy q
+// and reduces the whole 4096-element chunk for each (fixed lane order ->
+// deterministic; the j loop does not change any per-j sum).  kdev != nullptr
+// (GMRES iteration): nv = min(*kdev + 1, nv), the iteration count read on the
+// device.  sq: store sqrt of the dot (a norm; single-chunk case only).
+// xv != nullptr: one more vector, xv itself, is dotted with w as column nv
+// (its chunk sum is computed by the same code, so the result is bitwise that
+// of a separate norm launch); single chunk: sqrt of it goes to xout.
+// gt.on (single chunk, nv = 1): the thread that stores the norm then runs the
+// Givens step (givens_tail).
+__global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restrict__ V, long long ldv, int nv,
+                                                          const int *kdev, const double *__restrict__ w, long long n,
+                                                          double *partial, int ldp, int sq, const double *xv,
+                                                          double *xout, GivensTail gt) {
+    pdl_wait();
+    if (kdev) nv = min(*kdev + 1, nv);
+    const int ntot = nv + (xv ? 1 : 0);
+    if ((int)blockIdx.y * (kDotThreads / 32) >= ntot) return;
+    __shared__ double ws[kChunk];
+    const long long e0 = (long long)blockIdx.x * kChunk;
+    const int len = (int)std::min<long long>(kChunk, n - e0);
+    for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int j = blockIdx.y * (kDotThreads / 32) + wid; j < ntot; j += gridDim.y * (kDotThreads / 32)) {
+        const bool extra = j == nv;
+        const double *vj = (extra ? xv : V + (long long)j * ldv) + e0;
+        // four independent streams per lane keep enough loads in flight for HBM
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        int q = lane;
+        for (; q + 96 < len; q += 128) {
+            const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64),
+                         a3 = __ldcs(vj + q + 96);
+            acc0 = fma(a0, ws[q], acc0);
+            acc1 = fma(a1, ws[q + 32], acc1);
+            acc2 = fma(a2, ws[q + 64], acc2);
+            acc3 = fma(a3, ws[q + 96], acc3);
+        }
+        for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
+        double acc = (acc0 + acc1) + (acc2 + acc3);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        BIE_DCHECK(j < ldp || gridDim.x == 1);
+        if (lane == 0) {
+            if (extra && gridDim.x == 1) {
+                *xout = sqrt(acc);
+            } else {
+                partial[(long long)blockIdx.x * ldp + j] = sq ? sqrt(acc) : acc;
+                if (gt.on && j == 0 && gridDim.x == 1) givens_tail(gt);
+            }
+        }
+    }
+}
+
+// out[j] = (accumulate ? out[j] : 0) + sum_c partial[c * ldp + j]  (fixed order)
+// Sum of column j over the chunks in chunk order.  The loads are issued in
+// batches of 16 ahead of the (still sequential, so bitwise unchanged) adds: the
+// serial load-add loop was latency-bound (8.9 us per launch at 67 chunks).
+__device__ __forceinline__ double sum_chunks(const double *__restrict__ p, long long ldp, int nchunks) {
+    double t = 0.0;
+    int c = 0;
+    for (; c + 16 <= nchunks; c += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = p[(long long)(c + u) * ldp];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t += v[u];
+    }
+    for (; c < nchunks; ++c) t += p[(long long)c * ldp];
+    return t;
+}
+
+// xout != nullptr: column nv (the extra vector of k_multidot) -> sqrt into
+// *xout.  gt.on: thread 0 runs the Givens step after storing out[0].
+__global__ void k_reduce(const double *__restrict__ partial, int ldp, int nchunks, int nv, const int *kdev,
+                         double *out, int accumulate, int sq, double *xout, GivensTail gt) {
+    pdl_wait();
+    if (kdev) nv = min(*kdev + 1, nv);
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nv + (xout ? 1 : 0)) return;
+    const double t = sum_chunks(partial + j, ldp, nchunks);
+    if (j == nv) {
+        *xout = sqrt(t);
+        return;
+    }
+    const double r = accumulate ? out[j] + t : t;
+    out[j] = sq ? sqrt(r) : r;
+    if (gt.on && j == 0) givens_tail(gt);
+}
+
+// y[e] = beta * y[e] + alpha * sum_j V[j][e] * c[j]   (c in device memory, any nv).
+// The coefficients are staged through shared memory in tiles of kAxpyTile
+// (static 16 KB, so no dynamic-smem limit on nv = k + 1); the sum over j stays
+// one sequential FMA chain per element, so results do not depend on the tiling.
+constexpr int kAxpyTile = 2048;
+__device__ __forceinline__ double axpy_chain(const double *__restrict__ V, long long ldv, int j0, int j1,
+                                             const double *cs, long long e, double acc) {
+    int j = j0;
+    for (; j + 4 <= j1; j += 4) {
+        const double a0 = V[(long long)j * ldv + e], a1 = V[(long long)(j + 1) * ldv + e];
+        const double a2 = V[(long long)(j + 2) * ldv + e], a3 = V[(long long)(j + 3) * ldv + e];
+        acc = fma(a0, cs[j - j0], acc);
+        acc = fma(a1, cs[j + 1 - j0], acc);
+        acc = fma(a2, cs[j + 2 - j0], acc);
+        acc = fma(a3, cs[j + 3 - j0], acc);
+    }
+    for (; j < j1; ++j) acc = fma(V[(long long)j * ldv + e], cs[j - j0], acc);
+    return acc;
+}
+
+__global__ void __launch_bounds__(256) k_multiaxpy(const double *__restrict__ V, long long ldv, int nv,
+                                                   const int *kdev, const double *__restrict__ c, double alpha,
+                                                   double beta, double *y, long long n) {
+    pdl_wait();
+    if (kdev) nv = min(*kdev + 1, nv);
+    __shared__ double cs[kAxpyTile];
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = e < n;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < nv; j0 += kAxpyTile) {
+        const int j1 = min(nv, j0 + kAxpyTile);
+        __syncthreads();
+        for (int q = threadIdx.x; q < j1 - j0; q += blockDim.x) cs[q] = c[j0 + q];
+        __syncthreads();
+        if (act) acc = axpy_chain(V, ldv, j0, j1, cs, e, acc);
+    }
+    if (act) y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
+}
+
+__global__ void k_sqrt(const double *in, double *out) { *out = sqrt(*in); }
+
+// y = x / (*s)
+__global__ void k_scale_div(const double *x, const double *s, double *y, long long n) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) y[e] = x[e] / *s;
+}
+
+__global__ void k_sub(const double *a, const double *b, double *y, long long n) {
+    pdl_wait();
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) y[e] = a[e] - b[e];
+}
+
 // Hessenberg column k: H[:,k] = h + h2, H[k+1,k] = hk1; apply old rotations, new rotation.
 __global__ void k_givens(GmState s, int k, int ldh) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     givens_step(s.H + (long long)k * ldh, s.cs, s.sn, s.g, s.h, s.h2, s.scal, k);
 }
 
-// Graph-body form of the Givens step: the iteration index k = ctl[0] lives on
-// the device.  Writes hist[k + 1] = estimate, ctl[1] = converged (estimate < tol
-// or happy breakdown, the host check of reading C13), advances ctl[0] and, in
-// the CUDA-graph solve, sets the while-loop condition (continue while not
-// converged and k + 1 < max_iter).
-__global__ void k_givens_dev(GmState s, int *ctl, int ldh, int max_iter, double tol, double *hist,
-                             cudaGraphConditionalHandle cond, int use_cond) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int k = ctl[0];
-    unsigned cont = 0;
-    if (k < max_iter) {
-        givens_step(s.H + (long long)k * ldh, s.cs, s.sn, s.g, s.h, s.h2, s.scal, k);
-        const double est = s.scal[3];
-        const int conv = (est < tol || s.scal[4] != 0.0) ? 1 : 0;
-        hist[k + 1] = est;
-        ctl[1] = conv;
-        ctl[0] = k + 1;
-        cont = (!conv && k + 1 < max_iter) ? 1u : 0u;
-    }
-    if (use_cond) cudaGraphSetConditional(cond, cont);
-}
-
 // v = x / (*s) into the current-vector buffer and into V[ctl[0]] (when
 // ctl[0] < max_iter): the next Krylov vector, at the device-side index.
 __global__ void k_scale_store(const double *x, const double *s, double *V, long long n, const int *ctl,
                               int max_iter, double *vcur) {
+    pdl_wait();
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n) return;
     const double y = x[e] / *s;
@@ -243,6 +277,7 @@ __global__ void k_scale_store(const double *x, const double *s, double *V, long 
 
 // y = H^{-1} g (upper triangular, iters x iters), one CTA
 __global__ void k_trisolve(const double *H, int ldh, const double *g, double *y, int iters) {
+    pdl_wait();
     __shared__ double red[32];
     __shared__ double yi_s;
     for (int i = iters - 1; i >= 0; --i) {
@@ -270,19 +305,22 @@ struct Dot {
 // out[0..nv) = V[0..nv)^T w (deterministic).  kdev: nv = min(*kdev + 1, nv) on
 // the device (graph body; the grid is sized for the cap nv).  sq: out = sqrt.
 static int multidot(const double *V, long long ldv, int nv, const double *w, long long n, Dot &d, double *out,
-                    cudaStream_t st, const int *kdev = nullptr, int sq = 0) {
-    const int gy_full = (nv + kDotThreads / 32 - 1) / (kDotThreads / 32);
+                    cudaStream_t st, const int *kdev = nullptr, int sq = 0, const double *xv = nullptr,
+                    double *xout = nullptr, const GivensTail &gt = GivensTail{}) {
+    const int ncap = nv + (xv ? 1 : 0);
+    const int gy_full = (ncap + kDotThreads / 32 - 1) / (kDotThreads / 32);
     // device-side nv: cap the y extent (each warp loops over its vectors) so
     // that the mostly idle tail of a max_iter-sized grid stays small
     const int gy = kdev ? std::max(1, std::min(gy_full, (4 * 148 + d.nchunks - 1) / d.nchunks)) : gy_full;
     if (d.nchunks == 1) {  // one chunk (2N <= 4096): the partial IS the result, no reduction launch
-        k_multidot<<<dim3(1, gy), kDotThreads, 0, st>>>(V, ldv, nv, kdev, w, n, out, 0, sq);
+        BIE_LAUNCH(k_multidot, dim3(1, gy), kDotThreads, 0, st, V, ldv, nv, kdev, w, n, out, 0, sq, xv, xout, gt);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
     }
-    k_multidot<<<dim3(d.nchunks, gy), kDotThreads, 0, st>>>(V, ldv, nv, kdev, w, n, d.partial, d.ldp, 0);
-    k_reduce<<<(nv + 127) / 128, 128, 0, st>>>(d.partial, d.ldp, d.nchunks, nv, kdev, out, 0, sq);
+    BIE_LAUNCH(k_multidot, dim3(d.nchunks, gy), kDotThreads, 0, st, V, ldv, nv, kdev, w, n, d.partial, d.ldp, 0, xv,
+               xout, GivensTail{});
+    BIE_LAUNCH(k_reduce, (ncap + 127) / 128, 128, 0, st, d.partial, d.ldp, d.nchunks, nv, kdev, out, 0, sq, xout, gt);
     count_launch(2);
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
@@ -290,7 +328,7 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
 
 static int multiaxpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,
                      long long n, cudaStream_t st, const int *kdev = nullptr) {
-    k_multiaxpy<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(V, ldv, nv, kdev, c, alpha, beta, y, n);
+    BIE_LAUNCH(k_multiaxpy, (unsigned)((n + 255) / 256), 256, 0, st, V, ldv, nv, kdev, c, alpha, beta, y, n);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
@@ -514,9 +552,10 @@ int bie_krylov_trisolve(const double *H, int ldh, const double *g, double *y, in
 //
 // One GMRES iteration is a fixed sequence of launches whose only varying
 // argument, the iteration index k, lives on the device (ctl[0]): operator apply
-// on v_k (kept in vcur), ||w||, CGS2 over V[0..k], hk1, Givens (k_givens_dev)
+// on v_k (kept in vcur), CGS2 over V[0..k] (its first dot launch also gives
+// ||w||), hk1 with the Givens step in the same kernel's tail (givens_tail)
 // and v_{k+1} (k_scale_store).  The solve captures that sequence ONCE into the
-// body of a CUDA-graph conditional WHILE node; k_givens_dev sets the loop
+// body of a CUDA-graph conditional WHILE node; givens_tail sets the loop
 // condition, so a whole solve is one graph launch with no host round trip per
 // iteration.  The instantiated graph is cached on the geometry and reused while
 // the operator, BD handle, tol, max_iter and the workspace are unchanged.  With
@@ -610,16 +649,25 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     auto body = [&](cudaStream_t q, cudaGraphConditionalHandle cond, int use_cond) -> int {
         int r;
         if ((r = apply_op(vcur, w, q))) return r;
-        if ((r = norm_to(w, s.scal + 1, q))) return r;  // w0 = ||P^{-1} A v_k||
-        // CGS2 over V[0..k]
-        if ((r = multidot(V, n, ldh, w, n, d, s.h, q, ctl))) return r;
+        // CGS2 over V[0..k]; the first pass also yields w0 = ||P^{-1} A v_k|| (w as
+        // the extra column), the final norm hk1 runs the Givens step in its tail
+        if ((r = multidot(V, n, ldh - 1, w, n, d, s.h, q, ctl, 0, w, s.scal + 1))) return r;
         if ((r = multiaxpy(V, n, ldh, s.h, -1.0, 1.0, w, n, q, ctl))) return r;
         if ((r = multidot(V, n, ldh, w, n, d, s.h2, q, ctl))) return r;
         if ((r = multiaxpy(V, n, ldh, s.h2, -1.0, 1.0, w, n, q, ctl))) return r;
-        if ((r = norm_to(w, s.scal + 2, q))) return r;  // hk1
-        k_givens_dev<<<1, 1, 0, q>>>(s, ctl, ldh, max_iter, tol, hist_d, cond, use_cond);
-        k_scale_store<<<eb, 256, 0, q>>>(w, s.scal + 2, V, n, ctl, max_iter, vcur);
-        count_launch(2);
+        GivensTail gt;
+        gt.s = s;
+        gt.ctl = ctl;
+        gt.ldh = ldh;
+        gt.max_iter = max_iter;
+        gt.tol = tol;
+        gt.hist = hist_d;
+        gt.cond = cond;
+        gt.use_cond = use_cond;
+        gt.on = 1;
+        if ((r = multidot(w, 0, 1, w, n, d, s.scal + 2, q, nullptr, 1, nullptr, nullptr, gt))) return r;  // hk1
+        BIE_LAUNCH(k_scale_store, eb, 256, 0, q, w, s.scal + 2, V, n, ctl, max_iter, vcur);
+        count_launch(1);
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
     };

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -184,6 +185,35 @@ struct Geometry {
 
 // process-wide count of kernels launched by the library (bie_launch_count)
 void count_launch(int n = 1);
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL) for the kernels of one GMRES iteration
+// (matvec, BD apply, Krylov kernels; DESIGN.md s5 GMRES).  Each such kernel
+// starts with pdl_wait() (griddepcontrol.wait: blocks until the preceding grid
+// has completed and its memory is visible; a no-op for a normal launch), and
+// launch_pdl() lets the next grid be scheduled while this one drains, so the
+// launch latency between the ~20 short kernels of a small-N iteration overlaps
+// the previous kernel's tail.  Every kernel launched this way waits before it
+// touches memory, so completion stays transitive along the stream.
+// BIE_PDL=0 disables it (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // error -> cudaGetLastError()
+}
+#define BIE_LAUNCH(kern, grid, block, smem, st, ...) \
+    ::bie::launch_pdl(kern, dim3(grid), dim3(block), (size_t)(smem), (st), __VA_ARGS__)
 
 unsigned long long next_bd_serial();
 struct BlockDiag {
