@@ -32,6 +32,7 @@ namespace cg = cooperative_groups;
 namespace bie {
 
 constexpr int NB = 32;  // panel width
+constexpr int kSB = 4 * NB;  // super-panel of the delayed update (large single blocks)
 
 struct BDView {            // one size class
     double *mat;           // first matrix
@@ -516,38 +517,47 @@ __global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopS
 }
 
 // Apply the panel's row swaps to all columns of M (sequential in k, parallel over columns).
-__global__ void k_swap(BDView v, BDScratch s, int k0, int nbe) {
+__global__ void k_swap(BDView v, BDScratch s, int k0, int nbe, double *TS = nullptr, int tsw = 0) {
     const int m = blockIdx.y;
     const int col = blockIdx.x * blockDim.x + threadIdx.x;
     const int n2 = v.n2;
-    if (col >= n2) return;
-    double *M = v.mat + (long long)m * v.mstride;
+    if (col >= n2 + tsw) return;
+    // columns >= n2: the first tsw columns of TS ([n2][kSB]), the T-hat columns of
+    // the earlier sub-panels of the current super-panel, whose rows follow M's
+    double *base = col < n2 ? v.mat + (long long)m * v.mstride + col : TS + (col - n2);
+    const long long ld = col < n2 ? n2 : kSB;
     const int *piv = s.piv + (long long)m * n2;
     for (int c = 0; c < nbe; ++c) {
         int k = k0 + c, p = piv[k];
         if (p != k) {
-            double t = M[(long long)k * n2 + col];
-            M[(long long)k * n2 + col] = M[(long long)p * n2 + col];
-            M[(long long)p * n2 + col] = t;
+            double t = base[(long long)k * ld];
+            base[(long long)k * ld] = base[(long long)p * ld];
+            base[(long long)p * ld] = t;
         }
     }
 }
 
-__global__ void k_copy_T(BDView v, BDScratch s, int k0, int nbe) {
+// T = M[:, K]; with TS: also T-hat = T - E_K (identity on the pivot rows K)
+// into columns [tcol, tcol + NB) of TS -- the sub-panel's column of the
+// aggregated update (k_update_agg).
+__global__ void k_copy_T(BDView v, BDScratch s, int k0, int nbe, double *TS = nullptr, int tcol = 0) {
     const int m = blockIdx.y;
     const int n2 = v.n2;
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (long long)n2 * NB) return;
     const int r = (int)(q / NB), c = (int)(q % NB);
     const double *M = v.mat + (long long)m * v.mstride;
-    s.T[(long long)m * n2 * NB + q] = c < nbe ? M[(long long)r * n2 + k0 + c] : 0.0;
+    const double t = c < nbe ? M[(long long)r * n2 + k0 + c] : 0.0;
+    s.T[(long long)m * n2 * NB + q] = t;
+    if (TS) TS[(long long)r * kSB + tcol + c] = (c < nbe && r == k0 + c) ? t - 1.0 : t;
 }
 
 // G[c][j] = sum_c' A11i[c][c'] M[k0+c'][j]  (j outside K);  G[c][K] = A11i.
-__global__ void k_make_G(BDView v, BDScratch s, int k0, int nbe) {
+__global__ void k_make_G(BDView v, BDScratch s, int k0, int nbe, int jlo = 0, int jhi = 1 << 30) {
     const int m = blockIdx.y;
     const int n2 = v.n2;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= jhi) return;
     __shared__ double Ai[NB][NB];
     const double *A = s.A11i + (long long)m * NB * NB;
     for (int q = threadIdx.x; q < NB * NB; q += blockDim.x) Ai[q / NB][q % NB] = A[q];
@@ -654,12 +664,14 @@ __device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, do
                  : "d"(a), "d"(b));
 }
 constexpr int UT3 = 64;
-__global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k0, int nbe) {
+__global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k0, int nbe, int jlo = 0,
+                                                   int jhi = 1 << 30) {
     __shared__ double Ts[UT3][NB + 1];  // Ts[i][c] = T[i0 + i][c]
     __shared__ double Gs[NB][UT3 + 1];  // Gs[c][j] = G[c][j0 + j]
     const int m = blockIdx.z;
     const int n2 = v.n2;
-    const int i0 = blockIdx.y * UT3, j0 = blockIdx.x * UT3;
+    const int jend = min(n2, jhi);  // column bound of this launch
+    const int i0 = blockIdx.y * UT3, j0 = jlo + blockIdx.x * UT3;
     const double *T = s.T + (long long)m * n2 * NB;
     const double *G = s.G + (long long)m * NB * n2;
     double *M = v.mat + (long long)m * v.mstride;
@@ -682,7 +694,7 @@ __global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k
         for (int r = 0; r < PER; ++r) {
             const int q = tid + 128 * r;
             const int c = q / UT3, j = q % UT3;
-            gv[r] = (j0 + j < n2) ? G[(long long)c * n2 + j0 + j] : 0.0;
+            gv[r] = (j0 + j < jend) ? G[(long long)c * n2 + j0 + j] : 0.0;
         }
 #pragma unroll
         for (int r = 0; r < PER; ++r) {
@@ -717,7 +729,7 @@ __global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int gj = j0 + wc + 8 * j + 2 * gq;
-            base[i][j] = (gi < n2 && gj < n2) ? __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj))
+            base[i][j] = (gi < n2 && gj < jend) ? __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj))
                                               : make_double2(0.0, 0.0);
         }
     }
@@ -731,7 +743,7 @@ __global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k
         for (int j = 0; j < 4; ++j) {
             const int lj = wc + 8 * j + 2 * gq;
             const int gj = j0 + lj;
-            if (gj >= n2) continue;  // n2 even, gj even
+            if (gj >= jend) continue;  // n2, jend even, gj even
             double2 *dst = reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj);
             double2 o;
             if (rowK) {
@@ -743,6 +755,134 @@ __global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k
                 o = make_double2(b.x - acc[i][j][0], b.y - acc[i][j][1]);
             }
             __stcs(dst, o);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Delayed (aggregated) update of a large single block (the wall).
+// The NB-column sub-panels p = 0..nsub-1 of a kSB-column super-panel S are
+// factored and applied to the slab M[:, S] one by one (k_make_G / k_update3
+// restricted to S).  Every other column j only receives the row swaps; its
+// update, the product of the nsub elementary Gauss-Jordan steps
+//   x <- x - T-hat_p A11i_p x[K_p]     (T-hat_p = T_p - E_{K_p}: rows K_p become G)
+// is applied at once as x <- x - T-hat_S y with y = [y_0; ...; y_{nsub-1}],
+//   y_p = A11i_p (x[K_p] - sum_{q<p} T-hat_q[K_p, :] y_q)       (k_make_Y),
+// one rank-kSB DMMA pass over the block (k_update_agg) instead of nsub rank-NB
+// passes: a quarter of the HBM traffic for the same flops.  T-hat_q's rows follow
+// the later sub-panels' swaps (k_swap swaps TS with M), so the algebra is the
+// sequential one; only the rounding order of the updates differs.
+
+// y for every column j outside S: one thread per column, Y[kSB][n2] row-major.
+__global__ void __launch_bounds__(128) k_make_Y(BDView v, const double *__restrict__ TS,
+                                                const double *__restrict__ A11S, double *Y, int s0, int sbe,
+                                                int nsub) {
+    const int n2 = v.n2;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n2 - sbe) return;
+    const int j = t < s0 ? t : t + sbe;
+    const double *M = v.mat;
+    for (int p = 0; p < nsub; ++p) {
+        const int k0 = s0 + p * NB, nbe = min(NB, n2 - k0);
+        double acc[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) acc[c] = c < nbe ? M[(long long)(k0 + c) * n2 + j] : 0.0;
+        for (int q = 0; q < p; ++q) {
+#pragma unroll 4
+            for (int cc = 0; cc < NB; ++cc) {
+                const double y = Y[(long long)(q * NB + cc) * n2 + j];
+#pragma unroll
+                for (int c = 0; c < NB; ++c) acc[c] = fma(-__ldg(TS + (long long)(k0 + c) * kSB + q * NB + cc), y, acc[c]);
+            }
+        }
+        const double *A = A11S + (long long)p * NB * NB;
+        for (int c = 0; c < NB; ++c) {
+            double y = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < NB; ++cc)
+                if (cc < nbe) y = fma(__ldg(A + c * NB + cc), acc[cc], y);  // A11i is nbe x nbe
+            Y[(long long)(p * NB + c) * n2 + j] = c < nbe ? y : 0.0;
+        }
+    }
+}
+
+// M[:, j] -= TS[:, 0:K] Y[0:K, j] for the column tiles outside S (K = nsub NB),
+// on the FP64 tensor cores: k_update3's 64x64 DMMA tiles with the K dimension
+// looped in NB chunks through the same shared-memory tiles.
+__global__ void __launch_bounds__(128, 3) k_update_agg(BDView v, const double *__restrict__ TS,
+                                                       const double *__restrict__ Y, int s0, int sbe, int nsub) {
+    __shared__ double Ts[UT3][NB + 1];
+    __shared__ double Gs[NB][UT3 + 1];
+    const int n2 = v.n2;
+    const int i0 = blockIdx.y * UT3, j0 = blockIdx.x * UT3;
+    if (j0 >= s0 && j0 < s0 + sbe) return;  // the slab is final (s0, sbe multiples of UT3)
+    double *M = v.mat;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
+    const int gr = lane >> 2, gq = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int p = 0; p < nsub; ++p) {
+        constexpr int PER = UT3 * NB / 128;  // 16
+        double tv[PER], gv[PER];
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int q = tid + 128 * r;
+            const int i = q / NB, c = q % NB;
+            tv[r] = (i0 + i < n2) ? TS[(long long)(i0 + i) * kSB + p * NB + c] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int q = tid + 128 * r;
+            const int c = q / UT3, j = q % UT3;
+            gv[r] = (j0 + j < n2) ? Y[(long long)(p * NB + c) * n2 + j0 + j] : 0.0;
+        }
+        __syncthreads();  // the previous chunk's fragments are read
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int q = tid + 128 * r;
+            Ts[q / NB][q % NB] = tv[r];
+            Gs[q / UT3][q % UT3] = gv[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < NB / 4; ++kk) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = Ts[wr + 8 * i + gr][kk * 4 + gq];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Gs[kk * 4 + gq][wc + 8 * j + gr];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    double2 base[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gi = i0 + wr + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gj = j0 + wc + 8 * j + 2 * gq;
+            base[i][j] = (gi < n2 && gj < n2) ? __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj))
+                                              : make_double2(0.0, 0.0);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gi = i0 + wr + 8 * i + gr;
+        if (gi >= n2) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gj = j0 + wc + 8 * j + 2 * gq;
+            if (gj >= n2) continue;
+            __stcs(reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj),
+                   make_double2(base[i][j].x - acc[i][j][0], base[i][j].y - acc[i][j][1]));
         }
     }
 }
@@ -895,8 +1035,21 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     BIE_CUDA_TRY(cudaFuncSetAttribute(k_update2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_smem));
     BIE_CUDA_TRY(cudaFuncSetAttribute(k_panel_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(double) * NB * kSmemPanelRows)));
-    for (int k0 = 0; k0 < n2; k0 += NB) {
-        int nbe = std::min(NB, n2 - k0);
+    // large single block (the wall): super-panels of kSB columns with the delayed
+    // rank-kSB update of the columns outside the slab (k_make_Y / k_update_agg)
+    double *TS = nullptr, *Yb = nullptr, *A11S = nullptr;
+    // BIE_BD_AGG: 0 never, 1 whenever the block is factored cooperatively (tests),
+    // default: blocks of order >= 8192 (config 4: 0.83 -> 0.57 s; at order 1024-4096
+    // the extra launches cost more than the saved traffic)
+    int agg_mode = 2;
+    if (const char *e = getenv("BIE_BD_AGG")) agg_mode = std::max(0, std::min(1, atoi(e)));
+    const bool agg = coop && n2 % UT3 == 0 && (agg_mode == 1 || (agg_mode == 2 && n2 >= 8192));
+    if (agg) {
+        BIE_CUDA_TRY(cudaMallocAsync(&TS, sizeof(double) * (size_t)n2 * kSB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&Yb, sizeof(double) * (size_t)n2 * kSB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&A11S, sizeof(double) * 4 * NB * NB, st));
+    }
+    auto panel = [&](int k0, int nbe) -> int {
         if (coop) {
             int G = (n2 - k0 + 128 * rpt - 1) / (128 * rpt);
             void *args[] = {&v, &s, &cs, &k0, &nbe};
@@ -907,6 +1060,40 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
             int panel_threads = n2 >= 1024 ? 1024 : 256;
             k_panel<<<v.count, panel_threads, 0, st>>>(v, s, k0, nbe);
         }
+        return BIE_OK;
+    };
+    if (agg) {
+        for (int s0 = 0; s0 < n2; s0 += kSB) {
+            const int sbe = std::min(kSB, n2 - s0), nsub = (sbe + NB - 1) / NB;
+            for (int p = 0; p < nsub; ++p) {
+                const int k0 = s0 + p * NB, nbe = std::min(NB, n2 - k0);
+                BIE_RC_TRY(panel(k0, nbe));
+                k_swap<<<dim3((n2 + p * NB + 127) / 128, 1), 128, 0, st>>>(v, s, k0, nbe, TS, p * NB);
+                k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), 1), 256, 0, st>>>(v, s, k0, nbe, TS,
+                                                                                              p * NB);
+                BIE_CUDA_TRY(cudaMemcpyAsync(A11S + p * NB * NB, s.A11i, sizeof(double) * NB * NB,
+                                             cudaMemcpyDeviceToDevice, st));
+                k_make_G<<<dim3((sbe + 127) / 128, 1), 128, 0, st>>>(v, s, k0, nbe, s0, s0 + sbe);
+                k_update3<<<dim3((sbe + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3, 1), 128, 0, st>>>(v, s, k0, nbe, s0,
+                                                                                             s0 + sbe);
+                count_launch(5);
+                BIE_CUDA_TRY(cudaGetLastError());
+            }
+            if (n2 > sbe) {
+                k_make_Y<<<(n2 - sbe + 127) / 128, 128, 0, st>>>(v, TS, A11S, Yb, s0, sbe, nsub);
+                k_update_agg<<<dim3((n2 + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3), 128, 0, st>>>(v, TS, Yb, s0, sbe,
+                                                                                              nsub);
+                count_launch(2);
+                BIE_CUDA_TRY(cudaGetLastError());
+            }
+        }
+        cudaFreeAsync(TS, st);
+        cudaFreeAsync(Yb, st);
+        cudaFreeAsync(A11S, st);
+    }
+    for (int k0 = 0; k0 < n2 && !agg; k0 += NB) {
+        int nbe = std::min(NB, n2 - k0);
+        BIE_RC_TRY(panel(k0, nbe));
         k_swap<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);
         k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), v.count), 256, 0, st>>>(v, s, k0, nbe);
         k_make_G<<<dim3((n2 + 127) / 128, v.count), 128, 0, st>>>(v, s, k0, nbe);

@@ -402,3 +402,19 @@ def test_krylov_axpy_beyond_one_coefficient_tile(bie):
     bie.Krylov.axpy(Vd[2048 * n:], n, nv - 2048, cd[2048:], 1.0, 0.0, z, n)
     torch.cuda.synchronize()
     assert np.abs((y2 + z).cpu().numpy() - ref).max() <= 2 * bound.max()
+
+
+def test_bd_wall_delayed_update_parity(bie, monkeypatch):
+    """The delayed rank-128 wall update (k_make_Y / k_update_agg; by default only
+    for blocks of order >= 8192) forced on config 2's 1024-order wall: the same
+    inverse as the oracle's to 1e-12 and B X = I, as the per-panel sweep."""
+    monkeypatch.setenv("BIE_BD_AGG", "1")
+    p = make_problem(2)
+    g = bie.Geometry.from_problem(p)
+    og = oracle.OracleGeometry(p)
+    bd = bie.BlockDiag(g)
+    gi = bd.block_inverse(p.M)
+    oi = oracle.OracleBD(og).block_inverse(p.M)
+    assert np.abs(gi - oi).max() / np.abs(oi).max() < 1e-12
+    B = og.bd_block(p.M)
+    assert np.abs(gi @ B - np.eye(B.shape[0])).max() < 1e-12
