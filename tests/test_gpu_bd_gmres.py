@@ -418,3 +418,46 @@ def test_bd_wall_delayed_update_parity(bie, monkeypatch):
     assert np.abs(gi - oi).max() / np.abs(oi).max() < 1e-12
     B = og.bd_block(p.M)
     assert np.abs(gi @ B - np.eye(B.shape[0])).max() < 1e-12
+
+
+def test_gmres_graph_cache_matches_host_loop(bie, monkeypatch):
+    """The CUDA-graph GMRES loop (cached on the geometry, keyed by operator, BD
+    handle + serial, tol, max_iter and workspace) against the host-enqueued loop
+    (BIE_GMRES_GRAPH=0), bitwise, across changes of every key: tol, max_iter
+    (including max_iter = 1 and a larger one that regrows the workspace), a
+    destroyed and re-created BD, the structured BD, no preconditioner, the SLP
+    operator, and back."""
+    import torch
+
+    p = make_problem(2)
+    g = bie.Geometry.from_problem(p)
+    f = _t(rhs_pipe(p))
+
+    def both(solve, *a, **k):
+        x1, x2 = torch.zeros_like(f), torch.zeros_like(f)
+        monkeypatch.setenv("BIE_GMRES_GRAPH", "1")
+        r1 = solve(g, *a, f, x1, **k)
+        monkeypatch.setenv("BIE_GMRES_GRAPH", "0")
+        r2 = solve(g, *a, f, x2, **k)
+        monkeypatch.setenv("BIE_GMRES_GRAPH", "1")
+        assert r1["iters"] == r2["iters"] and r1["converged"] == r2["converged"]
+        assert np.array_equal(r1["hist"], r2["hist"])
+        assert torch.equal(x1, x2)
+        return r1
+
+    bd = bie.BlockDiag(g)
+    r_a = both(bie.gmres_solve, bd, tol=1e-8, max_iter=200)
+    r_b = both(bie.gmres_solve, bd, tol=1e-5, max_iter=200)
+    assert r_b["iters"] < r_a["iters"]
+    r_c = both(bie.gmres_solve, bd, tol=1e-8, max_iter=1)
+    assert r_c["iters"] == 1 and not r_c["converged"]
+    both(bie.gmres_solve, bd, tol=1e-8, max_iter=600)  # regrows the Krylov workspace
+    bd.close()
+    bd2 = bie.BlockDiag(g)  # a new factorisation (possibly at the same address)
+    r_d = both(bie.gmres_solve, bd2, tol=1e-8, max_iter=200)
+    assert np.array_equal(r_d["hist"], r_a["hist"])
+    both(bie.gmres_solve, bie.BlockDiag(g, structured=True), tol=1e-8, max_iter=200)
+    both(bie.gmres_solve, None, tol=1e-8, max_iter=120)
+    both(bie.gmres_solve_slp, bie.BlockDiag(g, op="slp"), tol=1e-8, max_iter=300)
+    r_e = both(bie.gmres_solve, bd2, tol=1e-8, max_iter=200)
+    assert np.array_equal(r_e["hist"], r_a["hist"])
