@@ -167,6 +167,52 @@ __global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restri
     }
 }
 
+// Small vectors (one chunk, n <= kChunk: configs 1-2): one CTA of 256 threads
+// per basis vector (grid-stride over j) and a fixed-order block reduction.
+// k_multidot's one warp per vector streamed a config-2 vector (3584 doubles)
+// with 4 loads in flight per lane: 11 us per launch, latency-bound.  Same
+// operands and outputs as k_multidot's single-chunk case (extra column xv ->
+// sqrt into xout; Givens tail).
+__global__ void __launch_bounds__(256) k_multidot_small(const double *__restrict__ V, long long ldv, int nv,
+                                                        const int *kdev, const double *__restrict__ w, int n,
+                                                        double *out, int sq, const double *xv, double *xout,
+                                                        GivensTail gt) {
+    pdl_wait();
+    if (kdev) nv = min(*kdev + 1, nv);
+    const int ntot = nv + (xv ? 1 : 0);
+    __shared__ double red[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int j = blockIdx.x; j < ntot; j += gridDim.x) {
+        const bool extra = j == nv;
+        const double *vj = extra ? xv : V + (long long)j * ldv;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int e = tid;
+        for (; e + 768 < n; e += 1024) {
+            const double v0 = vj[e], v1 = vj[e + 256], v2 = vj[e + 512], v3 = vj[e + 768];
+            a0 = fma(v0, w[e], a0);
+            a1 = fma(v1, w[e + 256], a1);
+            a2 = fma(v2, w[e + 512], a2);
+            a3 = fma(v3, w[e + 768], a3);
+        }
+        for (; e < n; e += 256) a0 = fma(vj[e], w[e], a0);
+        double acc = (a0 + a1) + (a2 + a3);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) red[wid] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double t = red[0];
+            for (int q = 1; q < 8; ++q) t += red[q];
+            if (extra) {
+                *xout = sqrt(t);
+            } else {
+                out[j] = sq ? sqrt(t) : t;
+                if (gt.on && j == 0) givens_tail(gt);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // out[j] = (accumulate ? out[j] : 0) + sum_c partial[c * ldp + j]  (fixed order)
 // Sum of column j over the chunks in chunk order.  The loads are issued in
 // batches of 16 ahead of the (still sequential, so bitwise unchanged) adds: the
@@ -242,6 +288,39 @@ __global__ void __launch_bounds__(256) k_multiaxpy(const double *__restrict__ V,
     if (act) y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * acc;
 }
 
+// Small vectors (n <= kChunk): 32 elements per CTA, warp w sums the vectors
+// j = w, w + 8, ... for its lane's element, the 8 partials are added in warp
+// order (fixed; 8x the memory-level parallelism of one chain per element).
+__global__ void __launch_bounds__(256) k_multiaxpy_small(const double *__restrict__ V, long long ldv, int nv,
+                                                         const int *kdev, const double *__restrict__ c, double alpha,
+                                                         double beta, double *y, long long n) {
+    pdl_wait();
+    if (kdev) nv = min(*kdev + 1, nv);
+    __shared__ double part[8][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long e = (long long)blockIdx.x * 32 + lane;
+    double acc = 0.0;
+    if (e < n) {
+        int j = wid;
+        for (; j + 24 < nv; j += 32) {
+            const double v0 = V[(long long)j * ldv + e], v1 = V[(long long)(j + 8) * ldv + e];
+            const double v2 = V[(long long)(j + 16) * ldv + e], v3 = V[(long long)(j + 24) * ldv + e];
+            acc = fma(v0, c[j], acc);
+            acc = fma(v1, c[j + 8], acc);
+            acc = fma(v2, c[j + 16], acc);
+            acc = fma(v3, c[j + 24], acc);
+        }
+        for (; j < nv; j += 8) acc = fma(V[(long long)j * ldv + e], c[j], acc);
+    }
+    part[wid][lane] = acc;
+    __syncthreads();
+    if (wid == 0 && e < n) {
+        double t = part[0][lane];
+        for (int q = 1; q < 8; ++q) t += part[q][lane];
+        y[e] = (beta == 0.0 ? 0.0 : beta * y[e]) + alpha * t;
+    }
+}
+
 __global__ void k_sqrt(const double *in, double *out) { *out = sqrt(*in); }
 
 // y = x / (*s)
@@ -312,8 +391,9 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
     // device-side nv: cap the y extent (each warp loops over its vectors) so
     // that the mostly idle tail of a max_iter-sized grid stays small
     const int gy = kdev ? std::max(1, std::min(gy_full, (4 * 148 + d.nchunks - 1) / d.nchunks)) : gy_full;
-    if (d.nchunks == 1) {  // one chunk (2N <= 4096): the partial IS the result, no reduction launch
-        BIE_LAUNCH(k_multidot, dim3(1, gy), kDotThreads, 0, st, V, ldv, nv, kdev, w, n, out, 0, sq, xv, xout, gt);
+    if (d.nchunks == 1) {  // one chunk (2N <= 4096): one CTA per vector, no reduction launch
+        BIE_LAUNCH(k_multidot_small, std::min(ncap, 2 * 148), 256, 0, st, V, ldv, nv, kdev, w, (int)n, out, sq, xv,
+                   xout, gt);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
@@ -328,7 +408,10 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
 
 static int multiaxpy(const double *V, long long ldv, int nv, const double *c, double alpha, double beta, double *y,
                      long long n, cudaStream_t st, const int *kdev = nullptr) {
-    BIE_LAUNCH(k_multiaxpy, (unsigned)((n + 255) / 256), 256, 0, st, V, ldv, nv, kdev, c, alpha, beta, y, n);
+    if (n <= kChunk)
+        BIE_LAUNCH(k_multiaxpy_small, (unsigned)((n + 31) / 32), 256, 0, st, V, ldv, nv, kdev, c, alpha, beta, y, n);
+    else
+        BIE_LAUNCH(k_multiaxpy, (unsigned)((n + 255) / 256), 256, 0, st, V, ldv, nv, kdev, c, alpha, beta, y, n);
     count_launch();
     BIE_CUDA_TRY(cudaGetLastError());
     return BIE_OK;
