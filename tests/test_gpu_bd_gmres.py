@@ -461,3 +461,20 @@ def test_gmres_graph_cache_matches_host_loop(bie, monkeypatch):
     both(bie.gmres_solve_slp, bie.BlockDiag(g, op="slp"), tol=1e-8, max_iter=300)
     r_e = both(bie.gmres_solve, bd2, tol=1e-8, max_iter=200)
     assert np.array_equal(r_e["hist"], r_a["hist"])
+
+
+def test_gmres_zero_rhs(bie, monkeypatch):
+    """f = 0: converged at iteration 0 with x = 0 and zero residuals (the
+    beta = 0 exit before any iteration), in both loop forms."""
+    import torch
+
+    p = make_problem(2)
+    g = bie.Geometry.from_problem(p)
+    bd = bie.BlockDiag(g, structured=True)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BIE_GMRES_GRAPH", mode)
+        f = torch.zeros(2 * p.N, dtype=torch.float64, device="cuda")
+        x = torch.full_like(f, 7.0)
+        r = bie.gmres_solve(g, bd, f, x, tol=1e-8, max_iter=50)
+        assert r["converged"] and r["iters"] == 0 and r["res_true"] == 0.0 and r["res_pc"] == 0.0
+        assert torch.count_nonzero(x).item() == 0

@@ -275,3 +275,20 @@ def test_matvec_all_rows_parity(bie, cid):
     y = _gpu_apply(bie, g, s, 1)
     ref = og.apply(s)
     assert _relerr(y[0], ref[0]) <= TOL
+
+
+@pytest.mark.parametrize("cid", [2, 3])
+def test_power_of_two_scaling_bitwise(bie, cid):
+    """Degenerate magnitudes: the operator is linear and every step of the GPU
+    path (pair sums in fixed-point limbs whose window follows max |Q|, the
+    in-block sums, the completion terms) scales exactly by a power of two, so
+    A(2^k sigma) = 2^k A(sigma) BITWISE for k = +-300 -- and A(0) = 0 exactly."""
+    p = make_problem(cid)
+    g, _ = _setup(bie, p)
+    s = density(p, nvec=1)
+    a = _gpu_apply(bie, g, s, 1)
+    for k in (300, -300):
+        b = _gpu_apply(bie, g, np.ldexp(s, k), 1)
+        assert np.array_equal(np.ldexp(a, k), b), k
+    z = _gpu_apply(bie, g, np.zeros_like(s), 1)
+    assert np.array_equal(z, np.zeros_like(z))
