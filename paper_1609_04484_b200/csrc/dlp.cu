@@ -44,14 +44,16 @@ __device__ __forceinline__ double rcp_approx(double x) {
 
 // Branch-free log for the pair loops (the library log() carries special-case
 // branches that keep ptxas from interleaving independent pairs): a Tang-style
-// table reduction.  d = 2^e m, m in [1, 2); k = top 7 mantissa bits;
-// tab[k] = (rc_k, 1/2 log rc_k) with rc_k = RN(1 / (1 + (k + 1/2)/128)).
-// r = m rc_k - 1 (one FMA, |r| < 2^-8), log m = log1p(r) - log rc_k with
-// log1p(r) = r (1 - r/2 + ... - r^5/6) (truncation r^7/7 < 2^-58.8).  Returns
-// hl = -1/2 log d directly (scaled coefficients): 8 FP64 instructions, one
-// shared-memory lookup and an I2F.F64 for the exponent.  (Round 1 used 64
-// entries and a degree-7 series, 9 instructions; the 128-entry table saves one
-// FMA per pair in every SLP pair loop and completion field.)  With EX the
+// table reduction.  d = 2^e m, m in [1, 2); k = top 8 mantissa bits;
+// tab[k] = (rc_k, 1/2 log rc_k) with rc_k = RN(1 / (1 + (k + 1/2)/256)).
+// r = m rc_k - 1 (one FMA, |r| < 2^-9), log m = log1p(r) - log rc_k with
+// log1p(r) = r (1 - r/2 + ... + r^4/5) (truncation r^6/6 < 2^-56.6, below the
+// rounding of e ln2 + 1/2 log rc_k; offline check against 40-digit logs: the
+// same worst-case error as round 1's form).  Returns hl = -1/2 log d directly
+// (scaled coefficients): 7 FP64 instructions, one shared-memory lookup and an
+// I2F.F64 for the exponent.  (Round 1: 64 entries and a degree-7 series, 9
+// instructions; the 256-entry table saves two FMAs per pair in every SLP pair
+// loop and completion field.)  With EX the
 // exponent comes as a double from a second table indexed by the biased exponent
 // bits (an LDS instead of the I2F, which occupies the FP64 pipe; 16 KiB more
 // shared memory, worth it in the symmetric SLP kernel, but not in the one-sided
@@ -59,15 +61,15 @@ __device__ __forceinline__ double rcp_approx(double x) {
 // d must be positive and normal (pair distances are).
 template <bool EX>
 struct LogTabT {
-    double2 e[128];
+    double2 e[256];
     double ex[EX ? 2048 : 1];  // b - 1023 for biased exponent b
 };
 using LogTab = LogTabT<false>;
 using LogTabX = LogTabT<true>;
 template <bool EX>
 __device__ __forceinline__ void log_tab_init(LogTabT<EX> &t, int tid, int nthreads) {
-    for (int k = tid; k < 128; k += nthreads) {
-        const double rc = 1.0 / (1.0 + (k + 0.5) / 128.0);
+    for (int k = tid; k < 256; k += nthreads) {
+        const double rc = 1.0 / (1.0 + (k + 0.5) / 256.0);
         t.e[k] = make_double2(rc, 0.5 * log(rc));  // -1/2 log(1/rc) = 1/2 log rc
     }
     if constexpr (EX)
@@ -77,10 +79,9 @@ template <bool EX>
 __device__ __forceinline__ double neg_half_log_tab(double d, const LogTabT<EX> &t) {
     const int hi = __double2hiint(d), lo = __double2loint(d);
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-    const double2 tk = t.e[(hi >> 13) & 127];
+    const double2 tk = t.e[(hi >> 12) & 255];
     const double r = fma(m, tk.x, -1.0);
-    double q = 0.5 / 6.0;  // -1/2 (1 - r/2 + r^2/3 - r^3/4 + r^4/5 - r^5/6); the r^6 term is < 2^-58.8
-    q = fma(q, r, -0.5 / 5.0);
+    double q = -0.5 / 5.0;  // -1/2 (1 - r/2 + r^2/3 - r^3/4 + r^4/5); the r^5 term is < 2^-56.6
     q = fma(q, r, 0.5 / 4.0);
     q = fma(q, r, -0.5 / 3.0);
     q = fma(q, r, 0.5 / 2.0);
