@@ -901,8 +901,9 @@ __device__ __forceinline__ double2 pore_completion(double2 xi, const double4 *__
             const double nlg = neg_half_log_tab(rho2, ps.lt);  // -log rho
             const double rl = fma(rx, pm.x, ry * pm.y) * ir;    // (r . lambda/4pi) / rho^2
             const double mr = pm.z * ir;                         // r_k mu / rho^2
-            cc.x += fma(nlg, pm.x, fma(rl, rx, mr * ry));
-            cc.y += fma(nlg, pm.y, fma(rl, ry, -mr * rx));
+            // accumulated term by term (3 FMA per component, no DMUL/DADD)
+            cc.x = fma(mr, ry, fma(rl, rx, fma(nlg, pm.x, cc.x)));
+            cc.y = fma(-mr, rx, fma(rl, ry, fma(nlg, pm.y, cc.y)));
         };
         int q = 0;
         for (; q + ILP <= nk; q += ILP) {
