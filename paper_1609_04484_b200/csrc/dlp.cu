@@ -78,7 +78,10 @@ __device__ __forceinline__ void log_tab_init(LogTabT<EX> &t, int tid, int nthrea
 template <bool EX>
 __device__ __forceinline__ double neg_half_log_tab(double d, const LogTabT<EX> &t) {
     const int hi = __double2hiint(d), lo = __double2loint(d);
-    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    // (hi & 0x000fffff) | 0x3ff00000 as one LOP3 (the constant in a register)
+    int mhi;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x000fffff), "r"(0x3ff00000));
+    const double m = __hiloint2double(mhi, lo);
     const double2 tk = t.e[(hi >> 12) & 255];
     const double r = fma(m, tk.x, -1.0);
     double q = -0.5 / 5.0;  // -1/2 (1 - r/2 + r^2/3 - r^3/4 + r^4/5); the r^5 term is < 2^-56.6
@@ -88,7 +91,8 @@ __device__ __forceinline__ double neg_half_log_tab(double d, const LogTabT<EX> &
     q = fma(q, r, -0.5);
     // e ln2 with ln2 rounded to double: the error |e| 2.3e-17 stays below half an
     // ulp of e ln2 itself for every exponent a pair distance can have
-    const double e = EX ? t.ex[(hi >> 20) & 2047] : (double)((hi >> 20) - 1023);
+    // d > 0: hi >> 20 is the biased exponent (no sign bit to mask)
+    const double e = EX ? t.ex[hi >> 20] : (double)((hi >> 20) - 1023);
     const double base = fma(e, -0.5 * 0.69314718055994528623, tk.y);
     return fma(r, q, base);
 }
