@@ -115,7 +115,9 @@ BIE_API int bie_pore_template(int n, double *unit);
  * nvec in [1, BIE_MAX_NVEC].  flags: BIE_FULL or BIE_D_ONLY.
  * Errors: BIE_EINVAL (null, nvec out of range, out == sigma, bad flags),
  * BIE_ECUDA (launch error; asynchronous faults surface at the next sync).
- * Never synchronises.
+ * Does not synchronise, except when the geometry's workspace is allocated or
+ * grown (the first symmetric-path apply, or the first apply with a larger
+ * nvec / row range), which allocates it synchronously.
  */
 BIE_API int bie_dlp_apply(bie_geometry_t g, const double *sigma, double *out, int nvec, unsigned flags, void *stream);
 
