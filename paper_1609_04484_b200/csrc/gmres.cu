@@ -921,15 +921,25 @@ namespace bie {
 static int batched_op(Geometry *g, BlockDiag *bd, const double *in, double *tmp, double *out, int nv,
                       cudaStream_t st, unsigned opf) {
     const long long n = 2LL * g->N;
+    // Operator: groups of 4 / 8 / 16 vectors through the one-sided multi-vector
+    // kernels (11 + 2 + 4 nvec FP64 instructions per pair: 7.25 per vector at
+    // nvec = 4), a remainder of 1-3 vectors one at a time through the symmetric
+    // kernel (10.5 per vector; the one-sided nvec = 1 / 2 / 3 forms cost 16 / 10.5
+    // / 9.7 plus a second launch).  The BD apply takes the whole chunk.
     for (int v0 = 0; v0 < nv; v0 += BIE_MAX_NVEC) {
         const int c = std::min(BIE_MAX_NVEC, nv - v0);
+        const int cw = c - c % 4;
+        double *dst = bd ? tmp : out;
+        if (cw > 0) {
+            int rc = dlp_apply_impl(g, in + v0 * n, dst + v0 * n, cw, opf, 0, g->N, st);
+            if (rc) return rc;
+        }
+        for (int v = v0 + cw; v < v0 + c; ++v) {
+            int rc = dlp_apply_impl(g, in + v * n, dst + v * n, 1, opf, 0, g->N, st);
+            if (rc) return rc;
+        }
         if (bd) {
-            int rc = dlp_apply_impl(g, in + v0 * n, tmp + v0 * n, c, opf, 0, g->N, st);
-            if (rc) return rc;
-            rc = blockdiag_apply_impl(bd, tmp + v0 * n, out + v0 * n, c, st);
-            if (rc) return rc;
-        } else {
-            int rc = dlp_apply_impl(g, in + v0 * n, out + v0 * n, c, opf, 0, g->N, st);
+            int rc = blockdiag_apply_impl(bd, tmp + v0 * n, out + v0 * n, c, st);
             if (rc) return rc;
         }
     }
@@ -1005,14 +1015,22 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     // partials of all active systems + est[2][64] + act[64] (as ints)
     const long long psys = (long long)d.nchunks * ldh;
     GB_TRY(ensure(ws.partial, ws.partial_cap, (size_t)(nrhs * psys + 256)));
-    if (!ws.pinned) GB_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * 1024));  // 64 x 8 + est + act
+    // host lookahead (as bie_gmres_solve's host-enqueued form): iteration k is
+    // enqueued before the estimates of iteration k - kLookB are read; each of the
+    // kRingB in-flight iterations has its own active list / estimate slots
+    constexpr int kLookB = 3, kRingB = kLookB + 1;
+    GB_TRY(ensure(ws.partial, ws.partial_cap, (size_t)(nrhs * psys + kRingB * 192)));
+    // pinned: 64 x 8 per-system scalars + kRingB x (est [128] + act [64 ints])
+    if (!ws.pinned) GB_TRY(cudaMallocHost(&ws.pinned, sizeof(double) * (512 + kRingB * 192)));
+    for (int q = 0; q < kRingB; ++q)
+        if (!ws.evs[q]) GB_TRY(cudaEventCreateWithFlags(&ws.evs[q], cudaEventDisableTiming));
     double *V = ws.V, *Win = ws.w, *Wt = ws.w + (size_t)nrhs * n, *Wout = ws.w + 2 * (size_t)nrhs * n;
     double *H = ws.H, *small = ws.small, *pinned = ws.pinned;
     d.partial = ws.partial;
-    double *d_est = ws.partial + nrhs * psys;
-    int *d_act = reinterpret_cast<int *>(d_est + 128);
-    double *h_est = pinned + 512;
-    int *h_act = reinterpret_cast<int *>(pinned + 640);
+    auto d_est_slot = [&](int q) { return ws.partial + nrhs * psys + (long long)q * 192; };
+    auto d_act_slot = [&](int q) { return reinterpret_cast<int *>(d_est_slot(q) + 128); };
+    auto h_est_slot = [&](int q) { return pinned + 512 + (long long)q * 192; };
+    auto h_act_slot = [&](int q) { return reinterpret_cast<int *>(h_est_slot(q) + 128); };
     const long long sysV = (long long)ldh * n, Hsys = (long long)ldh * max_iter, scal_off = 5LL * ldh;
     GB_TRY(cudaMemsetAsync(H, 0, sizeof(double) * (size_t)nrhs * ldh * max_iter, st));
     GB_TRY(cudaMemsetAsync(small, 0, sizeof(double) * (size_t)nrhs * smallper, st));
@@ -1056,10 +1074,40 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
         GB_TRY(cudaMemcpyAsync(S[r].g, S[r].scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
     // Iteration: every vector operation of all active systems in one batched
-    // launch (blockIdx.z / y = slot), one D2H of the estimates, one sync.
-    const unsigned dot_y = (unsigned)((ldh + kDotThreads / 32 - 1) / (kDotThreads / 32));
-    for (int k = 0; k < max_iter && !active.empty(); ++k) {
+    // launch (blockIdx.z / y = slot), one D2H of the estimates.  The host reads
+    // iteration k's estimates after iteration k + kLookB is enqueued; a system
+    // found converged then has run up to kLookB speculative iterations, which
+    // touch only its entries beyond the ones its finish reads (as in the single
+    // solve), and leaves the active set from the next enqueued iteration on.
+    std::vector<std::vector<int>> ring_act(kRingB);
+    int processed = 0;  // iterations whose estimates have been read
+    auto process = [&](int kk) -> int {
+        const int sl = kk % kRingB;
+        GB_TRY(cudaEventSynchronize(ws.evs[sl]));
+        const double *he = h_est_slot(sl);
+        std::vector<int> keep;
+        for (size_t q = 0; q < ring_act[sl].size(); ++q) {
+            const int r = ring_act[sl][q];
+            if (converged[r]) continue;  // detected at an earlier iteration: speculative entry
+            const double est = he[2 * q];
+            const bool brk = he[2 * q + 1] != 0.0;
+            hist_host[(size_t)r * ldh + kk + 1] = est;
+            it[r] = kk + 1;
+            if (est < tol || brk) converged[r] = 1;
+        }
+        for (int r : active)
+            if (!converged[r]) keep.push_back(r);
+        active.swap(keep);
+        processed = kk + 1;
+        return BIE_OK;
+    };
+    int k = 0;
+    for (; k < max_iter && !active.empty(); ++k) {
+        const int sl = k % kRingB;
+        ring_act[sl] = active;
         const int na = (int)active.size();
+        int *h_act = h_act_slot(sl), *d_act = d_act_slot(sl);
+        double *d_est = d_est_slot(sl);
         for (int q = 0; q < na; ++q) h_act[q] = active[q];
         GB_TRY(cudaMemcpyAsync(d_act, h_act, sizeof(int) * na, cudaMemcpyHostToDevice, st));
         k_gather_b<<<dim3(eb, na), 256, 0, st>>>(V, sysV, (long long)k * n, Win, n, d_act);
@@ -1067,7 +1115,6 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
         GB_RC(batched_op(g, bd, Win, Wt, Wout, na, st, opf));
         const int nv = k + 1;
         const unsigned gy = (unsigned)((nv + kDotThreads / 32 - 1) / (kDotThreads / 32));
-        (void)dot_y;
         // w0 = ||w||
         k_multidot_b<<<dim3(d.nchunks, 1, na), kDotThreads, 0, st>>>(nullptr, 0, 0, 1, Wout, n, d.partial, d.ldp,
                                                                       psys, d_act, 1);
@@ -1090,28 +1137,17 @@ static int gmres_batch_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
                                                 d_act, 1);
         k_givens_b<<<(na + 63) / 64, 64, 0, st>>>(H, Hsys, small, smallper, ldh, k, d_act, na, d_est);
         count_launch(11);
-        GB_TRY(cudaMemcpyAsync(h_est, d_est, sizeof(double) * 2 * na, cudaMemcpyDeviceToHost, st));
+        GB_TRY(cudaMemcpyAsync(h_est_slot(sl), d_est, sizeof(double) * 2 * na, cudaMemcpyDeviceToHost, st));
         if (k + 1 < max_iter) {
             k_scale_b<<<dim3(eb, na), 256, 0, st>>>(Wout, n, V, sysV, (long long)(k + 1) * n, small, smallper,
                                                      scal_off, d_act);
             count_launch();
         }
         GB_TRY(cudaGetLastError());
-        GB_TRY(cudaStreamSynchronize(st));
-        std::vector<int> next;
-        for (int q = 0; q < na; ++q) {
-            const int r = active[q];
-            const double est = h_est[2 * q];
-            const bool brk = h_est[2 * q + 1] != 0.0;
-            hist_host[(size_t)r * ldh + k + 1] = est;
-            it[r] = k + 1;
-            if (est < tol || brk)
-                converged[r] = 1;
-            else
-                next.push_back(r);
-        }
-        active.swap(next);
+        GB_TRY(cudaEventRecord(ws.evs[sl], st));
+        if (k >= kLookB) GB_RC(process(k - kLookB));
     }
+    while (processed < k) GB_RC(process(processed));  // the iterations still in flight
     // finish: y = H^{-1} g, x = V y per system; residual pair with batched operators
     for (int r = 0; r < nrhs; ++r) {
         iters[r] = it[r];
