@@ -1165,28 +1165,39 @@ int build_schedules(Geometry *g) {
     return BIE_OK;
 }
 
-// Symmetric DLP kernel variants (BIE_SYM_VARIANT, A/B only): 0 = (8 targets
-// per lane, 2 warps, 2 sources per step, lockstep groups of 4, step loop
-// unrolled by 2) -- the default, fastest measured (12.73 ms at config 4);
-// 1 = (4, 4, 2) capped at 3 CTAs of 4 warps per SM (3 warps per SMSP).
-// Round 1-2 sweeps of the other shapes: DESIGN.md s5.
-static const int kNumSymVar = 2;
+// Symmetric DLP kernel variants (BIE_SYM_VARIANT, A/B only; the default is
+// chosen by size in sym_prepare): 0 = (8 targets per lane, 2 warps, 2 sources
+// per step in lockstep groups of 4 targets) register-capped at 6 CTAs per SM
+// (170 registers, no spills: 3 warps per SMSP) -- N >= 65536, 12.71 ms at
+// config 4; 2 = the same uncapped (249 registers, 2 warps per SMSP, step loop
+// unrolled by two) -- smaller N, where the capped form's 888 CTAs share too
+// few work units (config 2 BD-GMRES 3.77 vs 3.95 ms, config 3 127.5 vs
+// 129.2 ms; config 4 12.79 ms); 1 = (4, 4, 2) capped at 3 CTAs of 4 warps per
+// SM.  Round 1-2 sweeps of the other shapes: DESIGN.md s5.
+static const int kNumSymVar = 3;
 static void *sym_kernel(int v) {
     if (v == 1) return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3>);
-    return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2, 4>);
+    if (v == 2) return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 0, 2, 4>);
+    return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 6, 0, 1, 4>);
 }
 static int sym_warps(int v) { return v == 1 ? 4 : 2; }
 static void launch_sym(int v, int P, const SymArgs &sa, cudaStream_t st) {
     if (v == 1)
         BIE_LAUNCH((k_dlp_sym<4, 4, 2, 3>), P, 128, 0, st, sa);
-    else
+    else if (v == 2)
         BIE_LAUNCH((k_dlp_sym<8, 2, 2, 1, 0, 2, 4>), P, 64, 0, st, sa);
+    else
+        BIE_LAUNCH((k_dlp_sym<8, 2, 2, 6, 0, 1, 4>), P, 64, 0, st, sa);
+}
+static void *slp_sym_kernel(int v) {
+    if (v == 1) return reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3, 1>);
+    return reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 1>);
 }
 static void launch_sym_slp(int v, int P, const SymArgs &sa, cudaStream_t st) {
-    switch (v) {
-        case 1: BIE_LAUNCH((k_dlp_sym<4, 4, 2, 3, 1>), P, 128, 0, st, sa); break;
-        default: BIE_LAUNCH((k_dlp_sym<8, 2, 2, 1, 1>), P, 64, 0, st, sa); break;
-    }
+    if (v == 1)
+        BIE_LAUNCH((k_dlp_sym<4, 4, 2, 3, 1>), P, 128, 0, st, sa);
+    else
+        BIE_LAUNCH((k_dlp_sym<8, 2, 2, 1, 1>), P, 64, 0, st, sa);
 }
 
 // Segment size of the dynamic work distribution: about 8 segments per CTA
@@ -1227,6 +1238,7 @@ static int sym_prepare(Geometry *g) {
     const int N = g->N;
     const int nTB = (N + kSymTB - 1) / kSymTB;
     const long long nC = (N + kSymChunk - 1) / kSymChunk;
+    g->sym_variant = N >= 65536 ? 0 : 2;  // see sym_kernel
     if (const char *e = getenv("BIE_SYM_VARIANT")) g->sym_variant = std::max(0, std::min(kNumSymVar - 1, atoi(e)));  // tuning knob
     if (const char *e = getenv("BIE_SLP_SYM_VARIANT")) g->slp_sym_variant = std::max(0, std::min(1, atoi(e)));
     std::vector<long long> off(nTB + 1, 0);
@@ -1237,9 +1249,7 @@ static int sym_prepare(Geometry *g) {
     const long long U = off[nTB];
     for (int op = 0; op < 2; ++op) {
         int occ = 0;
-        void *k = op ? (g->slp_sym_variant == 1 ? reinterpret_cast<void *>(&k_dlp_sym<4, 4, 2, 3, 1>)
-                                                : reinterpret_cast<void *>(&k_dlp_sym<8, 2, 2, 1, 1>))
-                     : sym_kernel(g->sym_variant);
+        void *k = op ? slp_sym_kernel(g->slp_sym_variant) : sym_kernel(g->sym_variant);
         const int threads = op ? (g->slp_sym_variant == 1 ? 128 : 64) : 32 * sym_warps(g->sym_variant);
         BIE_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, 0));
         g->sym_occ[op] = std::max(1, occ);

@@ -167,7 +167,7 @@ struct Geometry {
     unsigned long long *sym_acc = nullptr;  // [3][2N] fixed-point limbs of the pair sums (dlp.cu fx_add)
     int sym_occ[2] = {1, 1};      // resident CTAs per SM of the DLP / SLP symmetric kernel
     double *sym_diag = nullptr;   // [2N]
-    int sym_nTB = 0, sym_P = 0, sym_variant = 0;  // (8, 2, 2), lockstep groups of 4, unrolled by 2: fastest measured
+    int sym_nTB = 0, sym_P = 0, sym_variant = 0;  // (8, 2, 2), lockstep groups of 4, 6 CTAs/SM: fastest measured
     int slp_sym_variant = 0;  // (8, 2, 2): fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
     unsigned long long *sym_counter = nullptr;  // [0] dynamic segment counter, [1] max |Q| bits (accumulation window)
