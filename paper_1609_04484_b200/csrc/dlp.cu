@@ -159,8 +159,8 @@ struct PairArgs {
 // 1/rho^2: MUFU.RCP64H seed + one cubic Newton step (3 DFMA, rel. err ~2^-60).
 // OP = 1: the single-layer operator instead (NEXT-1).  sigma then holds the
 // pre-scaled S_j = w_j sigma_j / (4 pi) and nw is unused.
-template <int NV, int R, int TS, int OP = 0>
-__global__ void __launch_bounds__(kPairThreads) k_dlp_pairs(PairArgs a) {
+template <int NV, int R, int TS, int OP = 0, int MINB = 1>
+__global__ void __launch_bounds__(kPairThreads, MINB) k_dlp_pairs(PairArgs a) {
     extern __shared__ double2 smem[];  // [2][(2 + NV) * TS]
     constexpr int NT = kPairThreads;
     constexpr int TB = NT * R;
@@ -1088,8 +1088,10 @@ __global__ void __launch_bounds__(128) k_epilogue(EpiArgs a) {
 
 template <int NV, int R, int TS>
 static void *pair_kernel_ptr(int op) {
-    return op ? reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS, 1>)
-              : reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS, 0>);
+    // nvec = 16: register cap of 4 CTAs per SM (128 registers, no spills; was 142 at
+    // 3 CTAs/SM): config-4 DLP nvec-16 kernel 100.9 -> 95.7 ms
+    return op ? reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS, 1, (NV == 16 ? 4 : 1)>)
+              : reinterpret_cast<void *>(&k_dlp_pairs<NV, R, TS, 0, (NV == 16 ? 4 : 1)>);
 }
 
 static void *variant_kernel(int idx, int op = 0) {
@@ -1309,7 +1311,7 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
             case 1: k_dlp_pairs<2, 2, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
             case 2: k_dlp_pairs<4, 4, 256, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
             case 3: k_dlp_pairs<8, 1, 128, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
-            default: k_dlp_pairs<16, 1, 64, 1><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+            default: k_dlp_pairs<16, 1, 64, 1, 4><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         }
         return;
     }
@@ -1318,7 +1320,7 @@ static void launch_pairs(int vi, const PairSched &s, const PairArgs &a, cudaStre
         case 1: k_dlp_pairs<2, 2, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         case 2: k_dlp_pairs<4, 4, 256><<<s.P, kPairThreads, s.smem, st>>>(a); break;
         case 3: k_dlp_pairs<8, 1, 128><<<s.P, kPairThreads, s.smem, st>>>(a); break;
-        default: k_dlp_pairs<16, 1, 64><<<s.P, kPairThreads, s.smem, st>>>(a); break;
+        default: k_dlp_pairs<16, 1, 64, 0, 4><<<s.P, kPairThreads, s.smem, st>>>(a); break;
     }
 }
 
