@@ -1403,17 +1403,30 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
                        g->sym_acc);
             count_launch();
         }
+        // The in-block pairs (k_dlp_diag) depend only on sigma / S: they run on a
+        // side stream forked here and joined before the epilogue, so their CTAs
+        // fill the SMs that the persistent pair kernel's tail leaves idle
+        // (fork/join events; inside the GMRES graph this becomes a parallel branch).
+        if (!g->side) {
+            BIE_CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+            BIE_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+            BIE_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+        }
+        BIE_CUDA_TRY(cudaEventRecord(g->ev_fork, st));
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
         int rc = sym_launch(g, 0, g->sym_U, op, st);
         if (rc) return rc;
+        BIE_CUDA_TRY(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
         if (op)
-            BIE_LAUNCH(k_dlp_diag<1>, 2 * g->sym_nTB * g->sym_dsplit, 128, 0, st, g->pos, g->nw, sigma, g->sym_diag,
-                       N, 0, g->sym_dsplit);
+            k_dlp_diag<1><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, g->side>>>(g->pos, g->nw, sigma, g->sym_diag, N,
+                                                                               0, g->sym_dsplit);
         else
-            BIE_LAUNCH(k_dlp_diag<0>, 2 * g->sym_nTB * g->sym_dsplit, 128, 0, st, g->pos, g->nw, sigma, g->sym_diag,
-                       N, 0, g->sym_dsplit);
+            k_dlp_diag<0><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, g->side>>>(g->pos, g->nw, sigma, g->sym_diag, N,
+                                                                               0, g->sym_dsplit);
         count_launch();
         BIE_CUDA_TRY(cudaGetLastError());
+        BIE_CUDA_TRY(cudaEventRecord(g->ev_join, g->side));
+        BIE_CUDA_TRY(cudaStreamWaitEvent(st, g->ev_join, 0));
         if (ev[2]) BIE_CUDA_TRY(cudaEventRecord(ev[2], st));
         ea.sym = SymEpi{1, g->sym_acc, g->sym_counter + 1, g->sym_diag, g->sym_dsplit};
     }

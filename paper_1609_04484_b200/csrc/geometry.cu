@@ -286,6 +286,9 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     if (g->gm.pinned) cudaFreeHost(g->gm.pinned);
     for (auto &ev : g->gm.evs)
         if (ev) cudaEventDestroy(ev);
+    if (g->side) cudaStreamDestroy(g->side);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    if (g->ev_join) cudaEventDestroy(g->ev_join);
     if (g->gm.gexec) cudaGraphExecDestroy(g->gm.gexec);
     if (g->gm.graph) cudaGraphDestroy(g->gm.graph);
     if (g->gm.cap) cudaStreamDestroy(g->gm.cap);

@@ -167,6 +167,8 @@ struct Geometry {
     unsigned long long *sym_acc = nullptr;  // [3][2N] fixed-point limbs of the pair sums (dlp.cu fx_add)
     int sym_occ[2] = {1, 1};      // resident CTAs per SM of the DLP / SLP symmetric kernel
     double *sym_diag = nullptr;   // [2N]
+    cudaStream_t side = nullptr;  // in-block kernel beside the pair kernel (fork/join by events)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int sym_nTB = 0, sym_P = 0, sym_variant = 0;  // (8, 2, 2), lockstep groups of 4, 6 CTAs/SM: fastest measured
     int slp_sym_variant = 0;  // (8, 2, 2): fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch
