@@ -1378,15 +1378,15 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         g->prof_used += 4;
         BIE_CUDA_TRY(cudaEventRecord(ev[0], st));
     }
-    if (full) {
+    EpiArgs ea{};
+    const bool sym = nvec == 1 && row_begin == 0 && row_end == N && !(flags & BIE_ONE_SIDED) &&
+                     sym_prepare(g) == BIE_OK && g->sym_state == 1;
+    if (full && !sym) {  // (symmetric path: on the side stream with the in-block kernel, below)
         count_launch();
         BIE_LAUNCH(k_moments, g->M + 1, 256, 0, st, g->pos, g->nrm, g->w, g->pore, sigma, stride, nvec, g->M,
                    g->n_pore, g->wall_lo, N, g->wall_len, g->moments);
         BIE_CUDA_TRY(cudaGetLastError());
     }
-    EpiArgs ea{};
-    const bool sym = nvec == 1 && row_begin == 0 && row_end == N && !(flags & BIE_ONE_SIDED) &&
-                     sym_prepare(g) == BIE_OK && g->sym_state == 1;
     if (sym) {
         int rc = sym_pre(g, st);
         if (rc) return rc;
@@ -1417,6 +1417,11 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         int rc = sym_launch(g, 0, g->sym_U, op, st);
         if (rc) return rc;
         BIE_CUDA_TRY(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
+        if (full) {  // the completion moments, read only by the epilogue
+            k_moments<<<g->M + 1, 256, 0, g->side>>>(g->pos, g->nrm, g->w, g->pore, sigma_in, stride, nvec, g->M,
+                                                       g->n_pore, g->wall_lo, N, g->wall_len, g->moments);
+            count_launch();
+        }
         if (op)
             k_dlp_diag<1><<<2 * g->sym_nTB * g->sym_dsplit, 128, 0, g->side>>>(g->pos, g->nw, sigma, g->sym_diag, N,
                                                                                0, g->sym_dsplit);
