@@ -1407,11 +1407,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
         // side stream forked here and joined before the epilogue, so their CTAs
         // fill the SMs that the persistent pair kernel's tail leaves idle
         // (fork/join events; inside the GMRES graph this becomes a parallel branch).
-        if (!g->side) {
-            BIE_CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
-            BIE_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
-            BIE_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
-        }
+        BIE_RC_TRY(ensure_side_stream(g));
         BIE_CUDA_TRY(cudaEventRecord(g->ev_fork, st));
         if (ev[1]) BIE_CUDA_TRY(cudaEventRecord(ev[1], st));
         int rc = sym_launch(g, 0, g->sym_U, op, st);

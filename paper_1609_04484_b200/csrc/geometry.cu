@@ -18,6 +18,14 @@ static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 static std::atomic<unsigned long long> g_bd_serial{0};
 unsigned long long next_bd_serial() { return ++g_bd_serial; }
+int ensure_side_stream(Geometry *g) {
+    if (g->side) return BIE_OK;
+    BIE_CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+    BIE_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+    BIE_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+    return BIE_OK;
+}
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char *e = getenv("BIE_PDL");

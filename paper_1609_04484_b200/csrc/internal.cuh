@@ -257,5 +257,7 @@ int dlp_apply_impl(Geometry *g, const double *sigma, double *out, int nvec, unsi
 int build_schedules(Geometry *g);
 // blockdiag.cu
 int blockdiag_apply_impl(BlockDiag *bd, const double *in, double *out, int nvec, cudaStream_t s);
+// geometry.cu: the side stream and fork/join events of g (created on first use)
+int ensure_side_stream(Geometry *g);
 // gmres.cu kernels used by other units
 }  // namespace bie
