@@ -31,7 +31,8 @@
 namespace bie {
 
 constexpr int kChunk = 4096;      // elements of the 2N dimension per multidot CTA
-constexpr int kDotThreads = 128;  // 4 basis vectors share one staged w chunk
+constexpr int kDotThreads = 128;  // 4 basis vectors share one staged w chunk (batched kernels)
+constexpr int kDotThreads1 = 256;  // k_multidot: 8 warps share the staged chunk (occupancy, round 2)
 
 struct GmState {
     double *H;      // column-major: H[k * ldh + j], ldh = max_iter + 1
@@ -124,36 +125,37 @@ __device__ __forceinline__ void givens_tail(const GivensTail &t) {
 // of a separate norm launch); single chunk: sqrt of it goes to xout.
 // gt.on (single chunk, nv = 1): the thread that stores the norm then runs the
 // Givens step (givens_tail).
-__global__ void __launch_bounds__(kDotThreads) k_multidot(const double *__restrict__ V, long long ldv, int nv,
+__global__ void __launch_bounds__(kDotThreads1, 3) k_multidot(const double *__restrict__ V, long long ldv, int nv,
                                                           const int *kdev, const double *__restrict__ w, long long n,
                                                           double *partial, int ldp, int sq, const double *xv,
                                                           double *xout, GivensTail gt) {
     pdl_wait();
     if (kdev) nv = min(*kdev + 1, nv);
     const int ntot = nv + (xv ? 1 : 0);
-    if ((int)blockIdx.y * (kDotThreads / 32) >= ntot) return;
+    if ((int)blockIdx.y * (kDotThreads1 / 32) >= ntot) return;
     __shared__ double ws[kChunk];
     const long long e0 = (long long)blockIdx.x * kChunk;
     const int len = (int)std::min<long long>(kChunk, n - e0);
-    for (int q = threadIdx.x; q < kChunk; q += kDotThreads) ws[q] = q < len ? w[e0 + q] : 0.0;
+    for (int q = threadIdx.x; q < kChunk; q += kDotThreads1) ws[q] = q < len ? w[e0 + q] : 0.0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int j = blockIdx.y * (kDotThreads / 32) + wid; j < ntot; j += gridDim.y * (kDotThreads / 32)) {
+    for (int j = blockIdx.y * (kDotThreads1 / 32) + wid; j < ntot; j += gridDim.y * (kDotThreads1 / 32)) {
         const bool extra = j == nv;
         const double *vj = (extra ? xv : V + (long long)j * ldv) + e0;
-        // four independent streams per lane keep enough loads in flight for HBM
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+        // eight independent streams per lane: ~16 warps per SM with 4 loads each
+        // in flight left the kernel latency-bound at 0.70 of the HBM bandwidth
+        // (ncu, profiles/round2/gmres_vec_r2_summary.txt)
+        double ac[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         int q = lane;
-        for (; q + 96 < len; q += 128) {
-            const double a0 = __ldcs(vj + q), a1 = __ldcs(vj + q + 32), a2 = __ldcs(vj + q + 64),
-                         a3 = __ldcs(vj + q + 96);
-            acc0 = fma(a0, ws[q], acc0);
-            acc1 = fma(a1, ws[q + 32], acc1);
-            acc2 = fma(a2, ws[q + 64], acc2);
-            acc3 = fma(a3, ws[q + 96], acc3);
+        for (; q + 224 < len; q += 256) {
+            double a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = __ldcs(vj + q + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ac[u] = fma(a[u], ws[q + 32 * u], ac[u]);
         }
-        for (; q < len; q += 32) acc0 = fma(vj[q], ws[q], acc0);
-        double acc = (acc0 + acc1) + (acc2 + acc3);
+        for (; q < len; q += 32) ac[0] = fma(vj[q], ws[q], ac[0]);
+        double acc = ((ac[0] + ac[1]) + (ac[2] + ac[3])) + ((ac[4] + ac[5]) + (ac[6] + ac[7]));
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         BIE_DCHECK(j < ldp || gridDim.x == 1);
         if (lane == 0) {
@@ -387,10 +389,10 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
                     cudaStream_t st, const int *kdev = nullptr, int sq = 0, const double *xv = nullptr,
                     double *xout = nullptr, const GivensTail &gt = GivensTail{}) {
     const int ncap = nv + (xv ? 1 : 0);
-    const int gy_full = (ncap + kDotThreads / 32 - 1) / (kDotThreads / 32);
+    const int gy_full = (ncap + kDotThreads1 / 32 - 1) / (kDotThreads1 / 32);
     // device-side nv: cap the y extent (each warp loops over its vectors) so
     // that the mostly idle tail of a max_iter-sized grid stays small
-    const int gy = kdev ? std::max(1, std::min(gy_full, (4 * 148 + d.nchunks - 1) / d.nchunks)) : gy_full;
+    const int gy = kdev ? std::max(1, std::min(gy_full, (8 * 148 + d.nchunks - 1) / d.nchunks)) : gy_full;
     if (d.nchunks == 1) {  // one chunk (2N <= 4096): one CTA per vector, no reduction launch
         BIE_LAUNCH(k_multidot_small, std::min(ncap, 2 * 148), 256, 0, st, V, ldv, nv, kdev, w, (int)n, out, sq, xv,
                    xout, gt);
@@ -398,7 +400,7 @@ static int multidot(const double *V, long long ldv, int nv, const double *w, lon
         BIE_CUDA_TRY(cudaGetLastError());
         return BIE_OK;
     }
-    BIE_LAUNCH(k_multidot, dim3(d.nchunks, gy), kDotThreads, 0, st, V, ldv, nv, kdev, w, n, d.partial, d.ldp, 0, xv,
+    BIE_LAUNCH(k_multidot, dim3(d.nchunks, gy), kDotThreads1, 0, st, V, ldv, nv, kdev, w, n, d.partial, d.ldp, 0, xv,
                xout, GivensTail{});
     BIE_LAUNCH(k_reduce, (ncap + 127) / 128, 128, 0, st, d.partial, d.ldp, d.nchunks, nv, kdev, out, 0, sq, xout, gt);
     count_launch(2);
