@@ -782,6 +782,7 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
     BIE_CUDA_TRY(cudaMemcpyAsync(s.g, s.scal + 0, sizeof(double), cudaMemcpyDeviceToDevice, st));
     int it = 0;
     bool conv = false;
+    use_graph = use_graph && !ws.graph_off;
     if (use_graph) {
         const GmGraphKey key{bd, bd ? bd->serial : 0, opf, max_iter, tol, V, w, ws.small, ws.partial, g->partial,
                              g->slp_s};
@@ -793,29 +794,55 @@ static int gmres_solve_impl(const char *fn, unsigned opf, bie_geometry_t gh, bie
             // buffers the apply allocates lazily must exist before the capture
             BIE_RC_TRY(apply_op(vcur, w, st));
             if (!ws.cap) BIE_CUDA_TRY(cudaStreamCreateWithFlags(&ws.cap, cudaStreamNonBlocking));
-            BIE_CUDA_TRY(cudaGraphCreate(&ws.graph, 0));
-            cudaGraphConditionalHandle cond;
-            BIE_CUDA_TRY(cudaGraphConditionalHandleCreate(&cond, ws.graph, 1, cudaGraphCondAssignDefault));
-            cudaGraphNodeParams cp{};
-            cp.type = cudaGraphNodeTypeConditional;
-            cp.conditional.handle = cond;
-            cp.conditional.type = cudaGraphCondTypeWhile;
-            cp.conditional.size = 1;
-            cudaGraphNode_t node;
-            BIE_CUDA_TRY(cudaGraphAddNode(&node, ws.graph, nullptr, 0, &cp));
-            cudaGraph_t bg = cp.conditional.phGraph_out[0];
-            BIE_CUDA_TRY(cudaStreamBeginCaptureToGraph(ws.cap, bg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-            const long long c0 = bie_launch_count();
-            const int rb = body(ws.cap, cond, 1);
-            cudaGraph_t cap_out = nullptr;
-            const cudaError_t ce = cudaStreamEndCapture(ws.cap, &cap_out);
-            ws.body_launches = bie_launch_count() - c0;
-            count_launch(-(int)ws.body_launches);  // counted per executed iteration below
-            if (rb != BIE_OK) return rb;
-            BIE_CUDA_TRY(ce);
-            BIE_CUDA_TRY(cudaGraphInstantiate(&ws.gexec, ws.graph, 0));
-            ws.gkey = key;
+            // a driver without conditional graph nodes (or any capture failure)
+            // falls back to the host-enqueued loop for this geometry: same kernels
+            bool capturing = false;
+            auto capture = [&]() -> cudaError_t {
+                cudaError_t e = cudaGraphCreate(&ws.graph, 0);
+                if (e != cudaSuccess) return e;
+                cudaGraphConditionalHandle cond;
+                if ((e = cudaGraphConditionalHandleCreate(&cond, ws.graph, 1, cudaGraphCondAssignDefault))) return e;
+                cudaGraphNodeParams cp{};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = cond;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t node;
+                if ((e = cudaGraphAddNode(&node, ws.graph, nullptr, 0, &cp))) return e;
+                cudaGraph_t bg = cp.conditional.phGraph_out[0];
+                if ((e = cudaStreamBeginCaptureToGraph(ws.cap, bg, nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeRelaxed)))
+                    return e;
+                capturing = true;
+                const long long c0 = bie_launch_count();
+                const int rb = body(ws.cap, cond, 1);
+                cudaGraph_t cap_out = nullptr;
+                e = cudaStreamEndCapture(ws.cap, &cap_out);
+                capturing = false;
+                ws.body_launches = bie_launch_count() - c0;
+                count_launch(-(int)ws.body_launches);  // counted per executed iteration below
+                if (rb != BIE_OK) return cudaErrorUnknown;
+                if (e != cudaSuccess) return e;
+                return cudaGraphInstantiate(&ws.gexec, ws.graph, 0);
+            };
+            if (capture() != cudaSuccess) {
+                if (capturing) {
+                    cudaGraph_t dummy = nullptr;
+                    cudaStreamEndCapture(ws.cap, &dummy);
+                }
+                (void)cudaGetLastError();
+                if (ws.gexec) cudaGraphExecDestroy(ws.gexec);
+                if (ws.graph) cudaGraphDestroy(ws.graph);
+                ws.gexec = nullptr;
+                ws.graph = nullptr;
+                ws.graph_off = true;
+                use_graph = false;
+            } else {
+                ws.gkey = key;
+            }
         }
+    }
+    if (use_graph) {
         BIE_CUDA_TRY(cudaGraphLaunch(ws.gexec, st));
         BIE_CUDA_TRY(cudaMemcpyAsync(pinned + 1, ctl, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         BIE_CUDA_TRY(cudaStreamSynchronize(st));

@@ -129,6 +129,7 @@ struct GmresWork {
     cudaGraphExec_t gexec = nullptr;
     GmGraphKey gkey;
     long long body_launches = 0;  // kernels per iteration of the graph body
+    bool graph_off = false;       // capture failed once: host-enqueued loop from then on
 };
 
 struct Geometry {
