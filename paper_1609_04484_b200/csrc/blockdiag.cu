@@ -537,6 +537,38 @@ __global__ void k_swap(BDView v, BDScratch s, int k0, int nbe, double *TS = null
     }
 }
 
+// k_swap over a column subset (the lookahead schedule of the delayed update):
+// M columns [c0, c1) except [skip0, skip1), then the first tsw columns of TS.
+// Swaps of different columns are independent, so a super-panel's nk swaps may
+// reach the columns outside its slab later, in one launch, in the same order.
+__global__ void k_swap_rng(BDView v, BDScratch s, int k0, int nk, int c0, int c1, int skip0, int skip1,
+                           double *TS, int tsw) {
+    const int n2 = v.n2;
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    double *base;
+    long long ld;
+    if (t < c1 - c0) {
+        const int col = c0 + t;
+        if (col >= skip0 && col < skip1) return;
+        base = v.mat + col;
+        ld = n2;
+    } else {
+        t -= c1 - c0;
+        if (t >= tsw) return;
+        base = TS + t;
+        ld = kSB;
+    }
+    const int *piv = s.piv;
+    for (int c = 0; c < nk; ++c) {
+        const int k = k0 + c, p = piv[k];
+        if (p != k) {
+            const double x = base[(long long)k * ld];
+            base[(long long)k * ld] = base[(long long)p * ld];
+            base[(long long)p * ld] = x;
+        }
+    }
+}
+
 // T = M[:, K]; with TS: also T-hat = T - E_K (identity on the pivot rows K)
 // into columns [tcol, tcol + NB) of TS -- the sub-panel's column of the
 // aggregated update (k_update_agg).
@@ -666,8 +698,12 @@ __device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, do
 constexpr int UT3 = 64;
 __global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k0, int nbe, int jlo = 0,
                                                    int jhi = 1 << 30) {
-    __shared__ double Ts[UT3][NB + 1];  // Ts[i][c] = T[i0 + i][c]
-    __shared__ double Gs[NB][UT3 + 1];  // Gs[c][j] = G[c][j0 + j]
+    // row strides = 4 (mod 16) doubles: the DMMA fragment reads (lane (gr, gq) reads
+    // Ts[.. + gr][.. + gq] and Gs[.. + gq][.. + gr]) then touch 16 distinct 8-byte bank
+    // pairs per half-warp; with the +1 padding of round 1 they were 4-way conflicts
+    // (8 wavefronts per LDS.64, and the kernels were bound by shared-memory bandwidth)
+    __shared__ double Ts[UT3][NB + 4];  // Ts[i][c] = T[i0 + i][c]
+    __shared__ double Gs[NB][UT3 + 4];  // Gs[c][j] = G[c][j0 + j]
     const int m = blockIdx.z;
     const int n2 = v.n2;
     const int jend = min(n2, jhi);  // column bound of this launch
@@ -773,36 +809,63 @@ __global__ void __launch_bounds__(128, 4) k_update3(BDView v, BDScratch s, int k
 // the later sub-panels' swaps (k_swap swaps TS with M), so the algebra is the
 // sequential one; only the rounding order of the updates differs.
 
-// y for every column j outside S: one thread per column, Y[kSB][n2] row-major.
+// y for every column j outside S, Y[kSB][n2] row-major.  A CTA takes 32 columns
+// (lanes) x 4 row groups (warps; 8 of a sub-panel's NB pivot rows each): the
+// round-2 one-thread-per-column form left under one warp per scheduler with 253
+// registers and was latency-bound (0.215 ms per super-panel, on the lookahead's
+// critical path).  Same sums in the same order, so Y is bitwise unchanged.
+constexpr int kYCols = 32;
 __global__ void __launch_bounds__(128) k_make_Y(BDView v, const double *__restrict__ TS,
                                                 const double *__restrict__ A11S, double *Y, int s0, int sbe,
                                                 int nsub) {
+    __shared__ double s_acc[NB][kYCols + 1];
+    __shared__ double s_A[NB][NB + 1];
     const int n2 = v.n2;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n2 - sbe) return;
-    const int j = t < s0 ? t : t + sbe;
+    const int lane = threadIdx.x & 31, rg = threadIdx.x >> 5;
+    const int t = blockIdx.x * kYCols + lane;
+    const bool ok = t < n2 - sbe;
+    const int j = ok ? (t < s0 ? t : t + sbe) : 0;
     const double *M = v.mat;
     for (int p = 0; p < nsub; ++p) {
         const int k0 = s0 + p * NB, nbe = min(NB, n2 - k0);
-        double acc[NB];
+        for (int q = threadIdx.x; q < NB * NB; q += 128) s_A[q / NB][q % NB] = A11S[(long long)p * NB * NB + q];
+        double acc[8];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) acc[c] = c < nbe ? M[(long long)(k0 + c) * n2 + j] : 0.0;
+        for (int i = 0; i < 8; ++i) {
+            const int c = rg * 8 + i;
+            acc[i] = (ok && c < nbe) ? M[(long long)(k0 + c) * n2 + j] : 0.0;
+        }
         for (int q = 0; q < p; ++q) {
-#pragma unroll 4
+#pragma unroll 8
             for (int cc = 0; cc < NB; ++cc) {
-                const double y = Y[(long long)(q * NB + cc) * n2 + j];
+                const double y = ok ? Y[(long long)(q * NB + cc) * n2 + j] : 0.0;
 #pragma unroll
-                for (int c = 0; c < NB; ++c) acc[c] = fma(-__ldg(TS + (long long)(k0 + c) * kSB + q * NB + cc), y, acc[c]);
+                for (int i = 0; i < 8; ++i)
+                    acc[i] = fma(-__ldg(TS + (long long)(k0 + rg * 8 + i) * kSB + q * NB + cc), y, acc[i]);
             }
         }
-        const double *A = A11S + (long long)p * NB * NB;
-        for (int c = 0; c < NB; ++c) {
-            double y = 0.0;
 #pragma unroll
-            for (int cc = 0; cc < NB; ++cc)
-                if (cc < nbe) y = fma(__ldg(A + c * NB + cc), acc[cc], y);  // A11i is nbe x nbe
-            Y[(long long)(p * NB + c) * n2 + j] = c < nbe ? y : 0.0;
+        for (int i = 0; i < 8; ++i) s_acc[rg * 8 + i][lane] = acc[i];
+        __syncthreads();
+        double y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = 0.0;
+#pragma unroll 4
+        for (int cc = 0; cc < NB; ++cc) {
+            if (cc < nbe) {  // A11i is nbe x nbe
+                const double a = s_acc[cc][lane];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) y[i] = fma(s_A[rg * 8 + i][cc], a, y[i]);
+            }
         }
+        if (ok) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int c = rg * 8 + i;
+                Y[(long long)(p * NB + c) * n2 + j] = c < nbe ? y[i] : 0.0;
+            }
+        }
+        __syncthreads();  // Y of this sub-panel visible to the CTA's other warps; s_acc / s_A reusable
     }
 }
 
@@ -811,8 +874,8 @@ __global__ void __launch_bounds__(128) k_make_Y(BDView v, const double *__restri
 // looped in NB chunks through the same shared-memory tiles.
 __global__ void __launch_bounds__(128, 3) k_update_agg(BDView v, const double *__restrict__ TS,
                                                        const double *__restrict__ Y, int s0, int sbe, int nsub) {
-    __shared__ double Ts[UT3][NB + 1];
-    __shared__ double Gs[NB][UT3 + 1];
+    __shared__ double Ts[UT3][NB + 4];  // strides = 4 (mod 16): conflict-free fragment reads (k_update3)
+    __shared__ double Gs[NB][UT3 + 4];
     const int n2 = v.n2;
     const int i0 = blockIdx.y * UT3, j0 = blockIdx.x * UT3;
     if (j0 >= s0 && j0 < s0 + sbe) return;  // the slab is final (s0, sbe multiples of UT3)
@@ -881,6 +944,99 @@ __global__ void __launch_bounds__(128, 3) k_update_agg(BDView v, const double *_
         for (int j = 0; j < 4; ++j) {
             const int gj = j0 + wc + 8 * j + 2 * gq;
             if (gj >= n2) continue;
+            __stcs(reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj),
+                   make_double2(base[i][j].x - acc[i][j][0], base[i][j].y - acc[i][j][1]));
+        }
+    }
+}
+
+// k_update_agg with the K chunks staged by cp.async into double-buffered shared
+// memory (the default; the register-staged kernel above is the A/B alternative,
+// BIE_BD_AGGK=0): chunk p + 1 streams in while chunk p feeds the DMMAs, so a CTA
+// no longer idles through a global-load round trip per chunk.  n2 % UT3 == 0
+// (checked by the caller), so there are no ragged tiles.
+__device__ __forceinline__ void bd_cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+constexpr int kAggTsLd = NB + 4, kAggGsLd = UT3 + 4;  // doubles; = 4 (mod 16), rows 16-byte aligned
+constexpr int kAggStage = UT3 * kAggTsLd + NB * kAggGsLd;  // doubles per stage
+constexpr size_t kAggSmem = sizeof(double) * 2 * kAggStage;
+__global__ void __launch_bounds__(128, 3) k_update_agg_async(BDView v, const double *__restrict__ TS,
+                                                             const double *__restrict__ Y, int s0, int sbe,
+                                                             int nsub, int jt0 = 0, int x0 = -1, int x1 = -1) {
+    extern __shared__ __align__(16) double agg_smem[];
+    const int n2 = v.n2;
+    const int i0 = blockIdx.y * UT3, j0 = (jt0 + blockIdx.x) * UT3;
+    if (j0 >= s0 && j0 < s0 + sbe) return;  // the slab is final (s0, sbe multiples of UT3)
+    if (j0 >= x0 && j0 < x1) return;        // columns another launch of this update covers (lookahead)
+    double *M = v.mat;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int wr = (wid >> 1) * 32, wc = (wid & 1) * 32;
+    const int gr = lane >> 2, gq = lane & 3;
+    auto stage = [&](int buf, int p) {
+        double *Ts = agg_smem + buf * kAggStage, *Gs = Ts + UT3 * kAggTsLd;
+        // Ts: 64 rows x 32 doubles = 64 x 16 pieces of 16 B; Gs: 32 rows x 64 doubles = 32 x 32 pieces
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = tid + 128 * r;
+            const int i = q >> 4, c = (q & 15) * 2;
+            bd_cp_async16(Ts + i * kAggTsLd + c, TS + (long long)(i0 + i) * kSB + p * NB + c);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = tid + 128 * r;
+            const int c = q >> 5, j = (q & 31) * 2;
+            bd_cp_async16(Gs + c * kAggGsLd + j, Y + (long long)(p * NB + c) * n2 + j0 + j);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    stage(0, 0);
+    for (int p = 0; p < nsub; ++p) {
+        if (p + 1 < nsub) {
+            stage((p + 1) & 1, p + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double *Ts = agg_smem + (p & 1) * kAggStage, *Gs = Ts + UT3 * kAggTsLd;
+#pragma unroll
+        for (int kk = 0; kk < NB / 4; ++kk) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = Ts[(wr + 8 * i + gr) * kAggTsLd + kk * 4 + gq];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Gs[(kk * 4 + gq) * kAggGsLd + wc + 8 * j + gr];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        __syncthreads();  // this stage is overwritten by the fetch of chunk p + 2
+    }
+    double2 base[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gi = i0 + wr + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gj = j0 + wc + 8 * j + 2 * gq;
+            base[i][j] = __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gi = i0 + wr + 8 * i + gr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gj = j0 + wc + 8 * j + 2 * gq;
             __stcs(reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj),
                    make_double2(base[i][j].x - acc[i][j][0], base[i][j].y - acc[i][j][1]));
         }
@@ -1044,10 +1200,17 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     int agg_mode = 2;
     if (const char *e = getenv("BIE_BD_AGG")) agg_mode = std::max(0, std::min(1, atoi(e)));
     const bool agg = coop && n2 % UT3 == 0 && (agg_mode == 1 || (agg_mode == 2 && n2 >= 8192));
+    // BIE_BD_AGGK: 1 (default) cp.async double-buffered sweep, 0 register-staged (A/B)
+    bool agg_async = true;
+    if (const char *e = getenv("BIE_BD_AGGK")) agg_async = atoi(e) != 0;
     if (agg) {
-        BIE_CUDA_TRY(cudaMallocAsync(&TS, sizeof(double) * (size_t)n2 * kSB, st));
-        BIE_CUDA_TRY(cudaMallocAsync(&Yb, sizeof(double) * (size_t)n2 * kSB, st));
-        BIE_CUDA_TRY(cudaMallocAsync(&A11S, sizeof(double) * 4 * NB * NB, st));
+        BIE_CUDA_TRY(cudaFuncSetAttribute(k_update_agg_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kAggSmem));
+        // two parities: with the lookahead, super-panel S + 1 fills one set while the
+        // sweep of S reads the other
+        BIE_CUDA_TRY(cudaMallocAsync(&TS, sizeof(double) * 2 * (size_t)n2 * kSB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&Yb, sizeof(double) * 2 * (size_t)n2 * kSB, st));
+        BIE_CUDA_TRY(cudaMallocAsync(&A11S, sizeof(double) * 2 * 4 * NB * NB, st));
     }
     auto panel = [&](int k0, int nbe) -> int {
         if (coop) {
@@ -1062,7 +1225,89 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         }
         return BIE_OK;
     };
-    if (agg) {
+    // Lookahead (BIE_BD_LOOKAHEAD, default on with the cp.async sweep): the sub-panels of
+    // super-panel S + 1 are factored on a high-priority stream while the rank-kSB sweep of
+    // S still runs over the columns outside both slabs.  Per super-panel:
+    //   hp: A(S)  = sub-panel LUs, swaps / G / rank-NB updates restricted to the slab (+ T-hat);
+    //       wait for the previous sweep; swaps of S on the columns outside the slab;
+    //       Y(S); sweep of S on slab S + 1 only;
+    //   st: sweep of S on every other column (reads TS/Y of parity S & 1).
+    // The cooperative panel's CTAs take the SM slots the sweep's CTAs free as they retire.
+    bool lookahead = agg_async;
+    if (const char *e = getenv("BIE_BD_LOOKAHEAD")) lookahead = lookahead && atoi(e) != 0;
+    if (agg && lookahead) {
+        cudaStream_t hp = nullptr;
+        cudaEvent_t ev_y = nullptr, ev_b2 = nullptr, ev_f = nullptr;
+        int pr_lo = 0, pr_hi = 0;
+        BIE_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&pr_lo, &pr_hi));
+        BIE_CUDA_TRY(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, pr_hi));
+        BIE_CUDA_TRY(cudaEventCreateWithFlags(&ev_y, cudaEventDisableTiming));
+        BIE_CUDA_TRY(cudaEventCreateWithFlags(&ev_b2, cudaEventDisableTiming));
+        BIE_CUDA_TRY(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming));
+        auto cleanup = [&]() {
+            cudaStreamSynchronize(hp);
+            cudaStreamDestroy(hp);
+            cudaEventDestroy(ev_y);
+            cudaEventDestroy(ev_b2);
+            cudaEventDestroy(ev_f);
+        };
+        int rc = [&]() -> int {
+            BIE_CUDA_TRY(cudaEventRecord(ev_f, st));
+            BIE_CUDA_TRY(cudaStreamWaitEvent(hp, ev_f, 0));
+            BIE_CUDA_TRY(cudaEventRecord(ev_b2, st));  // "previous sweep done" for the first super-panel
+            const int nt = n2 / UT3;
+            for (int s0 = 0, S = 0; s0 < n2; s0 += kSB, ++S) {
+                const int sbe = std::min(kSB, n2 - s0), nsub = (sbe + NB - 1) / NB;
+                double *TSb = TS + (size_t)(S & 1) * n2 * kSB, *Ybb = Yb + (size_t)(S & 1) * n2 * kSB;
+                double *A11b = A11S + (size_t)(S & 1) * 4 * NB * NB;
+                for (int p = 0; p < nsub; ++p) {
+                    int k0 = s0 + p * NB, nbe = std::min(NB, n2 - k0);
+                    {
+                        int G = (n2 - k0 + 128 * rpt - 1) / (128 * rpt);
+                        void *args[] = {&v, &s, &cs, &k0, &nbe};
+                        BIE_CUDA_TRY(cudaLaunchCooperativeKernel(coop_kernel, G, 128, args, 0, hp));
+                    }
+                    k_swap_rng<<<(sbe + p * NB + 127) / 128, 128, 0, hp>>>(v, s, k0, nbe, s0, s0 + sbe, -1, -1, TSb,
+                                                                           p * NB);
+                    k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), 1), 256, 0, hp>>>(v, s, k0, nbe,
+                                                                                                  TSb, p * NB);
+                    BIE_CUDA_TRY(cudaMemcpyAsync(A11b + p * NB * NB, s.A11i, sizeof(double) * NB * NB,
+                                                 cudaMemcpyDeviceToDevice, hp));
+                    k_make_G<<<dim3((sbe + 127) / 128, 1), 128, 0, hp>>>(v, s, k0, nbe, s0, s0 + sbe);
+                    k_update3<<<dim3((sbe + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3, 1), 128, 0, hp>>>(v, s, k0, nbe,
+                                                                                                 s0, s0 + sbe);
+                    count_launch(5);
+                    BIE_CUDA_TRY(cudaGetLastError());
+                }
+                if (n2 > sbe) {
+                    const int s1 = s0 + sbe, s1e = std::min(n2, s1 + kSB);  // next slab [s1, s1e)
+                    BIE_CUDA_TRY(cudaStreamWaitEvent(hp, ev_b2, 0));  // the previous sweep wrote these columns
+                    k_swap_rng<<<(n2 + 127) / 128, 128, 0, hp>>>(v, s, s0, sbe, 0, n2, s0, s0 + sbe, nullptr, 0);
+                    k_make_Y<<<(n2 - sbe + kYCols - 1) / kYCols, 128, 0, hp>>>(v, TSb, A11b, Ybb, s0, sbe, nsub);
+                    count_launch(2);
+                    if (s1 < n2) {
+                        k_update_agg_async<<<dim3((s1e - s1) / UT3, nt), 128, kAggSmem, hp>>>(v, TSb, Ybb, s0, sbe,
+                                                                                              nsub, s1 / UT3);
+                        count_launch();
+                    }
+                    BIE_CUDA_TRY(cudaEventRecord(ev_y, hp));
+                    BIE_CUDA_TRY(cudaStreamWaitEvent(st, ev_y, 0));
+                    k_update_agg_async<<<dim3(nt, nt), 128, kAggSmem, st>>>(v, TSb, Ybb, s0, sbe, nsub, 0, s1, s1e);
+                    count_launch();
+                    BIE_CUDA_TRY(cudaEventRecord(ev_b2, st));
+                    BIE_CUDA_TRY(cudaGetLastError());
+                }
+            }
+            BIE_CUDA_TRY(cudaEventRecord(ev_y, hp));
+            BIE_CUDA_TRY(cudaStreamWaitEvent(st, ev_y, 0));
+            return BIE_OK;
+        }();
+        cleanup();
+        if (rc) return rc;
+        cudaFreeAsync(TS, st);
+        cudaFreeAsync(Yb, st);
+        cudaFreeAsync(A11S, st);
+    } else if (agg) {
         for (int s0 = 0; s0 < n2; s0 += kSB) {
             const int sbe = std::min(kSB, n2 - s0), nsub = (sbe + NB - 1) / NB;
             for (int p = 0; p < nsub; ++p) {
@@ -1080,9 +1325,12 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                 BIE_CUDA_TRY(cudaGetLastError());
             }
             if (n2 > sbe) {
-                k_make_Y<<<(n2 - sbe + 127) / 128, 128, 0, st>>>(v, TS, A11S, Yb, s0, sbe, nsub);
-                k_update_agg<<<dim3((n2 + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3), 128, 0, st>>>(v, TS, Yb, s0, sbe,
-                                                                                              nsub);
+                k_make_Y<<<(n2 - sbe + kYCols - 1) / kYCols, 128, 0, st>>>(v, TS, A11S, Yb, s0, sbe, nsub);
+                if (agg_async)
+                    k_update_agg_async<<<dim3(n2 / UT3, n2 / UT3), 128, kAggSmem, st>>>(v, TS, Yb, s0, sbe, nsub);
+                else
+                    k_update_agg<<<dim3((n2 + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3), 128, 0, st>>>(v, TS, Yb, s0, sbe,
+                                                                                                  nsub);
                 count_launch(2);
                 BIE_CUDA_TRY(cudaGetLastError());
             }

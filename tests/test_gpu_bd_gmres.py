@@ -420,6 +420,28 @@ def test_bd_wall_delayed_update_parity(bie, monkeypatch):
     assert np.abs(gi @ B - np.eye(B.shape[0])).max() < 1e-12
 
 
+@pytest.mark.parametrize("cid", [2, 3])
+def test_bd_wall_lookahead_bitwise(bie, monkeypatch, cid):
+    """The lookahead schedule of the delayed update (next super-panel factored on a
+    high-priority stream beside the sweep of the current one, cp.async-staged sweep
+    kernel) changes no arithmetic: the wall inverse is bitwise equal to the serial
+    schedule's (BIE_BD_LOOKAHEAD=0) and to the register-staged sweep's (BIE_BD_AGGK=0),
+    and repeatable (a stream-ordering race would change bits)."""
+    monkeypatch.setenv("BIE_BD_AGG", "1")
+    p = make_problem(cid)
+    g = bie.Geometry.from_problem(p)
+    ref = bie.BlockDiag(g, structured=True).block_inverse(p.M)
+    assert np.isfinite(ref).all()
+    again = bie.BlockDiag(g, structured=True).block_inverse(p.M)
+    assert np.array_equal(ref, again)
+    monkeypatch.setenv("BIE_BD_LOOKAHEAD", "0")
+    serial = bie.BlockDiag(g, structured=True).block_inverse(p.M)
+    assert np.array_equal(ref, serial)
+    monkeypatch.setenv("BIE_BD_AGGK", "0")
+    staged = bie.BlockDiag(g, structured=True).block_inverse(p.M)
+    assert np.array_equal(ref, staged)
+
+
 def test_gmres_graph_cache_matches_host_loop(bie, monkeypatch):
     """The CUDA-graph GMRES loop (cached on the geometry, keyed by operator, BD
     handle + serial, tol, max_iter and workspace) against the host-enqueued loop
