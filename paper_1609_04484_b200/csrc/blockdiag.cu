@@ -383,7 +383,7 @@ struct CoopScratch {
 };
 // RPT rows per thread: fewer CTAs make the per-column grid barrier cheaper.
 template <int RPT>
-__global__ void __launch_bounds__(128) k_panel_coop(BDView v, BDScratch s, CoopScratch cs, int k0, int nbe) {
+__global__ void __launch_bounds__(128, RPT == 1 ? 4 : 2) k_panel_coop(BDView v, BDScratch s, CoopScratch cs, int k0, int nbe) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double red_v[4];
     __shared__ int red_i[4];
@@ -962,7 +962,7 @@ __device__ __forceinline__ void bd_cp_async16(void *smem, const void *gmem) {
 constexpr int kAggTsLd = NB + 4, kAggGsLd = UT3 + 4;  // doubles; = 4 (mod 16), rows 16-byte aligned
 constexpr int kAggStage = UT3 * kAggTsLd + NB * kAggGsLd;  // doubles per stage
 constexpr size_t kAggSmem = sizeof(double) * 2 * kAggStage;
-__global__ void __launch_bounds__(128, 3) k_update_agg_async(BDView v, const double *__restrict__ TS,
+__global__ void __launch_bounds__(128, 4) k_update_agg_async(BDView v, const double *__restrict__ TS,
                                                              const double *__restrict__ Y, int s0, int sbe,
                                                              int nsub, int jt0 = 0, int x0 = -1, int x1 = -1) {
     extern __shared__ __align__(16) double agg_smem[];
@@ -1021,24 +1021,31 @@ __global__ void __launch_bounds__(128, 3) k_update_agg_async(BDView v, const dou
         }
         __syncthreads();  // this stage is overwritten by the fetch of chunk p + 2
     }
-    double2 base[4][4];
+    // epilogue in two halves of the warp tile's rows (8 double2 reads in flight per
+    // thread): with the whole tile's base values live beside the accumulators the
+    // kernel needs 160 registers; at <= 128 three of its CTAs leave room on the SM for
+    // one CTA of the cooperative panel that the lookahead schedule runs beside it
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int gi = i0 + wr + 8 * i + gr;
+    for (int h = 0; h < 2; ++h) {
+        double2 base[2][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gj = j0 + wc + 8 * j + 2 * gq;
-            base[i][j] = __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj));
+        for (int i = 0; i < 2; ++i) {
+            const int gi = i0 + wr + 8 * (2 * h + i) + gr;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int gj = j0 + wc + 8 * j + 2 * gq;
+                base[i][j] = __ldcs(reinterpret_cast<const double2 *>(M + (long long)gi * n2 + gj));
+            }
         }
-    }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int gi = i0 + wr + 8 * i + gr;
+        for (int i = 0; i < 2; ++i) {
+            const int gi = i0 + wr + 8 * (2 * h + i) + gr;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int gj = j0 + wc + 8 * j + 2 * gq;
-            __stcs(reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj),
-                   make_double2(base[i][j].x - acc[i][j][0], base[i][j].y - acc[i][j][1]));
+            for (int j = 0; j < 4; ++j) {
+                const int gj = j0 + wc + 8 * j + 2 * gq;
+                __stcs(reinterpret_cast<double2 *>(M + (long long)gi * n2 + gj),
+                       make_double2(base[i][j].x - acc[2 * h + i][j][0], base[i][j].y - acc[2 * h + i][j][1]));
+            }
         }
     }
 }
@@ -1251,6 +1258,17 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
             cudaEventDestroy(ev_b2);
             cudaEventDestroy(ev_f);
         };
+        // BIE_BD_TRACE=1 (diagnostic): per super-panel, CUDA-event times of the slab
+        // factorisation A(S) on hp and of the sweep B2(S) on st, printed to stderr
+        const bool trace = getenv("BIE_BD_TRACE") && atoi(getenv("BIE_BD_TRACE")) != 0;
+        std::vector<cudaEvent_t> tev;
+        auto mark = [&](cudaStream_t q) {
+            if (!trace) return;
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, q);
+            tev.push_back(e);
+        };
         int rc = [&]() -> int {
             BIE_CUDA_TRY(cudaEventRecord(ev_f, st));
             BIE_CUDA_TRY(cudaStreamWaitEvent(hp, ev_f, 0));
@@ -1260,6 +1278,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                 const int sbe = std::min(kSB, n2 - s0), nsub = (sbe + NB - 1) / NB;
                 double *TSb = TS + (size_t)(S & 1) * n2 * kSB, *Ybb = Yb + (size_t)(S & 1) * n2 * kSB;
                 double *A11b = A11S + (size_t)(S & 1) * 4 * NB * NB;
+                mark(hp);  // [4S]: A(S) begins
                 for (int p = 0; p < nsub; ++p) {
                     int k0 = s0 + p * NB, nbe = std::min(NB, n2 - k0);
                     {
@@ -1279,6 +1298,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                     count_launch(5);
                     BIE_CUDA_TRY(cudaGetLastError());
                 }
+                mark(hp);  // [4S + 1]: A(S) done
                 if (n2 > sbe) {
                     const int s1 = s0 + sbe, s1e = std::min(n2, s1 + kSB);  // next slab [s1, s1e)
                     BIE_CUDA_TRY(cudaStreamWaitEvent(hp, ev_b2, 0));  // the previous sweep wrote these columns
@@ -1292,7 +1312,9 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                     }
                     BIE_CUDA_TRY(cudaEventRecord(ev_y, hp));
                     BIE_CUDA_TRY(cudaStreamWaitEvent(st, ev_y, 0));
+                    mark(st);  // [4S + 2]: B2(S) begins
                     k_update_agg_async<<<dim3(nt, nt), 128, kAggSmem, st>>>(v, TSb, Ybb, s0, sbe, nsub, 0, s1, s1e);
+                    mark(st);  // [4S + 3]: B2(S) done
                     count_launch();
                     BIE_CUDA_TRY(cudaEventRecord(ev_b2, st));
                     BIE_CUDA_TRY(cudaGetLastError());
@@ -1303,6 +1325,27 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
             return BIE_OK;
         }();
         cleanup();
+        if (trace && rc == BIE_OK && tev.size() % 4 == 0 && !tev.empty()) {
+            cudaStreamSynchronize(st);
+            double sa = 0, sb = 0, gap = 0;
+            const size_t ns = tev.size() / 4;
+            float ms = 0;
+            for (size_t i = 0; i < ns; ++i) {
+                cudaEventElapsedTime(&ms, tev[4 * i], tev[4 * i + 1]);
+                sa += ms;
+                cudaEventElapsedTime(&ms, tev[4 * i + 2], tev[4 * i + 3]);
+                sb += ms;
+                if (i + 1 < ns) {
+                    cudaEventElapsedTime(&ms, tev[4 * i + 3], tev[4 * i + 6]);
+                    gap += ms;
+                }
+            }
+            cudaEventElapsedTime(&ms, tev[0], tev[tev.size() - 1]);
+            fprintf(stderr, "[bie bd trace] n2=%d super-panels=%zu  A(S) avg %.3f ms  B2(S) avg %.3f ms  "
+                            "gap between sweeps avg %.3f ms  total %.1f ms\n",
+                    n2, ns, sa / ns, sb / ns, gap / (ns - 1), ms);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
         if (rc) return rc;
         cudaFreeAsync(TS, st);
         cudaFreeAsync(Yb, st);
