@@ -970,33 +970,14 @@ __device__ __forceinline__ void bd_cp_async16(void *smem, const void *gmem) {
 constexpr int kAggTsLd = NB + 4, kAggGsLd = UT3 + 4;  // doubles; = 4 (mod 16), rows 16-byte aligned
 constexpr int kAggStage = UT3 * kAggTsLd + NB * kAggGsLd;  // doubles per stage
 constexpr size_t kAggSmem = sizeof(double) * 2 * kAggStage;
-constexpr long long kAggStagger = 9000;  // cycles: about a third of a 64x64x128 tile's time at 3 CTAs per SM
 __global__ void __launch_bounds__(128, 4) k_update_agg_async(BDView v, const double *__restrict__ TS,
                                                              const double *__restrict__ Y, int s0, int sbe,
-                                                             int nsub, int jt0 = 0, int x0 = -1, int x1 = -1,
-                                                             unsigned *arrive = nullptr) {
+                                                             int nsub, int jt0 = 0, int x0 = -1, int x1 = -1) {
     extern __shared__ __align__(16) double agg_smem[];
     const int n2 = v.n2;
     const int i0 = blockIdx.y * UT3, j0 = (jt0 + blockIdx.x) * UT3;
     if (j0 >= s0 && j0 < s0 + sbe) return;  // the slab is final (s0, sbe multiples of UT3)
     if (j0 >= x0 && j0 < x1) return;        // columns another launch of this update covers (lookahead)
-    // Stagger the first wave: every CTA does the same work, so the three CTAs of an SM
-    // would otherwise run in lockstep for the whole launch -- staging, DMMA phase and the
-    // C-tile epilogue all at the same time, the tensor pipe idle through every epilogue
-    // (ncu: 79% DMMA-active with math-pipe throttle as the top stall).  The k-th first-wave
-    // CTA to arrive on an SM waits k/3 of a tile period once; later CTAs inherit the phase
-    // of the slot they take over.
-    if (arrive && blockIdx.y * gridDim.x + blockIdx.x < 3 * 148) {
-        __shared__ unsigned s_slot;
-        if (threadIdx.x == 0) {
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            s_slot = atomicAdd(arrive + (smid % 160), 1u) % 3u;
-        }
-        __syncthreads();
-        const long long t_end = clock64() + (long long)s_slot * kAggStagger;
-        while (clock64() < t_end) __nanosleep(200);
-    }
     double *M = v.mat;
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
@@ -1228,7 +1209,6 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     // large single block (the wall): super-panels of kSB columns with the delayed
     // rank-kSB update of the columns outside the slab (k_make_Y / k_update_agg)
     double *TS = nullptr, *Yb = nullptr, *A11S = nullptr;
-    unsigned *agg_arrive = nullptr;  // per-SM arrival counters of the sweep's first wave (stagger)
     // BIE_BD_AGG: 0 never, 1 whenever the block is factored cooperatively (tests),
     // default: blocks of order >= 8192 (config 4: 0.83 -> 0.57 s; at order 1024-4096
     // the extra launches cost more than the saved traffic)
@@ -1246,10 +1226,6 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         BIE_CUDA_TRY(cudaMallocAsync(&TS, sizeof(double) * 2 * (size_t)n2 * kSB, st));
         BIE_CUDA_TRY(cudaMallocAsync(&Yb, sizeof(double) * 2 * (size_t)n2 * kSB, st));
         BIE_CUDA_TRY(cudaMallocAsync(&A11S, sizeof(double) * 2 * 4 * NB * NB, st));
-        if (!(getenv("BIE_BD_STAGGER") && atoi(getenv("BIE_BD_STAGGER")) == 0)) {
-            BIE_CUDA_TRY(cudaMallocAsync(&agg_arrive, sizeof(unsigned) * 160, st));
-            BIE_CUDA_TRY(cudaMemsetAsync(agg_arrive, 0, sizeof(unsigned) * 160, st));
-        }
     }
     auto panel = [&](int k0, int nbe) -> int {
         if (coop) {
@@ -1345,8 +1321,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                     BIE_CUDA_TRY(cudaEventRecord(ev_y, hp));
                     BIE_CUDA_TRY(cudaStreamWaitEvent(st, ev_y, 0));
                     mark(st);  // [4S + 2]: B2(S) begins
-                    k_update_agg_async<<<dim3(nt, nt), 128, kAggSmem, st>>>(v, TSb, Ybb, s0, sbe, nsub, 0, s1, s1e,
-                                                                            agg_arrive);
+                    k_update_agg_async<<<dim3(nt, nt), 128, kAggSmem, st>>>(v, TSb, Ybb, s0, sbe, nsub, 0, s1, s1e);
                     mark(st);  // [4S + 3]: B2(S) done
                     count_launch();
                     BIE_CUDA_TRY(cudaEventRecord(ev_b2, st));
@@ -1383,7 +1358,6 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         cudaFreeAsync(TS, st);
         cudaFreeAsync(Yb, st);
         cudaFreeAsync(A11S, st);
-        if (agg_arrive) cudaFreeAsync(agg_arrive, st);
     } else if (agg) {
         for (int s0 = 0; s0 < n2; s0 += kSB) {
             const int sbe = std::min(kSB, n2 - s0), nsub = (sbe + NB - 1) / NB;
@@ -1415,7 +1389,6 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         cudaFreeAsync(TS, st);
         cudaFreeAsync(Yb, st);
         cudaFreeAsync(A11S, st);
-        if (agg_arrive) cudaFreeAsync(agg_arrive, st);
     }
     for (int k0 = 0; k0 < n2 && !agg; k0 += NB) {
         int nbe = std::min(NB, n2 - k0);
