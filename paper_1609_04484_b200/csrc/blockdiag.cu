@@ -1269,13 +1269,13 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
         // BIE_BD_TRACE=1 (diagnostic): per super-panel, CUDA-event times of the slab
         // factorisation A(S) on hp and of the sweep B2(S) on st, printed to stderr
         const bool trace = getenv("BIE_BD_TRACE") && atoi(getenv("BIE_BD_TRACE")) != 0;
-        std::vector<cudaEvent_t> tev;
-        auto mark = [&](cudaStream_t q) {
+        std::vector<cudaEvent_t> tev, tsub;  // tsub: 3 per sub-panel (before / after the panel LU, after its slab update)
+        auto mark = [&](cudaStream_t q, bool sub = false) {
             if (!trace) return;
             cudaEvent_t e;
             cudaEventCreate(&e);
             cudaEventRecord(e, q);
-            tev.push_back(e);
+            (sub ? tsub : tev).push_back(e);
         };
         int rc = [&]() -> int {
             BIE_CUDA_TRY(cudaEventRecord(ev_f, st));
@@ -1289,11 +1289,13 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                 mark(hp);  // [4S]: A(S) begins
                 for (int p = 0; p < nsub; ++p) {
                     int k0 = s0 + p * NB, nbe = std::min(NB, n2 - k0);
+                    mark(hp, true);
                     {
                         int G = (n2 - k0 + 128 * rpt - 1) / (128 * rpt);
                         void *args[] = {&v, &s, &cs, &k0, &nbe};
                         BIE_CUDA_TRY(cudaLaunchCooperativeKernel(coop_kernel, G, 128, args, 0, hp));
                     }
+                    mark(hp, true);
                     k_swap_rng<<<(sbe + p * NB + 127) / 128, 128, 0, hp>>>(v, s, k0, nbe, s0, s0 + sbe, -1, -1, TSb,
                                                                            p * NB);
                     k_copy_T<<<dim3((unsigned)(((long long)n2 * NB + 255) / 256), 1), 256, 0, hp>>>(v, s, k0, nbe,
@@ -1303,6 +1305,7 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                     k_make_G<<<dim3((sbe + 127) / 128, 1), 128, 0, hp>>>(v, s, k0, nbe, s0, s0 + sbe);
                     k_update3<<<dim3((sbe + UT3 - 1) / UT3, (n2 + UT3 - 1) / UT3, 1), 128, 0, hp>>>(v, s, k0, nbe,
                                                                                                  s0, s0 + sbe);
+                    mark(hp, true);
                     count_launch(5);
                     BIE_CUDA_TRY(cudaGetLastError());
                 }
@@ -1353,7 +1356,20 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
                             "gap between sweeps avg %.3f ms  total %.1f ms\n",
                     n2, ns, sa / ns, sb / ns, gap / (ns - 1), ms);
         }
+        if (trace && rc == BIE_OK && tsub.size() % 3 == 0 && !tsub.empty()) {
+            double sp = 0, sr = 0;
+            float ms = 0;
+            for (size_t i = 0; i < tsub.size(); i += 3) {
+                cudaEventElapsedTime(&ms, tsub[i], tsub[i + 1]);
+                sp += ms;
+                cudaEventElapsedTime(&ms, tsub[i + 1], tsub[i + 2]);
+                sr += ms;
+            }
+            fprintf(stderr, "[bie bd trace] per sub-panel: panel LU avg %.3f ms, swap/T/G/slab update avg %.3f ms\n",
+                    sp / (tsub.size() / 3), sr / (tsub.size() / 3));
+        }
         for (cudaEvent_t e : tev) cudaEventDestroy(e);
+        for (cudaEvent_t e : tsub) cudaEventDestroy(e);
         if (rc) return rc;
         cudaFreeAsync(TS, st);
         cudaFreeAsync(Yb, st);
