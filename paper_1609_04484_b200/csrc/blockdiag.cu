@@ -1179,7 +1179,8 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     const bool coop = n2 > kSmemPanelRows && v.count == 1;
     CoopScratch cs{};
     // rows per thread of the cooperative panel (tuning knob BIE_PANEL_RPT = 1 | 2;
-    // measured config 4: 1 row 0.72-0.74 s factor, 2 rows 0.78-0.80 s)
+    // measured config 4, round 1: 1 row 0.72-0.74 s factor, 2 rows 0.78-0.80 s; with the
+    // round-2 lookahead schedule and one-division panel: 0.356 vs 0.354 s, 1 row kept)
     int rpt = 1;
     if (const char *e = getenv("BIE_PANEL_RPT")) rpt = std::max(1, std::min(2, atoi(e)));
     void *coop_kernel = rpt == 2 ? (void *)k_panel_coop<2> : (void *)k_panel_coop<1>;
