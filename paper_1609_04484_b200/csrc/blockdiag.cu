@@ -1211,11 +1211,12 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     // rank-kSB update of the columns outside the slab (k_make_Y / k_update_agg)
     double *TS = nullptr, *Yb = nullptr, *A11S = nullptr;
     // BIE_BD_AGG: 0 never, 1 whenever the block is factored cooperatively (tests),
-    // default: blocks of order >= 8192 (config 4: 0.83 -> 0.57 s; at order 1024-4096
-    // the extra launches cost more than the saved traffic)
+    // default: blocks of order >= 4096 (config 4: 0.83 -> 0.57 s in round 2's first form; with
+    // the lookahead schedule order 4096 gains too, config 3 36.6 -> 31.3 ms; at order 1024 the
+    // extra launches cost more than the saved traffic, 7.8 -> 8.6 ms)
     int agg_mode = 2;
     if (const char *e = getenv("BIE_BD_AGG")) agg_mode = std::max(0, std::min(1, atoi(e)));
-    const bool agg = coop && n2 % UT3 == 0 && (agg_mode == 1 || (agg_mode == 2 && n2 >= 8192));
+    const bool agg = coop && n2 % UT3 == 0 && (agg_mode == 1 || (agg_mode == 2 && n2 >= 4096));
     // BIE_BD_AGGK: 1 (default) cp.async double-buffered sweep, 0 register-staged (A/B)
     bool agg_async = true;
     if (const char *e = getenv("BIE_BD_AGGK")) agg_async = atoi(e) != 0;
@@ -1252,21 +1253,17 @@ static int factor_class(Geometry *g, BDView v, int lo0, int nodes, bool is_wall,
     bool lookahead = agg_async;
     if (const char *e = getenv("BIE_BD_LOOKAHEAD")) lookahead = lookahead && atoi(e) != 0;
     if (agg && lookahead) {
-        cudaStream_t hp = nullptr;
-        cudaEvent_t ev_y = nullptr, ev_b2 = nullptr, ev_f = nullptr;
-        int pr_lo = 0, pr_hi = 0;
-        BIE_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&pr_lo, &pr_hi));
-        BIE_CUDA_TRY(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, pr_hi));
-        BIE_CUDA_TRY(cudaEventCreateWithFlags(&ev_y, cudaEventDisableTiming));
-        BIE_CUDA_TRY(cudaEventCreateWithFlags(&ev_b2, cudaEventDisableTiming));
-        BIE_CUDA_TRY(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming));
-        auto cleanup = [&]() {
-            cudaStreamSynchronize(hp);
-            cudaStreamDestroy(hp);
-            cudaEventDestroy(ev_y);
-            cudaEventDestroy(ev_b2);
-            cudaEventDestroy(ev_f);
-        };
+        if (!g->bd_hp) {
+            int pr_lo = 0, pr_hi = 0;
+            BIE_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&pr_lo, &pr_hi));
+            BIE_CUDA_TRY(cudaStreamCreateWithPriority(&g->bd_hp, cudaStreamNonBlocking, pr_hi));
+            for (cudaEvent_t &e : g->bd_ev) BIE_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        cudaStream_t hp = g->bd_hp;
+        cudaEvent_t ev_y = g->bd_ev[0], ev_b2 = g->bd_ev[1], ev_f = g->bd_ev[2];
+        // hp is joined into st by the last event wait below; the host wait keeps the scratch
+        // frees (stream-ordered on st) and a later factor on another stream safely behind it
+        auto cleanup = [&]() { cudaStreamSynchronize(hp); };
         // BIE_BD_TRACE=1 (diagnostic): per super-panel, CUDA-event times of the slab
         // factorisation A(S) on hp and of the sweep B2(S) on st, printed to stderr
         const bool trace = getenv("BIE_BD_TRACE") && atoi(getenv("BIE_BD_TRACE")) != 0;

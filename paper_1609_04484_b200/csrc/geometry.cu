@@ -295,6 +295,9 @@ int bie_geometry_destroy(bie_geometry_t gh) {
     for (auto &ev : g->gm.evs)
         if (ev) cudaEventDestroy(ev);
     if (g->side) cudaStreamDestroy(g->side);
+    if (g->bd_hp) cudaStreamDestroy(g->bd_hp);
+    for (cudaEvent_t e : g->bd_ev)
+        if (e) cudaEventDestroy(e);
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);
     if (g->ev_join) cudaEventDestroy(g->ev_join);
     if (g->gm.gexec) cudaGraphExecDestroy(g->gm.gexec);

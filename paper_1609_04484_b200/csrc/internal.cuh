@@ -170,6 +170,10 @@ struct Geometry {
     double *sym_diag = nullptr;   // [2N]
     cudaStream_t side = nullptr;  // in-block kernel beside the pair kernel (fork/join by events)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // BD factor lookahead (blockdiag.cu): high-priority panel stream and its events, created on
+    // first use and kept (a fresh priority stream per factor showed host-side stalls of 0.1-0.7 s)
+    cudaStream_t bd_hp = nullptr;
+    cudaEvent_t bd_ev[3] = {nullptr, nullptr, nullptr};
     int sym_nTB = 0, sym_P = 0, sym_variant = 0;  // (8, 2, 2), lockstep groups of 4, 6 CTAs/SM: fastest measured
     int slp_sym_variant = 0;  // (8, 2, 2): fastest measured
     unsigned long long *sym_trace = nullptr;  // BIE_SYM_TRACE: per-CTA start/end times of the last launch

@@ -406,7 +406,7 @@ def test_krylov_axpy_beyond_one_coefficient_tile(bie):
 
 def test_bd_wall_delayed_update_parity(bie, monkeypatch):
     """The delayed rank-128 wall update (k_make_Y / k_update_agg; by default only
-    for blocks of order >= 8192) forced on config 2's 1024-order wall: the same
+    for blocks of order >= 4096) forced on config 2's 1024-order wall: the same
     inverse as the oracle's to 1e-12 and B X = I, as the per-panel sweep."""
     monkeypatch.setenv("BIE_BD_AGG", "1")
     p = make_problem(2)
