@@ -13,6 +13,12 @@
 //   3. k_copy_T   : T = M[:, K];   k_make_G : G = A11^{-1} M[K, :], G[:, K] = A11^{-1}
 //   4. k_update3  : M[i, :] = (i in K) ? G[i-k0, :] : base(i, :) - T[i, :] G
 //                   (base = M off K, 0 on K)  -- the rank-NB sweep on the FP64 tensor cores (DMMA).
+// Large single blocks (the wall, order >= 4096): super-panels of kSB = 4 NB columns with
+// the delayed rank-kSB update of the columns outside the slab (k_make_Y,
+// k_update_agg_async: cp.async double-buffered DMMA tiles) and a lookahead schedule:
+// the next super-panel's cooperative panel LUs (k_panel_coop) run on a high-priority
+// stream beside the sweep of the current one (k_swap_rng applies a super-panel's row
+// swaps to the outside columns afterwards).  DESIGN.md s5.
 // After the last panel, columns are unpermuted (A^{-1} = M P).  Batched over
 // all blocks of one size class (pores share one size; Gamma_0 is its own class).
 // Apply: one warp per row of the explicit inverses (HBM-bound batched GEMV).
