@@ -160,7 +160,10 @@ BIE_API int bie_field_eval(bie_geometry_t g, const double *sigma, const double *
  * includes N0).  Each block is inverted explicitly by Gauss-Jordan
  * elimination with partial pivoting (row of max |.|).  The handle owns the
  * inverses (sum_b (2 n_b)^2 doubles of device memory).
- * Synchronises `stream` once to read the pivot status.
+ * Synchronises `stream` once to read the pivot status.  Blocks of order >= 4096
+ * (the wall) are factored on `stream` plus one internal high-priority stream owned
+ * by the geometry (fork/join by events; the call waits for that stream before it
+ * returns), so `stream` must not be in capture mode.
  * Errors: BIE_ESINGULAR (message names the body), BIE_ENOMEM, BIE_ECUDA, BIE_EINVAL.
  */
 BIE_API int bie_blockdiag_factor(bie_geometry_t g, bie_blockdiag_t *out, void *stream);
